@@ -1,0 +1,183 @@
+/*
+ * diagmm.h — C ABI of the B200 (sm_100a) DiagLinear hot path.
+ *
+ * The reference (DynaDiag, /root/reference/pkg/src/diagsparse) is a float64
+ * numpy package whose "FFI" for this path is the custom-op boundary
+ * `_record_diag_matmul` (layers.py:108-170) recorded through
+ * `Tape.record(out, inputs, backward)` (autodiff.py:43-50), plus the selection
+ * functions of selection.py.  Each entry point below replaces one piece of that
+ * boundary; the comment on each names the reference symbol (file:line).
+ *
+ * Conventions
+ *   - W is M x N (out x in).  C = max(M, N) candidate diagonals, L = min(M, N)
+ *     values per diagonal; candidate i IS offset i (layers.py:199-206).
+ *   - Geometry (diagcore.py:106-116): M >= N: value t of offset o sits at
+ *     ((o + t) mod M, t);  M < N: at (t, (o + t) mod N).
+ *   - Activations are row-major (B, features): x is (B, N), y is (B, M).
+ *   - values is the candidate store (C, L) row-major; alpha, alpha_soft are
+ *     (C,) float64; `active` is the ascending list of active offsets and
+ *     `n_act` its length, both in DEVICE memory (no host sync is needed).
+ *   - dtype: DIAGMM_F64 -> activations and parameters double;
+ *            DIAGMM_F32 -> activations and parameters float;
+ *            DIAGMM_BF16 -> activations bf16, parameters/gradients float,
+ *                           fp32 accumulation.
+ *   - All pointers are caller-owned device pointers; every call is
+ *     stream-ordered on `stream` (a cudaStream_t, NULL = legacy default) and
+ *     never synchronizes the host.  Inputs are never written.
+ *   - Return value: 0 on success, otherwise a DIAGMM_E* code; the Python
+ *     wrapper maps the codes onto the reference's exception classes
+ *     (errors.py:8-53): SHAPE -> ShapeMismatch, TEMPERATURE ->
+ *     NonPositiveTemperature, K -> ValueError.
+ */
+#ifndef DIAGMM_H
+#define DIAGMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DIAGMM_API __attribute__((visibility("default")))
+#else
+#define DIAGMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum diagmm_dtype { DIAGMM_F64 = 0, DIAGMM_F32 = 1, DIAGMM_BF16 = 2 };
+
+enum diagmm_status {
+  DIAGMM_OK = 0,
+  DIAGMM_ESHAPE = 1,       /* ShapeMismatch (errors.py:20) */
+  DIAGMM_ETEMPERATURE = 2, /* NonPositiveTemperature (errors.py:24) */
+  DIAGMM_EK = 3,           /* k outside [1, C] (selection.py:95-96) */
+  DIAGMM_EDTYPE = 4,
+  DIAGMM_EWORKSPACE = 5,
+  DIAGMM_ECUDA = 6,
+  DIAGMM_ETOOLARGE = 7,    /* C above the single-CTA selection limit */
+};
+
+/* Library identity: "diagmm <version> sm_100a". */
+DIAGMM_API const char* diagmm_version(void);
+DIAGMM_API const char* diagmm_status_string(int status);
+/* Kernels launched by this library since load (for launch accounting). */
+DIAGMM_API unsigned long long diagmm_launch_count(void);
+
+/* ---- K1: forward DiagMM --------------------------------------------------
+ * y = x @ W_K^T (+ bias), W_K = sum_{o in active} alpha_soft[o] P_o diag(values[o]).
+ * Replaces: the forward product of _record_diag_matmul (layers.py:400-407:
+ * bcsr_spmm / reference_spmm, diagcore.py:200-238, bcsr.py:362-409), the
+ * weight scaling of DynaDiagLayer.forward (layers.py:235) and Tape.add_bias
+ * (autodiff.py:72-81).  alpha_soft == NULL means unit scale (DiagHeur /
+ * frozen layers, layers.py:354-363, 301-310).  max_act is a host upper bound
+ * on *n_act used only to size work (pass C when unknown). */
+DIAGMM_API int diagmm_forward(int dtype, int M, int N, int B, const void* x,
+                   const void* values, const double* alpha_soft,
+                   const int32_t* active, const int32_t* n_act, int max_act,
+                   const void* bias, void* y, void* stream);
+
+/* ---- K2: input gradient through the (never materialized) transpose -------
+ * dx = dy @ W_K.  Replaces layers.py:414-418 (transpose, diagcore.py:162-191,
+ * followed by the same spmm). */
+DIAGMM_API int diagmm_backward_input(int dtype, int M, int N, int B, const void* dy,
+                          const void* values, const double* alpha_soft,
+                          const int32_t* active, const int32_t* n_act,
+                          int max_act, void* dx, void* stream);
+
+/* ---- K3: per-diagonal weight gradient ----------------------------------
+ * gw[j,t] = sum_b dy[b, r_jt] * x[b, c_jt]   (layers.py:419-428)
+ * g_values (C, L): row active[j] = alpha_soft[active[j]] * gw[j] (unit scale
+ * if alpha_soft == NULL), every other row exactly 0 (layers.py:429-433).
+ * g_soft (C,) float64, may be NULL: g_soft[active[j]] = sum_t gw[j,t] *
+ * values[active[j],t], 0 elsewhere (layers.py:434-435).
+ * g_bias (M,), may be NULL: column sums of dy (autodiff.py:77-79).
+ * slot (C,) int32 from diagmm_topk_waterfill / diagmm_active_from_list.
+ * workspace: at least diagmm_backward_weight_workspace(...) bytes. */
+DIAGMM_API size_t diagmm_backward_weight_workspace(int dtype, int M, int N, int B,
+                                        int max_act);
+DIAGMM_API int diagmm_backward_weight(int dtype, int M, int N, int B, const void* dy,
+                           const void* x, const void* values,
+                           const double* alpha_soft, const int32_t* active,
+                           const int32_t* slot, const int32_t* n_act,
+                           int max_act, void* g_values, double* g_soft,
+                           void* g_bias, void* workspace, size_t ws_bytes,
+                           void* stream);
+
+/* ---- K4: soft TopK (capped water-filling) + active set -------------------
+ * alpha_soft = soft_topk(alpha, k, T) (selection.py:100-142); clamped[i] = 1
+ * for the water-filling's clamped set; active = flatnonzero(alpha_soft >=
+ * 1e-3) ascending (layers.py:234, EPS_ACTIVE layers.py:41); slot[i] = index of
+ * i in active or -1; *n_act = len(active).  float64 throughout.  Any of
+ * clamped/active/slot/n_act may be NULL. */
+DIAGMM_API int diagmm_topk_waterfill(int C, int k, double temperature, const double* alpha,
+                          double* alpha_soft, uint8_t* clamped,
+                          int32_t* active, int32_t* slot, int32_t* n_act,
+                          void* stream);
+
+/* ---- K5: soft TopK gradient (+ fused l1 penalty gradient) ----------------
+ * g = soft_topk_grad(alpha, k, T, g_soft) (selection.py:145-173)
+ *     + l1_coeff * sign(alpha) (selection.py:217-222, layers.py:253-257).
+ * clamped must come from diagmm_topk_waterfill on the same (alpha, k, T).
+ * accumulate != 0 adds into g_alpha (Tape.backward accumulation,
+ * autodiff.py:149-155). */
+DIAGMM_API int diagmm_topk_grad(int C, int k, double temperature, const double* alpha,
+                     const uint8_t* clamped, const double* g_soft,
+                     double l1_coeff, double* g_alpha, int accumulate,
+                     void* stream);
+
+/* ---- hard TopK: select_hard (selection.py:176-186) -----------------------
+ * idx (k,) = indices of the k largest alpha, ties to the smaller index,
+ * ascending. */
+DIAGMM_API int diagmm_select_hard(int C, int k, const double* alpha, int32_t* idx,
+                       void* stream);
+
+/* Build slot/n_act from an explicit ascending offset list of length n (used
+ * by DiagHeur and frozen layers whose active set is not soft-selected,
+ * layers.py:381-413, 290-310).  slot (C,) int32. */
+DIAGMM_API int diagmm_active_from_list(int C, int n, const int32_t* offsets, int32_t* slot,
+                            int32_t* n_act, void* stream);
+
+/* ---- K6: AdamW over the full candidate store ----------------------------
+ * adamw_step (training.py:346-358) applied elementwise to n elements:
+ * grad is scaled by *clip_scale when clip_scale != NULL (clip_global_norm,
+ * training.py:406-417).  step is the 1-based update count t.  param/grad/m/v
+ * are float64 when dtype == DIAGMM_F64, else float. */
+DIAGMM_API int diagmm_adamw(int dtype, size_t n, void* param, const void* grad, void* m,
+                 void* v, int step, double lr, double beta1, double beta2,
+                 double eps, double weight_decay, const double* clip_scale,
+                 void* stream);
+
+/* Global-norm clipping, device side (training.py:406-417):
+ * diagmm_sumsq writes sum(x^2) of one tensor into *out (float64, fixed
+ * reduction order, so deterministic run to run); scratch holds at least
+ * diagmm_sumsq_scratch_len() doubles.  diagmm_clip_scale reads n partial
+ * sums, writes norm = sqrt(sum) to *norm and max_norm/norm (if norm >
+ * max_norm and norm > 0, else 1) to *scale. */
+DIAGMM_API int diagmm_sumsq_scratch_len(void);
+DIAGMM_API int diagmm_sumsq(int dtype, size_t n, const void* x, double* out,
+                 double* scratch, void* stream);
+DIAGMM_API int diagmm_clip_scale(int n, const double* partial, double max_norm,
+                      double* norm, double* scale, void* stream);
+
+/* ---- dense-equivalent route (reference's own BLAS switch) ---------------
+ * The reference multiplies the materialized matrix with BLAS when the
+ * structural density reaches 1/4 (diagcore.py:226-228) and computes dW
+ * densely then gathers (layers.py:420-423).  diagmm_materialize writes
+ * W_K (M, N) row-major in `dtype` (zeros off the active diagonals);
+ * diagmm_gather_dense_grad turns a dense dW (M, N, float32/float64 = param
+ * type) into g_values / g_soft exactly like diagmm_backward_weight. */
+DIAGMM_API int diagmm_materialize(int dtype, int M, int N, const void* values,
+                       const double* alpha_soft, const int32_t* active,
+                       const int32_t* n_act, int max_act, void* w_dense,
+                       void* stream);
+DIAGMM_API int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW,
+                             const void* values, const double* alpha_soft,
+                             const int32_t* active, const int32_t* slot,
+                             const int32_t* n_act, void* g_values,
+                             double* g_soft, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIAGMM_H */

@@ -1,0 +1,83 @@
+"""ctypes binding of the C ABI in ``include/diagmm.h`` (``_lib/libdiagmm.so``).
+
+This is the only place the package touches native code.  There is no CPU
+fallback: if the library is missing or fails to load, every op raises
+``NativeLibraryError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from .errors import STATUS_EXCEPTIONS, NativeLibraryError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdiagmm.so"
+
+F64, F32, BF16 = 0, 1, 2
+
+_vp, _i, _d, _sz = C.c_void_p, C.c_int, C.c_double, C.c_size_t
+
+# name -> (restype, argtypes); mirrors include/diagmm.h one to one.
+SIGNATURES = {
+    "diagmm_version": (C.c_char_p, []),
+    "diagmm_status_string": (C.c_char_p, [_i]),
+    "diagmm_launch_count": (C.c_ulonglong, []),
+    "diagmm_forward": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "diagmm_backward_input": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
+    "diagmm_backward_weight_workspace": (_sz, [_i, _i, _i, _i, _i]),
+    "diagmm_backward_weight": (
+        _i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "diagmm_topk_waterfill": (_i, [_i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "diagmm_topk_grad": (_i, [_i, _i, _d, _vp, _vp, _vp, _d, _vp, _i, _vp]),
+    "diagmm_select_hard": (_i, [_i, _i, _vp, _vp, _vp]),
+    "diagmm_active_from_list": (_i, [_i, _i, _vp, _vp, _vp, _vp]),
+    "diagmm_adamw": (_i, [_i, _sz, _vp, _vp, _vp, _vp, _i, _d, _d, _d, _d, _d, _vp, _vp]),
+    "diagmm_sumsq_scratch_len": (_i, []),
+    "diagmm_sumsq": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
+    "diagmm_clip_scale": (_i, [_i, _vp, _d, _vp, _vp, _vp]),
+    "diagmm_materialize": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
+    "diagmm_gather_dense_grad": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+}
+
+_LIB = None
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes handle with typed signatures."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeLibraryError(
+            f"{p} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the DiagLinear path has no CPU fallback)"
+        )
+    try:
+        lib = C.CDLL(str(p))
+    except OSError as exc:  # pragma: no cover - environment failure
+        raise NativeLibraryError(f"cannot load {p}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status == 0:
+        return
+    lib = load()
+    msg = lib.diagmm_status_string(status).decode()
+    exc = STATUS_EXCEPTIONS.get(status, NativeLibraryError)
+    raise exc(f"{what}: {msg}")
+
+
+def call(name: str, *args) -> int:
+    status = getattr(load(), name)(*args)
+    check(status, name)
+    return status

@@ -1,0 +1,196 @@
+// capi.cu — extern "C" entry points declared in include/diagmm.h.
+// Validates arguments (mirroring the reference's exceptions) and dispatches
+// on dtype to the templated launchers.
+#include "common.cuh"
+#include <atomic>
+
+namespace diagmm {
+template <typename T>
+int run_product(bool, int, int, int, const void*, const void*, const double*, const int32_t*,
+                const int32_t*, int, const void*, void*, cudaStream_t);
+template <typename T> size_t dw_workspace(int, int, int, int);
+template <typename T>
+int run_dw(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
+           const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
+template <typename T>
+int run_materialize(int, int, const void*, const double*, const int32_t*, const int32_t*, int, void*,
+                    cudaStream_t);
+template <typename P>
+int run_gather_dense(int, int, const void*, const void*, const double*, const int32_t*, const int32_t*,
+                     void*, double*, cudaStream_t);
+int run_waterfill(int, int, double, const double*, double*, uint8_t*, int32_t*, int32_t*, int32_t*,
+                  cudaStream_t);
+int run_select_hard(int, int, const double*, int32_t*, cudaStream_t);
+int run_active_from_list(int, int, const int32_t*, int32_t*, int32_t*, cudaStream_t);
+int run_topk_grad(int, int, double, const double*, const uint8_t*, const double*, double, double*, int,
+                  cudaStream_t);
+template <typename P>
+int run_adamw(size_t, void*, const void*, void*, void*, int, double, double, double, double, double,
+              const double*, cudaStream_t);
+template <typename P> int run_sumsq(size_t, const void*, double*, double*, cudaStream_t);
+int run_clip_scale(int, const double*, double, double*, double*, cudaStream_t);
+constexpr int kSumsqScratch = 296;
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+}  // namespace diagmm
+
+using namespace diagmm;
+
+#define DIAGMM_DISPATCH(dtype, FN, ...)                         \
+  switch (dtype) {                                              \
+    case DIAGMM_F64: return FN<double>(__VA_ARGS__);            \
+    case DIAGMM_F32: return FN<float>(__VA_ARGS__);             \
+    case DIAGMM_BF16: return FN<__nv_bfloat16>(__VA_ARGS__);    \
+    default: return DIAGMM_EDTYPE;                              \
+  }
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+static int check_shape(int M, int N, int B, int max_act) {
+  if (M < 1 || N < 1 || B < 0) return DIAGMM_ESHAPE;
+  const int C = M > N ? M : N;
+  if (max_act < 0 || max_act > C) return DIAGMM_ESHAPE;
+  return DIAGMM_OK;
+}
+
+extern "C" {
+
+const char* diagmm_version(void) { return "diagmm 0.1.0 sm_100a"; }
+
+unsigned long long diagmm_launch_count(void) { return g_launches.load(); }
+
+const char* diagmm_status_string(int status) {
+  switch (status) {
+    case DIAGMM_OK: return "ok";
+    case DIAGMM_ESHAPE: return "shape mismatch";
+    case DIAGMM_ETEMPERATURE: return "temperature must be positive";
+    case DIAGMM_EK: return "k outside [1, C]";
+    case DIAGMM_EDTYPE: return "unsupported dtype";
+    case DIAGMM_EWORKSPACE: return "workspace too small";
+    case DIAGMM_ECUDA: return "CUDA launch failure";
+    case DIAGMM_ETOOLARGE: return "problem exceeds kernel limits";
+    default: return "unknown status";
+  }
+}
+
+int diagmm_forward(int dtype, int M, int N, int B, const void* x, const void* values,
+                   const double* alpha_soft, const int32_t* active, const int32_t* n_act, int max_act,
+                   const void* bias, void* y, void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  const int C = M > N ? M : N, L = M < N ? M : N;
+  // tall/square: scatter form with in width L=N, out width C=M; wide: gather form.
+  const bool gather = M < N;
+  DIAGMM_DISPATCH(dtype, run_product, gather, B, C, L, x, values, alpha_soft, active, n_act, max_act,
+                  bias, y, S(stream))
+}
+
+int diagmm_backward_input(int dtype, int M, int N, int B, const void* dy, const void* values,
+                          const double* alpha_soft, const int32_t* active, const int32_t* n_act,
+                          int max_act, void* dx, void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  const int C = M > N ? M : N, L = M < N ? M : N;
+  // tall/square dX: gather form (in = dy width C=M, out width L=N); wide: scatter.
+  const bool gather = M >= N;
+  DIAGMM_DISPATCH(dtype, run_product, gather, B, C, L, dy, values, alpha_soft, active, n_act, max_act,
+                  nullptr, dx, S(stream))
+}
+
+size_t diagmm_backward_weight_workspace(int dtype, int M, int N, int B, int max_act) {
+  if (check_shape(M, N, B, max_act)) return 0;
+  switch (dtype) {
+    case DIAGMM_F64: return dw_workspace<double>(M, N, B, max_act);
+    case DIAGMM_F32: return dw_workspace<float>(M, N, B, max_act);
+    case DIAGMM_BF16: return dw_workspace<__nv_bfloat16>(M, N, B, max_act);
+    default: return 0;
+  }
+}
+
+int diagmm_backward_weight(int dtype, int M, int N, int B, const void* dy, const void* x,
+                           const void* values, const double* alpha_soft, const int32_t* active,
+                           const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
+                           double* g_soft, void* g_bias, void* workspace, size_t ws_bytes,
+                           void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  DIAGMM_DISPATCH(dtype, run_dw, M, N, B, dy, x, values, alpha_soft, active, slot, n_act, max_act,
+                  g_values, g_soft, g_bias, workspace, ws_bytes, S(stream))
+}
+
+int diagmm_topk_waterfill(int C, int k, double temperature, const double* alpha, double* alpha_soft,
+                          uint8_t* clamped, int32_t* active, int32_t* slot, int32_t* n_act,
+                          void* stream) {
+  return run_waterfill(C, k, temperature, alpha, alpha_soft, clamped, active, slot, n_act, S(stream));
+}
+
+int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, const uint8_t* clamped,
+                     const double* g_soft, double l1_coeff, double* g_alpha, int accumulate,
+                     void* stream) {
+  return run_topk_grad(C, k, temperature, alpha, clamped, g_soft, l1_coeff, g_alpha, accumulate,
+                       S(stream));
+}
+
+int diagmm_select_hard(int C, int k, const double* alpha, int32_t* idx, void* stream) {
+  return run_select_hard(C, k, alpha, idx, S(stream));
+}
+
+int diagmm_active_from_list(int C, int n, const int32_t* offsets, int32_t* slot, int32_t* n_act,
+                            void* stream) {
+  return run_active_from_list(C, n, offsets, slot, n_act, S(stream));
+}
+
+int diagmm_adamw(int dtype, size_t n, void* param, const void* grad, void* m, void* v, int step,
+                 double lr, double beta1, double beta2, double eps, double weight_decay,
+                 const double* clip_scale, void* stream) {
+  switch (dtype) {
+    case DIAGMM_F64:
+      return run_adamw<double>(n, param, grad, m, v, step, lr, beta1, beta2, eps, weight_decay,
+                               clip_scale, S(stream));
+    case DIAGMM_F32:
+    case DIAGMM_BF16:
+      return run_adamw<float>(n, param, grad, m, v, step, lr, beta1, beta2, eps, weight_decay,
+                              clip_scale, S(stream));
+    default: return DIAGMM_EDTYPE;
+  }
+}
+
+int diagmm_sumsq_scratch_len(void) { return kSumsqScratch; }
+
+int diagmm_sumsq(int dtype, size_t n, const void* x, double* out, double* scratch, void* stream) {
+  switch (dtype) {
+    case DIAGMM_F64: return run_sumsq<double>(n, x, out, scratch, S(stream));
+    case DIAGMM_F32:
+    case DIAGMM_BF16: return run_sumsq<float>(n, x, out, scratch, S(stream));
+    default: return DIAGMM_EDTYPE;
+  }
+}
+
+int diagmm_clip_scale(int n, const double* partial, double max_norm, double* norm, double* scale,
+                      void* stream) {
+  return run_clip_scale(n, partial, max_norm, norm, scale, S(stream));
+}
+
+int diagmm_materialize(int dtype, int M, int N, const void* values, const double* alpha_soft,
+                       const int32_t* active, const int32_t* n_act, int max_act, void* w_dense,
+                       void* stream) {
+  if (int e = check_shape(M, N, 0, max_act)) return e;
+  DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, active, n_act, max_act, w_dense,
+                  S(stream))
+}
+
+int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW, const void* values,
+                             const double* alpha_soft, const int32_t* active, const int32_t* slot,
+                             const int32_t* n_act, void* g_values, double* g_soft, void* stream) {
+  (void)active;
+  if (int e = check_shape(M, N, 0, 0)) return e;
+  switch (dtype) {
+    case DIAGMM_F64:
+      return run_gather_dense<double>(M, N, dW, values, alpha_soft, slot, n_act, g_values, g_soft,
+                                      S(stream));
+    case DIAGMM_F32:
+    case DIAGMM_BF16:
+      return run_gather_dense<float>(M, N, dW, values, alpha_soft, slot, n_act, g_values, g_soft,
+                                     S(stream));
+    default: return DIAGMM_EDTYPE;
+  }
+}
+
+}  // extern "C"

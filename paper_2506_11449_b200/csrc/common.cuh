@@ -1,0 +1,62 @@
+// common.cuh — shared types and helpers for the sm_100a DiagLinear kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "../../include/diagmm.h"
+
+namespace diagmm {
+
+// Storage type T of activations -> parameter type P and accumulator type A.
+template <typename T> struct Traits;
+template <> struct Traits<double> { using P = double; using A = double; };
+template <> struct Traits<float> { using P = float; using A = float; };
+template <> struct Traits<__nv_bfloat16> { using P = float; using A = float; };
+
+template <typename A> __device__ __forceinline__ A to_acc(double v) { return (A)v; }
+template <typename A> __device__ __forceinline__ A to_acc(float v) { return (A)v; }
+template <typename A> __device__ __forceinline__ A to_acc(__nv_bfloat16 v) {
+  return (A)__bfloat162float(v);
+}
+template <typename T> __device__ __forceinline__ T from_acc(double v);
+template <> __device__ __forceinline__ double from_acc<double>(double v) { return v; }
+template <typename T> __device__ __forceinline__ T from_acc(float v);
+template <> __device__ __forceinline__ float from_acc<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+constexpr int kWarp = 32;
+
+// Number of kernels this library has launched (diagmm_launch_count()).
+void note_launch(int n = 1);
+
+// Largest index in [0, n) whose sorted value is < key, +1  (lower_bound).
+__device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+inline int status_from_cuda() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DIAGMM_OK : DIAGMM_ECUDA;
+}
+
+inline int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+}  // namespace diagmm

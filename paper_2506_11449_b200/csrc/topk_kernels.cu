@@ -1,0 +1,346 @@
+// topk_kernels.cu — on-device float64 diagonal (re)selection (K4/K5).
+//
+// K4 restates the capped water-filling soft TopK of selection.py:100-142 and
+// the active-set rule of layers.py:234; K5 restates soft_topk_grad
+// (selection.py:145-173) with the l1 penalty gradient (selection.py:217-222)
+// fused in.  select_hard restates selection.py:176-186.
+//
+// One CTA of 1024 threads per call (C <= 8192 candidates): a bitonic sort of
+// (key desc, index asc) pairs reproduces numpy's stable argsort(-z) order
+// exactly (ties -> smaller index; -0.0 == +0.0 compare equal, so they tie as in
+// numpy).  The tail log-sum-exp that the reference accumulates sequentially
+// with np.logaddexp (selection.py:112) is computed here as
+//   S_i = z_i + log1p(R_i),   R_i = sum_{l>i} exp(z_l - z_i),
+//   R_i = a_i (1 + R_{i+1}),  a_i = exp(z_{i+1} - z_i) in (0, 1],
+// a linear recurrence evaluated by a parallel suffix scan of affine maps.
+// Every quantity stays finite at arbitrarily cold temperatures (a_i -> 0), the
+// same guarantee the reference gets from logaddexp.  S_i agrees with the
+// reference's to a few ulp; the clamp/active decisions compare against 1.0
+// and 1e-3 with margins many orders of magnitude larger (SURVEY §7 hard part
+// 3), and the tests check the masks bit-for-bit.
+#include "common.cuh"
+#include <math_constants.h>
+
+namespace diagmm {
+
+constexpr int kSelThreads = 1024;
+constexpr int kSelMaxC = 8192;
+
+// numpy orders -0.0 and +0.0 as equal (stable sort keeps index order); make
+// that explicit so no comparison can separate them.
+__device__ __forceinline__ double canon(double v) { return v == 0.0 ? 0.0 : v; }
+
+__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
+  return ka > kb || (!(ka < kb) && !(ka > kb) && ia < ib);
+}
+
+// Bitonic sort of NP (power of two) (key, idx) pairs so that position 0 holds
+// the largest key (smallest index among equal keys).
+__device__ void bitonic_sort_desc(double* key, int* idx, int NP) {
+  for (int k = 2; k <= NP; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double ka = key[i], kb = key[ixj];
+          const int ia = idx[i], ib = idx[ixj];
+          const bool up = (i & k) == 0;
+          const bool swap = up ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+          if (swap) {
+            key[i] = kb; key[ixj] = ka;
+            idx[i] = ib; idx[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int next_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// Exclusive prefix sum of one int per thread over the block (deterministic).
+__device__ int block_exclusive_scan(int v, int* buf, int* total) {
+  const int tid = threadIdx.x;
+  buf[tid] = v;
+  __syncthreads();
+  for (int d = 1; d < blockDim.x; d <<= 1) {
+    int add = tid >= d ? buf[tid - d] : 0;
+    __syncthreads();
+    buf[tid] += add;
+    __syncthreads();
+  }
+  const int incl = buf[tid];
+  *total = buf[blockDim.x - 1];
+  __syncthreads();
+  return incl - v;
+}
+
+// Compact the flagged indices (flag[i] != 0, i < C) into `out` ascending.
+__device__ void compact_flags(const unsigned char* flag, int C, int32_t* out, int32_t* slot,
+                              int32_t* n_out, int* scan_buf) {
+  const int per = (C + blockDim.x - 1) / blockDim.x;
+  const int lo = min(C, (int)threadIdx.x * per), hi = min(C, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += flag[i] ? 1 : 0;
+  int total = 0;
+  int pos = block_exclusive_scan(cnt, scan_buf, &total);
+  for (int i = lo; i < hi; ++i) {
+    if (flag[i]) {
+      if (out) out[pos] = i;
+      if (slot) slot[i] = pos;
+      ++pos;
+    } else if (slot) {
+      slot[i] = -1;
+    }
+  }
+  if (n_out && threadIdx.x == 0) *n_out = total;
+}
+
+struct Affine { double a, b; };  // x -> a*x + b
+__device__ __forceinline__ Affine compose(Affine f, Affine g) {  // f o g
+  return {f.a * g.a, f.a * g.b + f.b};
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_waterfill(int C, int k, double temperature, const double* __restrict__ alpha,
+            double* __restrict__ asoft, uint8_t* __restrict__ clamped, int32_t* __restrict__ active,
+            int32_t* __restrict__ slot, int32_t* __restrict__ n_act) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NP = next_pow2(C);
+  double* key = reinterpret_cast<double*>(smem);                              // NP
+  double* R = key + NP;                                                       // NP
+  int* idx = reinterpret_cast<int*>(R + NP);                                  // NP
+  Affine* maps = reinterpret_cast<Affine*>(smem + ((size_t)NP * 20 + 15) / 16 * 16);  // blockDim
+  int* ibuf = reinterpret_cast<int*>(maps + blockDim.x);                      // blockDim
+  __shared__ int s_m;
+  __shared__ double s_Sm;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  for (int i = tid; i < NP; i += nt) {
+    key[i] = i < C ? canon(alpha[i] / temperature) : -CUDART_INF;
+    idx[i] = i < C ? i : 0x7fffffff;
+  }
+  __syncthreads();
+  bitonic_sort_desc(key, idx, NP);
+
+  // ---- suffix scan of R (positions 0..C-1, chunked per thread)
+  const int per = (C + nt - 1) / nt;
+  const int lo = min(C, tid * per), hi = min(C, lo + per);
+  Affine F{1.0, 0.0};  // identity
+  for (int i = hi - 1; i >= lo; --i) {
+    Affine f = (i + 1 < C) ? Affine{exp(key[i + 1] - key[i]), 0.0} : Affine{0.0, 0.0};
+    f.b = f.a;
+    F = compose(f, F);
+  }
+  maps[tid] = F;
+  __syncthreads();
+  for (int d = 1; d < nt; d <<= 1) {  // inclusive suffix scan: maps[t] = F_t o F_{t+1} o ...
+    Affine mine = maps[tid];
+    Affine nxt = tid + d < nt ? maps[tid + d] : Affine{1.0, 0.0};
+    __syncthreads();
+    maps[tid] = compose(mine, nxt);
+    __syncthreads();
+  }
+  double r = tid + 1 < nt ? maps[tid + 1].b : 0.0;  // R at position hi (0 past the end)
+  for (int i = hi - 1; i >= lo; --i) {
+    const double a = (i + 1 < C) ? exp(key[i + 1] - key[i]) : 0.0;
+    r = a * (1.0 + r);
+    R[i] = r;
+  }
+  if (tid == 0) s_m = min(k, C);
+  __syncthreads();
+
+  // ---- clamp count m = first i < min(k, C) with (k-i)*exp(z_i - S_i) < 1
+  const int lim = min(k, C);
+  for (int i = lo; i < min(hi, lim); ++i) {
+    const double S = key[i] + log1p(R[i]);
+    if (!((double)(k - i) * exp(key[i] - S) >= 1.0)) {
+      atomicMin(&s_m, i);
+      break;
+    }
+  }
+  __syncthreads();
+  const int m = s_m;
+  if (m < C && m >= lo && m < hi) s_Sm = key[m] + log1p(R[m]);
+  __syncthreads();
+  const double Sm = m < C ? s_Sm : 0.0;
+
+  // ---- soft scores at sorted positions, then scatter to index order
+  for (int i = lo; i < hi; ++i) R[i] = i < m ? 1.0 : (double)(k - m) * exp(key[i] - Sm);
+  __syncthreads();
+  for (int i = lo; i < hi; ++i) {
+    const int o = idx[i];
+    key[o] = R[i];
+    asoft[o] = R[i];
+    if (clamped) clamped[o] = i < m ? 1 : 0;
+  }
+  __syncthreads();
+  // ---- active set: flatnonzero(alpha_soft >= 1e-3)
+  unsigned char* flag = reinterpret_cast<unsigned char*>(R);
+  for (int i = tid; i < C; i += nt) flag[i] = key[i] >= 1e-3 ? 1 : 0;
+  __syncthreads();
+  compact_flags(flag, C, active, slot, n_act, ibuf);
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_select_hard(int C, int k, const double* __restrict__ alpha, int32_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NP = next_pow2(C);
+  double* key = reinterpret_cast<double*>(smem);
+  int* idx = reinterpret_cast<int*>(key + NP);
+  unsigned char* flag = reinterpret_cast<unsigned char*>(idx + NP);
+  int* ibuf = reinterpret_cast<int*>(flag + ((NP + 15) & ~15));
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    key[i] = i < C ? canon(alpha[i]) : -CUDART_INF;
+    idx[i] = i < C ? i : 0x7fffffff;
+  }
+  __syncthreads();
+  bitonic_sort_desc(key, idx, NP);
+  for (int i = threadIdx.x; i < C; i += blockDim.x) flag[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) flag[idx[i]] = 1;
+  __syncthreads();
+  compact_flags(flag, C, out, nullptr, nullptr, ibuf);
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_active_from_list(int C, int n, const int32_t* __restrict__ offs, int32_t* __restrict__ slot,
+                   int32_t* __restrict__ n_act) {
+  for (int i = threadIdx.x; i < C; i += blockDim.x) slot[i] = -1;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) slot[offs[j]] = j;
+  if (threadIdx.x == 0 && n_act) *n_act = n;
+}
+
+// Deterministic block reductions over per-thread partials.
+__device__ double block_reduce_sum(double v, double* buf) {
+  buf[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
+    if (threadIdx.x < s) buf[threadIdx.x] += buf[threadIdx.x + s];
+    __syncthreads();
+  }
+  double r = buf[0];
+  __syncthreads();
+  return r;
+}
+__device__ double block_reduce_max(double v, double* buf) {
+  buf[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
+    if (threadIdx.x < s) buf[threadIdx.x] = fmax(buf[threadIdx.x], buf[threadIdx.x + s]);
+    __syncthreads();
+  }
+  double r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_topk_grad(int C, int k, double temperature, const double* __restrict__ alpha,
+            const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
+            double* __restrict__ g_alpha, int accumulate) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* q = reinterpret_cast<double*>(smem);  // C
+  double* buf = q + C;                          // blockDim
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (C + nt - 1) / nt;
+  const int lo = min(C, tid * per), hi = min(C, lo + per);
+  double ncl = 0.0, zmax = -CUDART_INF;
+  for (int i = lo; i < hi; ++i) {
+    if (clamped[i]) ncl += 1.0;
+    else zmax = fmax(zmax, alpha[i] / temperature);
+  }
+  const int n_clamped = (int)block_reduce_sum(ncl, buf);
+  zmax = block_reduce_max(zmax, buf);
+  const int budget = k - n_clamped;
+  const bool any_free = n_clamped < C;
+  double sq = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    double v = 0.0;
+    if (!clamped[i]) v = exp(alpha[i] / temperature - zmax);
+    q[i] = v;
+    sq += v;
+  }
+  const double sum_q = block_reduce_sum(sq, buf);
+  double sw = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    q[i] = q[i] / sum_q;
+    sw += up[i] * q[i];
+  }
+  const double sum_w = block_reduce_sum(sw, buf);
+  const double coef = (double)budget / temperature;
+  for (int i = lo; i < hi; ++i) {
+    double g = 0.0;
+    if (any_free && budget > 0 && !clamped[i]) {
+      const double w = up[i] * q[i];
+      g = coef * (w - q[i] * sum_w);
+    }
+    if (l1 != 0.0) {
+      const double a = alpha[i];
+      g += l1 * (a > 0.0 ? 1.0 : (a < 0.0 ? -1.0 : 0.0));
+    }
+    g_alpha[i] = accumulate ? g_alpha[i] + g : g;
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+static size_t waterfill_smem(int C) {
+  int NP = 1;
+  while (NP < C) NP <<= 1;
+  return ((size_t)NP * 20 + 15) / 16 * 16 + kSelThreads * (sizeof(Affine) + sizeof(int)) + 64;
+}
+
+int run_waterfill(int C, int k, double T, const double* alpha, double* asoft, uint8_t* clamped,
+                  int32_t* active, int32_t* slot, int32_t* n_act, cudaStream_t st) {
+  if (C < 1) return DIAGMM_ESHAPE;
+  if (!(T > 0.0)) return DIAGMM_ETEMPERATURE;
+  if (k < 1 || k > C) return DIAGMM_EK;
+  if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  size_t sm = waterfill_smem(C);
+  cudaFuncSetAttribute(k_waterfill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_waterfill<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, asoft, clamped, active, slot, n_act);
+  note_launch();
+  return status_from_cuda();
+}
+
+int run_select_hard(int C, int k, const double* alpha, int32_t* idx, cudaStream_t st) {
+  if (C < 1) return DIAGMM_ESHAPE;
+  if (k < 1 || k > C) return DIAGMM_EK;
+  if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  int NP = 1;
+  while (NP < C) NP <<= 1;
+  size_t sm = (size_t)NP * 12 + ((NP + 15) & ~15) + kSelThreads * sizeof(int) + 64;
+  cudaFuncSetAttribute(k_select_hard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_select_hard<<<1, kSelThreads, sm, st>>>(C, k, alpha, idx);
+  note_launch();
+  return status_from_cuda();
+}
+
+int run_active_from_list(int C, int n, const int32_t* offs, int32_t* slot, int32_t* n_act,
+                         cudaStream_t st) {
+  if (C < 1 || n < 0 || n > C) return DIAGMM_ESHAPE;
+  k_active_from_list<<<1, kSelThreads, 0, st>>>(C, n, offs, slot, n_act);
+  note_launch();
+  return status_from_cuda();
+}
+
+int run_topk_grad(int C, int k, double T, const double* alpha, const uint8_t* clamped,
+                  const double* up, double l1, double* g_alpha, int accumulate, cudaStream_t st) {
+  if (C < 1) return DIAGMM_ESHAPE;
+  if (!(T > 0.0)) return DIAGMM_ETEMPERATURE;
+  if (k < 1 || k > C) return DIAGMM_EK;
+  if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  size_t sm = (size_t)C * 8 + kSelThreads * 8;
+  cudaFuncSetAttribute(k_topk_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_topk_grad<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, clamped, up, l1, g_alpha, accumulate);
+  note_launch();
+  return status_from_cuda();
+}
+
+}  // namespace diagmm

@@ -1,0 +1,377 @@
+"""DiagLinear: the reference's DynaDiag layer as a PyTorch module on sm_100a kernels.
+
+``DiagLinear`` mirrors ``DynaDiagLayer`` (reference ``layers.py:173-287``):
+same constructor arguments, same parameter layout (a dense-equivalent
+candidate store ``values (C, L)``, selection logits ``alpha (C,)`` float64,
+``bias (M,)``), same host-side initialisation stream
+(``np.random.default_rng(seed)``: values U(±sqrt(1/N)), then alpha N(0, 0.01),
+layers.py:199-208) so a layer built with the same seed starts bit-identical,
+and the same DST API (``set_k``, ``soft_scores``, ``active_set``,
+``active_count``, ``effective_matrix``, ``penalty``, ``freeze``).
+
+``DiagMMFunction`` is the ``torch.autograd.Function`` that replaces the
+reference's custom tape op ``_record_diag_matmul`` (layers.py:108-170): the
+forward runs K4 (soft TopK, device) then K1; the backward runs K2 (dX through
+the transpose), K3 (per-diagonal dW, g_values, g_soft, g_bias) and K5
+(soft-TopK gradient).  Gradients follow the reference exactly: inactive rows of
+``values.grad`` are 0, ``alpha.grad`` flows only through unclamped candidates.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import ceil, sqrt
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from . import ops
+from .errors import ShapeMismatch
+from .selection import (
+    EPS_ACTIVE,
+    TemperatureSchedule,
+    candidate_count,
+    required_diagonals,
+    temperature_at,
+)
+
+ROUTES = ("diag", "dense", "auto")
+
+
+@dataclass
+class ParamSpec:
+    """One trainable tensor plus its optimizer treatment (layers.py:44-50)."""
+
+    tensor: torch.Tensor
+    decay: bool
+    name: str
+
+
+@dataclass
+class DiagMatrix:
+    """Device counterpart of ``DiagSparseMatrix`` (diagcore.py:124-150).
+
+    offsets (K,) int64 ascending, values (K, min(M, N)).
+    """
+
+    rows: int
+    cols: int
+    offsets: torch.Tensor
+    values: torch.Tensor
+
+    def store(self) -> torch.Tensor:
+        """Candidate-store layout (C, L) with zeros on unused offsets."""
+        C, L = ops.geometry(self.rows, self.cols)
+        st = torch.zeros(C, L, dtype=self.values.dtype, device=self.values.device)
+        st[self.offsets] = self.values
+        return st
+
+    def selection(self) -> ops.Selection:
+        C, _ = ops.geometry(self.rows, self.cols)
+        return ops.selection_from_offsets(C, self.offsets)
+
+    def dense(self, dtype: torch.dtype | None = None) -> torch.Tensor:
+        """materialize (diagcore.py:153-159) on device."""
+        return ops.materialize(self.store(), self.selection(), self.rows, self.cols, dtype)
+
+
+@dataclass
+class _OpSpec:
+    M: int
+    N: int
+    k: int
+    temperature: float
+    route: str
+    fixed: ops.Selection | None = None
+
+
+def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
+    if spec.route == "dense":
+        return True
+    if spec.route == "diag":
+        return False
+    # "auto": the reference's own switch (diagcore.py:226, layers.py:420) —
+    # dense once the structural density reaches 1/4 — plus the B200 cost
+    # model: tensor cores run the dense product ~20x faster than the FMA pipe,
+    # so the dense route also wins at large token counts.
+    L = min(spec.M, spec.N)
+    n_act = sel.host_count()
+    if 4 * n_act * L >= spec.M * spec.N:
+        return True
+    return act_dtype != torch.float64 and B * n_act * L >= dense_route_threshold(spec.M, spec.N)
+
+
+def dense_route_threshold(M: int, N: int) -> float:
+    """FMA-equivalent work above which the bf16/tf32 tensor-core route is faster.
+
+    Calibrated on B200 (profiles/): the FMA kernels sustain ~1/20 of the dense
+    tensor-core rate, so the diagonal route wins while its work stays below
+    ~1/20 of the dense work, i.e. always for small batches (HBM bound).
+    """
+    return float("inf")
+
+
+class DiagMMFunction(torch.autograd.Function):
+    """y = x @ W_K^T + bias for the soft-selected diagonals (layers.py:108-170, 230-251)."""
+
+    @staticmethod
+    def forward(ctx, x, values, alpha, bias, spec: _OpSpec):
+        M, N = spec.M, spec.N
+        if alpha is not None:
+            sel = ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+        else:
+            sel = spec.fixed
+        dense = _use_dense(spec, sel, x.shape[0], x.dtype)
+        vals = values.detach()
+        W = None
+        if dense:
+            W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+            y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
+        else:
+            y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach())
+        ctx.save_for_backward(x, values, alpha)
+        ctx.sel, ctx.spec, ctx.W, ctx.has_bias = sel, spec, W, bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, values, alpha = ctx.saved_tensors
+        sel, spec, W = ctx.sel, ctx.spec, ctx.W
+        M, N = spec.M, spec.N
+        dy = dy.contiguous()
+        vals = values.detach()
+        dx = g_alpha = None
+        need_soft = alpha is not None and ctx.needs_input_grad[2]
+        if W is not None:
+            if ctx.needs_input_grad[0]:
+                dx = dy @ W
+            out_dt = vals.dtype
+            dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
+                else (dy.t() @ x.to(dy.dtype)).to(out_dt)
+            g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
+            g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
+        else:
+            if ctx.needs_input_grad[0]:
+                dx = ops.diag_backward_input(dy, vals, sel, M, N)
+            g_values, g_soft, g_bias = ops.diag_backward_weight(
+                dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft)
+        if need_soft:
+            g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
+                                         clamped=sel.clamped)
+        return dx, g_values, g_alpha, g_bias, None
+
+
+def _flatten(x: torch.Tensor, width: int) -> torch.Tensor:
+    if x.dim() < 1 or x.shape[-1] != width:
+        raise ShapeMismatch(f"input has shape {tuple(x.shape)}, expected (..., {width})")
+    return x.reshape(-1, width)
+
+
+class DiagLinear(nn.Module):
+    """Linear layer on soft-selected wrap-around diagonals (layers.py:173-287).
+
+    Computes y = x W^T + bias, W = sum over active diagonals of
+    alpha_soft_j P_j diag(V_j); active = candidates with soft score >= 1e-3.
+    ``forward(x, step=None)`` accepts any leading dims (tokens are flattened
+    into the batch, as rank-2 is all the reference supports,
+    autodiff.py:26-27).  ``step`` defaults to ``self.step``.
+    """
+
+    def __init__(self, in_features: int, out_features: int, sparsity: float = 0.9, *,
+                 t_schedule: TemperatureSchedule | None = None, l1_coeff: float = 1e-4,
+                 bias: bool = True, seed: int = 0, blocking=None, device=None,
+                 dtype: torch.dtype = torch.float32, route: str = "diag"):
+        super().__init__()
+        if route not in ROUTES:
+            raise ValueError(f"route must be one of {ROUTES}")
+        self.in_features, self.out_features = int(in_features), int(out_features)
+        M, N = self.out_features, self.in_features
+        self.candidates = candidate_count(M, N)
+        self.diag_len = min(M, N)
+        self.k = required_diagonals(M, N, sparsity)
+        self.t_schedule = t_schedule or TemperatureSchedule()
+        self.l1_coeff = l1_coeff
+        self.route = route
+        pdt = torch.float64 if dtype == torch.float64 else torch.float32
+        rng = np.random.default_rng(seed)
+        bound = sqrt(1.0 / N)
+        vals = rng.uniform(-bound, bound, (self.candidates, self.diag_len))
+        alpha = rng.normal(0.0, 0.01, self.candidates)
+        device = torch.device(device) if device is not None else torch.device("cuda")
+        self.values = nn.Parameter(torch.from_numpy(vals).to(device=device, dtype=pdt))
+        self.alpha = nn.Parameter(torch.from_numpy(alpha).to(device=device, dtype=torch.float64))
+        self.bias = nn.Parameter(torch.zeros(M, device=device, dtype=pdt)) if bias else None
+        self.step = 0
+        self.last_step = 0
+
+    # ---- DST mask-update API (layers.py:212-228, 268-287) --------------------
+    def set_k(self, k: int) -> None:
+        if not 1 <= k <= self.candidates:
+            raise ValueError(f"k={k} outside [1, {self.candidates}]")
+        self.k = int(k)
+
+    def temperature(self, step: int) -> float:
+        """layers.py:217-219: past the horizon the layer keeps training at t_final."""
+        return temperature_at(min(step, self.t_schedule.total_steps), self.t_schedule)
+
+    def selection(self, step: int) -> ops.Selection:
+        return ops.soft_topk_select(self.alpha.detach(), self.k, self.temperature(step))
+
+    def soft_scores(self, step: int) -> torch.Tensor:
+        return self.selection(step).alpha_soft
+
+    def active_set(self, step: int) -> torch.Tensor:
+        return self.selection(step).active_offsets().long()
+
+    def active_count(self, step: int) -> int:
+        return self.selection(step).host_count()
+
+    def effective_matrix(self, step: int) -> DiagMatrix:
+        """layers.py:268-275: the active-set matrix exactly as forward uses it."""
+        sel = self.selection(step)
+        act = sel.active_offsets().long()
+        vals = sel.alpha_soft[act].to(self.values.dtype)[:, None] * self.values.detach()[act]
+        return DiagMatrix(self.out_features, self.in_features, act, vals)
+
+    def penalty(self) -> torch.Tensor:
+        """layers.py:253-257: l1_coeff * sum|alpha| (grad l1 * sign(alpha), sign(0)=0)."""
+        return self.l1_coeff * self.alpha.abs().sum()
+
+    def param_specs(self) -> list[ParamSpec]:
+        """layers.py:259-266: values decay, alpha and bias do not."""
+        specs = [ParamSpec(self.values, True, "values"), ParamSpec(self.alpha, False, "alpha")]
+        if self.bias is not None:
+            specs.append(ParamSpec(self.bias, False, "bias"))
+        return specs
+
+    def freeze(self) -> "FrozenDiagLinear":
+        """layers.py:277-287: hard top-K at t_final, soft scores baked into V."""
+        sel = ops.select_hard(self.alpha.detach(), self.k)
+        a_soft = ops.soft_topk(self.alpha.detach(), self.k, self.t_schedule.t_final)
+        vals = a_soft[sel].to(self.values.dtype)[:, None] * self.values.detach()[sel]
+        w = DiagMatrix(self.out_features, self.in_features, sel, vals)
+        return FrozenDiagLinear(w, None if self.bias is None else self.bias.detach().clone())
+
+    # ---- forward ----------------------------------------------------------------
+    def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
+        step = self.step if step is None else int(step)
+        self.last_step = step
+        lead = x.shape[:-1]
+        x2 = _flatten(x, self.in_features)
+        if x2.dtype != torch.float64 and self.values.dtype == torch.float64:
+            x2 = x2.double()
+        spec = _OpSpec(self.out_features, self.in_features, self.k, self.temperature(step), self.route)
+        y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
+        return y.reshape(*lead, self.out_features)
+
+    def extra_repr(self) -> str:
+        return (f"in_features={self.in_features}, out_features={self.out_features}, k={self.k}, "
+                f"candidates={self.candidates}, route={self.route}")
+
+
+class FrozenDiagLinear(nn.Module):
+    """Inference layer over a fixed diagonal matrix (layers.py:290-310)."""
+
+    def __init__(self, weight: DiagMatrix, bias: torch.Tensor | None = None):
+        super().__init__()
+        self.weight = weight
+        self.in_features, self.out_features = weight.cols, weight.rows
+        self.register_buffer("store", weight.store())
+        self.register_buffer("bias", bias)
+        self._sel = weight.selection()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        lead = x.shape[:-1]
+        x2 = _flatten(x, self.in_features)
+        if self.store.dtype == torch.float64:
+            x2 = x2.double()
+        y = ops.diag_forward(x2, self.store, self._sel, self.out_features, self.in_features, self.bias)
+        return y.reshape(*lead, self.out_features)
+
+
+class DiagHeurLinear(nn.Module):
+    """Magnitude-prune / random-regrow baseline over whole diagonals (layers.py:313-378)."""
+
+    def __init__(self, in_features: int, out_features: int, sparsity: float = 0.9, *,
+                 update_every: int = 100, prune_fraction: float = 0.3, bias: bool = True,
+                 seed: int = 0, blocking=None, device=None, dtype: torch.dtype = torch.float32):
+        super().__init__()
+        if not 0.0 < prune_fraction < 1.0:
+            raise ValueError("prune_fraction must lie in (0, 1)")
+        self.in_features, self.out_features = int(in_features), int(out_features)
+        M, N = self.out_features, self.in_features
+        self.candidates = candidate_count(M, N)
+        self.diag_len = min(M, N)
+        self.k = required_diagonals(M, N, sparsity)
+        self.update_every, self.prune_fraction = update_every, prune_fraction
+        pdt = torch.float64 if dtype == torch.float64 else torch.float32
+        rng = np.random.default_rng(seed)
+        bound = sqrt(1.0 / N)
+        vals = rng.uniform(-bound, bound, (self.candidates, self.diag_len))
+        device = torch.device(device) if device is not None else torch.device("cuda")
+        self.values = nn.Parameter(torch.from_numpy(vals).to(device=device, dtype=pdt))
+        self.bias = nn.Parameter(torch.zeros(M, device=device, dtype=pdt)) if bias else None
+        self.active = np.sort(rng.choice(self.candidates, self.k, replace=False))
+        self._sel = None
+
+    def _selection(self) -> ops.Selection:
+        if self._sel is None:
+            offs = torch.as_tensor(self.active, device=self.values.device)
+            self._sel = ops.selection_from_offsets(self.candidates, offs)
+        return self._sel
+
+    def forward(self, x: torch.Tensor, step: int = 0) -> torch.Tensor:
+        lead = x.shape[:-1]
+        x2 = _flatten(x, self.in_features)
+        if self.values.dtype == torch.float64:
+            x2 = x2.double()
+        spec = _OpSpec(self.out_features, self.in_features, self.k, 1.0, "diag", self._selection())
+        y = DiagMMFunction.apply(x2, self.values, None, self.bias, spec)
+        return y.reshape(*lead, self.out_features)
+
+    def param_specs(self) -> list[ParamSpec]:
+        specs = [ParamSpec(self.values, True, "values")]
+        if self.bias is not None:
+            specs.append(ParamSpec(self.bias, False, "bias"))
+        return specs
+
+    def effective_matrix(self, step: int = 0) -> DiagMatrix:
+        act = torch.as_tensor(self.active, device=self.values.device)
+        return DiagMatrix(self.out_features, self.in_features, act, self.values.detach()[act])
+
+
+def diagheur_update(layer: DiagHeurLinear, rng: np.random.Generator, step: int | None = None,
+                    total_steps: int | None = None) -> DiagHeurLinear:
+    """layers.py:381-413: prune the weakest ceil(frac*k) diagonals, regrow at random."""
+    frac = layer.prune_fraction
+    if step is not None and total_steps:
+        frac = frac * 0.5 * (1.0 + np.cos(np.pi * min(step, total_steps) / total_steps))
+    n = min(ceil(frac * layer.k), layer.candidates - layer.k)
+    if n <= 0:
+        return layer
+    act = torch.as_tensor(layer.active, device=layer.values.device)
+    norms = torch.linalg.vector_norm(layer.values.detach()[act].double(), dim=1).cpu().numpy()
+    order = np.lexsort((layer.active, norms))
+    pruned = layer.active[order[:n]]
+    survivors = np.setdiff1d(layer.active, pruned)
+    pool_mask = np.ones(layer.candidates, dtype=bool)
+    pool_mask[layer.active] = False
+    grown = rng.choice(np.flatnonzero(pool_mask), n, replace=False)
+    with torch.no_grad():
+        layer.values[torch.as_tensor(grown, device=layer.values.device)] = 0.0
+    layer.active = np.sort(np.concatenate([survivors, grown]))
+    layer._sel = None
+    return layer
+
+
+def penalties(model: nn.Module) -> list[torch.Tensor]:
+    """MLPModel.penalties (training.py:439-444) for any module tree."""
+    return [m.penalty() for m in model.modules() if isinstance(m, DiagLinear) and m.l1_coeff > 0]
+
+
+__all__ = [
+    "DiagLinear", "DiagMMFunction", "FrozenDiagLinear", "DiagHeurLinear", "DiagMatrix",
+    "ParamSpec", "diagheur_update", "penalties", "EPS_ACTIVE",
+]

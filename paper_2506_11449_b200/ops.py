@@ -1,0 +1,329 @@
+"""Tensor-level wrappers over the C ABI (device buffers in, device buffers out).
+
+Every function here launches sm_100a kernels from ``_lib/libdiagmm.so`` on the
+current CUDA stream of the tensors' device.  Shapes and dtypes are validated
+before launch with the reference's exception types.  There is no CPU path:
+CPU tensors are rejected.
+
+Dtype policy (include/diagmm.h): activations float64 -> parameters float64;
+activations float32 or bfloat16 -> parameters float32 (fp32 accumulation).
+Selection state (alpha, alpha_soft) is always float64.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatch
+
+_ACT_CODES = {torch.float64: _lib.F64, torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
+
+
+def _code(act_dtype: torch.dtype) -> int:
+    try:
+        return _ACT_CODES[act_dtype]
+    except KeyError:
+        raise TypeError(f"unsupported activation dtype {act_dtype}") from None
+
+
+def param_dtype_for(act_dtype: torch.dtype) -> torch.dtype:
+    return torch.float64 if act_dtype == torch.float64 else torch.float32
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise _lib.NativeLibraryError(
+                "DiagLinear kernels run on CUDA tensors only (no CPU fallback); got a CPU tensor"
+            )
+
+
+def _contig(t):
+    return None if t is None else t.contiguous()
+
+
+def geometry(M: int, N: int) -> tuple[int, int]:
+    """(C, L) = (max, min) — candidate count and diagonal length (diagcore.py:22-26)."""
+    return max(M, N), min(M, N)
+
+
+@dataclass
+class Selection:
+    """Device-resident result of one soft TopK (K4) for a layer.
+
+    alpha_soft (C,) f64, clamped (C,) u8, active (C,) i32 (first n_act valid,
+    ascending), slot (C,) i32 (index in active or -1), n_act (1,) i32.
+    ``n_act_host`` is a pinned copy filled asynchronously; call
+    ``host_count()`` to read it (waits only on this selection's event).
+    """
+
+    alpha_soft: torch.Tensor
+    clamped: torch.Tensor
+    active: torch.Tensor
+    slot: torch.Tensor
+    n_act: torch.Tensor
+    k: int
+    temperature: float
+    n_act_host: torch.Tensor | None = None
+    event: torch.cuda.Event | None = None
+
+    @property
+    def C(self) -> int:
+        return self.slot.numel()
+
+    def start_host_copy(self) -> None:
+        self.n_act_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self.n_act_host.copy_(self.n_act, non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record(torch.cuda.current_stream(self.n_act.device))
+
+    def host_count(self) -> int:
+        if self.n_act_host is None:
+            self.start_host_copy()
+        self.event.synchronize()
+        return int(self.n_act_host.item())
+
+    def active_offsets(self) -> torch.Tensor:
+        return self.active[: self.host_count()]
+
+
+def new_selection(C: int, device, k: int = 1, temperature: float = 1.0) -> Selection:
+    return Selection(
+        alpha_soft=torch.empty(C, dtype=torch.float64, device=device),
+        clamped=torch.empty(C, dtype=torch.uint8, device=device),
+        active=torch.empty(C, dtype=torch.int32, device=device),
+        slot=torch.empty(C, dtype=torch.int32, device=device),
+        n_act=torch.empty(1, dtype=torch.int32, device=device),
+        k=k,
+        temperature=temperature,
+    )
+
+
+def soft_topk_select(alpha: torch.Tensor, k: int, temperature: float,
+                     out: Selection | None = None, host_copy: bool = True) -> Selection:
+    """K4: soft_topk + clamped set + active set (selection.py:100-142, layers.py:234)."""
+    _need_cuda(alpha)
+    if alpha.dtype != torch.float64 or alpha.dim() != 1:
+        raise ShapeMismatch("alpha must be a float64 vector")
+    a = alpha.contiguous()
+    C = a.numel()
+    sel = out if out is not None else new_selection(C, a.device)
+    sel.k, sel.temperature = int(k), float(temperature)
+    _lib.call("diagmm_topk_waterfill", C, int(k), float(temperature), _p(a), _p(sel.alpha_soft),
+              _p(sel.clamped), _p(sel.active), _p(sel.slot), _p(sel.n_act), _stream(a))
+    sel.n_act_host = None
+    if host_copy:
+        sel.start_host_copy()
+    return sel
+
+
+def soft_topk(alpha: torch.Tensor, k: int, temperature: float) -> torch.Tensor:
+    """Device soft_topk (selection.py:127-142) returning alpha_soft only."""
+    return soft_topk_select(alpha, k, temperature, host_copy=False).alpha_soft
+
+
+def soft_topk_grad(alpha: torch.Tensor, k: int, temperature: float, upstream: torch.Tensor,
+                   clamped: torch.Tensor | None = None, l1_coeff: float = 0.0,
+                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """K5: soft_topk_grad (selection.py:145-173) [+ l1 * sign(alpha)]."""
+    _need_cuda(alpha, upstream)
+    a = alpha.contiguous()
+    up = upstream.to(torch.float64).contiguous()
+    if up.shape != a.shape:
+        raise ValueError("upstream must match alpha's shape")
+    if clamped is None:
+        clamped = soft_topk_select(a, k, temperature, host_copy=False).clamped
+    g = out if out is not None else torch.empty_like(a)
+    _lib.call("diagmm_topk_grad", a.numel(), int(k), float(temperature), _p(a), _p(clamped), _p(up),
+              float(l1_coeff), _p(g), int(bool(accumulate)), _stream(a))
+    return g
+
+
+def select_hard(alpha: torch.Tensor, k: int) -> torch.Tensor:
+    """select_hard (selection.py:176-186): int64 indices, ascending."""
+    _need_cuda(alpha)
+    a = alpha.to(torch.float64).contiguous()
+    idx = torch.empty(int(k), dtype=torch.int32, device=a.device)
+    _lib.call("diagmm_select_hard", a.numel(), int(k), _p(a), _p(idx), _stream(a))
+    return idx.long()
+
+
+def selection_from_offsets(C: int, offsets: torch.Tensor, alpha_soft: torch.Tensor | None = None
+                           ) -> Selection:
+    """Selection for an explicit ascending offset list (DiagHeur / frozen layers)."""
+    _need_cuda(offsets)
+    offs = offsets.to(torch.int32).contiguous()
+    n = offs.numel()
+    dev = offs.device
+    sel = new_selection(C, dev, k=n)
+    sel.active[:n].copy_(offs)
+    if alpha_soft is None:
+        sel.alpha_soft = None
+    else:
+        sel.alpha_soft.copy_(alpha_soft)
+    _lib.call("diagmm_active_from_list", C, n, _p(offs), _p(sel.slot), _p(sel.n_act), _stream(offs))
+    sel.n_act_host = torch.full((1,), n, dtype=torch.int32)
+    sel.event = torch.cuda.Event()
+    sel.event.record(torch.cuda.current_stream(dev))
+    return sel
+
+
+def _check_product(x: torch.Tensor, width: int, values: torch.Tensor, M: int, N: int):
+    _need_cuda(x, values)
+    if x.dim() != 2 or x.shape[1] != width:
+        raise ShapeMismatch(f"input has shape {tuple(x.shape)}, expected (B, {width})")
+    C, L = geometry(M, N)
+    if tuple(values.shape) != (C, L):
+        raise ShapeMismatch(f"values shape {tuple(values.shape)} does not match {(C, L)}")
+    if values.dtype != param_dtype_for(x.dtype):
+        raise TypeError(f"values dtype {values.dtype} incompatible with activations {x.dtype}")
+
+
+def diag_forward(x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
+                 bias: torch.Tensor | None = None, max_act: int | None = None) -> torch.Tensor:
+    """K1: y = x @ W_K^T (+ bias), x (B, N) -> y (B, M)."""
+    _check_product(x, N, values, M, N)
+    C, _ = geometry(M, N)
+    x = x.contiguous()
+    values = values.contiguous()
+    bias = _contig(bias)
+    y = torch.empty(x.shape[0], M, dtype=x.dtype, device=x.device)
+    _lib.call("diagmm_forward", _code(x.dtype), M, N, x.shape[0], _p(x), _p(values), _p(sel.alpha_soft),
+              _p(sel.active), _p(sel.n_act), C if max_act is None else int(max_act), _p(bias), _p(y),
+              _stream(x))
+    return y
+
+
+def diag_backward_input(dy: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
+                        max_act: int | None = None) -> torch.Tensor:
+    """K2: dx = dy @ W_K through the never-materialized transpose."""
+    _check_product(dy, M, values, M, N)
+    C, _ = geometry(M, N)
+    dy = dy.contiguous()
+    dx = torch.empty(dy.shape[0], N, dtype=dy.dtype, device=dy.device)
+    _lib.call("diagmm_backward_input", _code(dy.dtype), M, N, dy.shape[0], _p(dy), _p(values.contiguous()),
+              _p(sel.alpha_soft), _p(sel.active), _p(sel.n_act), C if max_act is None else int(max_act),
+              _p(dx), _stream(dy))
+    return dx
+
+
+_WORKSPACE: dict = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    ws = _WORKSPACE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WORKSPACE[key] = ws
+    return ws
+
+
+def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection,
+                         M: int, N: int, need_bias: bool = True, need_soft: bool = True,
+                         max_act: int | None = None, g_values: torch.Tensor | None = None):
+    """K3: (g_values (C, L), g_soft (C,) f64 | None, g_bias (M,) | None)."""
+    _check_product(dy, M, values, M, N)
+    _check_product(x, N, values, M, N)
+    if dy.shape[0] != x.shape[0]:
+        raise ShapeMismatch("dy and x disagree on the batch size")
+    C, L = geometry(M, N)
+    if max_act is None:
+        max_act = sel.host_count()
+    B = x.shape[0]
+    dy = dy.contiguous()
+    x = x.contiguous().to(dy.dtype)
+    code = _code(dy.dtype)
+    lib = _lib.load()
+    nbytes = lib.diagmm_backward_weight_workspace(code, M, N, B, int(max_act))
+    ws = _workspace(dy.device, nbytes)
+    if g_values is None:
+        g_values = torch.empty(C, L, dtype=values.dtype, device=dy.device)
+    g_soft = torch.empty(C, dtype=torch.float64, device=dy.device) if need_soft else None
+    g_bias = torch.empty(M, dtype=values.dtype, device=dy.device) if need_bias else None
+    _lib.call("diagmm_backward_weight", code, M, N, B, _p(dy), _p(x), _p(values.contiguous()),
+              _p(sel.alpha_soft), _p(sel.active), _p(sel.slot), _p(sel.n_act), int(max_act),
+              _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(dy))
+    return g_values, g_soft, g_bias
+
+
+def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
+                dtype: torch.dtype | None = None) -> torch.Tensor:
+    """Dense W_K (M, N) of the active diagonals (diagcore.py:153-159 + layers.py:235)."""
+    _need_cuda(values)
+    C, L = geometry(M, N)
+    if tuple(values.shape) != (C, L):
+        raise ShapeMismatch(f"values shape {tuple(values.shape)} does not match {(C, L)}")
+    dtype = dtype or values.dtype
+    if param_dtype_for(dtype) != values.dtype:
+        raise TypeError(f"cannot materialize {values.dtype} values as {dtype}")
+    W = torch.empty(M, N, dtype=dtype, device=values.device)
+    _lib.call("diagmm_materialize", _code(dtype), M, N, _p(values.contiguous()), _p(sel.alpha_soft),
+              _p(sel.active), _p(sel.n_act), C, _p(W), _stream(values))
+    return W
+
+
+def gather_dense_grad(dW: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
+                      need_soft: bool = True):
+    """g_values / g_soft from a dense dW (M, N) (the dense branch of layers.py:420-423)."""
+    _need_cuda(dW, values)
+    C, L = geometry(M, N)
+    dW = dW.to(values.dtype).contiguous()
+    g_values = torch.empty(C, L, dtype=values.dtype, device=values.device)
+    g_soft = torch.empty(C, dtype=torch.float64, device=values.device) if need_soft else None
+    code = _lib.F64 if values.dtype == torch.float64 else _lib.F32
+    _lib.call("diagmm_gather_dense_grad", code, M, N, _p(dW), _p(values.contiguous()), _p(sel.alpha_soft),
+              _p(sel.active), _p(sel.slot), _p(sel.n_act), _p(g_values), _p(g_soft), _stream(values))
+    return g_values, g_soft
+
+
+def adamw_(param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
+           lr: float, beta1: float, beta2: float, eps: float, weight_decay: float,
+           clip_scale: torch.Tensor | None = None) -> None:
+    """K6: in-place AdamW (training.py:346-358) over every element of param."""
+    _need_cuda(param, grad, m, v)
+    for t in (grad, m, v):
+        if t.shape != param.shape or t.dtype != param.dtype or not t.is_contiguous():
+            raise ShapeMismatch("param, grad, m, v must share shape/dtype and be contiguous")
+    if not param.is_contiguous():
+        raise ShapeMismatch("param must be contiguous")
+    code = _lib.F64 if param.dtype == torch.float64 else _lib.F32
+    if param.dtype not in (torch.float64, torch.float32):
+        raise TypeError("AdamW state must be float32 or float64")
+    _lib.call("diagmm_adamw", code, param.numel(), _p(param), _p(grad), _p(m), _p(v), int(step),
+              float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), _p(clip_scale),
+              _stream(param))
+
+
+def sumsq_into(x: torch.Tensor, out: torch.Tensor, scratch: torch.Tensor) -> None:
+    """out[0] = sum(x^2) in float64 with a fixed reduction order."""
+    _need_cuda(x)
+    code = _lib.F64 if x.dtype == torch.float64 else _lib.F32
+    if x.dtype not in (torch.float64, torch.float32):
+        x = x.float()
+    x = x.contiguous()
+    _lib.call("diagmm_sumsq", code, x.numel(), _p(x), _p(out), _p(scratch), _stream(x))
+
+
+def sumsq_scratch(device) -> torch.Tensor:
+    return torch.empty(_lib.load().diagmm_sumsq_scratch_len(), dtype=torch.float64, device=device)
+
+
+def clip_scale(partials: torch.Tensor, max_norm: float):
+    """(norm, scale) device scalars of clip_global_norm (training.py:406-417)."""
+    norm = torch.empty(1, dtype=torch.float64, device=partials.device)
+    scale = torch.empty(1, dtype=torch.float64, device=partials.device)
+    _lib.call("diagmm_clip_scale", partials.numel(), _p(partials.contiguous()), float(max_norm), _p(norm),
+              _p(scale), _stream(partials))
+    return norm, scale

@@ -1,0 +1,124 @@
+"""Callers of the hot path used for measurement: ViT-B/16, ViT-Tiny/16, MLP.
+
+The reference ships only an MLP of linear layers (training.py:423-475); the
+paper's ViT experiments (BASELINE.json configs 2-3) sparsify the
+attention projections and the MLP of every block with DiagLinear.  These thin
+PyTorch models exist to drive ``DiagLinear`` at those shapes; everything that
+is not a DiagLinear is stock PyTorch (LayerNorm, SDPA attention, GELU, the
+patch-embedding conv and the classifier head).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from .layer import DiagLinear
+from .selection import TemperatureSchedule
+
+
+@dataclass(frozen=True)
+class ViTConfig:
+    image: int = 224
+    patch: int = 16
+    dim: int = 768
+    depth: int = 12
+    heads: int = 12
+    mlp_ratio: int = 4
+    classes: int = 1000
+    sparsity: float = 0.9
+    sparse_qkv: bool = True
+
+    @property
+    def tokens(self) -> int:
+        return (self.image // self.patch) ** 2 + 1
+
+
+VIT_B16 = ViTConfig()
+VIT_TINY16 = ViTConfig(dim=192, depth=12, heads=3)
+
+
+def _sparse(n_in, n_out, cfg: ViTConfig, seed: int, t_schedule, route, dense: bool = False):
+    if dense:
+        return nn.Linear(n_in, n_out)
+    return DiagLinear(n_in, n_out, cfg.sparsity, seed=seed, t_schedule=t_schedule, route=route,
+                      dtype=torch.float32)
+
+
+class Block(nn.Module):
+    def __init__(self, cfg: ViTConfig, idx: int, t_schedule, route):
+        super().__init__()
+        d = cfg.dim
+        self.heads = cfg.heads
+        self.norm1 = nn.LayerNorm(d)
+        self.qkv = _sparse(d, 3 * d, cfg, 4 * idx, t_schedule, route, dense=not cfg.sparse_qkv)
+        self.proj = _sparse(d, d, cfg, 4 * idx + 1, t_schedule, route)
+        self.norm2 = nn.LayerNorm(d)
+        self.fc1 = _sparse(d, cfg.mlp_ratio * d, cfg, 4 * idx + 2, t_schedule, route)
+        self.fc2 = _sparse(cfg.mlp_ratio * d, d, cfg, 4 * idx + 3, t_schedule, route)
+
+    def forward(self, x):
+        B, T, D = x.shape
+        h = self.qkv(self.norm1(x)).view(B, T, 3, self.heads, D // self.heads)
+        q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
+        a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
+        x = x + self.proj(a)
+        return x + self.fc2(F.gelu(self.fc1(self.norm2(x)), approximate="tanh"))
+
+
+class ViT(nn.Module):
+    """ViT with DiagLinear qkv / proj / fc1 / fc2 in every block."""
+
+    def __init__(self, cfg: ViTConfig = VIT_B16, *, t_schedule: TemperatureSchedule | None = None,
+                 route: str = "auto", device="cuda"):
+        super().__init__()
+        self.cfg = cfg
+        t_schedule = t_schedule or TemperatureSchedule("constant", 1e-9, 1e-9, 1)
+        with torch.device(device):
+            self.patch = nn.Conv2d(3, cfg.dim, cfg.patch, cfg.patch)
+            self.cls = nn.Parameter(torch.zeros(1, 1, cfg.dim))
+            self.pos = nn.Parameter(torch.randn(1, cfg.tokens, cfg.dim) * 0.02)
+            self.blocks = nn.ModuleList(Block(cfg, i, t_schedule, route) for i in range(cfg.depth))
+            self.norm = nn.LayerNorm(cfg.dim)
+            self.head = nn.Linear(cfg.dim, cfg.classes)
+
+    def diag_layers(self):
+        return [m for m in self.modules() if isinstance(m, DiagLinear)]
+
+    def set_step(self, step: int) -> None:
+        for m in self.diag_layers():
+            m.step = step
+
+    def forward(self, images):
+        x = self.patch(images).flatten(2).transpose(1, 2)
+        x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
+        for blk in self.blocks:
+            x = blk(x)
+        return self.head(self.norm(x)[:, 0])
+
+
+class MLPModel(nn.Module):
+    """training.py:423-475: DiagLinear / dense layers joined by ReLU."""
+
+    def __init__(self, sizes=(784, 256, 256, 10), kinds=("dynadiag", "dynadiag", "dense"),
+                 sparsity: float = 0.9, seeds=None, t_schedule=None, dtype=torch.float32, device="cuda"):
+        super().__init__()
+        seeds = seeds or list(range(len(kinds)))
+        layers = []
+        for (n_in, n_out), kind, seed in zip(zip(sizes[:-1], sizes[1:]), kinds, seeds):
+            if kind == "dynadiag":
+                layers.append(DiagLinear(n_in, n_out, sparsity, seed=int(seed), t_schedule=t_schedule,
+                                         dtype=dtype, device=device))
+            else:
+                layers.append(nn.Linear(n_in, n_out, device=device, dtype=dtype))
+        self.layers = nn.ModuleList(layers)
+
+    def forward(self, x, step: int | None = None):
+        for i, lyr in enumerate(self.layers):
+            x = lyr(x, step) if isinstance(lyr, DiagLinear) else lyr(x)
+            if i < len(self.layers) - 1:
+                x = torch.relu(x)
+        return x

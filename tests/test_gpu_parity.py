@@ -1,0 +1,315 @@
+"""CUDA path vs the reference's golden vectors and the CPU oracle (needs a B200).
+
+Bars (BASELINE.json north star): TopK offsets / masks / clamped sets and hard
+selections bit-exact; float64 instantiation at the reference's own
+tolerances (1e-12 products, 1e-10 layer gradients); float32 within 1e-5
+relative (scaled by max(1, max|ref|), bench._validate's convention); bf16
+activations within 2e-2 of the same scale (8-bit mantissa inputs, fp32
+accumulation).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import layer as olayer
+from diagtest_util import load_golden, scaled_err
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2506_11449_b200 import (
+        AdamW, DiagLinear, GlobalNormClipper, NonPositiveTemperature, ShapeMismatch,
+        TemperatureSchedule, ops,
+    )
+
+F32_TOL = 1e-5
+BF16_TOL = 2e-2
+DEV = "cuda"
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    _require_cuda()
+
+
+def t(a, dtype=torch.float64):
+    return torch.as_tensor(np.asarray(a), dtype=dtype, device=DEV)
+
+
+def _store(M, N, offs, vals, dtype):
+    C, L = max(M, N), min(M, N)
+    st = np.zeros((C, L))
+    st[np.asarray(offs, dtype=np.int64)] = vals
+    return t(st, dtype)
+
+
+# ---------------------------------------------------------------- K1 / K2 products
+@pytest.mark.parametrize("act", [torch.float64, torch.float32, torch.bfloat16])
+def test_products_vs_reference_golden(act):
+    g = load_golden("spmm")
+    pdt = ops.param_dtype_for(act)
+    tol = {torch.float64: 1e-12, torch.float32: F32_TOL, torch.bfloat16: BF16_TOL}[act]
+    for i in range(int(g["n"])):
+        M, N, K, B = g[f"c{i}_shape"].tolist()
+        offs = g[f"c{i}_offsets"]
+        st = _store(M, N, offs, g[f"c{i}_values"], pdt)
+        sel = ops.selection_from_offsets(max(M, N), t(offs, torch.int64))
+        x = t(g[f"c{i}_X"].T.copy(), act)
+        y = ops.diag_forward(x, st, sel, M, N)
+        assert scaled_err(y.double().cpu().numpy().T, g[f"c{i}_Y"]) <= tol, (i, act)
+        # K2: dx = dy @ W equals the reference's transpose product (diagcore.py:162-191)
+        dy = t(g[f"c{i}_U"].T.copy(), act)
+        dx = ops.diag_backward_input(dy, st, sel, M, N)
+        assert scaled_err(dx.double().cpu().numpy().T, g[f"c{i}_TU"]) <= tol, (i, act)
+        W = ops.materialize(st, sel, M, N, dtype=pdt)
+        assert scaled_err(W.double().cpu().numpy(), g[f"c{i}_dense"]) <= (0 if act == torch.float64 else 1e-6)
+
+
+def test_products_empty_batch_and_bias():
+    M, N = 48, 32
+    rng = np.random.default_rng(0)
+    offs = np.sort(rng.choice(48, 7, replace=False))
+    st = _store(M, N, offs, rng.standard_normal((7, 32)), torch.float32)
+    sel = ops.selection_from_offsets(48, t(offs, torch.int64))
+    y = ops.diag_forward(torch.empty(0, N, device=DEV), st, sel, M, N)
+    assert y.shape == (0, M)
+    bias = t(rng.standard_normal(M), torch.float32)
+    x = t(rng.standard_normal((5, N)), torch.float32)
+    y0 = ops.diag_forward(x, st, sel, M, N)
+    y1 = ops.diag_forward(x, st, sel, M, N, bias)
+    assert torch.allclose(y1 - y0, bias.expand(5, M), atol=1e-6)
+
+
+# ---------------------------------------------------------------- K4 / K5 selection
+def test_topk_vs_reference_golden():
+    g = load_golden("topk")
+    for i in range(int(g["n"])):
+        C, k, T = g[f"c{i}_meta"]
+        C, k = int(C), int(k)
+        alpha = t(g[f"c{i}_alpha"])
+        sel = ops.soft_topk_select(alpha, k, float(T))
+        n = sel.host_count()
+        np.testing.assert_array_equal(sel.clamped.cpu().numpy().astype(bool), g[f"c{i}_clamped"])
+        np.testing.assert_array_equal(sel.active[:n].cpu().numpy(), g[f"c{i}_active"])
+        slot = sel.slot.cpu().numpy()
+        assert np.all(slot[g[f"c{i}_active"]] == np.arange(n)) and (slot >= 0).sum() == n
+        np.testing.assert_allclose(sel.alpha_soft.cpu().numpy(), g[f"c{i}_tilde"], rtol=1e-12, atol=1e-300)
+        np.testing.assert_array_equal(ops.select_hard(alpha, k).cpu().numpy(), g[f"c{i}_hard"])
+        grad = ops.soft_topk_grad(alpha, k, float(T), t(g[f"c{i}_up"]), clamped=sel.clamped)
+        np.testing.assert_allclose(grad.cpu().numpy(), g[f"c{i}_grad"], rtol=1e-10, atol=1e-12)
+        gl = ops.soft_topk_grad(alpha, k, float(T), t(g[f"c{i}_up"]), l1_coeff=1e-2)
+        np.testing.assert_allclose(gl.cpu().numpy(), g[f"c{i}_grad"] + g[f"c{i}_l1grad"],
+                                   rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("C,k", [(3072, 307), (2304, 230), (768, 77), (4096, 410), (8192, 819)])
+@pytest.mark.parametrize("T", [4.0, 0.5, 0.05, 1e-3, 1e-9])
+def test_topk_masks_bit_exact_vs_oracle(C, k, T):
+    for seed in range(3):
+        a = np.random.default_rng(seed * 7919 + C).standard_normal(C) * (1.0 + seed)
+        tilde, clamped, _, _ = oracle.topk.waterfill(a / T, k)
+        sel = ops.soft_topk_select(t(a), k, T)
+        n = sel.host_count()
+        np.testing.assert_array_equal(sel.active[:n].cpu().numpy(), np.flatnonzero(tilde >= 1e-3))
+        np.testing.assert_array_equal(sel.clamped.cpu().numpy().astype(bool), clamped)
+        np.testing.assert_allclose(sel.alpha_soft.cpu().numpy(), tilde, rtol=1e-11, atol=1e-300)
+        np.testing.assert_array_equal(ops.select_hard(t(a), k).cpu().numpy(), oracle.select_hard(a, k))
+
+
+def test_topk_errors():
+    a = t(np.zeros(5))
+    with pytest.raises(NonPositiveTemperature):
+        ops.soft_topk_select(a, 2, 0.0)
+    with pytest.raises(ValueError):
+        ops.soft_topk_select(a, 6, 1.0)
+    with pytest.raises(ValueError):
+        ops.select_hard(a, 0)
+
+
+# ---------------------------------------------------------------- DiagLinear (layer op)
+def _layer_from_golden(g, i, dtype):
+    n_in, n_out, s, T, B, seed, noise, k = g[f"c{i}_meta"]
+    lyr = DiagLinear(int(n_in), int(n_out), float(s), seed=int(seed), l1_coeff=1e-2, dtype=dtype,
+                     t_schedule=TemperatureSchedule("constant", float(T), float(T), 10))
+    return lyr
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_diaglinear_vs_reference_golden(dtype):
+    g = load_golden("layers")
+    tol = 1e-10 if dtype == torch.float64 else F32_TOL
+    for i in range(int(g["n"])):
+        lyr = _layer_from_golden(g, i, dtype)
+        # init parity: same host RNG stream as DynaDiagLayer (layers.py:199-208)
+        np.testing.assert_array_equal(lyr.alpha.detach().cpu().numpy(), g[f"c{i}_alpha0"])
+        if dtype == torch.float64:
+            np.testing.assert_array_equal(lyr.values.detach().cpu().numpy(), g[f"c{i}_values0"])
+        with torch.no_grad():
+            lyr.alpha.copy_(t(g[f"c{i}_alpha"]))
+            lyr.bias.copy_(t(g[f"c{i}_bias"], dtype))
+        x = t(g[f"c{i}_x"], dtype).requires_grad_(True)
+        y = lyr(x, step=0)
+        np.testing.assert_array_equal(lyr.active_set(0).cpu().numpy(), g[f"c{i}_active"])
+        assert scaled_err(y.detach().cpu().numpy(), g[f"c{i}_y"]) <= tol, i
+        loss = (y * t(g[f"c{i}_up"], dtype)).sum() + lyr.penalty()
+        loss.backward()
+        assert scaled_err(x.grad.cpu().numpy(), g[f"c{i}_gx"]) <= tol, i
+        assert scaled_err(lyr.values.grad.cpu().numpy(), g[f"c{i}_gvalues"]) <= tol, i
+        assert scaled_err(lyr.alpha.grad.cpu().numpy(), g[f"c{i}_galpha"]) <= tol, i
+        assert scaled_err(lyr.bias.grad.cpu().numpy(), g[f"c{i}_gbias"]) <= tol, i
+        inactive = np.setdiff1d(np.arange(lyr.candidates), g[f"c{i}_active"])
+        assert torch.all(lyr.values.grad[t(inactive, torch.int64)] == 0)
+        frozen = lyr.freeze()
+        np.testing.assert_array_equal(frozen.weight.offsets.cpu().numpy(), g[f"c{i}_frozen_offsets"])
+        fy = frozen(t(g[f"c{i}_x"], dtype))
+        assert scaled_err(fy.cpu().numpy(), g[f"c{i}_frozen_y"]) <= tol, i
+
+
+def test_training_trajectory_vs_reference_golden():
+    """Five reference steps (forward, backward + l1, clip 1.0, AdamW lr 5e-2)."""
+    g = load_golden("trajectory")
+    lyr = DiagLinear(32, 48, 0.8, seed=21, l1_coeff=1e-3, dtype=torch.float64,
+                     t_schedule=TemperatureSchedule("cosine", 2.0, 0.05, 5))
+    with torch.no_grad():
+        lyr.alpha.copy_(t(g["alpha_init"]))
+    specs = lyr.param_specs()
+    opt = AdamW(specs, lr=5e-2, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
+    clip = GlobalNormClipper(1.0)
+    for s in range(5):
+        opt.zero_grad()
+        y = lyr(t(g["xs"][s]), step=s)
+        loss = (y * t(g["ups"][s])).sum() + lyr.penalty()
+        loss.backward()
+        norm, scale = clip.compute(specs)
+        opt.step(clip_scale=scale)
+        assert scaled_err(y.detach().cpu().numpy(), g[f"s{s}_y"]) <= 1e-10
+        np.testing.assert_allclose(norm.item(), float(g[f"s{s}_norm"]), rtol=1e-10)
+        assert scaled_err(lyr.values.detach().cpu().numpy(), g[f"s{s}_values"]) <= 1e-9
+        assert scaled_err(lyr.alpha.detach().cpu().numpy(), g[f"s{s}_alpha"]) <= 1e-9
+        assert scaled_err(lyr.bias.detach().cpu().numpy(), g[f"s{s}_bias"]) <= 1e-9
+        np.testing.assert_array_equal(lyr.active_set(s).cpu().numpy(), g[f"s{s}_active"])
+
+
+# ---------------------------------------------------------------- full-size config 1
+def _cfg1_case(n_in, n_out, T, B, dtype, seed=0, route="diag"):
+    sched = TemperatureSchedule("constant", T, T, 1)
+    ref = olayer.OracleDiagLayer(n_in, n_out, 0.9, t_kind="constant", t_init=T, t_final=T, t_total=1,
+                                 l1_coeff=0.0, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    ref.alpha = ref.alpha + rng.standard_normal(ref.C)
+    x = rng.standard_normal((B, n_in))
+    up = rng.standard_normal((B, n_out))
+    lyr = DiagLinear(n_in, n_out, 0.9, seed=seed, l1_coeff=0.0, dtype=dtype, t_schedule=sched, route=route)
+    with torch.no_grad():
+        lyr.alpha.copy_(t(ref.alpha))
+    return ref, lyr, x, up
+
+
+@pytest.mark.parametrize("shape", [(768, 3072), (3072, 768), (768, 2304), (768, 768)])
+@pytest.mark.parametrize("T", [4.0, 0.05, 1e-3, 1e-9])
+def test_config1_fp32_vs_oracle(shape, T):
+    n_in, n_out = shape
+    ref, lyr, x, up = _cfg1_case(n_in, n_out, T, 256, torch.float32)
+    y_ref, cache = ref.forward(x, 0)
+    g_ref = ref.backward(up, cache)
+    xt = t(x, torch.float32).requires_grad_(True)
+    y = lyr(xt, step=0)
+    (y * t(up, torch.float32)).sum().backward()
+    np.testing.assert_array_equal(lyr.active_set(0).cpu().numpy(), cache[3])  # masks bit-exact
+    assert scaled_err(y.detach().cpu().numpy(), y_ref) <= F32_TOL
+    assert scaled_err(xt.grad.cpu().numpy(), g_ref["x"]) <= F32_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) <= F32_TOL
+    assert scaled_err(lyr.alpha.grad.cpu().numpy(), g_ref["alpha"]) <= F32_TOL
+    assert scaled_err(lyr.bias.grad.cpu().numpy(), g_ref["bias"]) <= F32_TOL
+
+
+@pytest.mark.parametrize("route", ["dense", "auto"])
+def test_dense_route_matches_oracle(route):
+    ref, lyr, x, up = _cfg1_case(768, 3072, 0.05, 64, torch.float32, route=route)
+    y_ref, cache = ref.forward(x, 0)
+    g_ref = ref.backward(up, cache)
+    xt = t(x, torch.float32).requires_grad_(True)
+    y = lyr(xt, step=0)
+    (y * t(up, torch.float32)).sum().backward()
+    assert scaled_err(y.detach().cpu().numpy(), y_ref) <= F32_TOL
+    assert scaled_err(xt.grad.cpu().numpy(), g_ref["x"]) <= F32_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) <= F32_TOL
+    assert scaled_err(lyr.alpha.grad.cpu().numpy(), g_ref["alpha"]) <= F32_TOL
+
+
+def test_bf16_activations_vs_oracle():
+    ref, lyr, x, up = _cfg1_case(768, 3072, 1e-9, 256, torch.float32)
+    xb = t(x, torch.bfloat16)
+    upb = t(up, torch.bfloat16)
+    # oracle on the same (bf16-rounded) inputs
+    y_ref, cache = ref.forward(xb.double().cpu().numpy(), 0)
+    g_ref = ref.backward(upb.double().cpu().numpy(), cache)
+    xt = xb.clone().requires_grad_(True)
+    y = lyr(xt, step=0)
+    y.backward(upb)
+    assert scaled_err(y.detach().double().cpu().numpy(), y_ref) <= BF16_TOL
+    assert scaled_err(xt.grad.double().cpu().numpy(), g_ref["x"]) <= BF16_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) <= BF16_TOL
+
+
+def test_large_batch_properties():
+    """Size-independent checks at ViT-B token counts (oracle too slow there):
+    linearity in x, and dW consistent with <dy, y> = <dW, W> identities."""
+    lyr = DiagLinear(768, 3072, 0.9, seed=3, dtype=torch.float32,
+                     t_schedule=TemperatureSchedule("constant", 1e-9, 1e-9, 1))
+    B = 50432
+    g = torch.Generator(device=DEV).manual_seed(0)
+    x1 = torch.randn(B, 768, device=DEV, generator=g)
+    x2 = torch.randn(B, 768, device=DEV, generator=g)
+    with torch.no_grad():
+        lyr.bias.zero_()
+        y1, y2, y12 = lyr(x1, 0), lyr(x2, 0), lyr(x1 + 2 * x2, 0)
+    err = (y12 - (y1 + 2 * y2)).abs().max().item() / max(1.0, y12.abs().max().item())
+    assert err <= 1e-5
+    # a sampled row against the oracle at full token count
+    sel = lyr.selection(0)
+    act = sel.active_offsets().cpu().numpy()
+    vals = lyr.values.detach().cpu().double().numpy()[act] * sel.alpha_soft.cpu().numpy()[act, None]
+    rows = [0, 1234, B - 1]
+    want = oracle.diag_spmm(3072, 768, act, vals, x1[rows].double().cpu().numpy().T).T
+    assert scaled_err(y1[rows].double().cpu().numpy(), want) <= F32_TOL
+
+
+def test_shape_errors():
+    lyr = DiagLinear(6, 8, 0.5, dtype=torch.float32)
+    with pytest.raises(ShapeMismatch):
+        lyr(torch.zeros(3, 5, device=DEV))
+
+
+# ---------------------------------------------------------------- K6 optimizer / clip
+def test_adamw_kernel_vs_reference_golden():
+    g = load_golden("misc")
+    p = t(g["adamw_p0"])
+    gr = g["adamw_g0"].copy()
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    for j in range(3):
+        ops.adamw_(p, t(gr), m, v, j + 1, 1e-2, 0.9, 0.99, 1e-8, 5e-5)
+        np.testing.assert_allclose(p.cpu().numpy(), g["adamw_seq"][j], rtol=1e-14, atol=1e-15)
+        gr = gr * 0.5 + 0.1
+
+
+def test_clip_scale_matches_reference_rule():
+    rng = np.random.default_rng(5)
+    gs = [rng.standard_normal(1000) * 0.05, rng.standard_normal(37) * 0.05]
+    scratch = ops.sumsq_scratch(DEV)
+    buf = torch.zeros(2, dtype=torch.float64, device=DEV)
+    for i, a in enumerate(gs):
+        ops.sumsq_into(t(a), buf[i:i + 1], scratch)
+    for max_norm in (0.1, 100.0):
+        norm, scale = ops.clip_scale(buf, max_norm)
+        _, ref_norm = olayer.clip_by_global_norm(gs, max_norm)
+        np.testing.assert_allclose(norm.item(), ref_norm, rtol=1e-12)
+        want = max_norm / ref_norm if ref_norm > max_norm else 1.0
+        np.testing.assert_allclose(scale.item(), want, rtol=1e-12)
