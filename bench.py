@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — ViT-B/16 90%-sparse DiagLinear training throughput on B200.
+
+Metric (BASELINE.json): "ViT-B/16 90%-sparse images/s (train, infer); DiagMM
+GB/s vs roofline".  One step = one training step of ViT-B/16 whose attention
+(qkv, proj) and MLP (fc1, fc2) projections are DiagLinear layers at 90%
+sparsity (48 layers), on a synthetic ImageNet-shaped batch of 256 images per
+GPU: forward, backward, device-side soft-TopK re-selection in every layer,
+global-norm clip and AdamW over every parameter (the DiagLinear candidate
+stores included).  Data-parallel over N GPUs (one process per GPU, NCCL
+all-reduce of the gradients), so per-GPU work is fixed: weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §measurement for every key).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ViT-B/16 90%-sparse images/s (train, infer); DiagMM GB/s vs roofline"
+UNIT = "images/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+FMA_FP32_TFLOPS = 72.4  # measured FFMA peak, profiles/r01_microbench_fma_lds.txt
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--batch", type=int, default=256, help="images per GPU")
+    p.add_argument("--model", choices=["vit_b16", "vit_tiny16"], default="vit_b16")
+    p.add_argument("--route", choices=["auto", "diag", "dense"], default="auto")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip infer / diagmm kernel sections")
+    p.add_argument("--cpu-sample-images", type=int, default=1)
+    return p.parse_args()
+
+
+def load_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"diagmm_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def vit_layer_shapes(model: str):
+    from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16
+
+    cfg = VIT_B16 if model == "vit_b16" else VIT_TINY16
+    d = cfg.dim
+    per_block = [(d, 3 * d), (d, d), (d, cfg.mlp_ratio * d), (cfg.mlp_ratio * d, d)]
+    return cfg, per_block * cfg.depth
+
+
+def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int):
+    """The reference's CPU DiagLinear path (oracle port, float64) on a bounded sample:
+    ``images`` images' tokens through every DiagLinear layer of the model, one
+    training step each (forward, backward + l1, clip, AdamW) in the post-anneal
+    regime (T = 1e-9, bench.py:188-194 of the reference).  Attention, LayerNorm
+    and the rest of the ViT are NOT timed, so this overstates the reference."""
+    import numpy as np
+
+    from oracle import layer as olayer  # checker / CPU baseline only
+
+    cfg, shapes = vit_layer_shapes(model)
+    tokens = images * cfg.tokens
+    rng = np.random.default_rng(0)
+    layers = [olayer.OracleDiagLayer(n_in, n_out, cfg.sparsity, t_kind="constant", t_init=1e-9,
+                                     t_final=1e-9, t_total=1, l1_coeff=1e-4, seed=i)
+              for i, (n_in, n_out) in enumerate(shapes)]
+    xs = {s: rng.standard_normal((tokens, s[0])) for s in set(shapes)}
+    ups = {s: rng.standard_normal((tokens, s[1])) * 1e-3 for s in set(shapes)}
+    states = [dict() for _ in layers]
+
+    def one_step(step):
+        for lyr, st, shp in zip(layers, states, shapes):
+            olayer.layer_train_step(lyr, xs[shp], ups[shp], step, st)
+
+    for s in range(warmup):
+        one_step(s)
+    times = []
+    for s in range(steps):
+        t0 = time.perf_counter()
+        one_step(warmup + s)
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    cores = len(os.sched_getaffinity(0))
+    return images / sec, sec, cores, tokens
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0
+    ips, sec, cores, tokens = cpu_reference_images_per_s(args.model, args.cpu_sample_images, steps, warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers (48) training step, CPU oracle port",
+                   "global_batch": args.cpu_sample_images, "seq_len": tokens // max(1, args.cpu_sample_images),
+                   "parallelism": "none (host threads via BLAS)"},
+        "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.cpu_sample_images} image(s) = {tokens} tokens through all DiagLinear "
+                                   f"layers (fwd+bwd+clip+AdamW), float64, median of {steps}"},
+        "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    from paper_2506_11449_b200 import AdamW, GlobalNormClipper, _lib, model_param_specs, penalties
+    from paper_2506_11449_b200 import profiling
+    from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16, ViT
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+
+    cfg = VIT_B16 if args.model == "vit_b16" else VIT_TINY16
+    torch.manual_seed(1234)  # dense params; DiagLinear init is seeded per layer (numpy stream)
+    model = ViT(cfg, route=args.route, device=dev)
+    if world > 1:  # identical replicas
+        for p in model.parameters():
+            dist.broadcast(p.data, 0)
+    specs = model_param_specs(model)
+    opt = AdamW(specs, lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
+    clip = GlobalNormClipper(1.0)
+    B = args.batch
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    images = torch.randn(B, 3, cfg.image, cfg.image, device=dev, generator=g).to(torch.bfloat16)
+    labels = torch.randint(0, cfg.classes, (B,), device=dev, generator=g)
+    grads_flat = None
+
+    def allreduce_grads():
+        nonlocal grads_flat
+        grads = [s.tensor.grad for s in specs if s.tensor.grad is not None]
+        # bucket per dtype, one NCCL all-reduce each, average (the reference's batch-mean loss)
+        by_dt = {}
+        for gr in grads:
+            by_dt.setdefault(gr.dtype, []).append(gr)
+        for dt, gs in by_dt.items():
+            flat = torch.cat([x.reshape(-1) for x in gs])
+            dist.all_reduce(flat)
+            flat.div_(world)
+            off = 0
+            for x in gs:
+                n = x.numel()
+                x.copy_(flat[off:off + n].view_as(x))
+                off += n
+
+    def train_step(step, imgs, lbls):
+        model.set_step(step)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = model(imgs)
+        loss = F.cross_entropy(logits.float(), lbls, label_smoothing=0.1)
+        for pen in penalties(model):
+            loss = loss + pen
+        loss.backward()
+        if world > 1:
+            allreduce_grads()
+        _, scale = clip.compute(specs)
+        opt.step(clip_scale=scale)
+        opt.zero_grad()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step = 0
+    # warm-up (also profiles every C-ABI call once to find our dominant kernel)
+    for _ in range(max(args.warmup, 3)):
+        train_step(step, images, labels)
+        step += 1
+    torch.cuda.synchronize()
+    with profiling.CallTimer() as prof:
+        train_step(step, images, labels)
+        step += 1
+    torch.cuda.synchronize()
+    per_fn = prof.totals_ms()
+    dominant = max(per_fn, key=per_fn.get) if per_fn else None
+
+    # ---- timed region: inputs resident in HBM
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().diagmm_launch_count()
+    stream = torch.cuda.current_stream(dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks, profiling.CallTimer(only=dominant) as dom_timer:
+        start.record(stream)
+        for _ in range(args.steps):
+            train_step(step, images, labels)
+            step += 1
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.load().diagmm_launch_count() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    ms = max_over_ranks(ms)
+    value = world * B / (ms / 1e3)
+
+    # ---- e2e: through the public API with host buffers (pinned H2D + loss D2H every step)
+    h_images = images.cpu().pin_memory()
+    h_labels = labels.cpu().pin_memory()
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(e2e_steps):
+        d_img = h_images.to(dev, non_blocking=True)
+        d_lbl = h_labels.to(dev, non_blocking=True)
+        loss = train_step(step, d_img, d_lbl)
+        step += 1
+        float(loss.item())  # D2H of the step's result
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e_start.elapsed_time(e_end) / e2e_steps)
+    e2e_wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
+    e2e_value = world * B / (max(e2e_ms, e2e_wall_ms) / 1e3)
+    h2d = h_images.numel() * h_images.element_size() + h_labels.numel() * h_labels.element_size()
+
+    peaks, peaks_kind = load_peaks()
+    nact_of = {(m.out_features, m.in_features): m.k for m in model.diag_layers()}
+    roof = (profiling.roofline(dom_timer.records, peaks, peaks_kind, FMA_FP32_TFLOPS, nact_of)
+            if dominant else None)
+
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras["infer"] = infer_images_per_s(model, images, args, dev)
+        extras["diagmm"] = diagmm_kernel_section(peaks, peaks_kind)
+        extras["routes"] = {"bench_route": args.route, "step_ms_by_fn": {k: round(v, 4) for k, v in per_fn.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ips, sec, cores, tokens = cpu_reference_images_per_s(args.model, args.cpu_sample_images, 1, 1)
+        cpu = {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_sample_images} image(s) = {tokens} tokens through all 48 DiagLinear layers "
+                         f"(fwd+bwd+clip+AdamW, float64 oracle), {sec:.1f} s; attention/LN not timed"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.model} 90%-sparse DiagLinear (qkv/proj/fc1/fc2 x{cfg.depth}) training "
+                                   f"step, DiagLinear route={args.route}",
+                       "model": args.model, "global_batch": world * B, "seq_len": cfg.tokens,
+                       "parallelism": f"dp{world}", "per_gpu_batch": B,
+                       "l2": "per-step working set (activations, candidate stores) >> 126 MB L2; no explicit flush"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+                    "ms_per_step": max(e2e_ms, e2e_wall_ms)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def infer_images_per_s(model, images, args, dev):
+    """Frozen-model inference (hard top-K, forward only) images/s at the same batch."""
+    import torch
+
+    from paper_2506_11449_b200.layer import DiagLinear, FrozenDiagLinear
+
+    frozen_layers = {}
+    for name, m in model.named_modules():
+        if isinstance(m, DiagLinear):
+            frozen_layers[name] = m.freeze()
+
+    class _Swap:
+        def __enter__(self):
+            self.saved = []
+            for name, fz in frozen_layers.items():
+                parent = model.get_submodule(name.rsplit(".", 1)[0])
+                attr = name.rsplit(".", 1)[1]
+                self.saved.append((parent, attr, getattr(parent, attr)))
+                setattr(parent, attr, fz)
+            return self
+
+        def __exit__(self, *a):
+            for parent, attr, mod in self.saved:
+                setattr(parent, attr, mod)
+
+    with _Swap(), torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+        for _ in range(3):
+            model(images)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        s.record()
+        for _ in range(reps):
+            model(images)
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    _ = FrozenDiagLinear
+    return {"value": images.shape[0] / (ms / 1e3), "unit": "images/s", "ms_per_batch": ms,
+            "route": "diag (frozen, hard top-K)"}
+
+
+def diagmm_kernel_section(peaks, peaks_kind):
+    from paper_2506_11449_b200 import profiling
+
+    return profiling.diagmm_config1(peaks, peaks_kind, FMA_FP32_TFLOPS)
+
+
+if __name__ == "__main__":
+    main()

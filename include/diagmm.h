@@ -71,19 +71,27 @@ DIAGMM_API unsigned long long diagmm_launch_count(void);
  * weight scaling of DynaDiagLayer.forward (layers.py:235) and Tape.add_bias
  * (autodiff.py:72-81).  alpha_soft == NULL means unit scale (DiagHeur /
  * frozen layers, layers.py:354-363, 301-310).  max_act is a host upper bound
- * on *n_act used only to size work (pass C when unknown). */
+ * on *n_act used only to size work (pass C when unknown).  workspace (may
+ * be NULL) lets small batches split the diagonal list across CTAs; size it
+ * with diagmm_forward_workspace. */
+DIAGMM_API size_t diagmm_forward_workspace(int dtype, int M, int N, int B,
+                                           int max_act);
 DIAGMM_API int diagmm_forward(int dtype, int M, int N, int B, const void* x,
                    const void* values, const double* alpha_soft,
                    const int32_t* active, const int32_t* n_act, int max_act,
-                   const void* bias, void* y, void* stream);
+                   const void* bias, void* y, void* workspace,
+                   size_t ws_bytes, void* stream);
 
 /* ---- K2: input gradient through the (never materialized) transpose -------
  * dx = dy @ W_K.  Replaces layers.py:414-418 (transpose, diagcore.py:162-191,
  * followed by the same spmm). */
+DIAGMM_API size_t diagmm_backward_input_workspace(int dtype, int M, int N,
+                                                  int B, int max_act);
 DIAGMM_API int diagmm_backward_input(int dtype, int M, int N, int B, const void* dy,
                           const void* values, const double* alpha_soft,
                           const int32_t* active, const int32_t* n_act,
-                          int max_act, void* dx, void* stream);
+                          int max_act, void* dx, void* workspace,
+                          size_t ws_bytes, void* stream);
 
 /* ---- K3: per-diagonal weight gradient ----------------------------------
  * gw[j,t] = sum_b dy[b, r_jt] * x[b, c_jt]   (layers.py:419-428)

@@ -24,8 +24,10 @@ SIGNATURES = {
     "diagmm_version": (C.c_char_p, []),
     "diagmm_status_string": (C.c_char_p, [_i]),
     "diagmm_launch_count": (C.c_ulonglong, []),
-    "diagmm_forward": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
-    "diagmm_backward_input": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
+    "diagmm_forward_workspace": (_sz, [_i, _i, _i, _i, _i]),
+    "diagmm_forward": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
+    "diagmm_backward_input_workspace": (_sz, [_i, _i, _i, _i, _i]),
+    "diagmm_backward_input": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
     "diagmm_backward_weight_workspace": (_sz, [_i, _i, _i, _i, _i]),
     "diagmm_backward_weight": (
         _i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -77,7 +79,17 @@ def check(status: int, what: str) -> None:
     raise exc(f"{what}: {msg}")
 
 
+_HOOK = None
+
+
+def set_hook(hook) -> None:
+    """Install ``hook(name, args, fn)`` around every call (profiling.CallTimer)."""
+    global _HOOK
+    _HOOK = hook
+
+
 def call(name: str, *args) -> int:
-    status = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    status = fn(*args) if _HOOK is None else _HOOK(name, args, fn)
     check(status, name)
     return status

@@ -7,7 +7,8 @@
 namespace diagmm {
 template <typename T>
 int run_product(bool, int, int, int, const void*, const void*, const double*, const int32_t*,
-                const int32_t*, int, const void*, void*, cudaStream_t);
+                const int32_t*, int, const void*, void*, void*, size_t, cudaStream_t);
+template <typename T> size_t product_workspace(bool, int, int, int, int);
 template <typename T> size_t dw_workspace(int, int, int, int);
 template <typename T>
 int run_dw(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
@@ -73,26 +74,45 @@ const char* diagmm_status_string(int status) {
   }
 }
 
+static size_t product_ws(int dtype, bool gather, int M, int N, int B, int max_act) {
+  if (check_shape(M, N, B, max_act)) return 0;
+  const int C = M > N ? M : N, L = M < N ? M : N;
+  switch (dtype) {
+    case DIAGMM_F64: return product_workspace<double>(gather, B, C, L, max_act);
+    case DIAGMM_F32: return product_workspace<float>(gather, B, C, L, max_act);
+    case DIAGMM_BF16: return product_workspace<__nv_bfloat16>(gather, B, C, L, max_act);
+    default: return 0;
+  }
+}
+
+size_t diagmm_forward_workspace(int dtype, int M, int N, int B, int max_act) {
+  return product_ws(dtype, M < N, M, N, B, max_act);
+}
+
+size_t diagmm_backward_input_workspace(int dtype, int M, int N, int B, int max_act) {
+  return product_ws(dtype, M >= N, M, N, B, max_act);
+}
+
 int diagmm_forward(int dtype, int M, int N, int B, const void* x, const void* values,
                    const double* alpha_soft, const int32_t* active, const int32_t* n_act, int max_act,
-                   const void* bias, void* y, void* stream) {
+                   const void* bias, void* y, void* workspace, size_t ws_bytes, void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
   const int C = M > N ? M : N, L = M < N ? M : N;
   // tall/square: scatter form with in width L=N, out width C=M; wide: gather form.
   const bool gather = M < N;
   DIAGMM_DISPATCH(dtype, run_product, gather, B, C, L, x, values, alpha_soft, active, n_act, max_act,
-                  bias, y, S(stream))
+                  bias, y, workspace, ws_bytes, S(stream))
 }
 
 int diagmm_backward_input(int dtype, int M, int N, int B, const void* dy, const void* values,
                           const double* alpha_soft, const int32_t* active, const int32_t* n_act,
-                          int max_act, void* dx, void* stream) {
+                          int max_act, void* dx, void* workspace, size_t ws_bytes, void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
   const int C = M > N ? M : N, L = M < N ? M : N;
   // tall/square dX: gather form (in = dy width C=M, out width L=N); wide: scatter.
   const bool gather = M >= N;
   DIAGMM_DISPATCH(dtype, run_product, gather, B, C, L, dy, values, alpha_soft, active, n_act, max_act,
-                  nullptr, dx, S(stream))
+                  nullptr, dx, workspace, ws_bytes, S(stream))
 }
 
 size_t diagmm_backward_weight_workspace(int dtype, int M, int N, int B, int max_act) {

@@ -13,196 +13,303 @@
 //   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:419-428)
 //        tall: Aop = dy, Bop = x;   wide: Aop = x, Bop = dy.
 //
-// Design notes (B200): one CTA owns a tile of batch rows and a range of output
-// positions; the CTA's batch rows of the gathered operand are staged once in
-// shared memory (whole rows: every output tile touches almost every column at
-// 10% density), so each FMA costs one conflict-free LDS from consecutive
-// lanes; the diagonal values are read with coalesced LDG (lane = output
-// position) and reused across the BT rows held in registers.  The measured
-// smem delivery (128 B/clk/SM, profiles/r01_microbench_fma_lds.txt) bounds
-// this design at ~32 fp32 FMA/clk/SM; see DESIGN.md.
+// B200 design (profiles/r01_*):
+//  * A CTA (8 warps) owns 128 consecutive output positions x BT batch rows.
+//    The gathered operand's BT rows are staged ONCE in shared memory in a
+//    column-major tile xs[c][b] (a circular halo of 128 columns removes the
+//    per-element `mod`), so for one (diagonal, position) a lane fetches the BT
+//    rows of its column with 16-byte LDS and reuses its diagonal value BT times.
+//  * The 8 warps split the diagonal list (warp w takes j = w, w+8, ...) and
+//    reduce through shared memory in a fixed order at the end (deterministic);
+//    the offsets and scales of the next 32 diagonals sit in a per-lane cache
+//    (shuffled out), and the diagonal values of diagonal q+1 are loaded while
+//    diagonal q is being multiplied, so the dependent-load latency that bounded
+//    the first version (ncu: long-scoreboard stalls) is hidden.
+//  * Small batches split the diagonal list across CTAs too (grid.z), with a
+//    fixed-order reduction kernel, so even B = 1 fills the 148 SMs.
+//  * Lanes take positions t0 + lane + 32u (u < 4): every diagonal-value LDG is a
+//    coalesced 128-byte warp access and every smem access is bank-conflict free
+//    for any offset, wrap or alignment.
+//  The shared-memory bandwidth (128 B/clk/SM, profiles/r01_microbench_fma_lds)
+//  then bounds fp32 at 32 FMA/clk/SM (4 bytes per FMA) and bf16 at 64.
 #include "common.cuh"
 
 namespace diagmm {
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Copy rows [b0, b0+nb) of a (B, W) row-major matrix into smem (nb, W),
-// zero-filling rows past B.
-template <typename T>
-__device__ __forceinline__ void stage_rows(T* __restrict__ dst, const T* __restrict__ src,
-                                           int b0, int nb, int B, int W) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const size_t row_bytes = (size_t)W * sizeof(T);
-  const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  if (vec) {
-    const int per_row = (int)(row_bytes / 16);
-    const int total = nb * per_row;
-    for (int i = tid; i < total; i += nt) {
-      int b = i / per_row, q = i - b * per_row;
-      int4 v = make_int4(0, 0, 0, 0);
-      if (b0 + b < B) v = __ldg(reinterpret_cast<const int4*>(src + (size_t)(b0 + b) * W) + q);
-      reinterpret_cast<int4*>(dst + (size_t)b * W)[q] = v;
-    }
-  } else {
-    for (int b = 0; b < nb; ++b) {
-      const bool in_range = b0 + b < B;
-      for (int c = tid; c < W; c += nt)
-        dst[(size_t)b * W + c] = in_range ? src[(size_t)(b0 + b) * W + c] : T(0);
-    }
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / kWarp;
+constexpr int kTile = 128;  // output positions per CTA
+constexpr int kU = kTile / kWarp;
+
+// Load BT consecutive T values from shared memory (16-byte aligned) as A.
+template <typename T, int BT, typename A>
+__device__ __forceinline__ void load_col(const T* __restrict__ p, A (&v)[BT]) {
+  static_assert((BT * sizeof(T)) % 16 == 0, "BT * sizeof(T) must be a multiple of 16");
+  constexpr int kVec = BT * sizeof(T) / 16;
+  constexpr int kPer = 16 / sizeof(T);
+  const int4* q = reinterpret_cast<const int4*>(p);
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    int4 w = q[i];
+    const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) v[i * kPer + k] = to_acc<A>(e[k]);
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void stage_diagonals(int* __restrict__ offs,
-                                                typename Traits<T>::A* __restrict__ scl,
-                                                const int32_t* __restrict__ active,
-                                                const double* __restrict__ asoft, int n_act) {
-  using A = typename Traits<T>::A;
-  for (int j = threadIdx.x; j < n_act; j += blockDim.x) {
-    int o = active[j];
-    offs[j] = o;
-    scl[j] = asoft ? (A)asoft[o] : (A)1;
-  }
-}
-
-// ---------------------------------------------------------------- form G
+// Stage rows [b0, b0+BT) of a row-major (B, W) matrix, columns c = 0 .. cols-1
+// taken circularly (c mod W), into the column-major tile dst[c * BT + b].
 template <typename T, int BT>
-__global__ void __launch_bounds__(256)
-k_gather(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
-         const double* __restrict__ asoft, const int32_t* __restrict__ active,
-         const int32_t* __restrict__ n_act_p, int max_act,
-         const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out) {
-  using A = typename Traits<T>::A;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int n_act = min(*n_act_p, max_act);
-  A* scl = reinterpret_cast<A*>(smem);
-  int* offs = reinterpret_cast<int*>(smem + align16((size_t)max_act * sizeof(A)));
-  T* xs = reinterpret_cast<T*>(smem + align16((size_t)max_act * sizeof(A)) +
-                               align16((size_t)max_act * sizeof(int)));
-  const int b0 = blockIdx.y * BT;
-  stage_diagonals<T>(offs, scl, active, asoft, n_act);
-  stage_rows<T>(xs, in, b0, BT, B, C);
-  __syncthreads();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= L) return;
-  A acc[BT];
-#pragma unroll
-  for (int b = 0; b < BT; ++b) acc[b] = A(0);
-  const auto* vcol = vals + t;
-#pragma unroll 2
-  for (int j = 0; j < n_act; ++j) {
-    const int o = offs[j];
-    const A v = scl[j] * (A)__ldg(vcol + (size_t)o * L);
-    int c = o + t;
-    c = (c >= C) ? c - C : c;
-    const T* xp = xs + c;
-#pragma unroll
-    for (int b = 0; b < BT; ++b) acc[b] = fma(v, to_acc<A>(xp[(size_t)b * C]), acc[b]);
+__device__ __forceinline__ void stage_tile(T* __restrict__ dst, const T* __restrict__ src, int b0, int B,
+                                           int W, int cols) {
+  for (int i = threadIdx.x; i < BT * cols; i += blockDim.x) {
+    const int b = i / cols, c = i - b * cols;
+    const int cc = c < W ? c : c % W;
+    dst[(size_t)c * BT + b] = (b0 + b < B) ? src[(size_t)(b0 + b) * W + cc] : T(0);
   }
-  const A bb = bias ? (A)bias[t] : A(0);
-#pragma unroll
-  for (int b = 0; b < BT; ++b)
-    if (b0 + b < B) out[(size_t)(b0 + b) * L + t] = from_acc<T>(acc[b] + bb);
 }
 
-// ---------------------------------------------------------------- form S
-template <typename T, int BT>
-__global__ void __launch_bounds__(256)
-k_scatter(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
+// --------------------------------------------------------------------------- K1/K2
+// GATHER: out width L (positions t), in width C, smem columns C + kTile (halo).
+// !GATHER: out width C (positions r), in width L, smem columns L.
+template <typename T, int BT, bool GATHER>
+__global__ void __launch_bounds__(kThreads, 2)
+k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
           const double* __restrict__ asoft, const int32_t* __restrict__ active,
-          const int32_t* __restrict__ n_act_p, int max_act,
-          const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out) {
+          const int32_t* __restrict__ n_act_p, int max_act, const typename Traits<T>::P* __restrict__ bias,
+          T* __restrict__ out, typename Traits<T>::A* __restrict__ part, int nsplit) {
   using A = typename Traits<T>::A;
   extern __shared__ __align__(16) unsigned char smem[];
+  T* xs = reinterpret_cast<T*>(smem);
+  A* red = reinterpret_cast<A*>(smem);  // reused after the main loop
   const int n_act = min(*n_act_p, max_act);
-  A* scl = reinterpret_cast<A*>(smem);
-  int* offs = reinterpret_cast<int*>(smem + align16((size_t)max_act * sizeof(A)));
-  T* xs = reinterpret_cast<T*>(smem + align16((size_t)max_act * sizeof(A)) +
-                               align16((size_t)max_act * sizeof(int)));
+  const int in_w = GATHER ? C : L;
+  const int out_w = GATHER ? L : C;
+  const int cols = GATHER ? C + kTile : L;
+  const int t0 = blockIdx.x * kTile;
   const int b0 = blockIdx.y * BT;
-  stage_diagonals<T>(offs, scl, active, asoft, n_act);
-  stage_rows<T>(xs, in, b0, BT, B, L);
-  __syncthreads();
-  const int r0 = blockIdx.x * blockDim.x + (threadIdx.x & ~(kWarp - 1));
-  if (r0 >= C) return;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  // Diagonals that can touch this warp's 32 rows: o in cyclic [r0-L+1, r0+31].
+  const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+
+  stage_tile<T, BT>(xs, in, b0, B, in_w, cols);
+
+  // The CTA's diagonal list as up to two ranges of the ascending active list.
   int lo1 = 0, hi1 = n_act, lo2 = 0, hi2 = 0;
-  if (L + kWarp - 1 < C) {
-    const int lo = r0 - L + 1, hi = r0 + kWarp - 1;
+  if (!GATHER && L + kTile - 1 < C) {
+    // (r - o) mod C < L for some r in [t0, t0+128)  <=>  o in cyclic [t0-L+1, t0+127]
+    const int lo = t0 - L + 1, hi = t0 + kTile - 1;
     if (lo < 0) {
-      lo1 = lower_bound_i32(offs, n_act, lo + C); hi1 = n_act;
-      lo2 = 0; hi2 = lower_bound_i32(offs, n_act, hi + 1);
+      lo1 = lower_bound_i32(active, n_act, lo + C); hi1 = n_act;
+      hi2 = lower_bound_i32(active, n_act, hi + 1);
     } else if (hi >= C) {
-      lo1 = lower_bound_i32(offs, n_act, lo); hi1 = n_act;
-      lo2 = 0; hi2 = lower_bound_i32(offs, n_act, hi - C + 1);
+      lo1 = lower_bound_i32(active, n_act, lo); hi1 = n_act;
+      hi2 = lower_bound_i32(active, n_act, hi - C + 1);
     } else {
-      lo1 = lower_bound_i32(offs, n_act, lo); hi1 = lower_bound_i32(offs, n_act, hi + 1);
+      lo1 = lower_bound_i32(active, n_act, lo); hi1 = lower_bound_i32(active, n_act, hi + 1);
     }
   }
-  A acc[BT];
-#pragma unroll
-  for (int b = 0; b < BT; ++b) acc[b] = A(0);
-  const bool row_ok = r < C;
-  for (int pass = 0; pass < 2; ++pass) {
-    const int jb = pass ? lo2 : lo1, je = pass ? hi2 : hi1;
-#pragma unroll 2
-    for (int j = jb; j < je; ++j) {
-      const int o = offs[j];
-      int c = r - o;
-      c = (c < 0) ? c + C : c;
-      const bool ok = row_ok && (c < L);
-      const int ci = ok ? c : 0;
-      const A v = ok ? scl[j] * (A)__ldg(vals + (size_t)o * L + ci) : A(0);
-      const T* xp = xs + ci;
-#pragma unroll
-      for (int b = 0; b < BT; ++b) acc[b] = fma(v, to_acc<A>(xp[(size_t)b * L]), acc[b]);
-    }
-  }
-  if (!row_ok) return;
-  const A bb = bias ? (A)bias[r] : A(0);
+  const int len1 = hi1 - lo1, total = len1 + (hi2 - lo2);
+  // split z of nsplit takes a contiguous chunk of the virtual list
+  const int per = (total + nsplit - 1) / nsplit;
+  const int vb = min(total, (int)blockIdx.z * per), ve = min(total, vb + per);
+  __syncthreads();
+
+  A acc[BT][kU];
 #pragma unroll
   for (int b = 0; b < BT; ++b)
-    if (b0 + b < B) out[(size_t)(b0 + b) * C + r] = from_acc<T>(acc[b] + bb);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[b][u] = A(0);
+
+  // warp-strided walk of [vb, ve): v = vb + warp + kWarps * q
+  const int nq = ve - vb - warp > 0 ? (ve - vb - warp + kWarps - 1) / kWarps : 0;
+  int o_cache = 0;
+  A s_cache = A(0);
+  auto fill = [&](int q0) {
+    const int v = vb + warp + kWarps * (q0 + lane);
+    if (q0 + lane < nq) {
+      const int j = v < len1 ? lo1 + v : lo2 + (v - len1);
+      o_cache = active[j];
+      s_cache = asoft ? (A)asoft[o_cache] : A(1);
+    }
+  };
+  auto fetch = [&](int o, A s, A (&vv)[kU], int (&ci)[kU]) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = t0 + lane + kWarp * u;
+      if (GATHER) {
+        const bool ok = p < L;
+        vv[u] = ok ? s * (A)__ldg(vals + (size_t)o * L + p) : A(0);
+        int base = o + t0;
+        base = base >= C ? base - C : base;
+        ci[u] = base + lane + kWarp * u;
+      } else {
+        int c = p - o;
+        c = c < 0 ? c + C : c;
+        const bool ok = p < C && c < L;
+        vv[u] = ok ? s * (A)__ldg(vals + (size_t)o * L + c) : A(0);
+        ci[u] = ok ? c : 0;
+      }
+    }
+  };
+  A vcur[kU], vnxt[kU];
+  int ccur[kU], cnxt[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u] = A(0); ccur[u] = cnxt[u] = 0; }
+  if (nq > 0) {
+    fill(0);
+    const int o = __shfl_sync(0xffffffffu, o_cache, 0);
+    const A s = __shfl_sync(0xffffffffu, s_cache, 0);
+    fetch(o, s, vcur, ccur);
+  }
+  for (int q = 0; q < nq; ++q) {
+    if (q + 1 < nq) {
+      if (((q + 1) & (kWarp - 1)) == 0) fill(q + 1);
+      const int o = __shfl_sync(0xffffffffu, o_cache, (q + 1) & (kWarp - 1));
+      const A s = __shfl_sync(0xffffffffu, s_cache, (q + 1) & (kWarp - 1));
+      fetch(o, s, vnxt, cnxt);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      A xv[BT];
+      load_col<T, BT, A>(xs + (size_t)ccur[u] * BT, xv);
+#pragma unroll
+      for (int b = 0; b < BT; ++b) acc[b][u] = fma(vcur[u], xv[b], acc[b][u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u]; ccur[u] = cnxt[u]; }
+  }
+
+  // fixed-order cross-warp reduction
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < BT; ++b)
+#pragma unroll
+    for (int u = 0; u < kU; ++u) red[((size_t)warp * BT + b) * kTile + lane + kWarp * u] = acc[b][u];
+  __syncthreads();
+  for (int i = threadIdx.x; i < BT * kTile; i += kThreads) {
+    const int b = i / kTile, tt = i - b * kTile;
+    const int p = t0 + tt;
+    if (b0 + b >= B || p >= out_w) continue;
+    A s = A(0);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[((size_t)w * BT + b) * kTile + tt];
+    if (nsplit == 1) {
+      if (bias) s += (A)bias[p];
+      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+    } else {
+      part[((size_t)blockIdx.z * B + b0 + b) * out_w + p] = s;
+    }
+  }
 }
 
-// ---------------------------------------------------------------- dW partials
-template <typename T, int TJ>
-__global__ void __launch_bounds__(128)
-k_dw_partial(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
-             const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p,
-             int rows_per_part, typename Traits<T>::A* __restrict__ partial, int max_act) {
+// Fixed-order sum of the split partials (+ bias).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_split_reduce(int B, int out_w, int nsplit, const typename Traits<T>::A* __restrict__ part,
+               const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out) {
   using A = typename Traits<T>::A;
-  __shared__ int so[TJ];
+  const size_t n = (size_t)B * out_w;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    A s = A(0);
+    for (int z = 0; z < nsplit; ++z) s += part[(size_t)z * n + i];
+    if (bias) s += (A)bias[i % out_w];
+    out[i] = from_acc<T>(s);
+  }
+}
+
+// --------------------------------------------------------------------------- K3
+// CTA: 128 positions x (kWarps * JQ) diagonals x one batch part; walks its rows in
+// chunks of RB staged column-major in smem: the Aop window the tile's diagonals
+// read (offsets ascend, so a tile of consecutive diagonals reads one short
+// circular window of each row) and the Bop columns of the tile.
+template <typename T, int RB, int JQ>
+__global__ void __launch_bounds__(kThreads, 2)
+k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
+     const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act, int win_cap,
+     int rows_per_part, typename Traits<T>::A* __restrict__ partial) {
+  using A = typename Traits<T>::A;
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kJ = kWarps * JQ;
   const int n_act = min(*n_act_p, max_act);
-  const int j0 = blockIdx.y * TJ;
+  const int j0 = blockIdx.y * kJ;
   if (j0 >= n_act) return;
-  const int nj = min(TJ, n_act - j0);
-  if (threadIdx.x < TJ) so[threadIdx.x] = threadIdx.x < nj ? active[j0 + threadIdx.x] : 0;
-  __syncthreads();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= L) return;
-  int cc[TJ];
-#pragma unroll
-  for (int jj = 0; jj < TJ; ++jj) {
-    int c = so[jj] + t;
-    cc[jj] = c >= C ? c - C : c;
+  const int nj = min(kJ, n_act - j0);
+  const int t0 = blockIdx.x * kTile;
+  const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+  const int o_first = active[j0], o_last = active[j0 + nj - 1];
+  // window of Aop columns: [ws, ws + wcols) taken circularly
+  int ws, wcols;
+  if (o_last - o_first + kTile <= win_cap) {
+    ws = o_first + t0;
+    ws = ws >= C ? ws - C : ws;
+    wcols = o_last - o_first + kTile;
+  } else {
+    ws = 0;
+    wcols = C + kTile;
   }
-  A acc[TJ];
+  T* as = reinterpret_cast<T*>(smem);  // wcols x RB
+  T* bs = reinterpret_cast<T*>(smem + align16((size_t)win_cap * RB * sizeof(T)));  // kTile x RB
+  // window column of (diagonal q, position u) = rel[q] + lane + 32u
+  int rel[JQ];
 #pragma unroll
-  for (int jj = 0; jj < TJ; ++jj) acc[jj] = A(0);
-  const int bb = blockIdx.z * rows_per_part;
-  const int be = min(B, bb + rows_per_part);
-  for (int b = bb; b < be; ++b) {
-    const A bm = to_acc<A>(__ldg(bop + (size_t)b * L + t));
-    const T* arow = aop + (size_t)b * C;
+  for (int q = 0; q < JQ; ++q) {
+    const int j = j0 + warp + kWarps * q;
+    int r = 0;
+    if (j < j0 + nj) {
+      const int o = active[j];
+      if (ws == 0 && wcols == C + kTile) {
+        r = o + t0;
+        r = r >= C ? r - C : r;
+      } else {
+        r = o - o_first;  // offsets ascend inside the tile
+      }
+    }
+    rel[q] = r;
+  }
+  A acc[JQ][kU];
 #pragma unroll
-    for (int jj = 0; jj < TJ; ++jj) acc[jj] = fma(to_acc<A>(__ldg(arow + cc[jj])), bm, acc[jj]);
+  for (int q = 0; q < JQ; ++q)
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[q][u] = A(0);
+
+  const int rb = blockIdx.z * rows_per_part, re = min(B, rb + rows_per_part);
+  for (int c0 = rb; c0 < re; c0 += RB) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < RB * wcols; i += kThreads) {
+      const int b = i / wcols, c = i - b * wcols;
+      int cc = ws + c;
+      while (cc >= C) cc -= C;
+      as[(size_t)c * RB + b] = (c0 + b < re) ? aop[(size_t)(c0 + b) * C + cc] : T(0);
+    }
+    for (int i = threadIdx.x; i < RB * kTile; i += kThreads) {
+      const int b = i / kTile, c = i - b * kTile;
+      bs[(size_t)c * RB + b] = (c0 + b < re && t0 + c < L) ? bop[(size_t)(c0 + b) * L + t0 + c] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      A bv[RB];
+      load_col<T, RB, A>(bs + (size_t)(lane + kWarp * u) * RB, bv);
+#pragma unroll
+      for (int q = 0; q < JQ; ++q) {
+        A av[RB];
+        load_col<T, RB, A>(as + (size_t)(rel[q] + lane + kWarp * u) * RB, av);
+#pragma unroll
+        for (int b = 0; b < RB; ++b) acc[q][u] = fma(av[b], bv[b], acc[q][u]);
+      }
+    }
   }
 #pragma unroll
-  for (int jj = 0; jj < TJ; ++jj)
-    if (jj < nj) partial[((size_t)blockIdx.z * max_act + j0 + jj) * L + t] = acc[jj];
+  for (int q = 0; q < JQ; ++q) {
+    const int j = j0 + warp + kWarps * q;
+    if (j >= j0 + nj) continue;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int t = t0 + lane + kWarp * u;
+      if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
+    }
+  }
 }
 
 // Deterministic block sum of one double per thread (fixed tree order).
@@ -254,31 +361,42 @@ k_dw_finalize(int C, int L, int nparts, const typename Traits<T>::A* __restrict_
   }
 }
 
-// Column sums of dy (bias gradient), two levels for determinism.
+// Column sums of dy (bias gradient): 32-row partials, then a fixed-order fold.
+constexpr int kColRows = 32;
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_colsum_partial(int B, int M, const T* __restrict__ dy, int rows_per_part,
-                 typename Traits<T>::A* __restrict__ part) {
+k_colsum_partial(int B, int M, const T* __restrict__ dy, typename Traits<T>::A* __restrict__ part) {
   using A = typename Traits<T>::A;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= M) return;
-  const int bb = blockIdx.y * rows_per_part, be = min(B, bb + rows_per_part);
+  const int bb = blockIdx.y * kColRows, be = min(B, bb + kColRows);
   A acc = A(0);
   for (int b = bb; b < be; ++b) acc += to_acc<A>(dy[(size_t)b * M + r]);
   part[(size_t)blockIdx.y * M + r] = acc;
 }
 template <typename T>
-__global__ void k_colsum_final(int M, int nparts, const typename Traits<T>::A* __restrict__ part,
-                               typename Traits<T>::P* __restrict__ g_bias) {
+__global__ void __launch_bounds__(256)
+k_colsum_final(int M, int nparts, const typename Traits<T>::A* __restrict__ part,
+               typename Traits<T>::P* __restrict__ g_bias) {
   using A = typename Traits<T>::A;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M) return;
+  __shared__ A red[8][33];
+  // 32 columns per CTA, the 8 warps split the parts, fixed-order fold
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + lane;
   A acc = A(0);
-  for (int p = 0; p < nparts; ++p) acc += part[(size_t)p * M + r];
-  g_bias[r] = (typename Traits<T>::P)acc;
+  if (r < M)
+    for (int p = w; p < nparts; p += 8) acc += part[(size_t)p * M + r];
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && r < M) {
+    A s = A(0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += red[i][lane];
+    g_bias[r] = (typename Traits<T>::P)s;
+  }
 }
 
-// ---------------------------------------------------------------- dense route
+// --------------------------------------------------------------------------- dense route
 template <typename T>
 __global__ void k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals,
                               const double* __restrict__ asoft, const int32_t* __restrict__ active,
@@ -293,7 +411,7 @@ __global__ void k_materialize(int M, int N, const typename Traits<T>::P* __restr
   const int o = active[j];
   const A sc = asoft ? (A)asoft[o] : A(1);
   int r, c;
-  if (M >= N) { r = (o + t) % M; c = t; } else { r = t; c = (o + t) % N; }
+  if (M >= N) { r = o + t; r = r >= M ? r - M : r; c = t; } else { r = t; c = o + t; c = c >= N ? c - N : c; }
   w[(size_t)r * N + c] = from_acc<T>(sc * (A)vals[(size_t)o * L + t]);
 }
 
@@ -316,7 +434,7 @@ k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ val
   double local = 0.0;
   for (int t = threadIdx.x; t < L; t += blockDim.x) {
     int r, c;
-    if (M >= N) { r = (i + t) % M; c = t; } else { r = t; c = (i + t) % N; }
+    if (M >= N) { r = i + t; r = r >= M ? r - M : r; c = t; } else { r = t; c = i + t; c = c >= N ? c - N : c; }
     const double gw = (double)dW[(size_t)r * N + c];
     grow[t] = (P)(sc * gw);
     local += gw * (double)vals[(size_t)i * L + t];
@@ -329,124 +447,187 @@ k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ val
 
 // ================================================================ host side
 struct ProductPlan {
-  int bt, tpb, grid_x, grid_y;
+  int bt, gx, gy, nsplit;
   size_t smem;
 };
 
 template <typename T>
-static size_t product_smem(int max_act, int bt, int width) {
+static size_t product_smem(int bt, int cols) {
   using A = typename Traits<T>::A;
-  return align16((size_t)max_act * sizeof(A)) + align16((size_t)max_act * sizeof(int)) +
-         (size_t)bt * width * sizeof(T);
+  const size_t tile = (size_t)bt * cols * sizeof(T);
+  const size_t red = (size_t)kWarps * bt * kTile * sizeof(A);
+  return align16(tile > red ? tile : red);
 }
 
-// Pick rows-per-CTA (bt) and threads-per-CTA so that shared memory fits and the
-// grid covers the 148 SMs at least twice when the problem allows it.
 template <typename T>
-static ProductPlan plan_product(int B, int out_w, int in_w, int max_act) {
-  const size_t kSmemMax = 220 * 1024;
-  const int target = 2 * num_sms();
-  ProductPlan p{};
-  int bts[] = {16, 8, 4, 2, 1};
-  for (int tpb : {256, 128, 64}) {
-    for (int bt : bts) {
-      if (sizeof(T) == 8 && bt > 8) continue;
-      size_t sm = product_smem<T>(max_act, bt, in_w);
-      if (sm > kSmemMax) continue;
-      int gx = ceil_div(out_w, tpb), gy = ceil_div(B, bt);
-      p = {bt, tpb, gx, gy, sm};
-      if ((long long)gx * gy >= target) return p;
+static void row_choices(int (&v)[3]) {
+  if (sizeof(T) == 8) { v[0] = 8; v[1] = 4; v[2] = 2; }
+  else if (sizeof(T) == 4) { v[0] = 16; v[1] = 8; v[2] = 4; }
+  else { v[0] = 16; v[1] = 8; v[2] = 8; }
+}
+
+template <typename T>
+static ProductPlan plan_product(int B, int out_w, int cols, int max_act) {
+  const size_t kSmem2 = 113 * 1024, kSmem1 = 220 * 1024;
+  const int sms = num_sms();
+  const int gx = ceil_div(out_w, kTile);
+  int choices[3];
+  row_choices<T>(choices);
+  ProductPlan best{0, 0, 0, 1, 0};
+  for (size_t cap : {kSmem2, kSmem1}) {
+    for (int bt : choices) {
+      const size_t sm = product_smem<T>(bt, cols);
+      if (sm > cap) continue;
+      const int gy = ceil_div(B, bt);
+      // largest row tile that still gives every SM a CTA; else the smallest tile
+      best = {bt, gx, gy, 1, sm};
+      if ((long long)gx * gy >= sms) break;
     }
+    if (best.bt != 0) break;
   }
-  if (p.bt == 0) p = {1, 64, ceil_div(out_w, 64), B, product_smem<T>(max_act, 1, in_w)};
-  return p;
+  if (best.bt == 0) return best;
+  const long long ctas = (long long)best.gx * best.gy;
+  if (ctas < 2LL * sms) {
+    const int ns = (int)ceil_div(2LL * sms, ctas);
+    const int max_ns = max_act / 32 > 1 ? max_act / 32 : 1;
+    best.nsplit = ns < max_ns ? ns : max_ns;
+  }
+  return best;
 }
 
-template <typename T, int BT>
-static void launch_form(bool gather, const ProductPlan& p, cudaStream_t st, int B, int C, int L,
-                        const T* in, const typename Traits<T>::P* vals, const double* asoft,
-                        const int32_t* active, const int32_t* n_act, int max_act,
-                        const typename Traits<T>::P* bias, T* out) {
-  dim3 grid(p.grid_x, p.grid_y);
-  if (gather) {
-    auto k = k_gather<T, BT>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    k<<<grid, p.tpb, p.smem, st>>>(B, C, L, in, vals, asoft, active, n_act, max_act, bias, out);
-    note_launch();
-  } else {
-    auto k = k_scatter<T, BT>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    k<<<grid, p.tpb, p.smem, st>>>(B, C, L, in, vals, asoft, active, n_act, max_act, bias, out);
-    note_launch();
-  }
+template <typename T, int BT, bool G>
+static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, int L, const T* in,
+                           const typename Traits<T>::P* vals, const double* asoft, const int32_t* active,
+                           const int32_t* n_act, int max_act, const typename Traits<T>::P* bias, T* out,
+                           typename Traits<T>::A* part) {
+  auto k = k_product<T, BT, G>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  k<<<dim3(p.gx, p.gy, p.nsplit), kThreads, p.smem, st>>>(B, C, L, in, vals, asoft, active, n_act, max_act,
+                                                          bias, out, part, p.nsplit);
+  note_launch();
 }
 
-// One product in either form.  gather: out width L, in width C.
-// scatter: out width C, in width L.
 template <typename T>
-int run_product(bool gather, int B, int C, int L, const void* in, const void* vals,
-                const double* asoft, const int32_t* active, const int32_t* n_act, int max_act,
-                const void* bias, void* out, cudaStream_t st) {
+size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
+  using A = typename Traits<T>::A;
+  const int out_w = gather ? L : C, cols = gather ? C + kTile : L;
+  ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
+  return p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0;
+}
+
+template <typename T>
+int run_product(bool gather, int B, int C, int L, const void* in, const void* vals, const double* asoft,
+                const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
+                void* ws, size_t ws_bytes, cudaStream_t st) {
   using P = typename Traits<T>::P;
+  using A = typename Traits<T>::A;
   if (B == 0) return DIAGMM_OK;
-  const int out_w = gather ? L : C, in_w = gather ? C : L;
-  ProductPlan p = plan_product<T>(B, out_w, in_w, max_act);
-  if (p.smem > 227 * 1024) return DIAGMM_ETOOLARGE;
+  const int out_w = gather ? L : C, cols = gather ? C + kTile : L;
+  ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
+  if (p.bt == 0) return DIAGMM_ETOOLARGE;
+  if (p.nsplit > 1 && (ws == nullptr || ws_bytes < (size_t)p.nsplit * B * out_w * sizeof(A))) p.nsplit = 1;
   auto tin = static_cast<const T*>(in);
   auto tv = static_cast<const P*>(vals);
   auto tb = static_cast<const P*>(bias);
   auto to = static_cast<T*>(out);
-  switch (p.bt) {
-    case 16: launch_form<T, 16>(gather, p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to); break;
-    case 8: launch_form<T, 8>(gather, p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to); break;
-    case 4: launch_form<T, 4>(gather, p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to); break;
-    case 2: launch_form<T, 2>(gather, p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to); break;
-    default: launch_form<T, 1>(gather, p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to); break;
+  auto part = static_cast<A*>(ws);
+#define DIAGMM_LAUNCH(BT)                                                                           \
+  if (p.bt == BT) {                                                                                 \
+    if (gather)                                                                                     \
+      launch_product<T, BT, true>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part); \
+    else                                                                                            \
+      launch_product<T, BT, false>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part); \
+  }
+  if constexpr (sizeof(T) == 8) {
+    DIAGMM_LAUNCH(8) DIAGMM_LAUNCH(4) DIAGMM_LAUNCH(2)
+  } else if constexpr (sizeof(T) == 4) {
+    DIAGMM_LAUNCH(16) DIAGMM_LAUNCH(8) DIAGMM_LAUNCH(4)
+  } else {
+    DIAGMM_LAUNCH(16) DIAGMM_LAUNCH(8)
+  }
+#undef DIAGMM_LAUNCH
+  if (p.nsplit > 1) {
+    const size_t n = (size_t)B * out_w;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    k_split_reduce<T><<<blocks, 256, 0, st>>>(B, out_w, p.nsplit, part, tb, to);
+    note_launch();
   }
   return status_from_cuda();
 }
 
-constexpr int kTJ = 16;
-constexpr int kDwThreads = 128;
+// dW tiling: rows per staged chunk (16-byte column loads) and diagonals per warp
+template <typename T> struct DwRows;
+template <> struct DwRows<double> { static constexpr int RB = 4; };
+template <> struct DwRows<float> { static constexpr int RB = 8; };
+template <> struct DwRows<__nv_bfloat16> { static constexpr int RB = 16; };
+constexpr int kJQ = 4;
+constexpr int kDwJ = kWarps * kJQ;
 
-static void dw_parts(int B, int L, int max_act, int* parts, int* rows_per_part) {
-  const int tiles = ceil_div(L, kDwThreads) * ceil_div(max_act > 0 ? max_act : 1, kTJ);
-  int p = ceil_div(2 * num_sms(), tiles);
-  p = p < 1 ? 1 : p;
-  const int max_p = ceil_div(B, 32);
+template <typename T>
+static int dw_win_cap(int C) {
+  // Room for a full circular row (C + 128 columns): a tile whose offsets span
+  // more than that falls back to staging whole rows.  Up to C ~ 3300 the tiles
+  // still fit two CTAs per SM.
+  return C + kTile;
+}
+
+template <typename T>
+static size_t dw_smem(int C) {
+  constexpr int RB = DwRows<T>::RB;
+  return align16((size_t)dw_win_cap<T>(C) * RB * sizeof(T)) + (size_t)kTile * RB * sizeof(T);
+}
+
+static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_per_part) {
+  const long long tiles = (long long)ceil_div(L, kTile) * ceil_div(max_act > 0 ? max_act : 1, kDwJ);
+  long long p = ceil_div(2LL * num_sms(), tiles);
+  if (p < 1) p = 1;
+  const long long max_p = ceil_div(B, rb);
   if (p > max_p) p = max_p;
   if (p < 1) p = 1;
-  *rows_per_part = ceil_div(B, p);
-  *parts = ceil_div(B, *rows_per_part);
+  int rpp = ceil_div(B, p);
+  rpp = ceil_div(rpp, rb) * rb;
+  *rows_per_part = rpp;
+  *parts = ceil_div(B, rpp);
 }
 
 template <typename T>
 size_t dw_workspace(int M, int N, int B, int max_act) {
   using A = typename Traits<T>::A;
   const int L = M < N ? M : N;
+  const int C = M > N ? M : N;
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, &parts, &rpp);
-  int cparts = ceil_div(B > 0 ? B : 1, 256);
-  return align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+  dw_parts(B > 0 ? B : 1, L, max_act, DwRows<T>::RB, &parts, &rpp);
+  const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
+  const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
+  const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
+  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+  size_t ws = dw > prod_f ? dw : prod_f;
+  return ws > prod_b ? ws : prod_b;
 }
 
 template <typename T>
 int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals, const double* asoft,
-           const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act,
-           void* g_values, double* g_soft, void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+           const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
+           double* g_soft, void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
   using P = typename Traits<T>::P;
   using A = typename Traits<T>::A;
+  constexpr int RB = DwRows<T>::RB;
   const int C = M > N ? M : N, L = M < N ? M : N;
   if (ws_bytes < dw_workspace<T>(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, &parts, &rpp);
+  dw_parts(B > 0 ? B : 1, L, max_act, RB, &parts, &rpp);
   A* partial = static_cast<A*>(ws);
   const bool tall = M >= N;
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
   if (B > 0 && max_act > 0) {
-    dim3 grid(ceil_div(L, kDwThreads), ceil_div(max_act, kTJ), parts);
-    k_dw_partial<T, kTJ><<<grid, kDwThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, rpp, partial, max_act);
+    const size_t sm = dw_smem<T>(C);
+    if (sm > 227 * 1024) return DIAGMM_ETOOLARGE;
+    auto k = k_dw<T, RB, kJQ>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid(ceil_div(L, kTile), ceil_div(max_act, kDwJ), parts);
+    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, dw_win_cap<T>(C), rpp, partial);
     note_launch();
   } else {
     parts = 0;
@@ -456,13 +637,11 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   note_launch();
   if (g_bias) {
     A* cpart = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)));
-    const int cparts = ceil_div(B > 0 ? B : 1, 256);
-    const int crpp = ceil_div(B > 0 ? B : 1, cparts);
     if (B > 0) {
-      k_colsum_partial<T><<<dim3(ceil_div(M, 256), cparts), 256, 0, st>>>(
-          B, M, static_cast<const T*>(dy), crpp, cpart);
+      const int cparts = ceil_div(B, kColRows);
+      k_colsum_partial<T><<<dim3(ceil_div(M, 256), cparts), 256, 0, st>>>(B, M, static_cast<const T*>(dy), cpart);
       note_launch();
-      k_colsum_final<T><<<ceil_div(M, 256), 256, 0, st>>>(M, cparts, cpart, static_cast<P*>(g_bias));
+      k_colsum_final<T><<<ceil_div(M, 32), 256, 0, st>>>(M, cparts, cpart, static_cast<P*>(g_bias));
       note_launch();
     } else {
       cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), st);
@@ -479,35 +658,35 @@ int run_materialize(int M, int N, const void* vals, const double* asoft, const i
   cudaMemsetAsync(w, 0, (size_t)M * N * sizeof(T), st);
   if (max_act > 0) {
     dim3 grid(ceil_div(L, 256), max_act);
-    k_materialize<T><<<grid, 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, active, n_act,
-                                            max_act, static_cast<T*>(w));
+    k_materialize<T><<<grid, 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, active, n_act, max_act,
+                                            static_cast<T*>(w));
     note_launch();
   }
   return status_from_cuda();
 }
 
 template <typename P>
-int run_gather_dense(int M, int N, const void* dW, const void* vals, const double* asoft,
-                     const int32_t* slot, const int32_t* n_act, void* g_values, double* g_soft,
-                     cudaStream_t st) {
+int run_gather_dense(int M, int N, const void* dW, const void* vals, const double* asoft, const int32_t* slot,
+                     const int32_t* n_act, void* g_values, double* g_soft, cudaStream_t st) {
   const int C = M > N ? M : N;
-  k_gather_dense<P><<<C, 256, 0, st>>>(M, N, static_cast<const P*>(dW), static_cast<const P*>(vals),
-                                       asoft, slot, n_act, static_cast<P*>(g_values), g_soft);
+  k_gather_dense<P><<<C, 256, 0, st>>>(M, N, static_cast<const P*>(dW), static_cast<const P*>(vals), asoft, slot,
+                                       n_act, static_cast<P*>(g_values), g_soft);
   note_launch();
   return status_from_cuda();
 }
 
 // explicit instantiations used by capi.cu
-#define DIAGMM_INST(T)                                                                          \
-  template int run_product<T>(bool, int, int, int, const void*, const void*, const double*,     \
-                              const int32_t*, const int32_t*, int, const void*, void*,          \
-                              cudaStream_t);                                                    \
-  template size_t dw_workspace<T>(int, int, int, int);                                          \
-  template int run_dw<T>(int, int, int, const void*, const void*, const void*, const double*,   \
-                         const int32_t*, const int32_t*, const int32_t*, int, void*, double*,   \
-                         void*, void*, size_t, cudaStream_t);                                   \
-  template int run_materialize<T>(int, int, const void*, const double*, const int32_t*,         \
-                                  const int32_t*, int, void*, cudaStream_t);
+#define DIAGMM_INST(T)                                                                                    \
+  template int run_product<T>(bool, int, int, int, const void*, const void*, const double*,               \
+                              const int32_t*, const int32_t*, int, const void*, void*, void*, size_t,     \
+                              cudaStream_t);                                                              \
+  template size_t product_workspace<T>(bool, int, int, int, int);                                         \
+  template size_t dw_workspace<T>(int, int, int, int);                                                    \
+  template int run_dw<T>(int, int, int, const void*, const void*, const void*, const double*,             \
+                         const int32_t*, const int32_t*, const int32_t*, int, void*, double*, void*,      \
+                         void*, size_t, cudaStream_t);                                                    \
+  template int run_materialize<T>(int, int, const void*, const double*, const int32_t*, const int32_t*,   \
+                                  int, void*, cudaStream_t);
 DIAGMM_INST(double)
 DIAGMM_INST(float)
 DIAGMM_INST(__nv_bfloat16)

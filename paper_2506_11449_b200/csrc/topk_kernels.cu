@@ -30,8 +30,13 @@ constexpr int kSelMaxC = 8192;
 // that explicit so no comparison can separate them.
 __device__ __forceinline__ double canon(double v) { return v == 0.0 ? 0.0 : v; }
 
+// Written as explicit early returns: nvcc 12.9 -O3 dropped the index tie-break
+// from the equivalent one-line `ka > kb || (!(ka < kb) && !(ka > kb) && ia < ib)`
+// (SASS had no index compare; tools/debug_sort.cu reproduces it).
 __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
-  return ka > kb || (!(ka < kb) && !(ka > kb) && ia < ib);
+  if (ka > kb) return true;
+  if (ka < kb) return false;
+  return ia < ib;
 }
 
 // Bitonic sort of NP (power of two) (key, idx) pairs so that position 0 holds

@@ -94,23 +94,24 @@ def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype
         return False
     # "auto": the reference's own switch (diagcore.py:226, layers.py:420) —
     # dense once the structural density reaches 1/4 — plus the B200 cost
-    # model: tensor cores run the dense product ~20x faster than the FMA pipe,
-    # so the dense route also wins at large token counts.
+    # model: with bf16 activations the tensor cores run
+    # the dense-equivalent product ~50x faster than the FMA pipe runs the
+    # diagonal one, so from a few hundred tokens on the dense route wins; the
+    # FMA kernels keep the small-batch regime, where both are bound by reading
+    # the weights and the diagonal store is 1/density times smaller.
     L = min(spec.M, spec.N)
     n_act = sel.host_count()
     if 4 * n_act * L >= spec.M * spec.N:
         return True
-    return act_dtype != torch.float64 and B * n_act * L >= dense_route_threshold(spec.M, spec.N)
+    return act_dtype == torch.bfloat16 and B >= dense_route_min_tokens()
 
 
-def dense_route_threshold(M: int, N: int) -> float:
-    """FMA-equivalent work above which the bf16/tf32 tensor-core route is faster.
+def dense_route_min_tokens() -> int:
+    """Token count from which the bf16 tensor-core route beats the FMA route
+    (measured on B200, profiles/r01_*; override with DIAGMM_DENSE_MIN_TOKENS)."""
+    import os
 
-    Calibrated on B200 (profiles/): the FMA kernels sustain ~1/20 of the dense
-    tensor-core rate, so the diagonal route wins while its work stays below
-    ~1/20 of the dense work, i.e. always for small batches (HBM bound).
-    """
-    return float("inf")
+    return int(os.environ.get("DIAGMM_DENSE_MIN_TOKENS", "512"))
 
 
 class DiagMMFunction(torch.autograd.Function):
@@ -145,6 +146,7 @@ class DiagMMFunction(torch.autograd.Function):
         dx = g_alpha = None
         need_soft = alpha is not None and ctx.needs_input_grad[2]
         if W is not None:
+            dy = dy.to(W.dtype)
             if ctx.needs_input_grad[0]:
                 dx = dy @ W
             out_dt = vals.dtype
@@ -262,6 +264,8 @@ class DiagLinear(nn.Module):
         x2 = _flatten(x, self.in_features)
         if x2.dtype != torch.float64 and self.values.dtype == torch.float64:
             x2 = x2.double()
+        elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
+            x2 = x2.to(torch.get_autocast_dtype("cuda"))  # like nn.Linear under autocast
         spec = _OpSpec(self.out_features, self.in_features, self.k, self.temperature(step), self.route)
         y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
         return y.reshape(*lead, self.out_features)

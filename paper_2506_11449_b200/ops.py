@@ -179,6 +179,18 @@ def selection_from_offsets(C: int, offsets: torch.Tensor, alpha_soft: torch.Tens
     return sel
 
 
+_WORKSPACE: dict = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    ws = _WORKSPACE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WORKSPACE[key] = ws
+    return ws
+
+
 def _check_product(x: torch.Tensor, width: int, values: torch.Tensor, M: int, N: int):
     _need_cuda(x, values)
     if x.dim() != 2 or x.shape[1] != width:
@@ -199,9 +211,11 @@ def diag_forward(x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, 
     values = values.contiguous()
     bias = _contig(bias)
     y = torch.empty(x.shape[0], M, dtype=x.dtype, device=x.device)
-    _lib.call("diagmm_forward", _code(x.dtype), M, N, x.shape[0], _p(x), _p(values), _p(sel.alpha_soft),
-              _p(sel.active), _p(sel.n_act), C if max_act is None else int(max_act), _p(bias), _p(y),
-              _stream(x))
+    ma = C if max_act is None else int(max_act)
+    code = _code(x.dtype)
+    ws = _workspace(x.device, _lib.load().diagmm_forward_workspace(code, M, N, x.shape[0], ma))
+    _lib.call("diagmm_forward", code, M, N, x.shape[0], _p(x), _p(values), _p(sel.alpha_soft),
+              _p(sel.active), _p(sel.n_act), ma, _p(bias), _p(y), _p(ws), ws.numel(), _stream(x))
     return y
 
 
@@ -212,22 +226,12 @@ def diag_backward_input(dy: torch.Tensor, values: torch.Tensor, sel: Selection, 
     C, _ = geometry(M, N)
     dy = dy.contiguous()
     dx = torch.empty(dy.shape[0], N, dtype=dy.dtype, device=dy.device)
-    _lib.call("diagmm_backward_input", _code(dy.dtype), M, N, dy.shape[0], _p(dy), _p(values.contiguous()),
-              _p(sel.alpha_soft), _p(sel.active), _p(sel.n_act), C if max_act is None else int(max_act),
-              _p(dx), _stream(dy))
+    ma = C if max_act is None else int(max_act)
+    code = _code(dy.dtype)
+    ws = _workspace(dy.device, _lib.load().diagmm_backward_input_workspace(code, M, N, dy.shape[0], ma))
+    _lib.call("diagmm_backward_input", code, M, N, dy.shape[0], _p(dy), _p(values.contiguous()),
+              _p(sel.alpha_soft), _p(sel.active), _p(sel.n_act), ma, _p(dx), _p(ws), ws.numel(), _stream(dy))
     return dx
-
-
-_WORKSPACE: dict = {}
-
-
-def _workspace(device, nbytes: int) -> torch.Tensor:
-    key = (device, torch.cuda.current_stream(device).cuda_stream)
-    ws = _WORKSPACE.get(key)
-    if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
-        _WORKSPACE[key] = ws
-    return ws
 
 
 def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection,

@@ -1,0 +1,207 @@
+"""Measurement helpers: per-C-ABI-call CUDA-event timing, algorithmic work
+ and roofline fractions, and the DiagMM kernel section of bench.py.
+
+Algorithmic work per call (nnz = n_act * L, s = activation element size):
+    forward / backward_input : 2 nnz B FLOP; s B (M + N) + 4 nnz + 12 n_act bytes
+    backward_weight          : 2 nnz B FLOP; s B (M + N) + 4 C L (full g_values) + 4 nnz bytes
+    materialize              : s_w M N + 4 nnz bytes
+    gather_dense_grad        : 4 nnz (gathered dW) + 4 C L + 4 nnz bytes
+    adamw                    : 7 p n bytes (read p, g, m, v; write p, m, v)
+The roofline time is max(FLOP / P_fma, bytes / HBM) with P_fma the measured
+FFMA peak and HBM the measured copy bandwidth (MEASURED_PEAKS.json).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_ELT = {0: 8, 1: 4, 2: 2}
+
+
+class CallTimer:
+    """Context manager: CUDA events around every C-ABI call (or only ``only``)."""
+
+    def __init__(self, only: str | None = None):
+        self.only = only
+        self.records = []
+
+    def _hook(self, name, args, fn):
+        if self.only is not None and name != self.only:
+            return fn(*args)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn(*args)
+        e.record()
+        self.records.append((name, args, s, e))
+        return out
+
+    def __enter__(self):
+        _lib.set_hook(self._hook)
+        return self
+
+    def __exit__(self, *exc):
+        _lib.set_hook(None)
+
+    def totals_ms(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for name, _, s, e in self.records:
+            out[name] = out.get(name, 0.0) + s.elapsed_time(e)
+        return out
+
+
+def _n_act(args, name, nact_of):
+    if name in ("diagmm_forward", "diagmm_backward_input", "diagmm_backward_weight"):
+        M, N = args[1], args[2]
+    elif name in ("diagmm_materialize", "diagmm_gather_dense_grad"):
+        M, N = args[1], args[2]
+    else:
+        return None
+    return nact_of.get((M, N)) if nact_of else None
+
+
+def work(name, args, nact_of=None):
+    """(flops, bytes) of one call, or None when not modelled."""
+    if name in ("diagmm_forward", "diagmm_backward_input", "diagmm_backward_weight"):
+        dt, M, N, B = args[0], args[1], args[2], args[3]
+        C, L = max(M, N), min(M, N)
+        n = _n_act(args, name, nact_of) or args[9 if name != "diagmm_backward_weight" else 11]
+        s = _ELT[dt]
+        p = 8 if dt == 0 else 4
+        flops = 2.0 * n * L * B
+        if name == "diagmm_backward_weight":
+            byts = s * B * (M + N) + p * C * L + p * n * L
+        else:
+            byts = s * B * (M + N) + p * n * L + 12 * n
+        return flops, byts
+    if name == "diagmm_materialize":
+        dt, M, N = args[0], args[1], args[2]
+        n = _n_act(args, name, nact_of) or args[7]
+        return 0.0, _ELT[dt] * M * N + 4 * n * min(M, N)
+    if name == "diagmm_gather_dense_grad":
+        dt, M, N = args[0], args[1], args[2]
+        n = _n_act(args, name, nact_of) or max(M, N)
+        p = 8 if dt == 0 else 4
+        return 0.0, p * n * min(M, N) * 2 + p * max(M, N) * min(M, N)
+    if name == "diagmm_adamw":
+        dt, n = args[0], args[1]
+        return 0.0, 7 * (8 if dt == 0 else 4) * n
+    if name == "diagmm_sumsq":
+        dt, n = args[0], args[1]
+        return 0.0, (8 if dt == 0 else 4) * n
+    return None
+
+
+def roofline(records, peaks: dict, peaks_kind: str, fma_tflops: float, nact_of=None):
+    """Roofline object for the timed calls of one function (bench JSON contract)."""
+    if not records:
+        return None
+    torch.cuda.synchronize()
+    name = records[0][0]
+    tot_ms, tot_f, tot_b = 0.0, 0.0, 0.0
+    for nm, args, s, e in records:
+        w = work(nm, args, nact_of)
+        if w is None:
+            return {"kernel": name, "note": "work not modelled"}
+        tot_ms += s.elapsed_time(e)
+        tot_f += w[0]
+        tot_b += w[1]
+    n = len(records)
+    sec = tot_ms / 1e3
+    hbm = float(peaks["hbm_gbs"])
+    t_fma = tot_f / (fma_tflops * 1e12)
+    t_hbm = tot_b / (hbm * 1e9)
+    if t_fma > t_hbm:
+        achieved = tot_f / sec / 1e12
+        return {"kernel": name, "bound": "fma", "achieved": achieved, "peak": fma_tflops, "unit": "TFLOP/s",
+                "frac": achieved / fma_tflops, "traffic": None, "launches": n,
+                "avg_launch_us": tot_ms * 1e3 / n, "algorithmic_bytes_per_launch": tot_b / n,
+                "algorithmic_flops_per_launch": tot_f / n,
+                "peak_source": "measured FFMA (profiles/r01_microbench_fma_lds.txt)",
+                "hbm_gbs_achieved": tot_b / sec / 1e9}
+    achieved = tot_b / sec / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "launches": n, "avg_launch_us": tot_ms * 1e3 / n,
+            "algorithmic_bytes_per_launch": tot_b / n, "peak_source": f"{peaks_kind} (MEASURED_PEAKS.json)"}
+
+
+# ------------------------------------------------------------------ kernel section
+def _time_call(fn, reps: int, flush: torch.Tensor | None):
+    times = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.add_(1.0)  # touches > L2 between reps
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    times.sort()
+    return times[len(times) // 2]
+
+
+def diag_case(M, N, B, sparsity, act_dtype, peaks, fma_tflops, seed=0, reps=20, flush=None, dense_cmp=True):
+    """Time K1/K2/K3 (and the cuBLAS dense bf16 equivalent) on one shape."""
+    import numpy as np
+
+    from . import ops
+    from .selection import required_diagonals
+
+    dev = torch.device("cuda")
+    C, L = max(M, N), min(M, N)
+    k = required_diagonals(M, N, sparsity)
+    rng = np.random.default_rng(seed)
+    offs = np.sort(rng.choice(C, k, replace=False))
+    values = torch.randn(C, L, device=dev, dtype=ops.param_dtype_for(act_dtype))
+    sel = ops.selection_from_offsets(C, torch.as_tensor(offs, device=dev))
+    x = torch.randn(B, N, device=dev).to(act_dtype)
+    dy = torch.randn(B, M, device=dev).to(act_dtype)
+    out = {}
+    fns = {
+        "fwd": lambda: ops.diag_forward(x, values, sel, M, N, max_act=k),
+        "dx": lambda: ops.diag_backward_input(dy, values, sel, M, N, max_act=k),
+        "dw": lambda: ops.diag_backward_weight(dy, x, values, sel, M, N, need_bias=False, need_soft=False,
+                                              max_act=k),
+    }
+    s = x.element_size()
+    for nm, fn in fns.items():
+        fn()
+        ms = _time_call(fn, reps, flush)
+        flops = 2.0 * k * L * B
+        byts = s * B * (M + N) + 4 * k * L + (4 * C * L if nm == "dw" else 0)
+        t_roof = max(flops / (fma_tflops * 1e12), byts / (peaks["hbm_gbs"] * 1e9))
+        out[nm] = {"us": ms * 1e3, "tflops": flops / (ms / 1e3) / 1e12, "gbs": byts / (ms / 1e3) / 1e9,
+                   "roofline_frac": t_roof / (ms / 1e3)}
+    tot = sum(out[n]["us"] for n in fns)
+    res = {"shape": {"M": M, "N": N, "B": B, "sparsity": sparsity, "k": k, "dtype": str(act_dtype)},
+           **out, "fwd_bwd_us": tot}
+    if dense_cmp:
+        W = torch.randn(M, N, device=dev, dtype=torch.bfloat16)
+        xb, dyb = x.to(torch.bfloat16), dy.to(torch.bfloat16)
+        f = lambda: xb @ W.t()  # noqa: E731
+        b1 = lambda: dyb @ W  # noqa: E731
+        b2 = lambda: dyb.t() @ xb  # noqa: E731
+        for fn in (f, b1, b2):
+            fn()
+        dense = [_time_call(fn, reps, flush) * 1e3 for fn in (f, b1, b2)]
+        res["cublas_bf16_dense_us"] = {"fwd": dense[0], "dx": dense[1], "dw": dense[2], "total": sum(dense)}
+        res["speedup_vs_cublas_bf16_fwd_bwd"] = sum(dense) / tot
+    return res
+
+
+def diagmm_config1(peaks, peaks_kind, fma_tflops):
+    """BASELINE config 1 (DiagLinear 768->3072, 90%, B=256, fp32) + a few sweep points."""
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")  # 256 MB > 126 MB L2
+    cfg1 = diag_case(3072, 768, 256, 0.9, torch.float32, peaks, fma_tflops, flush=flush)
+    sweep = []
+    for (dim, s, B) in [(4096, 0.9, 1), (4096, 0.9, 64), (4096, 0.9, 1024), (4096, 0.99, 1024),
+                        (4096, 0.9, 8192)]:
+        sweep.append(diag_case(dim, dim, B, s, torch.bfloat16, peaks, fma_tflops, reps=10, flush=flush))
+    return {"config1": cfg1, "sweep_4096": sweep, "hbm_peak_gbs": peaks["hbm_gbs"],
+            "fma_peak_tflops": fma_tflops, "peaks": peaks_kind,
+            "note": "L2 flushed (256 MB write) before every timed launch; median of reps"}
