@@ -13,25 +13,29 @@
 //   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:419-428)
 //        tall: Aop = dy, Bop = x;   wide: Aop = x, Bop = dy.
 //
-// B200 design (profiles/r01_*):
-//  * A CTA (8 warps) owns 128 consecutive output positions x BT batch rows.
-//    The gathered operand's BT rows are staged ONCE in shared memory in a
-//    column-major tile xs[c][b] (a circular halo of 128 columns removes the
-//    per-element `mod`), so for one (diagonal, position) a lane fetches the BT
-//    rows of its column with 16-byte LDS and reuses its diagonal value BT times.
-//  * The 8 warps split the diagonal list (warp w takes j = w, w+8, ...) and
-//    reduce through shared memory in a fixed order at the end (deterministic);
-//    the offsets and scales of the next 32 diagonals sit in a per-lane cache
-//    (shuffled out), and the diagonal values of diagonal q+1 are loaded while
-//    diagonal q is being multiplied, so the dependent-load latency that bounded
-//    the first version (ncu: long-scoreboard stalls) is hidden.
-//  * Small batches split the diagonal list across CTAs too (grid.z), with a
-//    fixed-order reduction kernel, so even B = 1 fills the 148 SMs.
-//  * Lanes take positions t0 + lane + 32u (u < 4): every diagonal-value LDG is a
-//    coalesced 128-byte warp access and every smem access is bank-conflict free
-//    for any offset, wrap or alignment.
-//  The shared-memory bandwidth (128 B/clk/SM, profiles/r01_microbench_fma_lds)
-//  then bounds fp32 at 32 FMA/clk/SM (4 bytes per FMA) and bf16 at 64.
+// B200 design (measurements in profiles/):
+//  * Staging: the gathered operand's rows are copied global->shared by the TMA
+//    engine (cp.async.bulk, one instruction per row segment, completion on an
+//    mbarrier); a circular halo of 128 columns after each row removes the
+//    per-element `mod`.  Every output tile of a 10%-dense wrap-around matrix
+//    touches almost every input column, so whole rows are staged once per CTA
+//    and reused by every diagonal.
+//  * Lanes take positions p0 + lane + 32u (u < 4): every diagonal-value load is a
+//    coalesced 128-byte warp access and every shared-memory read is
+//    bank-conflict free for any offset, wrap or alignment.
+//  * Offsets/scales of the next 32 diagonals live in a per-lane cache (shuffled
+//    out) and the values of diagonal q+1 are loaded while diagonal q is being
+//    multiplied, hiding the dependent global-load latency.
+//  * Two tilings: WIDE (large batch) — each warp owns 128 positions of a
+//    1024-position tile and walks every diagonal that can touch them, BT rows
+//    in registers, no cross-warp reduction; SPLIT (small batch) — the 8 warps
+//    (and, via grid.z, several CTAs) split the diagonal list of one 128-position
+//    tile and reduce in a fixed order (deterministic), so B = 1 fills 148 SMs.
+//  * dW: a CTA owns 256 positions x 64 consecutive diagonals; because offsets
+//    ascend, the tile reads one short circular window of each Aop row.  Row
+//    chunks stream through a two-stage TMA/mbarrier pipeline.
+//  Shared-memory delivery (128 B/clk/SM, profiles/r01_microbench_fma_lds.txt)
+//  bounds every FMA that needs a fresh gathered operand at 32 fp32 FMA/clk/SM.
 #include "common.cuh"
 
 namespace diagmm {
@@ -40,80 +44,115 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / kWarp;
-constexpr int kTile = 128;  // output positions per CTA
-constexpr int kU = kTile / kWarp;
+constexpr int kWarpPos = 128;              // positions per warp
+constexpr int kU = kWarpPos / kWarp;       // positions per lane
+constexpr int kHalo = 128;                 // circular halo after each staged row
+constexpr int kWideTile = kWarps * kWarpPos;  // 1024 positions per WIDE CTA
+constexpr int kSplitTile = kWarpPos;          // 128 positions per SPLIT CTA
 
-// Load BT consecutive T values from shared memory (16-byte aligned) as A.
-template <typename T, int BT, typename A>
-__device__ __forceinline__ void load_col(const T* __restrict__ p, A (&v)[BT]) {
-  static_assert((BT * sizeof(T)) % 16 == 0, "BT * sizeof(T) must be a multiple of 16");
-  constexpr int kVec = BT * sizeof(T) / 16;
-  constexpr int kPer = 16 / sizeof(T);
-  const int4* q = reinterpret_cast<const int4*>(p);
-#pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    int4 w = q[i];
-    const T* e = reinterpret_cast<const T*>(&w);
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) v[i * kPer + k] = to_acc<A>(e[k]);
+// Row stride (elements) of a staged tile holding `cols` columns: 16-byte multiple.
+template <typename T>
+__host__ __device__ inline int row_stride(int cols) {
+  constexpr int v = 16 / sizeof(T);
+  return (cols + v - 1) / v * v;
+}
+
+// Stage rows [b0, b0+nb) of a row-major (B, W) matrix into dst (row stride rs):
+// columns [0, W) followed by `halo` columns taken circularly from column 0.
+// TMA bulk copies when aligned (one elected thread), else a coalesced loop.
+template <typename T>
+__device__ __forceinline__ void stage_rows(T* __restrict__ dst, int rs, const T* __restrict__ src, int b0,
+                                           int nb, int B, int W, int halo, bool bulk, uint64_t* bar) {
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      uint32_t bytes = 0;
+      const int hv = halo < W ? halo : 0;
+      for (int b = 0; b < nb && b0 + b < B; ++b) bytes += (uint32_t)((W + hv) * sizeof(T));
+      mbar_expect_tx(bar, bytes);
+      for (int b = 0; b < nb && b0 + b < B; ++b) {
+        const T* row = src + (size_t)(b0 + b) * W;
+        bulk_g2s(dst + (size_t)b * rs, row, (uint32_t)(W * sizeof(T)), bar);
+        if (hv) bulk_g2s(dst + (size_t)b * rs + W, row, (uint32_t)(hv * sizeof(T)), bar);
+      }
+    }
+    for (int b = B - b0; b < nb; ++b)  // rows past the batch: zeros
+      for (int c = threadIdx.x; c < W + halo; c += blockDim.x) dst[(size_t)b * rs + c] = T(0);
+  } else {
+    for (int b = 0; b < nb; ++b) {
+      const bool in = b0 + b < B;
+      const T* row = src + (size_t)(b0 + b) * W;
+      for (int c = threadIdx.x; c < W + halo; c += blockDim.x) {
+        int cc = c;
+        while (cc >= W) cc -= W;
+        dst[(size_t)b * rs + c] = in ? row[cc] : T(0);
+      }
+    }
   }
 }
 
-// Stage rows [b0, b0+BT) of a row-major (B, W) matrix, columns c = 0 .. cols-1
-// taken circularly (c mod W), into the column-major tile dst[c * BT + b].
-template <typename T, int BT>
-__device__ __forceinline__ void stage_tile(T* __restrict__ dst, const T* __restrict__ src, int b0, int B,
-                                           int W, int cols) {
-  for (int i = threadIdx.x; i < BT * cols; i += blockDim.x) {
-    const int b = i / cols, c = i - b * cols;
-    const int cc = c < W ? c : c % W;
-    dst[(size_t)c * BT + b] = (b0 + b < B) ? src[(size_t)(b0 + b) * W + cc] : T(0);
+// Diagonal range touching positions [p0, p0+n) in the S form: o in cyclic
+// [p0 - L + 1, p0 + n - 1] -> up to two ranges of the ascending active list.
+__device__ __forceinline__ void scatter_ranges(const int32_t* active, int n_act, int C, int L, int p0, int n,
+                                               int& lo1, int& hi1, int& lo2, int& hi2) {
+  lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0;
+  if (L + n - 1 >= C) return;
+  const int lo = p0 - L + 1, hi = p0 + n - 1;
+  if (lo < 0) {
+    lo1 = lower_bound_i32(active, n_act, lo + C); hi1 = n_act;
+    hi2 = lower_bound_i32(active, n_act, hi + 1);
+  } else if (hi >= C) {
+    lo1 = lower_bound_i32(active, n_act, lo); hi1 = n_act;
+    hi2 = lower_bound_i32(active, n_act, hi - C + 1);
+  } else {
+    lo1 = lower_bound_i32(active, n_act, lo); hi1 = lower_bound_i32(active, n_act, hi + 1);
   }
 }
 
 // --------------------------------------------------------------------------- K1/K2
-// GATHER: out width L (positions t), in width C, smem columns C + kTile (halo).
-// !GATHER: out width C (positions r), in width L, smem columns L.
-template <typename T, int BT, bool GATHER>
+// GATHER: out width L (positions t), in width C, staged columns C + halo.
+// !GATHER: out width C (positions r), in width L, staged columns L.
+template <typename T, int BT, bool GATHER, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 2)
 k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
           const double* __restrict__ asoft, const int32_t* __restrict__ active,
           const int32_t* __restrict__ n_act_p, int max_act, const typename Traits<T>::P* __restrict__ bias,
-          T* __restrict__ out, typename Traits<T>::A* __restrict__ part, int nsplit) {
+          T* __restrict__ out, typename Traits<T>::A* __restrict__ part, int nsplit, int bulk) {
   using A = typename Traits<T>::A;
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* xs = reinterpret_cast<T*>(smem);
-  A* red = reinterpret_cast<A*>(smem);  // reused after the main loop
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  T* xs = reinterpret_cast<T*>(smem + 128);
+  A* red = reinterpret_cast<A*>(smem + 128);  // SPLIT: reused after the main loop
   const int n_act = min(*n_act_p, max_act);
   const int in_w = GATHER ? C : L;
   const int out_w = GATHER ? L : C;
-  const int cols = GATHER ? C + kTile : L;
-  const int t0 = blockIdx.x * kTile;
+  const int halo = GATHER ? kHalo : 0;
+  const int rs = row_stride<T>(in_w + halo);
+  constexpr int TT = WIDE ? kWideTile : kSplitTile;
+  const int t0 = blockIdx.x * TT;
   const int b0 = blockIdx.y * BT;
   const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+  const int p0 = WIDE ? t0 + warp * kWarpPos : t0;  // this warp's first position
 
-  stage_tile<T, BT>(xs, in, b0, B, in_w, cols);
-
-  // The CTA's diagonal list as up to two ranges of the ascending active list.
-  int lo1 = 0, hi1 = n_act, lo2 = 0, hi2 = 0;
-  if (!GATHER && L + kTile - 1 < C) {
-    // (r - o) mod C < L for some r in [t0, t0+128)  <=>  o in cyclic [t0-L+1, t0+127]
-    const int lo = t0 - L + 1, hi = t0 + kTile - 1;
-    if (lo < 0) {
-      lo1 = lower_bound_i32(active, n_act, lo + C); hi1 = n_act;
-      hi2 = lower_bound_i32(active, n_act, hi + 1);
-    } else if (hi >= C) {
-      lo1 = lower_bound_i32(active, n_act, lo); hi1 = n_act;
-      hi2 = lower_bound_i32(active, n_act, hi - C + 1);
-    } else {
-      lo1 = lower_bound_i32(active, n_act, lo); hi1 = lower_bound_i32(active, n_act, hi + 1);
-    }
-  }
-  const int len1 = hi1 - lo1, total = len1 + (hi2 - lo2);
-  // split z of nsplit takes a contiguous chunk of the virtual list
-  const int per = (total + nsplit - 1) / nsplit;
-  const int vb = min(total, (int)blockIdx.z * per), ve = min(total, vb + per);
+  if (bulk && threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
+  stage_rows<T>(xs, rs, in, b0, BT, B, in_w, halo, bulk != 0, bar);
+
+  int lo1, hi1, lo2, hi2;
+  if (GATHER) { lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0; }
+  else scatter_ranges(active, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
+  const int len1 = hi1 - lo1, total = len1 + (hi2 - lo2);
+  int vb, stride, nq;
+  if (WIDE) {
+    vb = 0; stride = 1;
+    nq = p0 < out_w ? total : 0;
+  } else {
+    const int per = (total + nsplit - 1) / nsplit;
+    const int cb = min(total, (int)blockIdx.z * per), ce = min(total, cb + per);
+    vb = cb + warp; stride = kWarps;
+    nq = ce - vb > 0 ? (ce - vb + kWarps - 1) / kWarps : 0;
+  }
+  __syncthreads();
+  if (bulk) mbar_wait(bar, 0);
 
   A acc[BT][kU];
 #pragma unroll
@@ -121,27 +160,25 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T
 #pragma unroll
     for (int u = 0; u < kU; ++u) acc[b][u] = A(0);
 
-  // warp-strided walk of [vb, ve): v = vb + warp + kWarps * q
-  const int nq = ve - vb - warp > 0 ? (ve - vb - warp + kWarps - 1) / kWarps : 0;
   int o_cache = 0;
   A s_cache = A(0);
   auto fill = [&](int q0) {
-    const int v = vb + warp + kWarps * (q0 + lane);
     if (q0 + lane < nq) {
+      const int v = vb + stride * (q0 + lane);
       const int j = v < len1 ? lo1 + v : lo2 + (v - len1);
       o_cache = active[j];
       s_cache = asoft ? (A)asoft[o_cache] : A(1);
     }
   };
   auto fetch = [&](int o, A s, A (&vv)[kU], int (&ci)[kU]) {
+    int base = o + p0;
+    base = base >= C ? base - C : base;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int p = t0 + lane + kWarp * u;
+      const int p = p0 + lane + kWarp * u;
       if (GATHER) {
         const bool ok = p < L;
         vv[u] = ok ? s * (A)__ldg(vals + (size_t)o * L + p) : A(0);
-        int base = o + t0;
-        base = base >= C ? base - C : base;
         ci[u] = base + lane + kWarp * u;
       } else {
         int c = p - o;
@@ -158,42 +195,51 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T
   for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u] = A(0); ccur[u] = cnxt[u] = 0; }
   if (nq > 0) {
     fill(0);
-    const int o = __shfl_sync(0xffffffffu, o_cache, 0);
-    const A s = __shfl_sync(0xffffffffu, s_cache, 0);
-    fetch(o, s, vcur, ccur);
+    fetch(__shfl_sync(0xffffffffu, o_cache, 0), __shfl_sync(0xffffffffu, s_cache, 0), vcur, ccur);
   }
   for (int q = 0; q < nq; ++q) {
     if (q + 1 < nq) {
-      if (((q + 1) & (kWarp - 1)) == 0) fill(q + 1);
-      const int o = __shfl_sync(0xffffffffu, o_cache, (q + 1) & (kWarp - 1));
-      const A s = __shfl_sync(0xffffffffu, s_cache, (q + 1) & (kWarp - 1));
-      fetch(o, s, vnxt, cnxt);
+      const int qn = q + 1;
+      if ((qn & (kWarp - 1)) == 0) fill(qn);
+      fetch(__shfl_sync(0xffffffffu, o_cache, qn & (kWarp - 1)),
+            __shfl_sync(0xffffffffu, s_cache, qn & (kWarp - 1)), vnxt, cnxt);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      A xv[BT];
-      load_col<T, BT, A>(xs + (size_t)ccur[u] * BT, xv);
+      const T* xp = xs + ccur[u];
 #pragma unroll
-      for (int b = 0; b < BT; ++b) acc[b][u] = fma(vcur[u], xv[b], acc[b][u]);
+      for (int b = 0; b < BT; ++b) acc[b][u] = fma(vcur[u], to_acc<A>(xp[(size_t)b * rs]), acc[b][u]);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u]; ccur[u] = cnxt[u]; }
   }
 
-  // fixed-order cross-warp reduction
+  if (WIDE) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = p0 + lane + kWarp * u;
+      if (p >= out_w) continue;
+      const A bb = bias ? (A)bias[p] : A(0);
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+        if (b0 + b < B) out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(acc[b][u] + bb);
+    }
+    return;
+  }
+  // SPLIT: fixed-order cross-warp reduction through shared memory
   __syncthreads();
 #pragma unroll
   for (int b = 0; b < BT; ++b)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) red[((size_t)warp * BT + b) * kTile + lane + kWarp * u] = acc[b][u];
+    for (int u = 0; u < kU; ++u) red[((size_t)warp * BT + b) * kWarpPos + lane + kWarp * u] = acc[b][u];
   __syncthreads();
-  for (int i = threadIdx.x; i < BT * kTile; i += kThreads) {
-    const int b = i / kTile, tt = i - b * kTile;
+  for (int i = threadIdx.x; i < BT * kWarpPos; i += kThreads) {
+    const int b = i / kWarpPos, tt = i - b * kWarpPos;
     const int p = t0 + tt;
     if (b0 + b >= B || p >= out_w) continue;
     A s = A(0);
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[((size_t)w * BT + b) * kTile + tt];
+    for (int w = 0; w < kWarps; ++w) s += red[((size_t)w * BT + b) * kWarpPos + tt];
     if (nsplit == 1) {
       if (bias) s += (A)bias[p];
       out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
@@ -219,94 +265,169 @@ k_split_reduce(int B, int out_w, int nsplit, const typename Traits<T>::A* __rest
 }
 
 // --------------------------------------------------------------------------- K3
-// CTA: 128 positions x (kWarps * JQ) diagonals x one batch part; walks its rows in
-// chunks of RB staged column-major in smem: the Aop window the tile's diagonals
-// read (offsets ascend, so a tile of consecutive diagonals reads one short
-// circular window of each row) and the Bop columns of the tile.
-template <typename T, int RB, int JQ>
-__global__ void __launch_bounds__(kThreads, 2)
+constexpr int kDwPosWarps = 2;                         // warps along positions
+constexpr int kDwTile = kDwPosWarps * kWarpPos;        // 256 positions per CTA
+constexpr int kDwGroups = kWarps / kDwPosWarps;        // 4 diagonal groups
+template <typename T> struct DwRows;
+template <> struct DwRows<double> { static constexpr int RB = 4; };
+template <> struct DwRows<float> { static constexpr int RB = 4; };
+template <> struct DwRows<__nv_bfloat16> { static constexpr int RB = 8; };
+constexpr int kJW = 16;                                // diagonals per warp
+constexpr int kDwJ = kDwGroups * kJW;                  // 64 diagonals per CTA
+
+struct DwStage {  // per-stage layout offsets (bytes, from the stage base)
+  int a_off, b_off, bytes;
+};
+
+template <typename T>
+__host__ __device__ inline DwStage dw_stage(int win_cap) {
+  constexpr int RB = DwRows<T>::RB;
+  DwStage s;
+  s.a_off = 0;
+  s.b_off = (int)align16((size_t)RB * row_stride<T>(win_cap) * sizeof(T));
+  s.bytes = s.b_off + (int)align16((size_t)RB * kDwTile * sizeof(T));
+  return s;
+}
+
+// CTA: kDwTile positions x kDwJ diagonals x one batch part.  Warp w: positions
+// t0 + (w % 2)*128 + lane + 32u, diagonals j0 + (w / 2)*kJW + q.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
 k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
      const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act, int win_cap,
-     int rows_per_part, typename Traits<T>::A* __restrict__ partial) {
+     int rows_per_part, typename Traits<T>::A* __restrict__ partial, int bulk) {
   using A = typename Traits<T>::A;
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int kJ = kWarps * JQ;
+  constexpr int RB = DwRows<T>::RB;
+  constexpr int V = 16 / sizeof(T);  // elements per 16 bytes
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 2 stages
+  unsigned char* stage_base = smem + 128;
+  const DwStage L_ = dw_stage<T>(win_cap);
   const int n_act = min(*n_act_p, max_act);
-  const int j0 = blockIdx.y * kJ;
+  const int j0 = blockIdx.y * kDwJ;
   if (j0 >= n_act) return;
-  const int nj = min(kJ, n_act - j0);
-  const int t0 = blockIdx.x * kTile;
+  const int nj = min(kDwJ, n_act - j0);
+  const int t0 = blockIdx.x * kDwTile;
   const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+  const int pw = warp % kDwPosWarps, grp = warp / kDwPosWarps;
+  const int pbase = pw * kWarpPos;
+  const int tcols = min(kDwTile, L - t0);
   const int o_first = active[j0], o_last = active[j0 + nj - 1];
-  // window of Aop columns: [ws, ws + wcols) taken circularly
-  int ws, wcols;
-  if (o_last - o_first + kTile <= win_cap) {
-    ws = o_first + t0;
-    ws = ws >= C ? ws - C : ws;
-    wcols = o_last - o_first + kTile;
-  } else {
-    ws = 0;
-    wcols = C + kTile;
-  }
-  T* as = reinterpret_cast<T*>(smem);  // wcols x RB
-  T* bs = reinterpret_cast<T*>(smem + align16((size_t)win_cap * RB * sizeof(T)));  // kTile x RB
-  // window column of (diagonal q, position u) = rel[q] + lane + 32u
-  int rel[JQ];
+  // Aop window: columns (o_first + t0) .. (o_last + t0 + kDwTile - 1), circular
+  int ws = o_first + t0;
+  ws = ws >= C ? ws - C : ws;
+  const int aws = bulk ? ws / V * V : ws;  // 16-byte aligned start for TMA
+  const int lead = ws - aws;
+  // staged columns, a whole number of 16-byte units (TMA sizes are multiples of 16 B)
+  const int wcols = (o_last - o_first + kDwTile + lead + V - 1) / V * V;
+  const bool direct = wcols > win_cap;  // window too wide for smem: read Aop from global
+  const int ars = row_stride<T>(win_cap);
+  int oq[kJW];
 #pragma unroll
-  for (int q = 0; q < JQ; ++q) {
-    const int j = j0 + warp + kWarps * q;
-    int r = 0;
-    if (j < j0 + nj) {
-      const int o = active[j];
-      if (ws == 0 && wcols == C + kTile) {
-        r = o + t0;
-        r = r >= C ? r - C : r;
-      } else {
-        r = o - o_first;  // offsets ascend inside the tile
-      }
-    }
-    rel[q] = r;
+  for (int q = 0; q < kJW; ++q) {
+    const int j = j0 + grp * kJW + q;
+    oq[q] = j < j0 + nj ? active[j] : -1;
   }
-  A acc[JQ][kU];
+  A acc[kJW][kU];
 #pragma unroll
-  for (int q = 0; q < JQ; ++q)
+  for (int q = 0; q < kJW; ++q)
 #pragma unroll
     for (int u = 0; u < kU; ++u) acc[q][u] = A(0);
 
   const int rb = blockIdx.z * rows_per_part, re = min(B, rb + rows_per_part);
-  for (int c0 = rb; c0 < re; c0 += RB) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < RB * wcols; i += kThreads) {
-      const int b = i / wcols, c = i - b * wcols;
-      int cc = ws + c;
-      while (cc >= C) cc -= C;
-      as[(size_t)c * RB + b] = (c0 + b < re) ? aop[(size_t)(c0 + b) * C + cc] : T(0);
+  const int nchunks = re > rb ? (re - rb + RB - 1) / RB : 0;
+  if (bulk && threadIdx.x == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); }
+  __syncthreads();
+
+  // issue chunk c into stage (c & 1)
+  auto issue = [&](int c) {
+    unsigned char* base = stage_base + (size_t)(c & 1) * L_.bytes;
+    T* as = reinterpret_cast<T*>(base + L_.a_off);
+    T* bs = reinterpret_cast<T*>(base + L_.b_off);
+    const int r0 = rb + c * RB;
+    const int nr = min(RB, re - r0);
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        uint32_t bytes = 0;
+        // window [aws, aws + wcols) circularly: at most two linear pieces, both
+        // multiples of V because C, aws and wcols are (wcols <= win_cap <= C)
+        const int seg1 = direct ? 0 : min(wcols, C - aws);
+        const int seg2r = direct ? 0 : wcols - seg1;
+        const int bcols = (tcols + V - 1) / V * V;
+        bytes = (uint32_t)nr * (uint32_t)((seg1 + seg2r + bcols) * sizeof(T));
+        mbar_expect_tx(&bars[c & 1], bytes);
+        for (int r = 0; r < nr; ++r) {
+          const T* arow = aop + (size_t)(r0 + r) * C;
+          if (seg1) bulk_g2s(as + (size_t)r * ars, arow + aws, (uint32_t)(seg1 * sizeof(T)), &bars[c & 1]);
+          if (seg2r) bulk_g2s(as + (size_t)r * ars + seg1, arow, (uint32_t)(seg2r * sizeof(T)), &bars[c & 1]);
+          bulk_g2s(bs + (size_t)r * kDwTile, bop + (size_t)(r0 + r) * L + t0, (uint32_t)(bcols * sizeof(T)),
+                   &bars[c & 1]);
+        }
+      }
+    } else {
+      for (int r = 0; r < RB; ++r) {
+        const bool in = r < nr;
+        if (!direct)
+          for (int i = threadIdx.x; i < wcols; i += kThreads) {
+            int cc = aws + i;
+            while (cc >= C) cc -= C;
+            as[(size_t)r * ars + i] = in ? aop[(size_t)(r0 + r) * C + cc] : T(0);
+          }
+        for (int i = threadIdx.x; i < kDwTile; i += kThreads)
+          bs[(size_t)r * kDwTile + i] = (in && i < tcols) ? bop[(size_t)(r0 + r) * L + t0 + i] : T(0);
+      }
     }
-    for (int i = threadIdx.x; i < RB * kTile; i += kThreads) {
-      const int b = i / kTile, c = i - b * kTile;
-      bs[(size_t)c * RB + b] = (c0 + b < re && t0 + c < L) ? bop[(size_t)(c0 + b) * L + t0 + c] : T(0);
-    }
-    __syncthreads();
+  };
+
+  if (nchunks > 0) issue(0);
+  for (int c = 0; c < nchunks; ++c) {
+    __syncthreads();  // stage (c+1)&1 is free (its previous chunk was consumed)
+    if (c + 1 < nchunks) issue(c + 1);
+    if (bulk) mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    else __syncthreads();
+    const unsigned char* base = stage_base + (size_t)(c & 1) * L_.bytes;
+    const T* as = reinterpret_cast<const T*>(base + L_.a_off);
+    const T* bs = reinterpret_cast<const T*>(base + L_.b_off);
+    const int r0 = rb + c * RB;
+    const int nr = min(RB, re - r0);
+#pragma unroll 1
+    for (int r = 0; r < nr; ++r) {
+      A bm[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      A bv[RB];
-      load_col<T, RB, A>(bs + (size_t)(lane + kWarp * u) * RB, bv);
+      for (int u = 0; u < kU; ++u) bm[u] = to_acc<A>(bs[(size_t)r * kDwTile + pbase + lane + kWarp * u]);
+      if (!direct) {
+        const T* arow = as + (size_t)r * ars + lead + pbase + lane;
 #pragma unroll
-      for (int q = 0; q < JQ; ++q) {
-        A av[RB];
-        load_col<T, RB, A>(as + (size_t)(rel[q] + lane + kWarp * u) * RB, av);
+        for (int q = 0; q < kJW; ++q) {
+          if (oq[q] < 0) continue;
+          const T* ap = arow + (oq[q] - o_first);
 #pragma unroll
-        for (int b = 0; b < RB; ++b) acc[q][u] = fma(av[b], bv[b], acc[q][u]);
+          for (int u = 0; u < kU; ++u) acc[q][u] = fma(to_acc<A>(ap[kWarp * u]), bm[u], acc[q][u]);
+        }
+      } else {
+        const T* arow = aop + (size_t)(r0 + r) * C;
+#pragma unroll
+        for (int q = 0; q < kJW; ++q) {
+          if (oq[q] < 0) continue;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            int col = oq[q] + t0 + pbase + lane + kWarp * u;
+            col = col >= C ? col - C : col;
+            col = col >= C ? col - C : col;
+            acc[q][u] = fma(to_acc<A>(__ldg(arow + col)), bm[u], acc[q][u]);
+          }
+        }
       }
     }
   }
 #pragma unroll
-  for (int q = 0; q < JQ; ++q) {
-    const int j = j0 + warp + kWarps * q;
-    if (j >= j0 + nj) continue;
+  for (int q = 0; q < kJW; ++q) {
+    const int j = j0 + grp * kJW + q;
+    if (oq[q] < 0) continue;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int t = t0 + lane + kWarp * u;
+      const int t = t0 + pbase + lane + kWarp * u;
       if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
     }
   }
@@ -446,71 +567,72 @@ k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ val
 }
 
 // ================================================================ host side
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 struct ProductPlan {
   int bt, gx, gy, nsplit;
+  bool wide;
   size_t smem;
 };
 
 template <typename T>
-static size_t product_smem(int bt, int cols) {
+static size_t product_smem(bool wide, int bt, int cols) {
   using A = typename Traits<T>::A;
-  const size_t tile = (size_t)bt * cols * sizeof(T);
-  const size_t red = (size_t)kWarps * bt * kTile * sizeof(A);
-  return align16(tile > red ? tile : red);
-}
-
-template <typename T>
-static void row_choices(int (&v)[3]) {
-  if (sizeof(T) == 8) { v[0] = 8; v[1] = 4; v[2] = 2; }
-  else if (sizeof(T) == 4) { v[0] = 16; v[1] = 8; v[2] = 4; }
-  else { v[0] = 16; v[1] = 8; v[2] = 8; }
+  const size_t tile = (size_t)bt * row_stride<T>(cols) * sizeof(T);
+  const size_t red = wide ? 0 : (size_t)kWarps * bt * kWarpPos * sizeof(A);
+  return 128 + align16(tile > red ? tile : red);
 }
 
 template <typename T>
 static ProductPlan plan_product(int B, int out_w, int cols, int max_act) {
   const size_t kSmem2 = 113 * 1024, kSmem1 = 220 * 1024;
   const int sms = num_sms();
-  const int gx = ceil_div(out_w, kTile);
-  int choices[3];
-  row_choices<T>(choices);
-  ProductPlan best{0, 0, 0, 1, 0};
+  // WIDE: the largest row tile whose grid still covers the SMs
+  const int wide_bt[3] = {sizeof(T) == 8 ? 8 : 16, sizeof(T) == 8 ? 4 : 8, sizeof(T) == 8 ? 2 : 4};
+  const int gxw = ceil_div(out_w, kWideTile);
   for (size_t cap : {kSmem2, kSmem1}) {
-    for (int bt : choices) {
-      const size_t sm = product_smem<T>(bt, cols);
+    for (int bt : wide_bt) {
+      const size_t sm = product_smem<T>(true, bt, cols);
       if (sm > cap) continue;
-      const int gy = ceil_div(B, bt);
-      // largest row tile that still gives every SM a CTA; else the smallest tile
-      best = {bt, gx, gy, 1, sm};
-      if ((long long)gx * gy >= sms) break;
+      const long long ctas = (long long)gxw * ceil_div(B, bt);
+      if (ctas >= sms) return {bt, gxw, ceil_div(B, bt), 1, true, sm};
     }
-    if (best.bt != 0) break;
   }
-  if (best.bt == 0) return best;
-  const long long ctas = (long long)best.gx * best.gy;
+  // SPLIT: small batches; diagonals split across warps and across CTAs
+  const int split_bt[3] = {8, 4, 1};
+  ProductPlan p{0, 0, 0, 1, false, 0};
+  for (int bt : split_bt) {
+    const size_t sm = product_smem<T>(false, bt, cols);
+    if (sm > kSmem1) continue;
+    p = {bt, ceil_div(out_w, kSplitTile), ceil_div(B, bt), 1, false, sm};
+    if (bt <= B) break;
+  }
+  if (p.bt == 0) return p;
+  const long long ctas = (long long)p.gx * p.gy;
   if (ctas < 2LL * sms) {
     const int ns = (int)ceil_div(2LL * sms, ctas);
-    const int max_ns = max_act / 32 > 1 ? max_act / 32 : 1;
-    best.nsplit = ns < max_ns ? ns : max_ns;
+    const int max_ns = max_act / 16 > 1 ? max_act / 16 : 1;
+    p.nsplit = ns < max_ns ? ns : max_ns;
   }
-  return best;
+  return p;
 }
 
-template <typename T, int BT, bool G>
+template <typename T, int BT, bool G, bool W>
 static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, int L, const T* in,
                            const typename Traits<T>::P* vals, const double* asoft, const int32_t* active,
                            const int32_t* n_act, int max_act, const typename Traits<T>::P* bias, T* out,
-                           typename Traits<T>::A* part) {
-  auto k = k_product<T, BT, G>;
+                           typename Traits<T>::A* part, int bulk) {
+  auto k = k_product<T, BT, G, W>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   k<<<dim3(p.gx, p.gy, p.nsplit), kThreads, p.smem, st>>>(B, C, L, in, vals, asoft, active, n_act, max_act,
-                                                          bias, out, part, p.nsplit);
+                                                          bias, out, part, p.nsplit, bulk);
   note_launch();
 }
 
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   using A = typename Traits<T>::A;
-  const int out_w = gather ? L : C, cols = gather ? C + kTile : L;
+  const int out_w = gather ? L : C, cols = gather ? C + kHalo : L;
   ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
   return p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0;
 }
@@ -522,30 +644,31 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   using P = typename Traits<T>::P;
   using A = typename Traits<T>::A;
   if (B == 0) return DIAGMM_OK;
-  const int out_w = gather ? L : C, cols = gather ? C + kTile : L;
+  const int out_w = gather ? L : C, in_w = gather ? C : L;
+  const int cols = in_w + (gather ? kHalo : 0);
   ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
   if (p.bt == 0) return DIAGMM_ETOOLARGE;
   if (p.nsplit > 1 && (ws == nullptr || ws_bytes < (size_t)p.nsplit * B * out_w * sizeof(A))) p.nsplit = 1;
+  const int bulk = ((size_t)in_w * sizeof(T)) % 16 == 0 && aligned16(in) && (!gather || in_w >= kHalo);
   auto tin = static_cast<const T*>(in);
   auto tv = static_cast<const P*>(vals);
   auto tb = static_cast<const P*>(bias);
   auto to = static_cast<T*>(out);
   auto part = static_cast<A*>(ws);
-#define DIAGMM_LAUNCH(BT)                                                                           \
-  if (p.bt == BT) {                                                                                 \
-    if (gather)                                                                                     \
-      launch_product<T, BT, true>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part); \
-    else                                                                                            \
-      launch_product<T, BT, false>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part); \
+#define DIAGMM_GO(BT, W)                                                                                     \
+  if (p.bt == BT && p.wide == W) {                                                                           \
+    if (gather)                                                                                              \
+      launch_product<T, BT, true, W>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, bulk);  \
+    else                                                                                                     \
+      launch_product<T, BT, false, W>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, bulk); \
   }
   if constexpr (sizeof(T) == 8) {
-    DIAGMM_LAUNCH(8) DIAGMM_LAUNCH(4) DIAGMM_LAUNCH(2)
-  } else if constexpr (sizeof(T) == 4) {
-    DIAGMM_LAUNCH(16) DIAGMM_LAUNCH(8) DIAGMM_LAUNCH(4)
+    DIAGMM_GO(8, true) DIAGMM_GO(4, true) DIAGMM_GO(2, true)
   } else {
-    DIAGMM_LAUNCH(16) DIAGMM_LAUNCH(8)
+    DIAGMM_GO(16, true) DIAGMM_GO(8, true) DIAGMM_GO(4, true)
   }
-#undef DIAGMM_LAUNCH
+  DIAGMM_GO(8, false) DIAGMM_GO(4, false) DIAGMM_GO(1, false)
+#undef DIAGMM_GO
   if (p.nsplit > 1) {
     const size_t n = (size_t)B * out_w;
     int blocks = (int)((n + 255) / 256);
@@ -556,30 +679,20 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   return status_from_cuda();
 }
 
-// dW tiling: rows per staged chunk (16-byte column loads) and diagonals per warp
-template <typename T> struct DwRows;
-template <> struct DwRows<double> { static constexpr int RB = 4; };
-template <> struct DwRows<float> { static constexpr int RB = 8; };
-template <> struct DwRows<__nv_bfloat16> { static constexpr int RB = 16; };
-constexpr int kJQ = 4;
-constexpr int kDwJ = kWarps * kJQ;
-
+// ---- dW
 template <typename T>
-static int dw_win_cap(int C) {
-  // Room for a full circular row (C + 128 columns): a tile whose offsets span
-  // more than that falls back to staging whole rows.  Up to C ~ 3300 the tiles
-  // still fit two CTAs per SM.
-  return C + kTile;
-}
-
-template <typename T>
-static size_t dw_smem(int C) {
-  constexpr int RB = DwRows<T>::RB;
-  return align16((size_t)dw_win_cap<T>(C) * RB * sizeof(T)) + (size_t)kTile * RB * sizeof(T);
+static int dw_win_cap(int C, int max_act) {
+  constexpr int V = 16 / sizeof(T);
+  const double span = max_act > 0 ? (double)kDwJ * C / max_act : (double)C;
+  int cap = (int)(kDwTile + 2.5 * span) + 2 * V;
+  cap = cap < C ? cap : C;
+  // keep two stages within the shared-memory budget
+  while (cap > kDwTile && 128 + 2 * (size_t)dw_stage<T>(cap).bytes > 200 * 1024) cap -= 64;
+  return cap;
 }
 
 static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_per_part) {
-  const long long tiles = (long long)ceil_div(L, kTile) * ceil_div(max_act > 0 ? max_act : 1, kDwJ);
+  const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwJ);
   long long p = ceil_div(2LL * num_sms(), tiles);
   if (p < 1) p = 1;
   const long long max_p = ceil_div(B, rb);
@@ -602,8 +715,8 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
   const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
   const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
   const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
-  size_t ws = dw > prod_f ? dw : prod_f;
-  return ws > prod_b ? ws : prod_b;
+  size_t w = dw > prod_f ? dw : prod_f;
+  return w > prod_b ? w : prod_b;
 }
 
 template <typename T>
@@ -613,6 +726,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   using P = typename Traits<T>::P;
   using A = typename Traits<T>::A;
   constexpr int RB = DwRows<T>::RB;
+  constexpr int V = 16 / sizeof(T);
   const int C = M > N ? M : N, L = M < N ? M : N;
   if (ws_bytes < dw_workspace<T>(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
   int parts, rpp;
@@ -622,12 +736,13 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
   if (B > 0 && max_act > 0) {
-    const size_t sm = dw_smem<T>(C);
-    if (sm > 227 * 1024) return DIAGMM_ETOOLARGE;
-    auto k = k_dw<T, RB, kJQ>;
+    const int cap = dw_win_cap<T>(C, max_act);
+    const size_t sm = 128 + 2 * (size_t)dw_stage<T>(cap).bytes;
+    const int bulk = C % V == 0 && L % V == 0 && aligned16(aop) && aligned16(bop);
+    auto k = k_dw<T>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid(ceil_div(L, kTile), ceil_div(max_act, kDwJ), parts);
-    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, dw_win_cap<T>(C), rpp, partial);
+    dim3 grid(ceil_div(L, kDwTile), ceil_div(max_act, kDwJ), parts);
+    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, bulk);
     note_launch();
   } else {
     parts = 0;
