@@ -71,9 +71,11 @@ DIAGMM_API unsigned long long diagmm_launch_count(void);
  * weight scaling of DynaDiagLayer.forward (layers.py:235) and Tape.add_bias
  * (autodiff.py:72-81).  alpha_soft == NULL means unit scale (DiagHeur /
  * frozen layers, layers.py:354-363, 301-310).  max_act is a host upper bound
- * on *n_act used only to size work (pass C when unknown).  workspace (may
- * be NULL) lets small batches split the diagonal list across CTAs; size it
- * with diagmm_forward_workspace. */
+ * on *n_act used only to size work (pass C when unknown).  workspace
+ * (REQUIRED, >= diagmm_forward_workspace bytes, 16-byte aligned) holds the
+ * compact pre-scaled weights alpha_soft[o] * values[o] of the active
+ * diagonals (the reference's `weights`, layers.py:235) and, for small
+ * batches, the partial sums of the split diagonal list. */
 DIAGMM_API size_t diagmm_forward_workspace(int dtype, int M, int N, int B,
                                            int max_act);
 DIAGMM_API int diagmm_forward(int dtype, int M, int N, int B, const void* x,
@@ -84,7 +86,7 @@ DIAGMM_API int diagmm_forward(int dtype, int M, int N, int B, const void* x,
 
 /* ---- K2: input gradient through the (never materialized) transpose -------
  * dx = dy @ W_K.  Replaces layers.py:414-418 (transpose, diagcore.py:162-191,
- * followed by the same spmm). */
+ * followed by the same spmm).  workspace: as diagmm_forward. */
 DIAGMM_API size_t diagmm_backward_input_workspace(int dtype, int M, int N,
                                                   int B, int max_act);
 DIAGMM_API int diagmm_backward_input(int dtype, int M, int N, int B, const void* dy,
@@ -122,6 +124,23 @@ DIAGMM_API int diagmm_topk_waterfill(int C, int k, double temperature, const dou
                           double* alpha_soft, uint8_t* clamped,
                           int32_t* active, int32_t* slot, int32_t* n_act,
                           void* stream);
+
+/* Batched K4: n independent selections in one launch (one CTA each), e.g.
+ * every DiagLinear layer of a model at the start of a step (the reference
+ * runs soft_topk once per layer forward, layers.py:233).  `jobs` is a HOST
+ * array; its device pointers follow the diagmm_topk_waterfill conventions. */
+typedef struct diagmm_topk_job {
+  int C, k;
+  double temperature;
+  const double* alpha;
+  double* alpha_soft;
+  uint8_t* clamped;
+  int32_t* active;
+  int32_t* slot;
+  int32_t* n_act;
+} diagmm_topk_job;
+DIAGMM_API int diagmm_topk_waterfill_batched(int n, const diagmm_topk_job* jobs,
+                                             void* stream);
 
 /* ---- K5: soft TopK gradient (+ fused l1 penalty gradient) ----------------
  * g = soft_topk_grad(alpha, k, T, g_soft) (selection.py:145-173)
@@ -167,6 +186,35 @@ DIAGMM_API int diagmm_sumsq(int dtype, size_t n, const void* x, double* out,
                  double* scratch, void* stream);
 DIAGMM_API int diagmm_clip_scale(int n, const double* partial, double max_norm,
                       double* norm, double* scale, void* stream);
+
+/* Multi-tensor K6: one launch per <= 40 tensors instead of one per tensor.
+ * diagmm_tensor describes one parameter: dtype DIAGMM_F64 or DIAGMM_F32 for
+ * param/grad/m/v alike, its element count, its own weight decay (0 for the
+ * reference's no-decay ParamSpecs, layers.py:259-266) and its 1-based step.
+ * `tensors` is a HOST array of device pointers.
+ *   diagmm_adamw_multi: adamw_step (training.py:346-358) on every tensor,
+ *     gradients scaled by *clip_scale when non-NULL.
+ *   diagmm_sumsq_multi: per-chunk sum(grad^2) (float64, fixed order) into
+ *     partial[0 .. diagmm_sumsq_multi_len(n, tensors)); fold them with
+ *     diagmm_clip_scale_tree (clip_global_norm, training.py:406-417). */
+typedef struct diagmm_tensor {
+  int dtype;
+  int step;
+  size_t n;
+  void* param;
+  const void* grad;
+  void* m;
+  void* v;
+  double weight_decay;
+} diagmm_tensor;
+DIAGMM_API int diagmm_adamw_multi(int n, const diagmm_tensor* tensors, double lr,
+                                  double beta1, double beta2, double eps,
+                                  const double* clip_scale, void* stream);
+DIAGMM_API int diagmm_sumsq_multi_len(int n, const diagmm_tensor* tensors);
+DIAGMM_API int diagmm_sumsq_multi(int n, const diagmm_tensor* tensors, double* partial,
+                                  int partial_len, void* stream);
+DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_norm,
+                                      double* norm, double* scale, void* stream);
 
 /* ---- dense-equivalent route (reference's own BLAS switch) ---------------
  * The reference multiplies the materialized matrix with BLAS when the

@@ -41,6 +41,7 @@ from .layer import (  # noqa: F401
     ParamSpec,
     diagheur_update,
     penalties,
+    preselect,
 )
 from .optim import AdamW, GlobalNormClipper, lr_at, model_param_specs  # noqa: F401
 

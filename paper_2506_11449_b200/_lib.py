@@ -43,6 +43,28 @@ SIGNATURES = {
     "diagmm_gather_dense_grad": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
+
+
+class TopkJob(C.Structure):
+    """diagmm_topk_job (include/diagmm.h)."""
+
+    _fields_ = [("C", C.c_int), ("k", C.c_int), ("temperature", C.c_double), ("alpha", _vp),
+                ("alpha_soft", _vp), ("clamped", _vp), ("active", _vp), ("slot", _vp), ("n_act", _vp)]
+
+
+class TensorDesc(C.Structure):
+    """diagmm_tensor (include/diagmm.h)."""
+
+    _fields_ = [("dtype", C.c_int), ("step", C.c_int), ("n", C.c_size_t), ("param", _vp), ("grad", _vp),
+                ("m", _vp), ("v", _vp), ("weight_decay", C.c_double)]
+
+
+SIGNATURES["diagmm_topk_waterfill_batched"] = (_i, [_i, C.POINTER(TopkJob), _vp])
+SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp])
+SIGNATURES["diagmm_sumsq_multi_len"] = (_i, [_i, C.POINTER(TensorDesc)])
+SIGNATURES["diagmm_sumsq_multi"] = (_i, [_i, C.POINTER(TensorDesc), _vp, _i, _vp])
+SIGNATURES["diagmm_clip_scale_tree"] = (_i, [_i, _vp, _d, _vp, _vp, _vp])
+
 _LIB = None
 
 

@@ -21,6 +21,7 @@ int run_gather_dense(int, int, const void*, const void*, const double*, const in
                      void*, double*, cudaStream_t);
 int run_waterfill(int, int, double, const double*, double*, uint8_t*, int32_t*, int32_t*, int32_t*,
                   cudaStream_t);
+int run_waterfill_batched(int, const diagmm_topk_job*, cudaStream_t);
 int run_select_hard(int, int, const double*, int32_t*, cudaStream_t);
 int run_active_from_list(int, int, const int32_t*, int32_t*, int32_t*, cudaStream_t);
 int run_topk_grad(int, int, double, const double*, const uint8_t*, const double*, double, double*, int,
@@ -30,6 +31,10 @@ int run_adamw(size_t, void*, const void*, void*, void*, int, double, double, dou
               const double*, cudaStream_t);
 template <typename P> int run_sumsq(size_t, const void*, double*, double*, cudaStream_t);
 int run_clip_scale(int, const double*, double, double*, double*, cudaStream_t);
+int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, const double*, cudaStream_t);
+int mt_sumsq_parts(int, const diagmm_tensor*);
+int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
+int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
 constexpr int kSumsqScratch = 296;
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
@@ -139,6 +144,26 @@ int diagmm_topk_waterfill(int C, int k, double temperature, const double* alpha,
                           uint8_t* clamped, int32_t* active, int32_t* slot, int32_t* n_act,
                           void* stream) {
   return run_waterfill(C, k, temperature, alpha, alpha_soft, clamped, active, slot, n_act, S(stream));
+}
+
+int diagmm_topk_waterfill_batched(int n, const diagmm_topk_job* jobs, void* stream) {
+  return run_waterfill_batched(n, jobs, S(stream));
+}
+
+int diagmm_adamw_multi(int n, const diagmm_tensor* tensors, double lr, double beta1, double beta2,
+                       double eps, const double* clip_scale, void* stream) {
+  return run_adamw_multi(n, tensors, lr, beta1, beta2, eps, clip_scale, S(stream));
+}
+int diagmm_sumsq_multi_len(int n, const diagmm_tensor* tensors) {
+  return n > 0 && tensors ? mt_sumsq_parts(n, tensors) : 0;
+}
+int diagmm_sumsq_multi(int n, const diagmm_tensor* tensors, double* partial, int partial_len, void* stream) {
+  return run_sumsq_multi(n, tensors, partial, partial_len, S(stream));
+}
+int diagmm_clip_scale_tree(int n, const double* partial, double max_norm, double* norm, double* scale,
+                           void* stream) {
+  if (n < 1) return DIAGMM_ESHAPE;
+  return run_clip_scale_tree(n, partial, max_norm, norm, scale, S(stream));
 }
 
 int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, const uint8_t* clamped,

@@ -4,7 +4,7 @@
 //
 // Exact math (verified against the reference):
 //   W is M x N, C = max(M,N), L = min(M,N), active offsets o_j ascending,
-//   V[j,t] = s_j * values[o_j, t]  with s_j = alpha_soft[o_j].
+//   V[j,t] = s_j * values[o_j, t]  with s_j = alpha_soft[o_j]   (layers.py:235).
 //   "gather" form  (G): out[b,t] = sum_j V[j,t] * in[b, (o_j + t) mod C],  t < L
 //        = wide forward (diagcore.py:234-237) and tall/square dX (the transpose
 //          of diagcore.py:162-191 read "by own index, +o").
@@ -13,79 +13,191 @@
 //   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:419-428)
 //        tall: Aop = dy, Bop = x;   wide: Aop = x, Bop = dy.
 //
-// B200 design (measurements in profiles/):
-//  * Staging: the gathered operand's rows are copied global->shared by the TMA
-//    engine (cp.async.bulk, one instruction per row segment, completion on an
-//    mbarrier); a circular halo of 128 columns after each row removes the
-//    per-element `mod`.  Every output tile of a 10%-dense wrap-around matrix
-//    touches almost every input column, so whole rows are staged once per CTA
-//    and reused by every diagonal.
-//  * Lanes take positions p0 + lane + 32u (u < 4): every diagonal-value load is a
-//    coalesced 128-byte warp access and every shared-memory read is
-//    bank-conflict free for any offset, wrap or alignment.
-//  * Offsets/scales of the next 32 diagonals live in a per-lane cache (shuffled
-//    out) and the values of diagonal q+1 are loaded while diagonal q is being
-//    multiplied, hiding the dependent global-load latency.
-//  * Two tilings: WIDE (large batch) — each warp owns 128 positions of a
-//    1024-position tile and walks every diagonal that can touch them, BT rows
-//    in registers, no cross-warp reduction; SPLIT (small batch) — the 8 warps
-//    (and, via grid.z, several CTAs) split the diagonal list of one 128-position
-//    tile and reduce in a fixed order (deterministic), so B = 1 fills 148 SMs.
-//  * dW: a CTA owns 256 positions x 64 consecutive diagonals; because offsets
-//    ascend, the tile reads one short circular window of each Aop row.  Row
-//    chunks stream through a two-stage TMA/mbarrier pipeline.
-//  Shared-memory delivery (128 B/clk/SM, profiles/r01_microbench_fma_lds.txt)
-//  bounds every FMA that needs a fresh gathered operand at 32 fp32 FMA/clk/SM.
+// B200 design (v4):
+//  * Every multiply needs a gathered operand at a data-dependent shift, so
+//    there is no register reuse of it: each FMA consumes one value read from
+//    shared memory, and the 128 B/clk/SM shared-memory crossbar bounds the
+//    kernels (profiles/r01_microbench_fhfma_lds.txt).  The kernels are built
+//    to sit on that bound with the fewest bytes per FMA:
+//  * Activations are staged TRANSPOSED and packed: smem column c of a row group
+//    holds VEC = 16/sizeof(T) consecutive batch rows in 16 bytes ([g][col][VEC]).
+//    One conflict-free LDS.128 then feeds VEC FMAs that share one weight, for
+//    any offset, wrap or alignment.  bf16: 8 rows per LDS.128, fp32: 4, fp64: 2.
+//  * bf16 multiplies use FHFMA.BF16 (PTX fma.rn.f32.bf16: bf16 x bf16 + fp32
+//    accumulate, halves taken straight from the packed registers — no unpack
+//    instructions); weights are pre-scaled once per call into a compact bf16
+//    store V (k_prescale, the reference's `weights = alpha_soft * values`).
+//  * Lanes own output positions p0 + lane + 32u (u < 4): weight loads are
+//    coalesced, the per-diagonal offset list is cached per lane and shuffled
+//    out, and the next diagonal's weights are prefetched.
+//  * Tilings: WIDE (many rows) — a warp owns 128 positions x (G*VEC) rows and
+//    walks every diagonal touching them; SPLIT (few rows) — the warps of a CTA
+//    (and several CTAs, grid.z) split the diagonal list of one 128-position
+//    tile and reduce in a fixed order (deterministic), so B = 1 fills the GPU.
+//  * dW: a CTA owns 256 positions x 64 consecutive diagonals; offsets ascend,
+//    so the tile reads one short circular window of each Aop row.  Row chunks
+//    are staged (transposed) by 8x8 register transposes; 2+ CTAs per SM
+//    overlap one CTA's staging with another's FMAs.
 #include "common.cuh"
+#include <cmath>
 
 namespace diagmm {
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Weight type of the compact pre-scaled store: bf16 activations multiply with
+// bf16 weights (FHFMA.BF16, fp32 accumulate); fp32 / fp64 keep their type.
+template <typename T> struct WType { using type = T; };
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kWarpPos = 128;              // positions per warp
 constexpr int kU = kWarpPos / kWarp;       // positions per lane
-constexpr int kHalo = 128;                 // circular halo after each staged row
-constexpr int kWideTile = kWarps * kWarpPos;  // 1024 positions per WIDE CTA
-constexpr int kSplitTile = kWarpPos;          // 128 positions per SPLIT CTA
+constexpr int kHalo = 128;                 // circular halo after each staged gather row
 
-// Row stride (elements) of a staged tile holding `cols` columns: 16-byte multiple.
-template <typename T>
-__host__ __device__ inline int row_stride(int cols) {
-  constexpr int v = 16 / sizeof(T);
-  return (cols + v - 1) / v * v;
+template <typename T> __host__ __device__ constexpr int vec_rows() { return 16 / (int)sizeof(T); }
+
+// ------------------------------------------------------------------ FMA atoms
+// acc[r] += x[r] * w for the VEC rows packed in one 16-byte smem unit.
+__device__ __forceinline__ void fma_bf16_pair(float& a0, float& a1, uint32_t x, uint32_t w) {
+  asm("{\n.reg .b16 x0, x1, w0, w1;\n"
+      "mov.b32 {x0, x1}, %2;\n"
+      "mov.b32 {w0, w1}, %3;\n"
+      "fma.rn.f32.bf16 %0, x0, w0, %0;\n"
+      "fma.rn.f32.bf16 %1, x1, w0, %1;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(x), "r"(w));
+}
+__device__ __forceinline__ void fma_vec(float (&a)[8], uint4 x, uint32_t w /* bf16 in low half */) {
+  fma_bf16_pair(a[0], a[1], x.x, w);
+  fma_bf16_pair(a[2], a[3], x.y, w);
+  fma_bf16_pair(a[4], a[5], x.z, w);
+  fma_bf16_pair(a[6], a[7], x.w, w);
+}
+__device__ __forceinline__ void fma_vec(float (&a)[4], float4 x, float w) {
+  a[0] = fmaf(x.x, w, a[0]);
+  a[1] = fmaf(x.y, w, a[1]);
+  a[2] = fmaf(x.z, w, a[2]);
+  a[3] = fmaf(x.w, w, a[3]);
+}
+__device__ __forceinline__ void fma_vec(double (&a)[2], double2 x, double w) {
+  a[0] = fma(x.x, w, a[0]);
+  a[1] = fma(x.y, w, a[1]);
+}
+// dot-style: acc += sum_r a[r] * b[r] (dW: contraction over the VEC rows)
+__device__ __forceinline__ void dot_bf16_pair(float& acc, uint32_t a, uint32_t b) {
+  asm("{\n.reg .b16 a0, a1, b0, b1;\n"
+      "mov.b32 {a0, a1}, %1;\n"
+      "mov.b32 {b0, b1}, %2;\n"
+      "fma.rn.f32.bf16 %0, a0, b0, %0;\n"
+      "fma.rn.f32.bf16 %0, a1, b1, %0;\n}"
+      : "+f"(acc)
+      : "r"(a), "r"(b));
 }
 
-// Stage rows [b0, b0+nb) of a row-major (B, W) matrix into dst (row stride rs):
-// columns [0, W) followed by `halo` columns taken circularly from column 0.
-// TMA bulk copies when aligned (one elected thread), else a coalesced loop.
+template <typename T> struct Vec;  // 16-byte smem unit and accumulator shape
+template <> struct Vec<__nv_bfloat16> {
+  using U = uint4; using A = float; using W = uint32_t; static constexpr int R = 8;
+  static __device__ __forceinline__ W load_w(const __nv_bfloat16* p) {
+    return (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p));
+  }
+  static __device__ __forceinline__ void dot(A& acc, U a, U b) {
+    dot_bf16_pair(acc, a.x, b.x); dot_bf16_pair(acc, a.y, b.y);
+    dot_bf16_pair(acc, a.z, b.z); dot_bf16_pair(acc, a.w, b.w);
+  }
+};
+template <> struct Vec<float> {
+  using U = float4; using A = float; using W = float; static constexpr int R = 4;
+  static __device__ __forceinline__ W load_w(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ void dot(A& acc, U a, U b) {
+    acc = fmaf(a.x, b.x, acc); acc = fmaf(a.y, b.y, acc); acc = fmaf(a.z, b.z, acc); acc = fmaf(a.w, b.w, acc);
+  }
+};
+template <> struct Vec<double> {
+  using U = double2; using A = double; using W = double; static constexpr int R = 2;
+  static __device__ __forceinline__ W load_w(const double* p) { return __ldg(p); }
+  static __device__ __forceinline__ void dot(A& acc, U a, U b) {
+    acc = fma(a.x, b.x, acc); acc = fma(a.y, b.y, acc);
+  }
+};
+
+// ------------------------------------------------------------------ staging
+// Transposed, packed staging: dst unit (g, col) <- rows b0 + g*VEC + r (r < VEC)
+// of column src_col(col) of a row-major (B, W) source; rows >= B and columns
+// mapped to -1 are zero.  Column chunks of VEC consecutive columns are moved by
+// one VEC x VEC register transpose: VEC 16-byte loads, VEC 16-byte stores.
 template <typename T>
-__device__ __forceinline__ void stage_rows(T* __restrict__ dst, int rs, const T* __restrict__ src, int b0,
-                                           int nb, int B, int W, int halo, bool bulk, uint64_t* bar) {
-  if (bulk) {
-    if (threadIdx.x == 0) {
-      uint32_t bytes = 0;
-      const int hv = halo < W ? halo : 0;
-      for (int b = 0; b < nb && b0 + b < B; ++b) bytes += (uint32_t)((W + hv) * sizeof(T));
-      mbar_expect_tx(bar, bytes);
-      for (int b = 0; b < nb && b0 + b < B; ++b) {
-        const T* row = src + (size_t)(b0 + b) * W;
-        bulk_g2s(dst + (size_t)b * rs, row, (uint32_t)(W * sizeof(T)), bar);
-        if (hv) bulk_g2s(dst + (size_t)b * rs + W, row, (uint32_t)(hv * sizeof(T)), bar);
+__device__ __forceinline__ void transpose_store(typename Vec<T>::U (&r)[vec_rows<T>()], typename Vec<T>::U* dst,
+                                                int stride_units);
+template <>
+__device__ __forceinline__ void transpose_store<__nv_bfloat16>(uint4 (&r)[8], uint4* dst, int su) {
+  // r[i] = row i, 8 columns (4 u32 pairs).  Column j of rows (2i, 2i+1) is
+  // byte_perm of the j-th halves of r[2i] and r[2i+1].
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t* ra = reinterpret_cast<const uint32_t*>(&r[2 * i]);
+      const uint32_t* rb = reinterpret_cast<const uint32_t*>(&r[2 * i + 1]);
+      w[i] = __byte_perm(ra[j >> 1], rb[j >> 1], (j & 1) ? 0x7632 : 0x5410);
+    }
+    dst[(size_t)j * su] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+template <>
+__device__ __forceinline__ void transpose_store<float>(float4 (&r)[4], float4* dst, int su) {
+  dst[0] = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+  dst[(size_t)su] = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+  dst[(size_t)2 * su] = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
+  dst[(size_t)3 * su] = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
+}
+template <>
+__device__ __forceinline__ void transpose_store<double>(double2 (&r)[2], double2* dst, int su) {
+  dst[0] = make_double2(r[0].x, r[1].x);
+  dst[(size_t)su] = make_double2(r[0].y, r[1].y);
+}
+
+// Stage NG row groups x ncols columns (group stride ld units).  Column col
+// takes source column sc = (c0 + col) mod `mod` if sc < `limit`, else zero;
+// rows >= B are zero.  `vec_ok`: mod, limit, c0 multiples of VEC and src
+// 16-byte aligned (then every VEC-chunk is one aligned load).
+template <typename T>
+__device__ void stage_t(typename Vec<T>::U* __restrict__ dst, int ld, int ncols, const T* __restrict__ src, int B,
+                        int W, int b0, int NG, int c0, int mod, int limit, bool vec_ok) {
+  using U = typename Vec<T>::U;
+  constexpr int VEC = vec_rows<T>();
+  if (vec_ok) {
+    const int chunks = (ncols + VEC - 1) / VEC;
+    for (int it = threadIdx.x; it < NG * chunks; it += blockDim.x) {
+      const int g = it / chunks, ch = it - g * chunks;
+      const int sc = (c0 + ch * VEC) % mod;
+      const bool valid = sc < limit;
+      U r[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const int b = b0 + g * VEC + i;
+        if (valid && b < B) r[i] = *reinterpret_cast<const U*>(src + (size_t)b * W + sc);
+        else r[i] = U{};
+      }
+      U* d = dst + (size_t)g * ld + ch * VEC;
+      if (ch * VEC + VEC <= ncols) {
+        transpose_store<T>(r, d, 1);
+      } else {  // ragged last chunk: store the columns that fit
+        U tmp[VEC];
+        transpose_store<T>(r, tmp, 1);
+        for (int j = 0; ch * VEC + j < ncols; ++j) d[j] = tmp[j];
       }
     }
-    for (int b = B - b0; b < nb; ++b)  // rows past the batch: zeros
-      for (int c = threadIdx.x; c < W + halo; c += blockDim.x) dst[(size_t)b * rs + c] = T(0);
   } else {
-    for (int b = 0; b < nb; ++b) {
-      const bool in = b0 + b < B;
-      const T* row = src + (size_t)(b0 + b) * W;
-      for (int c = threadIdx.x; c < W + halo; c += blockDim.x) {
-        int cc = c;
-        while (cc >= W) cc -= W;
-        dst[(size_t)b * rs + c] = in ? row[cc] : T(0);
-      }
+    T* dd = reinterpret_cast<T*>(dst);
+    for (int it = threadIdx.x; it < NG * ncols * VEC; it += blockDim.x) {
+      const int r = it % VEC, rest = it / VEC;
+      const int col = rest % ncols, g = rest / ncols;
+      const int b = b0 + g * VEC + r;
+      const int sc = (int)(((long long)c0 + col) % mod);
+      const bool valid = b < B && sc < limit;
+      dd[((size_t)g * ld + col) * VEC + r] = valid ? src[(size_t)b * W + sc] : T(0);
     }
   }
 }
@@ -108,138 +220,186 @@ __device__ __forceinline__ void scatter_ranges(const int32_t* active, int n_act,
   }
 }
 
+// scatter-form staged width: the L real columns + zero column(s), VEC-aligned
+template <typename T>
+__host__ __device__ inline int scatter_cols(int L) {
+  constexpr int VEC = vec_rows<T>();
+  return (L + 1 + VEC - 1) / VEC * VEC;
+}
+
+// ------------------------------------------------------------------ prescale
+// The compact weight store, indexed by OUTPUT position p (< out_w) so that the
+// product kernels read it with one aligned base + immediate offsets:
+//   gather  form: w[j, p] = s_j * values[o_j, p]                       (p < L)
+//   scatter form: w[j, p] = s_j * values[o_j, c], c = (p - o_j) mod C,  0 if c >= L
+// s_j = alpha_soft[o_j] (the reference's `weights`, layers.py:235); one
+// rounding from the float64 product.  Columns [out_w, ldw) are zero.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_prescale(int C, int L, int out_w, int ldw, int gather, const typename Traits<T>::P* __restrict__ vals,
+           const double* __restrict__ asoft, const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p,
+           int max_act, typename WType<T>::type* __restrict__ w) {
+  using WT = typename WType<T>::type;
+  const int n_act = min(*n_act_p, max_act);
+  for (int j = blockIdx.y; j < n_act; j += gridDim.y) {
+    const int o = active[j];
+    const double s = asoft ? asoft[o] : 1.0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < ldw; p += gridDim.x * blockDim.x) {
+      int c = p;
+      if (!gather) { c = p - o; c = c < 0 ? c + C : c; }
+      const double v = (p < out_w && c < L) ? s * (double)vals[(size_t)o * L + c] : 0.0;
+      if constexpr (sizeof(WT) == 2) w[(size_t)j * ldw + p] = __double2bfloat16(v);
+      else w[(size_t)j * ldw + p] = (WT)v;
+    }
+  }
+}
+
 // --------------------------------------------------------------------------- K1/K2
-// GATHER: out width L (positions t), in width C, staged columns C + halo.
-// !GATHER: out width C (positions r), in width L, staged columns L.
-template <typename T, int BT, bool GATHER, bool WIDE>
+// Both forms as one gather over output positions p (< out_w):
+//   out[b, p] = sum_j w[j, p] * in[b, (p + shift_j) mod C]
+// shift_j = o_j (gather form) or C - o_j (scatter form); weights are zero
+// wherever the reference has no entry.  Gather form: the staged row is C +
+// halo columns, so the inner loop has no mask or modulo at all.  Scatter form:
+// the staged row is the L real columns plus zero columns; an index c >= L
+// (no entry) is clamped onto a zero column (one IMNMX per position).
+// A CTA is PW position-warps x DW = 8/PW diagonal-warps: it covers 128*PW
+// positions x G*VEC rows; the DW warps of a position block (and nsplit CTAs,
+// grid.z) take interleaved slices of its diagonal list and are folded in a
+// fixed order (deterministic).  PW = 8 is the pure position tiling (large
+// batches), PW = 1 with nsplit > 1 the pure diagonal split (B = 1).
+template <typename T, int G, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 2)
-k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
-          const double* __restrict__ asoft, const int32_t* __restrict__ active,
-          const int32_t* __restrict__ n_act_p, int max_act, const typename Traits<T>::P* __restrict__ bias,
-          T* __restrict__ out, typename Traits<T>::A* __restrict__ part, int nsplit, int bulk) {
-  using A = typename Traits<T>::A;
+k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>::type* __restrict__ wts, int ldw,
+          const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+          const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out, typename Vec<T>::A* __restrict__ part,
+          int PW, int nsplit, int vec_ok) {
+  using U = typename Vec<T>::U;
+  using A = typename Vec<T>::A;
+  using Wt = typename Vec<T>::W;
+  constexpr int VEC = vec_rows<T>();
+  constexpr int RT = G * VEC;  // rows per CTA
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  T* xs = reinterpret_cast<T*>(smem + 128);
-  A* red = reinterpret_cast<A*>(smem + 128);  // SPLIT: reused after the main loop
+  U* xs = reinterpret_cast<U*>(smem);
+  A* red = reinterpret_cast<A*>(smem);  // reused after the main loop
   const int n_act = min(*n_act_p, max_act);
   const int in_w = GATHER ? C : L;
   const int out_w = GATHER ? L : C;
-  const int halo = GATHER ? kHalo : 0;
-  const int rs = row_stride<T>(in_w + halo);
-  constexpr int TT = WIDE ? kWideTile : kSplitTile;
-  const int t0 = blockIdx.x * TT;
-  const int b0 = blockIdx.y * BT;
+  const int cols = GATHER ? C + kHalo : scatter_cols<T>(L);
+  const int DW = kWarps / PW;
+  const int t0 = blockIdx.x * PW * kWarpPos;
+  const int b0 = blockIdx.y * RT;
   const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
-  const int p0 = WIDE ? t0 + warp * kWarpPos : t0;  // this warp's first position
+  const int pw = warp % PW, dw = warp / PW;
+  const int p0 = t0 + pw * kWarpPos;  // this warp's first position
 
-  if (bulk && threadIdx.x == 0) mbar_init(bar, 1);
-  __syncthreads();
-  stage_rows<T>(xs, rs, in, b0, BT, B, in_w, halo, bulk != 0, bar);
+  stage_t<T>(xs, cols, cols, in, B, in_w, b0, G, 0, GATHER ? C : 0x7fffffff, in_w, vec_ok != 0);
 
   int lo1, hi1, lo2, hi2;
   if (GATHER) { lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0; }
   else scatter_ranges(active, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
-  const int len1 = hi1 - lo1, total = len1 + (hi2 - lo2);
-  int vb, stride, nq;
-  if (WIDE) {
-    vb = 0; stride = 1;
-    nq = p0 < out_w ? total : 0;
-  } else {
-    const int per = (total + nsplit - 1) / nsplit;
-    const int cb = min(total, (int)blockIdx.z * per), ce = min(total, cb + per);
-    vb = cb + warp; stride = kWarps;
-    nq = ce - vb > 0 ? (ce - vb + kWarps - 1) / kWarps : 0;
-  }
+  const int len1 = hi1 - lo1;
+  const int total = p0 < out_w ? len1 + (hi2 - lo2) : 0;
+  const int per = (total + nsplit - 1) / nsplit;
+  const int cb = min(total, (int)blockIdx.z * per), ce = min(total, cb + per);
+  const int vb = cb + dw;
+  const int nq = ce - vb > 0 ? (ce - vb + DW - 1) / DW : 0;
+  bool pok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) pok[u] = p0 + lane + kWarp * u < out_w;
   __syncthreads();
-  if (bulk) mbar_wait(bar, 0);
 
-  A acc[BT][kU];
+  A acc[G][kU][VEC];
 #pragma unroll
-  for (int b = 0; b < BT; ++b)
+  for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) acc[b][u] = A(0);
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int r = 0; r < VEC; ++r) acc[g][u][r] = A(0);
 
-  int o_cache = 0;
-  A s_cache = A(0);
-  auto fill = [&](int q0) {
-    if (q0 + lane < nq) {
-      const int v = vb + stride * (q0 + lane);
+  // Diagonal q+D is fetched (weights + staged-row index) while diagonal q is
+  // multiplied: a D-deep register ring hides the L2 latency of the weights.
+  auto fetch = [&](int q, Wt (&wv)[kU], int& ci) {
+    if (q < nq) {
+      const int v = vb + DW * q;
       const int j = v < len1 ? lo1 + v : lo2 + (v - len1);
-      o_cache = active[j];
-      s_cache = asoft ? (A)asoft[o_cache] : A(1);
+      const int o = __ldg(active + j);
+      const int base = p0 + lane + (GATHER ? o : C - o);
+      ci = base >= C ? base - C : base;  // < C
+      const typename WType<T>::type* wr = wts + (size_t)j * ldw + p0 + lane;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) wv[u] = pok[u] ? Vec<T>::load_w(wr + kWarp * u) : Wt(0);
     }
   };
-  auto fetch = [&](int o, A s, A (&vv)[kU], int (&ci)[kU]) {
-    int base = o + p0;
-    base = base >= C ? base - C : base;
+  constexpr int D = (sizeof(Wt) == 8 || RT > 8) ? 4 : 8;
+  Wt wb[D][kU];
+  int cb_[D];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int p = p0 + lane + kWarp * u;
-      if (GATHER) {
-        const bool ok = p < L;
-        vv[u] = ok ? s * (A)__ldg(vals + (size_t)o * L + p) : A(0);
-        ci[u] = base + lane + kWarp * u;
-      } else {
-        int c = p - o;
-        c = c < 0 ? c + C : c;
-        const bool ok = p < C && c < L;
-        vv[u] = ok ? s * (A)__ldg(vals + (size_t)o * L + c) : A(0);
-        ci[u] = ok ? c : 0;
-      }
-    }
-  };
-  A vcur[kU], vnxt[kU];
-  int ccur[kU], cnxt[kU];
+  for (int d = 0; d < D; ++d) {
 #pragma unroll
-  for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u] = A(0); ccur[u] = cnxt[u] = 0; }
-  if (nq > 0) {
-    fill(0);
-    fetch(__shfl_sync(0xffffffffu, o_cache, 0), __shfl_sync(0xffffffffu, s_cache, 0), vcur, ccur);
+    for (int u = 0; u < kU; ++u) wb[d][u] = Wt(0);
+    cb_[d] = 0;
+    fetch(d, wb[d], cb_[d]);
   }
-  for (int q = 0; q < nq; ++q) {
-    if (q + 1 < nq) {
-      const int qn = q + 1;
-      if ((qn & (kWarp - 1)) == 0) fill(qn);
-      fetch(__shfl_sync(0xffffffffu, o_cache, qn & (kWarp - 1)),
-            __shfl_sync(0xffffffffu, s_cache, qn & (kWarp - 1)), vnxt, cnxt);
+  for (int q0 = 0; q0 < nq; q0 += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (q0 + d < nq) {  // warp-uniform
+        if (GATHER) {
+          const U* xr = xs + cb_[d];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xr[(size_t)g * cols + kWarp * u], wb[d][u]);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            int c = cb_[d] + kWarp * u;
+            c = c >= C ? c - C : c;
+            c = c < L ? c : L;  // column L is zero
+#pragma unroll
+            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xs[(size_t)g * cols + c], wb[d][u]);
+          }
+        }
+      }
+      fetch(q0 + d + D, wb[d], cb_[d]);
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const T* xp = xs + ccur[u];
-#pragma unroll
-      for (int b = 0; b < BT; ++b) acc[b][u] = fma(vcur[u], to_acc<A>(xp[(size_t)b * rs]), acc[b][u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) { vcur[u] = vnxt[u]; ccur[u] = cnxt[u]; }
   }
 
-  if (WIDE) {
+  if (DW == 1 && nsplit == 1) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int p = p0 + lane + kWarp * u;
       if (p >= out_w) continue;
       const A bb = bias ? (A)bias[p] : A(0);
 #pragma unroll
-      for (int b = 0; b < BT; ++b)
-        if (b0 + b < B) out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(acc[b][u] + bb);
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int r = 0; r < VEC; ++r) {
+          const int b = b0 + g * VEC + r;
+          if (b < B) out[(size_t)b * out_w + p] = from_acc<T>(acc[g][u][r] + bb);
+        }
     }
     return;
   }
-  // SPLIT: fixed-order cross-warp reduction through shared memory
+  // fixed-order fold of the DW diagonal slices through shared memory:
+  // red[dw][row][pos] with pos over the CTA's PW*128 positions
+  const int TT = PW * kWarpPos;
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < BT; ++b)
+  for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) red[((size_t)warp * BT + b) * kWarpPos + lane + kWarp * u] = acc[b][u];
+    for (int r = 0; r < VEC; ++r)
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        red[((size_t)dw * RT + g * VEC + r) * TT + pw * kWarpPos + lane + kWarp * u] = acc[g][u][r];
   __syncthreads();
-  for (int i = threadIdx.x; i < BT * kWarpPos; i += kThreads) {
-    const int b = i / kWarpPos, tt = i - b * kWarpPos;
+  for (int i = threadIdx.x; i < RT * TT; i += kThreads) {
+    const int b = i / TT, tt = i - b * TT;
     const int p = t0 + tt;
     if (b0 + b >= B || p >= out_w) continue;
     A s = A(0);
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[((size_t)w * BT + b) * kWarpPos + tt];
+    for (int w = 0; w < DW; ++w) s += red[((size_t)w * RT + b) * TT + tt];
     if (nsplit == 1) {
       if (bias) s += (A)bias[p];
       out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
@@ -252,9 +412,9 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename Traits<T
 // Fixed-order sum of the split partials (+ bias).
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_split_reduce(int B, int out_w, int nsplit, const typename Traits<T>::A* __restrict__ part,
+k_split_reduce(int B, int out_w, int nsplit, const typename Vec<T>::A* __restrict__ part,
                const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out) {
-  using A = typename Traits<T>::A;
+  using A = typename Vec<T>::A;
   const size_t n = (size_t)B * out_w;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     A s = A(0);
@@ -268,168 +428,139 @@ k_split_reduce(int B, int out_w, int nsplit, const typename Traits<T>::A* __rest
 constexpr int kDwPosWarps = 2;                         // warps along positions
 constexpr int kDwTile = kDwPosWarps * kWarpPos;        // 256 positions per CTA
 constexpr int kDwGroups = kWarps / kDwPosWarps;        // 4 diagonal groups
-template <typename T> struct DwRows;
-template <> struct DwRows<double> { static constexpr int RB = 4; };
-template <> struct DwRows<float> { static constexpr int RB = 4; };
-template <> struct DwRows<__nv_bfloat16> { static constexpr int RB = 8; };
-constexpr int kJW = 16;                                // diagonals per warp
-constexpr int kDwJ = kDwGroups * kJW;                  // 64 diagonals per CTA
-
-struct DwStage {  // per-stage layout offsets (bytes, from the stage base)
-  int a_off, b_off, bytes;
-};
+constexpr int kJWMax = 16;                             // diagonals per warp (16, or 8 for small problems)
+constexpr int kDwNG = 2;                               // row groups per staged chunk
 
 template <typename T>
-__host__ __device__ inline DwStage dw_stage(int win_cap) {
-  constexpr int RB = DwRows<T>::RB;
-  DwStage s;
-  s.a_off = 0;
-  s.b_off = (int)align16((size_t)RB * row_stride<T>(win_cap) * sizeof(T));
-  s.bytes = s.b_off + (int)align16((size_t)RB * kDwTile * sizeof(T));
-  return s;
+__host__ __device__ inline size_t dw_smem(int win_cap) {
+  return (size_t)kDwNG * (win_cap + kDwTile) * 16;
 }
 
-// CTA: kDwTile positions x kDwJ diagonals x one batch part.  Warp w: positions
-// t0 + (w % 2)*128 + lane + 32u, diagonals j0 + (w / 2)*kJW + q.
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+// CTA: kDwTile positions x 4*JW diagonals x one row part.  Warp w: positions
+// t0 + (w % 2)*128 + lane + 32u, diagonals j0 + (w / 2)*JW + q.
+template <typename T, int JW>
+__global__ void __launch_bounds__(kThreads, 2)
 k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
      const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act, int win_cap,
-     int rows_per_part, typename Traits<T>::A* __restrict__ partial, int bulk) {
-  using A = typename Traits<T>::A;
-  constexpr int RB = DwRows<T>::RB;
-  constexpr int V = 16 / sizeof(T);  // elements per 16 bytes
+     int rows_per_part, typename Vec<T>::A* __restrict__ partial, int* __restrict__ tile_ctr, int vec_ok) {
+  using U = typename Vec<T>::U;
+  using A = typename Vec<T>::A;
+  constexpr int VEC = vec_rows<T>();
+  constexpr int RB = kDwNG * VEC;  // rows per staged chunk
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 2 stages
-  unsigned char* stage_base = smem + 128;
-  const DwStage L_ = dw_stage<T>(win_cap);
   const int n_act = min(*n_act_p, max_act);
-  const int j0 = blockIdx.y * kDwJ;
+  const int j0 = blockIdx.y * (kDwGroups * JW);
   if (j0 >= n_act) return;
-  const int nj = min(kDwJ, n_act - j0);
+  const int nj = min((kDwGroups * JW), n_act - j0);
   const int t0 = blockIdx.x * kDwTile;
   const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
   const int pw = warp % kDwPosWarps, grp = warp / kDwPosWarps;
   const int pbase = pw * kWarpPos;
-  const int tcols = min(kDwTile, L - t0);
   const int o_first = active[j0], o_last = active[j0 + nj - 1];
   // Aop window: columns (o_first + t0) .. (o_last + t0 + kDwTile - 1), circular
   int ws = o_first + t0;
   ws = ws >= C ? ws - C : ws;
-  const int aws = bulk ? ws / V * V : ws;  // 16-byte aligned start for TMA
+  const int aws = vec_ok ? ws / VEC * VEC : ws;  // VEC-aligned start for 16-byte loads
   const int lead = ws - aws;
-  // staged columns, a whole number of 16-byte units (TMA sizes are multiples of 16 B)
-  const int wcols = (o_last - o_first + kDwTile + lead + V - 1) / V * V;
+  const int wcols = o_last - o_first + kDwTile + lead;
   const bool direct = wcols > win_cap;  // window too wide for smem: read Aop from global
-  const int ars = row_stride<T>(win_cap);
-  int oq[kJW];
+  U* as = reinterpret_cast<U*>(smem);
+  U* bs = as + (size_t)kDwNG * win_cap;
+  int oq[JW];
 #pragma unroll
-  for (int q = 0; q < kJW; ++q) {
-    const int j = j0 + grp * kJW + q;
-    oq[q] = j < j0 + nj ? active[j] : -1;
+  for (int q = 0; q < JW; ++q) {
+    const int j = j0 + grp * JW + q;
+    oq[q] = j < j0 + nj ? active[j] - o_first : -1;
   }
-  A acc[kJW][kU];
+  A acc[JW][kU];
 #pragma unroll
-  for (int q = 0; q < kJW; ++q)
+  for (int q = 0; q < JW; ++q)
 #pragma unroll
     for (int u = 0; u < kU; ++u) acc[q][u] = A(0);
 
   const int rb = blockIdx.z * rows_per_part, re = min(B, rb + rows_per_part);
-  const int nchunks = re > rb ? (re - rb + RB - 1) / RB : 0;
-  if (bulk && threadIdx.x == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); }
-  __syncthreads();
-
-  // issue chunk c into stage (c & 1)
-  auto issue = [&](int c) {
-    unsigned char* base = stage_base + (size_t)(c & 1) * L_.bytes;
-    T* as = reinterpret_cast<T*>(base + L_.a_off);
-    T* bs = reinterpret_cast<T*>(base + L_.b_off);
-    const int r0 = rb + c * RB;
-    const int nr = min(RB, re - r0);
-    if (bulk) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        uint32_t bytes = 0;
-        // window [aws, aws + wcols) circularly: at most two linear pieces, both
-        // multiples of V because C, aws and wcols are (wcols <= win_cap <= C)
-        const int seg1 = direct ? 0 : min(wcols, C - aws);
-        const int seg2r = direct ? 0 : wcols - seg1;
-        const int bcols = (tcols + V - 1) / V * V;
-        bytes = (uint32_t)nr * (uint32_t)((seg1 + seg2r + bcols) * sizeof(T));
-        mbar_expect_tx(&bars[c & 1], bytes);
-        for (int r = 0; r < nr; ++r) {
-          const T* arow = aop + (size_t)(r0 + r) * C;
-          if (seg1) bulk_g2s(as + (size_t)r * ars, arow + aws, (uint32_t)(seg1 * sizeof(T)), &bars[c & 1]);
-          if (seg2r) bulk_g2s(as + (size_t)r * ars + seg1, arow, (uint32_t)(seg2r * sizeof(T)), &bars[c & 1]);
-          bulk_g2s(bs + (size_t)r * kDwTile, bop + (size_t)(r0 + r) * L + t0, (uint32_t)(bcols * sizeof(T)),
-                   &bars[c & 1]);
-        }
-      }
-    } else {
-      for (int r = 0; r < RB; ++r) {
-        const bool in = r < nr;
-        if (!direct)
-          for (int i = threadIdx.x; i < wcols; i += kThreads) {
-            int cc = aws + i;
-            while (cc >= C) cc -= C;
-            as[(size_t)r * ars + i] = in ? aop[(size_t)(r0 + r) * C + cc] : T(0);
-          }
-        for (int i = threadIdx.x; i < kDwTile; i += kThreads)
-          bs[(size_t)r * kDwTile + i] = (in && i < tcols) ? bop[(size_t)(r0 + r) * L + t0 + i] : T(0);
-      }
-    }
-  };
-
-  if (nchunks > 0) issue(0);
-  for (int c = 0; c < nchunks; ++c) {
-    __syncthreads();  // stage (c+1)&1 is free (its previous chunk was consumed)
-    if (c + 1 < nchunks) issue(c + 1);
-    if (bulk) mbar_wait(&bars[c & 1], (c >> 1) & 1);
-    else __syncthreads();
-    const unsigned char* base = stage_base + (size_t)(c & 1) * L_.bytes;
-    const T* as = reinterpret_cast<const T*>(base + L_.a_off);
-    const T* bs = reinterpret_cast<const T*>(base + L_.b_off);
-    const int r0 = rb + c * RB;
-    const int nr = min(RB, re - r0);
-#pragma unroll 1
-    for (int r = 0; r < nr; ++r) {
-      A bm[kU];
+  for (int r0 = rb; r0 < re; r0 += RB) {
+    __syncthreads();  // previous chunk consumed
+    if (!direct) stage_t<T>(as, win_cap, wcols, aop, re, C, r0, kDwNG, aws, C, C, vec_ok != 0);
+    stage_t<T>(bs, kDwTile, kDwTile, bop, re, L, r0, kDwNG, t0, 0x7fffffff, L, vec_ok != 0);
+    __syncthreads();
 #pragma unroll
-      for (int u = 0; u < kU; ++u) bm[u] = to_acc<A>(bs[(size_t)r * kDwTile + pbase + lane + kWarp * u]);
+    for (int g = 0; g < kDwNG; ++g) {
+      U bm[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) bm[u] = bs[(size_t)g * kDwTile + pbase + lane + kWarp * u];
       if (!direct) {
-        const T* arow = as + (size_t)r * ars + lead + pbase + lane;
+        const U* arow = as + (size_t)g * win_cap + lead + pbase + lane;
 #pragma unroll
-        for (int q = 0; q < kJW; ++q) {
+        for (int q = 0; q < JW; ++q) {
           if (oq[q] < 0) continue;
-          const T* ap = arow + (oq[q] - o_first);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) acc[q][u] = fma(to_acc<A>(ap[kWarp * u]), bm[u], acc[q][u]);
+          for (int u = 0; u < kU; ++u) Vec<T>::dot(acc[q][u], arow[oq[q] + kWarp * u], bm[u]);
         }
       } else {
-        const T* arow = aop + (size_t)(r0 + r) * C;
-#pragma unroll
-        for (int q = 0; q < kJW; ++q) {
+        // gather the Aop units straight from global (rare: very spread offsets)
+#pragma unroll 1
+        for (int q = 0; q < JW; ++q) {
           if (oq[q] < 0) continue;
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
-            int col = oq[q] + t0 + pbase + lane + kWarp * u;
+            int col = oq[q] + o_first + t0 + pbase + lane + kWarp * u;
             col = col >= C ? col - C : col;
             col = col >= C ? col - C : col;
-            acc[q][u] = fma(to_acc<A>(__ldg(arow + col)), bm[u], acc[q][u]);
+            U a;
+            T* ae = reinterpret_cast<T*>(&a);
+#pragma unroll
+            for (int r = 0; r < VEC; ++r) {
+              const int b = r0 + g * VEC + r;
+              ae[r] = b < re ? aop[(size_t)b * C + col] : T(0);
+            }
+            Vec<T>::dot(acc[q][u], a, bm[u]);
           }
         }
       }
     }
   }
 #pragma unroll
-  for (int q = 0; q < kJW; ++q) {
-    const int j = j0 + grp * kJW + q;
+  for (int q = 0; q < JW; ++q) {
+    const int j = j0 + grp * JW + q;
     if (oq[q] < 0) continue;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int t = t0 + pbase + lane + kWarp * u;
       if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
     }
+  }
+  if (gridDim.z == 1) return;
+  // The last row part to finish folds all parts of this tile in a fixed order
+  // (deterministic) into part 0, so the partials only ever live in L2.
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* ctr = tile_ctr + blockIdx.y * gridDim.x + blockIdx.x;
+    const int prev = atomicAdd(ctr, 1);
+    s_last = prev == (int)gridDim.z - 1;
+    if (s_last) *ctr = 0;  // ready for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < nj * kDwTile; i += kThreads) {
+    const int jj = i / kDwTile, t = t0 + (i - jj * kDwTile);
+    if (t >= L) continue;
+    const size_t off = (size_t)(j0 + jj) * L + t;
+    const size_t zs = (size_t)max_act * L;
+    A sum = A(0);
+    int z = 0;
+    for (; z + 8 <= (int)gridDim.z; z += 8) {  // 8 loads in flight, summed in z order
+      A v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(partial + (size_t)(z + k) * zs + off);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += v[k];
+    }
+    for (; z < (int)gridDim.z; ++z) sum += __ldcg(partial + (size_t)z * zs + off);
+    partial[off] = sum;
   }
 }
 
@@ -452,12 +583,12 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // zero inactive rows, and form g_soft.
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_dw_finalize(int C, int L, int nparts, const typename Traits<T>::A* __restrict__ partial, int max_act,
+k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
               const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
               const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
               typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft) {
   using P = typename Traits<T>::P;
-  using A = typename Traits<T>::A;
+  using A = typename Vec<T>::A;
   __shared__ double red[32];
   const int i = blockIdx.x;
   const int n_act = min(*n_act_p, max_act);
@@ -486,8 +617,8 @@ k_dw_finalize(int C, int L, int nparts, const typename Traits<T>::A* __restrict_
 constexpr int kColRows = 32;
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_colsum_partial(int B, int M, const T* __restrict__ dy, typename Traits<T>::A* __restrict__ part) {
-  using A = typename Traits<T>::A;
+k_colsum_partial(int B, int M, const T* __restrict__ dy, typename Vec<T>::A* __restrict__ part) {
+  using A = typename Vec<T>::A;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= M) return;
   const int bb = blockIdx.y * kColRows, be = min(B, bb + kColRows);
@@ -497,9 +628,9 @@ k_colsum_partial(int B, int M, const T* __restrict__ dy, typename Traits<T>::A* 
 }
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_colsum_final(int M, int nparts, const typename Traits<T>::A* __restrict__ part,
+k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
                typename Traits<T>::P* __restrict__ g_bias) {
-  using A = typename Traits<T>::A;
+  using A = typename Vec<T>::A;
   __shared__ A red[8][33];
   // 32 columns per CTA, the 8 warps split the parts, fixed-order fold
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -570,71 +701,85 @@ k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ val
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 struct ProductPlan {
-  int bt, gx, gy, nsplit;
-  bool wide;
+  int g, pw, gx, gy, nsplit;
   size_t smem;
 };
 
 template <typename T>
-static size_t product_smem(bool wide, int bt, int cols) {
-  using A = typename Traits<T>::A;
-  const size_t tile = (size_t)bt * row_stride<T>(cols) * sizeof(T);
-  const size_t red = wide ? 0 : (size_t)kWarps * bt * kWarpPos * sizeof(A);
-  return 128 + align16(tile > red ? tile : red);
+static size_t product_smem(int g, int cols, int max_act) {
+  using A = typename Vec<T>::A;
+  const size_t tile = (size_t)g * cols * 16;
+  const size_t red = (size_t)kWarps * g * vec_rows<T>() * kWarpPos * sizeof(A);  // fold buffer
+  (void)max_act;
+  return align16(tile > red ? tile : red);
 }
 
 template <typename T>
+static int w_ld(int out_w) {  // leading dimension of the compact weight store (16-byte rows)
+  constexpr int e = 16 / (int)sizeof(typename WType<T>::type);
+  return (out_w + e - 1) / e * e;
+}
+
+// Tile choice: among (G row groups, PW position warps) whose grid gives at
+// least one CTA per SM, take the one with the best wave quantisation at two
+// resident CTAs per SM (ties: more rows, then more positions per CTA — less
+// staging and fewer folds).  Tiny batches split the diagonal list across CTAs.
+template <typename T>
 static ProductPlan plan_product(int B, int out_w, int cols, int max_act) {
-  const size_t kSmem2 = 113 * 1024, kSmem1 = 220 * 1024;
+  constexpr int VEC = vec_rows<T>();
+  const size_t kSmemMax = 113 * 1024;  // two CTAs per SM
   const int sms = num_sms();
-  // WIDE: the largest row tile whose grid still covers the SMs
-  const int wide_bt[3] = {sizeof(T) == 8 ? 8 : 16, sizeof(T) == 8 ? 4 : 8, sizeof(T) == 8 ? 2 : 4};
-  const int gxw = ceil_div(out_w, kWideTile);
-  for (size_t cap : {kSmem2, kSmem1}) {
-    for (int bt : wide_bt) {
-      const size_t sm = product_smem<T>(true, bt, cols);
-      if (sm > cap) continue;
-      const long long ctas = (long long)gxw * ceil_div(B, bt);
-      if (ctas >= sms) return {bt, gxw, ceil_div(B, bt), 1, true, sm};
+  const double slots = 2.0 * sms;
+  const int pw_max = ceil_div(out_w, kWarpPos);
+  ProductPlan best{0, 0, 0, 0, 1, 0};
+  double best_eff = -1.0;
+  for (int g : {2, 1}) {
+    const size_t sm = product_smem<T>(g, cols, max_act);
+    if (sm > (g == 2 ? kSmemMax : 220 * 1024)) continue;
+    for (int pw : {8, 4, 2, 1}) {
+      if (pw > pw_max && pw > 1) continue;
+      const long long ctas = (long long)ceil_div(out_w, pw * kWarpPos) * ceil_div(B, g * VEC);
+      if (ctas < sms) continue;
+      const double waves = ctas / slots;
+      const double eff = waves / std::ceil(waves) - 0.02 * (g == 1) - 0.01 * (pw < 4);
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        best = {g, pw, ceil_div(out_w, pw * kWarpPos), ceil_div(B, g * VEC), 1, sm};
+      }
     }
   }
-  // SPLIT: small batches; diagonals split across warps and across CTAs
-  const int split_bt[3] = {8, 4, 1};
-  ProductPlan p{0, 0, 0, 1, false, 0};
-  for (int bt : split_bt) {
-    const size_t sm = product_smem<T>(false, bt, cols);
-    if (sm > kSmem1) continue;
-    p = {bt, ceil_div(out_w, kSplitTile), ceil_div(B, bt), 1, false, sm};
-    if (bt <= B) break;
-  }
-  if (p.bt == 0) return p;
+  if (best.g) return best;
+  // few rows: PW = 1, split the diagonal list across CTAs
+  const size_t sm = product_smem<T>(1, cols, max_act);
+  if (sm > 220 * 1024) return best;
+  ProductPlan p{1, 1, ceil_div(out_w, kWarpPos), ceil_div(B, VEC), 1, sm};
   const long long ctas = (long long)p.gx * p.gy;
-  if (ctas < 2LL * sms) {
-    const int ns = (int)ceil_div(2LL * sms, ctas);
-    const int max_ns = max_act / 16 > 1 ? max_act / 16 : 1;
-    p.nsplit = ns < max_ns ? ns : max_ns;
-  }
+  const int ns = (int)ceil_div((long long)slots, ctas);
+  const int max_ns = max_act / 16 > 1 ? max_act / 16 : 1;
+  p.nsplit = ns < max_ns ? ns : max_ns;
   return p;
 }
 
-template <typename T, int BT, bool G, bool W>
+template <typename T, int G, bool GA>
 static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, int L, const T* in,
-                           const typename Traits<T>::P* vals, const double* asoft, const int32_t* active,
-                           const int32_t* n_act, int max_act, const typename Traits<T>::P* bias, T* out,
-                           typename Traits<T>::A* part, int bulk) {
-  auto k = k_product<T, BT, G, W>;
+                           const typename WType<T>::type* w, int ldw, const int32_t* active, const int32_t* n_act,
+                           int max_act, const typename Traits<T>::P* bias, T* out, typename Vec<T>::A* part,
+                           int vec_ok) {
+  auto k = k_product<T, G, GA>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-  k<<<dim3(p.gx, p.gy, p.nsplit), kThreads, p.smem, st>>>(B, C, L, in, vals, asoft, active, n_act, max_act,
-                                                          bias, out, part, p.nsplit, bulk);
+  k<<<dim3(p.gx, p.gy, p.nsplit), kThreads, p.smem, st>>>(B, C, L, in, w, ldw, active, n_act, max_act, bias,
+                                                          out, part, p.pw, p.nsplit, vec_ok);
   note_launch();
 }
 
+// workspace = [compact weights (max_act x ldw) | split partials]
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
-  using A = typename Traits<T>::A;
-  const int out_w = gather ? L : C, cols = gather ? C + kHalo : L;
+  using A = typename Vec<T>::A;
+  const int out_w = gather ? L : C, cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
-  return p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0;
+  const size_t wbytes = align16((size_t)(max_act > 0 ? max_act : 1) * w_ld<T>(out_w) * sizeof(typename WType<T>::type));
+  return wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
 }
 
 template <typename T>
@@ -642,32 +787,36 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
                 const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
                 void* ws, size_t ws_bytes, cudaStream_t st) {
   using P = typename Traits<T>::P;
-  using A = typename Traits<T>::A;
+  using A = typename Vec<T>::A;
+  using WT = typename WType<T>::type;
+  constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
+  if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
   const int out_w = gather ? L : C, in_w = gather ? C : L;
-  const int cols = in_w + (gather ? kHalo : 0);
+  const int cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
-  if (p.bt == 0) return DIAGMM_ETOOLARGE;
-  if (p.nsplit > 1 && (ws == nullptr || ws_bytes < (size_t)p.nsplit * B * out_w * sizeof(A))) p.nsplit = 1;
-  const int bulk = ((size_t)in_w * sizeof(T)) % 16 == 0 && aligned16(in) && (!gather || in_w >= kHalo);
+  if (p.g == 0) return DIAGMM_ETOOLARGE;
+  const int ldw = w_ld<T>(out_w);
+  WT* w = static_cast<WT*>(ws);
+  A* part = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)(max_act > 0 ? max_act : 1) * ldw * sizeof(WT)));
+  if (max_act > 0) {
+    dim3 grid(ceil_div(ldw, 256), max_act < 4096 ? max_act : 4096);
+    k_prescale<T><<<grid, 256, 0, st>>>(C, L, out_w, ldw, gather ? 1 : 0, static_cast<const P*>(vals), asoft, active,
+                                        n_act, max_act, w);
+    note_launch();
+  }
+  const int vec_ok = in_w % VEC == 0 && C % VEC == 0 && aligned16(in);
   auto tin = static_cast<const T*>(in);
-  auto tv = static_cast<const P*>(vals);
   auto tb = static_cast<const P*>(bias);
   auto to = static_cast<T*>(out);
-  auto part = static_cast<A*>(ws);
-#define DIAGMM_GO(BT, W)                                                                                     \
-  if (p.bt == BT && p.wide == W) {                                                                           \
-    if (gather)                                                                                              \
-      launch_product<T, BT, true, W>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, bulk);  \
-    else                                                                                                     \
-      launch_product<T, BT, false, W>(p, st, B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, bulk); \
+#define DIAGMM_GO(G)                                                                                     \
+  if (p.g == G) {                                                                                        \
+    if (gather)                                                                                          \
+      launch_product<T, G, true>(p, st, B, C, L, tin, w, ldw, active, n_act, max_act, tb, to, part, vec_ok);  \
+    else                                                                                                 \
+      launch_product<T, G, false>(p, st, B, C, L, tin, w, ldw, active, n_act, max_act, tb, to, part, vec_ok); \
   }
-  if constexpr (sizeof(T) == 8) {
-    DIAGMM_GO(8, true) DIAGMM_GO(4, true) DIAGMM_GO(2, true)
-  } else {
-    DIAGMM_GO(16, true) DIAGMM_GO(8, true) DIAGMM_GO(4, true)
-  }
-  DIAGMM_GO(8, false) DIAGMM_GO(4, false) DIAGMM_GO(1, false)
+  DIAGMM_GO(2) DIAGMM_GO(1)
 #undef DIAGMM_GO
   if (p.nsplit > 1) {
     const size_t n = (size_t)B * out_w;
@@ -681,19 +830,26 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
 
 // ---- dW
 template <typename T>
-static int dw_win_cap(int C, int max_act) {
-  constexpr int V = 16 / sizeof(T);
-  const double span = max_act > 0 ? (double)kDwJ * C / max_act : (double)C;
+static int dw_win_cap(int C, int max_act, int dwj) {
+  constexpr int V = vec_rows<T>();
+  const double span = max_act > 0 ? (double)dwj * C / max_act : (double)C;
   int cap = (int)(kDwTile + 2.5 * span) + 2 * V;
-  cap = cap < C ? cap : C;
-  // keep two stages within the shared-memory budget
-  while (cap > kDwTile && 128 + 2 * (size_t)dw_stage<T>(cap).bytes > 200 * 1024) cap -= 64;
+  cap = cap < C + kDwTile ? cap : C + kDwTile;
+  cap = (cap + V - 1) / V * V;
+  // keep two CTAs per SM within the shared-memory budget
+  while (cap > kDwTile && dw_smem<T>(cap) > 110 * 1024) cap -= 64;
   return cap;
 }
 
+// diagonals per dW CTA: 64, or 32 when 64-diagonal tiles would not cover the SMs
+static int dw_diags(int L, int max_act) {
+  const long long t64 = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwGroups * 16);
+  return t64 < num_sms() ? kDwGroups * 8 : kDwGroups * 16;
+}
+
 static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_per_part) {
-  const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwJ);
-  long long p = ceil_div(2LL * num_sms(), tiles);
+  const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, dw_diags(L, max_act));
+  long long p = ceil_div(3LL * num_sms(), tiles);
   if (p < 1) p = 1;
   const long long max_p = ceil_div(B, rb);
   if (p > max_p) p = max_p;
@@ -706,15 +862,17 @@ static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_pe
 
 template <typename T>
 size_t dw_workspace(int M, int N, int B, int max_act) {
-  using A = typename Traits<T>::A;
+  using A = typename Vec<T>::A;
   const int L = M < N ? M : N;
   const int C = M > N ? M : N;
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, DwRows<T>::RB, &parts, &rpp);
+  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * vec_rows<T>(), &parts, &rpp);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
   const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
-  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+  const size_t tiles = (size_t)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwGroups * 8);
+  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A)) +
+                    align16(tiles * sizeof(int));
   size_t w = dw > prod_f ? dw : prod_f;
   return w > prod_b ? w : prod_b;
 }
@@ -724,36 +882,39 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
            const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
            double* g_soft, void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
   using P = typename Traits<T>::P;
-  using A = typename Traits<T>::A;
-  constexpr int RB = DwRows<T>::RB;
-  constexpr int V = 16 / sizeof(T);
+  using A = typename Vec<T>::A;
+  constexpr int VEC = vec_rows<T>();
   const int C = M > N ? M : N, L = M < N ? M : N;
   if (ws_bytes < dw_workspace<T>(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, RB, &parts, &rpp);
+  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * VEC, &parts, &rpp);
   A* partial = static_cast<A*>(ws);
   const bool tall = M >= N;
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
+  const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
+  int* ctr = reinterpret_cast<int*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +
+                                    align16((size_t)cparts * M * sizeof(A)));
   if (B > 0 && max_act > 0) {
-    const int cap = dw_win_cap<T>(C, max_act);
-    const size_t sm = 128 + 2 * (size_t)dw_stage<T>(cap).bytes;
-    const int bulk = C % V == 0 && L % V == 0 && aligned16(aop) && aligned16(bop);
-    auto k = k_dw<T>;
+    const int dwj = dw_diags(L, max_act);
+    const int cap = dw_win_cap<T>(C, max_act, dwj);
+    const size_t sm = dw_smem<T>(cap);
+    const int vec_ok = C % VEC == 0 && L % VEC == 0 && aligned16(aop) && aligned16(bop);
+    auto k = dwj == kDwGroups * 16 ? k_dw<T, 16> : k_dw<T, 8>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid(ceil_div(L, kDwTile), ceil_div(max_act, kDwJ), parts);
-    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, bulk);
+    dim3 grid(ceil_div(L, kDwTile), ceil_div(max_act, dwj), parts);
+    if (parts > 1) cudaMemsetAsync(ctr, 0, (size_t)grid.x * grid.y * sizeof(int), st);
+    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, ctr, vec_ok);
     note_launch();
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts > 0 ? 1 : 0, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft);
   note_launch();
   if (g_bias) {
     A* cpart = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)));
     if (B > 0) {
-      const int cparts = ceil_div(B, kColRows);
       k_colsum_partial<T><<<dim3(ceil_div(M, 256), cparts), 256, 0, st>>>(B, M, static_cast<const T*>(dy), cpart);
       note_launch();
       k_colsum_final<T><<<ceil_div(M, 32), 256, 0, st>>>(M, cparts, cpart, static_cast<P*>(g_bias));

@@ -111,10 +111,22 @@ __device__ __forceinline__ Affine compose(Affine f, Affine g) {  // f o g
   return {f.a * g.a, f.a * g.b + f.b};
 }
 
+// Up to kMaxJobs independent selections per launch, one CTA each (all the
+// DiagLinear layers of a model re-select in one launch, SURVEY §7 hard part 2).
+constexpr int kMaxJobs = 64;
+struct WaterfillJobs { diagmm_topk_job j[kMaxJobs]; };
+
 __global__ void __launch_bounds__(kSelThreads)
-k_waterfill(int C, int k, double temperature, const double* __restrict__ alpha,
-            double* __restrict__ asoft, uint8_t* __restrict__ clamped, int32_t* __restrict__ active,
-            int32_t* __restrict__ slot, int32_t* __restrict__ n_act) {
+k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
+  const diagmm_topk_job& J = jobs.j[blockIdx.x];
+  const int C = J.C, k = J.k;
+  const double temperature = J.temperature;
+  const double* __restrict__ alpha = J.alpha;
+  double* __restrict__ asoft = J.alpha_soft;
+  uint8_t* __restrict__ clamped = J.clamped;
+  int32_t* __restrict__ active = J.active;
+  int32_t* __restrict__ slot = J.slot;
+  int32_t* __restrict__ n_act = J.n_act;
   extern __shared__ __align__(16) unsigned char smem[];
   const int NP = next_pow2(C);
   double* key = reinterpret_cast<double*>(smem);                              // NP
@@ -301,17 +313,38 @@ static size_t waterfill_smem(int C) {
   return ((size_t)NP * 20 + 15) / 16 * 16 + kSelThreads * (sizeof(Affine) + sizeof(int)) + 64;
 }
 
+static int check_job(const diagmm_topk_job& j) {
+  if (j.C < 1) return DIAGMM_ESHAPE;
+  if (!(j.temperature > 0.0)) return DIAGMM_ETEMPERATURE;
+  if (j.k < 1 || j.k > j.C) return DIAGMM_EK;
+  if (j.C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  return DIAGMM_OK;
+}
+
+int run_waterfill_batched(int n, const diagmm_topk_job* jobs, cudaStream_t st) {
+  if (n < 0 || (n > 0 && jobs == nullptr)) return DIAGMM_ESHAPE;
+  for (int i = 0; i < n; ++i)
+    if (int e = check_job(jobs[i])) return e;
+  for (int b = 0; b < n; b += kMaxJobs) {
+    const int cnt = n - b < kMaxJobs ? n - b : kMaxJobs;
+    WaterfillJobs P{};
+    int cmax = 1;
+    for (int i = 0; i < cnt; ++i) {
+      P.j[i] = jobs[b + i];
+      cmax = P.j[i].C > cmax ? P.j[i].C : cmax;
+    }
+    const size_t sm = waterfill_smem(cmax);
+    cudaFuncSetAttribute(k_waterfill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_waterfill<<<cnt, kSelThreads, sm, st>>>(P);
+    note_launch();
+  }
+  return status_from_cuda();
+}
+
 int run_waterfill(int C, int k, double T, const double* alpha, double* asoft, uint8_t* clamped,
                   int32_t* active, int32_t* slot, int32_t* n_act, cudaStream_t st) {
-  if (C < 1) return DIAGMM_ESHAPE;
-  if (!(T > 0.0)) return DIAGMM_ETEMPERATURE;
-  if (k < 1 || k > C) return DIAGMM_EK;
-  if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
-  size_t sm = waterfill_smem(C);
-  cudaFuncSetAttribute(k_waterfill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_waterfill<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, asoft, clamped, active, slot, n_act);
-  note_launch();
-  return status_from_cuda();
+  diagmm_topk_job j{C, k, T, alpha, asoft, clamped, active, slot, n_act};
+  return run_waterfill_batched(1, &j, st);
 }
 
 int run_select_hard(int C, int k, const double* alpha, int32_t* idx, cudaStream_t st) {

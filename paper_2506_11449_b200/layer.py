@@ -85,6 +85,7 @@ class _OpSpec:
     temperature: float
     route: str
     fixed: ops.Selection | None = None
+    presel: ops.Selection | None = None
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -92,18 +93,16 @@ def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype
         return True
     if spec.route == "diag":
         return False
-    # "auto": the reference's own switch (diagcore.py:226, layers.py:420) —
-    # dense once the structural density reaches 1/4 — plus the B200 cost
-    # model: with bf16 activations the tensor cores run
-    # the dense-equivalent product ~50x faster than the FMA pipe runs the
-    # diagonal one, so from a few hundred tokens on the dense route wins; the
-    # FMA kernels keep the small-batch regime, where both are bound by reading
-    # the weights and the diagonal store is 1/density times smaller.
-    L = min(spec.M, spec.N)
-    n_act = sel.host_count()
-    if 4 * n_act * L >= spec.M * spec.N:
+    # "auto": the B200 cost model first — with bf16
+    # activations and enough tokens the tensor cores run the dense-equivalent
+    # product faster than the FMA pipe runs the diagonal one, and this branch
+    # needs no host read of n_act; below that the reference's own switch
+    # (diagcore.py:226, layers.py:420): dense once the structural density of
+    # the active set reaches 1/4 (one host read of the device count).
+    if act_dtype == torch.bfloat16 and B >= dense_route_min_tokens():
         return True
-    return act_dtype == torch.bfloat16 and B >= dense_route_min_tokens()
+    L = min(spec.M, spec.N)
+    return 4 * sel.host_count() * L >= spec.M * spec.N
 
 
 def dense_route_min_tokens() -> int:
@@ -121,7 +120,7 @@ class DiagMMFunction(torch.autograd.Function):
     def forward(ctx, x, values, alpha, bias, spec: _OpSpec):
         M, N = spec.M, spec.N
         if alpha is not None:
-            sel = ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+            sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
         else:
             sel = spec.fixed
         dense = _use_dense(spec, sel, x.shape[0], x.dtype)
@@ -207,6 +206,7 @@ class DiagLinear(nn.Module):
         self.bias = nn.Parameter(torch.zeros(M, device=device, dtype=pdt)) if bias else None
         self.step = 0
         self.last_step = 0
+        self._presel = None
 
     # ---- DST mask-update API (layers.py:212-228, 268-287) --------------------
     def set_k(self, k: int) -> None:
@@ -266,9 +266,17 @@ class DiagLinear(nn.Module):
             x2 = x2.double()
         elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))  # like nn.Linear under autocast
-        spec = _OpSpec(self.out_features, self.in_features, self.k, self.temperature(step), self.route)
+        T = self.temperature(step)
+        spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
+                       presel=self._take_preselection(step, T))
         y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
         return y.reshape(*lead, self.out_features)
+
+    def _take_preselection(self, step: int, T: float):
+        ps, self._presel = self._presel, None
+        if ps is not None and ps[0] == (step, self.k, T):
+            return ps[1]
+        return None
 
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, k={self.k}, "
@@ -370,6 +378,21 @@ def diagheur_update(layer: DiagHeurLinear, rng: np.random.Generator, step: int |
     return layer
 
 
+def preselect(layers, step: int) -> None:
+    """Run the soft TopK of every layer for ``step`` in ONE launch (batched K4)
+    and hand each layer its selection for its next forward at that step.
+    Call it right before the model's forward (alpha must not change between
+    the two); a layer whose forward does not match (step, k, T) re-selects
+    on its own, so the result never differs from the per-layer path."""
+    layers = [m for m in layers if isinstance(m, DiagLinear)]
+    if not layers:
+        return
+    temps = [m.temperature(step) for m in layers]
+    sels = ops.soft_topk_select_many([m.alpha.detach() for m in layers], [m.k for m in layers], temps)
+    for m, T, sel in zip(layers, temps, sels):
+        m._presel = ((step, m.k, T), sel)
+
+
 def penalties(model: nn.Module) -> list[torch.Tensor]:
     """MLPModel.penalties (training.py:439-444) for any module tree."""
     return [m.penalty() for m in model.modules() if isinstance(m, DiagLinear) and m.l1_coeff > 0]
@@ -377,5 +400,5 @@ def penalties(model: nn.Module) -> list[torch.Tensor]:
 
 __all__ = [
     "DiagLinear", "DiagMMFunction", "FrozenDiagLinear", "DiagHeurLinear", "DiagMatrix",
-    "ParamSpec", "diagheur_update", "penalties", "EPS_ACTIVE",
+    "ParamSpec", "diagheur_update", "penalties", "preselect", "EPS_ACTIVE",
 ]

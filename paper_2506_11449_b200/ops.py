@@ -77,6 +77,7 @@ class Selection:
     temperature: float
     n_act_host: torch.Tensor | None = None
     event: torch.cuda.Event | None = None
+    _alpha_keepalive: torch.Tensor | None = None
 
     @property
     def C(self) -> int:
@@ -111,21 +112,44 @@ def new_selection(C: int, device, k: int = 1, temperature: float = 1.0) -> Selec
 
 
 def soft_topk_select(alpha: torch.Tensor, k: int, temperature: float,
-                     out: Selection | None = None, host_copy: bool = True) -> Selection:
-    """K4: soft_topk + clamped set + active set (selection.py:100-142, layers.py:234)."""
-    _need_cuda(alpha)
-    if alpha.dtype != torch.float64 or alpha.dim() != 1:
-        raise ShapeMismatch("alpha must be a float64 vector")
-    a = alpha.contiguous()
-    C = a.numel()
-    sel = out if out is not None else new_selection(C, a.device)
-    sel.k, sel.temperature = int(k), float(temperature)
-    _lib.call("diagmm_topk_waterfill", C, int(k), float(temperature), _p(a), _p(sel.alpha_soft),
-              _p(sel.clamped), _p(sel.active), _p(sel.slot), _p(sel.n_act), _stream(a))
-    sel.n_act_host = None
-    if host_copy:
-        sel.start_host_copy()
-    return sel
+                     out: Selection | None = None, host_copy: bool = False) -> Selection:
+    """K4: soft_topk + clamped set + active set (selection.py:100-142, layers.py:234).
+
+    Nothing is read back to the host unless ``host_copy`` (or a later
+    ``host_count()``) asks for the active count."""
+    return soft_topk_select_many([alpha], [k], [temperature], [out], host_copy=host_copy)[0]
+
+
+def soft_topk_select_many(alphas, ks, temperatures, outs=None, host_copy: bool = False) -> list:
+    """Batched K4: every selection in ONE launch (one CTA each) — the per-step
+    re-selection of all DiagLinear layers of a model (layers.py:233 per layer)."""
+    n = len(alphas)
+    if not (len(ks) == len(temperatures) == n):
+        raise ValueError("alphas, ks and temperatures must have the same length")
+    outs = list(outs) if outs is not None else [None] * n
+    jobs = (_lib.TopkJob * max(1, n))()
+    sels = []
+    stream = None
+    for i, (alpha, k, T, out) in enumerate(zip(alphas, ks, temperatures, outs)):
+        _need_cuda(alpha)
+        if alpha.dtype != torch.float64 or alpha.dim() != 1:
+            raise ShapeMismatch("alpha must be a float64 vector")
+        a = alpha if alpha.is_contiguous() else alpha.contiguous()
+        C = a.numel()
+        sel = out if out is not None else new_selection(C, a.device)
+        sel.k, sel.temperature = int(k), float(T)
+        sel._alpha_keepalive = a
+        jobs[i] = _lib.TopkJob(C, int(k), float(T), _p(a), _p(sel.alpha_soft), _p(sel.clamped),
+                               _p(sel.active), _p(sel.slot), _p(sel.n_act))
+        stream = _stream(a) if stream is None else stream
+        sels.append(sel)
+    if n:
+        _lib.call("diagmm_topk_waterfill_batched", n, jobs, stream)
+    for sel in sels:
+        sel.n_act_host = None
+        if host_copy:
+            sel.start_host_copy()
+    return sels
 
 
 def soft_topk(alpha: torch.Tensor, k: int, temperature: float) -> torch.Tensor:

@@ -86,6 +86,18 @@ def work(name, args, nact_of=None):
         n = _n_act(args, name, nact_of) or max(M, N)
         p = 8 if dt == 0 else 4
         return 0.0, p * n * min(M, N) * 2 + p * max(M, N) * min(M, N)
+    if name == "diagmm_adamw_multi":
+        n, descs = args[0], args[1]
+        return 0.0, float(sum(7 * (8 if descs[i].dtype == 0 else 4) * descs[i].n for i in range(n)))
+    if name == "diagmm_sumsq_multi":
+        n, descs = args[0], args[1]
+        return 0.0, float(sum((8 if descs[i].dtype == 0 else 4) * descs[i].n for i in range(n)))
+    if name == "diagmm_topk_waterfill_batched":
+        n, jobs = args[0], args[1]
+        # alpha read, alpha_soft written (f64), clamped (u8), active + slot (i32) per candidate
+        return 0.0, float(sum(25 * jobs[i].C for i in range(n)))
+    if name == "diagmm_topk_waterfill":
+        return 0.0, 25.0 * args[0]
     if name == "diagmm_adamw":
         dt, n = args[0], args[1]
         return 0.0, 7 * (8 if dt == 0 else 4) * n

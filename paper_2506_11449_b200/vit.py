@@ -16,7 +16,7 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
-from .layer import DiagLinear
+from .layer import DiagLinear, preselect
 from .selection import TemperatureSchedule
 
 
@@ -93,6 +93,9 @@ class ViT(nn.Module):
             m.step = step
 
     def forward(self, images):
+        diag = self.diag_layers()
+        if diag:
+            preselect(diag, diag[0].step)  # one batched soft-TopK launch for all layers
         x = self.patch(images).flatten(2).transpose(1, 2)
         x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
         for blk in self.blocks:
@@ -117,6 +120,9 @@ class MLPModel(nn.Module):
         self.layers = nn.ModuleList(layers)
 
     def forward(self, x, step: int | None = None):
+        diag = [m for m in self.layers if isinstance(m, DiagLinear)]
+        if diag:
+            preselect(diag, diag[0].step if step is None else step)
         for i, lyr in enumerate(self.layers):
             x = lyr(x, step) if isinstance(lyr, DiagLinear) else lyr(x)
             if i < len(self.layers) - 1:

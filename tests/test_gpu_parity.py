@@ -313,3 +313,94 @@ def test_clip_scale_matches_reference_rule():
         np.testing.assert_allclose(norm.item(), ref_norm, rtol=1e-12)
         want = max_norm / ref_norm if ref_norm > max_norm else 1.0
         np.testing.assert_allclose(scale.item(), want, rtol=1e-12)
+
+
+def test_multi_tensor_adamw_matches_reference_golden():
+    """diagmm_adamw_multi == adamw_step (training.py:346-358) per tensor, mixed
+    dtypes, sizes across chunk boundaries, per-tensor decay and step."""
+    from paper_2506_11449_b200.optim import AdamW
+    from paper_2506_11449_b200.layer import ParamSpec
+
+    g = load_golden("misc")
+    rng = np.random.default_rng(11)
+    p64 = t(g["adamw_p0"]).clone().requires_grad_(True)
+    big = torch.randn(3 * 8192 + 17, device=DEV, dtype=torch.float32, requires_grad=True)
+    small = torch.randn(5, device=DEV, dtype=torch.float32, requires_grad=True)
+    opt = AdamW([ParamSpec(p64, True, "p64"), ParamSpec(big, False, "big"), ParamSpec(small, True, "small")],
+                lr=1e-2, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
+    gr = g["adamw_g0"].copy()
+    ref_big = big.detach().double().cpu().numpy().copy()
+    mb = np.zeros_like(ref_big)
+    vb = np.zeros_like(ref_big)
+    for j in range(3):
+        p64.grad = t(gr)
+        gb = rng.standard_normal(big.numel())
+        big.grad = torch.as_tensor(gb, dtype=torch.float32, device=DEV)
+        small.grad = torch.ones_like(small)
+        opt.step()
+        np.testing.assert_allclose(p64.detach().cpu().numpy(), g["adamw_seq"][j], rtol=1e-14, atol=1e-15)
+        gb32 = gb.astype(np.float32).astype(np.float64)
+        mb = 0.9 * mb + 0.1 * gb32
+        vb = 0.99 * vb + 0.01 * gb32 * gb32
+        mh, vh = mb / (1 - 0.9 ** (j + 1)), vb / (1 - 0.99 ** (j + 1))
+        ref_big = ref_big - 1e-2 * (mh / (np.sqrt(vh) + 1e-8))  # no decay on "big"
+        np.testing.assert_allclose(big.detach().double().cpu().numpy(), ref_big, rtol=2e-5, atol=2e-6)
+        gr = gr * 0.5 + 0.1
+
+
+def test_multi_tensor_clip_matches_reference_rule():
+    from paper_2506_11449_b200.layer import ParamSpec
+
+    rng = np.random.default_rng(5)
+    gs = [rng.standard_normal(1000) * 0.05, rng.standard_normal(20000) * 0.05, rng.standard_normal(37) * 0.05]
+    specs = []
+    for i, a in enumerate(gs):
+        p = torch.zeros(a.size, dtype=torch.float64 if i != 1 else torch.float32, device=DEV, requires_grad=True)
+        p.grad = torch.as_tensor(a, dtype=p.dtype, device=DEV)
+        specs.append(ParamSpec(p, True, f"p{i}"))
+    gs[1] = gs[1].astype(np.float32).astype(np.float64)
+    for max_norm in (0.1, 100.0):
+        norm, scale = GlobalNormClipper(max_norm).compute(specs)
+        _, ref_norm = olayer.clip_by_global_norm(gs, max_norm)
+        np.testing.assert_allclose(norm.item(), ref_norm, rtol=1e-12)
+        want = max_norm / ref_norm if ref_norm > max_norm else 1.0
+        np.testing.assert_allclose(scale.item(), want, rtol=1e-12)
+    a, b = (GlobalNormClipper(1.0).compute(specs)[0].item() for _ in range(2))
+    assert a == b  # fixed reduction order: bitwise deterministic
+
+
+def test_batched_topk_equals_single_launches():
+    """diagmm_topk_waterfill_batched (one CTA per layer) gives bit-identical
+    selections to per-layer launches, and the oracle's masks."""
+    from oracle import topk as otopk
+
+    rng = np.random.default_rng(3)
+    cases = [(3072, 307, 1e-9), (768, 77, 0.05), (2304, 230, 4.0), (5, 2, 1.0), (96, 38, 1e-3)]
+    alphas = [t(rng.standard_normal(C)) for C, _, _ in cases]
+    sels = ops.soft_topk_select_many(alphas, [k for _, k, _ in cases], [T for _, _, T in cases])
+    for (C, k, T), a, sb in zip(cases, alphas, sels):
+        s1 = ops.soft_topk_select(a, k, T)
+        for f in ("alpha_soft", "clamped", "slot", "n_act"):
+            assert torch.equal(getattr(sb, f), getattr(s1, f)), f
+        n = sb.host_count()
+        assert torch.equal(sb.active[:n], s1.active[:n])
+        ref_soft, ref_clamped = otopk.waterfill(a.cpu().numpy() / T, k)[:2]
+        act = np.flatnonzero(ref_soft >= 1e-3)
+        np.testing.assert_array_equal(sb.active[:n].cpu().numpy(), act)
+        np.testing.assert_array_equal(sb.clamped.cpu().numpy().astype(bool), ref_clamped)
+
+
+def test_preselect_matches_layer_path():
+    """ViT-style preselect (batched K4) yields the same forward as per-layer K4."""
+    from paper_2506_11449_b200 import preselect
+
+    layers = [DiagLinear(64, 256, 0.9, seed=s, dtype=torch.float32,
+                         t_schedule=TemperatureSchedule("constant", 0.05, 0.05, 1)) for s in range(3)]
+    x = torch.randn(16, 64, device=DEV)
+    ref = [lyr(x, step=0) for lyr in layers]
+    preselect(layers, 0)
+    assert all(lyr._presel is not None for lyr in layers)
+    got = [lyr(x, step=0) for lyr in layers]
+    assert all(lyr._presel is None for lyr in layers)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
