@@ -208,9 +208,9 @@ def main():
     cfg = VIT_B16 if args.model == "vit_b16" else VIT_TINY16
     torch.manual_seed(1234)  # dense params; DiagLinear init is seeded per layer (numpy stream)
     model = ViT(cfg, route=args.route, device=dev)
-    if world > 1:  # identical replicas
-        for p in model.parameters():
-            dist.broadcast(p.data, 0)
+    from paper_2506_11449_b200.dp import GradientAllReducer, broadcast_parameters
+
+    broadcast_parameters(model)  # identical replicas
     specs = model_param_specs(model)
     opt = AdamW(specs, lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
     clip = GlobalNormClipper(1.0)
@@ -218,24 +218,7 @@ def main():
     g = torch.Generator(device=dev).manual_seed(100 + rank)
     images = torch.randn(B, 3, cfg.image, cfg.image, device=dev, generator=g).to(torch.bfloat16)
     labels = torch.randint(0, cfg.classes, (B,), device=dev, generator=g)
-    grads_flat = None
-
-    def allreduce_grads():
-        nonlocal grads_flat
-        grads = [s.tensor.grad for s in specs if s.tensor.grad is not None]
-        # bucket per dtype, one NCCL all-reduce each, average (the reference's batch-mean loss)
-        by_dt = {}
-        for gr in grads:
-            by_dt.setdefault(gr.dtype, []).append(gr)
-        for dt, gs in by_dt.items():
-            flat = torch.cat([x.reshape(-1) for x in gs])
-            dist.all_reduce(flat)
-            flat.div_(world)
-            off = 0
-            for x in gs:
-                n = x.numel()
-                x.copy_(flat[off:off + n].view_as(x))
-                off += n
+    allreduce_grads = GradientAllReducer([s.tensor for s in specs])
 
     def train_step(step, imgs, lbls):
         model.set_step(step)

@@ -66,7 +66,7 @@ DIAGMM_API unsigned long long diagmm_launch_count(void);
 
 /* ---- K1: forward DiagMM --------------------------------------------------
  * y = x @ W_K^T (+ bias), W_K = sum_{o in active} alpha_soft[o] P_o diag(values[o]).
- * Replaces: the forward product of _record_diag_matmul (layers.py:400-407:
+ * Replaces: the forward product of _record_diag_matmul (layers.py:130-137:
  * bcsr_spmm / reference_spmm, diagcore.py:200-238, bcsr.py:362-409), the
  * weight scaling of DynaDiagLayer.forward (layers.py:235) and Tape.add_bias
  * (autodiff.py:72-81).  alpha_soft == NULL means unit scale (DiagHeur /
@@ -85,7 +85,7 @@ DIAGMM_API int diagmm_forward(int dtype, int M, int N, int B, const void* x,
                    size_t ws_bytes, void* stream);
 
 /* ---- K2: input gradient through the (never materialized) transpose -------
- * dx = dy @ W_K.  Replaces layers.py:414-418 (transpose, diagcore.py:162-191,
+ * dx = dy @ W_K.  Replaces layers.py:144-148 (transpose, diagcore.py:162-191,
  * followed by the same spmm).  workspace: as diagmm_forward. */
 DIAGMM_API size_t diagmm_backward_input_workspace(int dtype, int M, int N,
                                                   int B, int max_act);
@@ -96,11 +96,11 @@ DIAGMM_API int diagmm_backward_input(int dtype, int M, int N, int B, const void*
                           size_t ws_bytes, void* stream);
 
 /* ---- K3: per-diagonal weight gradient ----------------------------------
- * gw[j,t] = sum_b dy[b, r_jt] * x[b, c_jt]   (layers.py:419-428)
+ * gw[j,t] = sum_b dy[b, r_jt] * x[b, c_jt]   (layers.py:149-158)
  * g_values (C, L): row active[j] = alpha_soft[active[j]] * gw[j] (unit scale
- * if alpha_soft == NULL), every other row exactly 0 (layers.py:429-433).
+ * if alpha_soft == NULL), every other row exactly 0 (layers.py:159-163).
  * g_soft (C,) float64, may be NULL: g_soft[active[j]] = sum_t gw[j,t] *
- * values[active[j],t], 0 elsewhere (layers.py:434-435).
+ * values[active[j],t], 0 elsewhere (layers.py:164-165).
  * g_bias (M,), may be NULL: column sums of dy (autodiff.py:77-79).
  * slot (C,) int32 from diagmm_topk_waterfill / diagmm_active_from_list.
  * workspace: at least diagmm_backward_weight_workspace(...) bytes. */
@@ -219,7 +219,7 @@ DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_n
 /* ---- dense-equivalent route (reference's own BLAS switch) ---------------
  * The reference multiplies the materialized matrix with BLAS when the
  * structural density reaches 1/4 (diagcore.py:226-228) and computes dW
- * densely then gathers (layers.py:420-423).  diagmm_materialize writes
+ * densely then gathers (layers.py:150-153).  diagmm_materialize writes
  * W_K (M, N) row-major in `dtype` (zeros off the active diagonals);
  * diagmm_gather_dense_grad turns a dense dW (M, N, float32/float64 = param
  * type) into g_values / g_soft exactly like diagmm_backward_weight. */

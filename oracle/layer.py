@@ -18,7 +18,7 @@ from .topk import EPS_ACTIVE, l1_term, select_hard, soft_topk, soft_topk_grad, t
 
 
 def _product(rows, cols, offsets, vals, X, use_csr):
-    """layers.py:403-407 — blocked (scipy CSR) product while few diagonals are active,
+    """layers.py:133-137 — blocked (scipy CSR) product while few diagonals are active,
     the diagonal-by-diagonal reference product otherwise."""
     if use_csr:
         return csr_spmm(rows, cols, offsets, vals, X)
@@ -26,7 +26,7 @@ def _product(rows, cols, offsets, vals, X, use_csr):
 
 
 def diag_matmul_forward(x, weights, active, rows, cols, use_csr=False):
-    """layers.py:396-407: y = x @ W^T for W built from the active diagonals' weights."""
+    """layers.py:126-137: y = x @ W^T for W built from the active diagonals' weights."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim != 2 or x.shape[1] != cols:
         raise ValueError(f"input has shape {x.shape}, expected (B, {cols})")
@@ -35,7 +35,7 @@ def diag_matmul_forward(x, weights, active, rows, cols, use_csr=False):
 
 def diag_matmul_backward(up, x, values, weights, active, rows, cols, alpha=None,
                          alpha_soft=None, k=None, temperature=None, use_csr=False):
-    """layers.py:413-437 — (gx, g_values[, g_alpha]) for upstream ``up`` (B, M)."""
+    """layers.py:143-167 — (gx, g_values[, g_alpha]) for upstream ``up`` (B, M)."""
     offs = [int(a) for a in active]
     offs_t, w_t = transpose_diagonals(rows, cols, offs, weights)
     gx = _product(cols, rows, offs_t, w_t, np.asarray(up).T, use_csr).T

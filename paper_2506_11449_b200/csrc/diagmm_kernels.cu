@@ -10,7 +10,7 @@
 //          of diagcore.py:162-191 read "by own index, +o").
 //   "scatter" form (S): out[b,r] = sum_j [c=(r-o_j) mod C < L] V[j,c]*in[b,c], r < C
 //        = tall/square forward (diagcore.py:230-233) and wide dX.
-//   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:419-428)
+//   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:149-158)
 //        tall: Aop = dy, Bop = x;   wide: Aop = x, Bop = dy.
 //
 // B200 design (v4):

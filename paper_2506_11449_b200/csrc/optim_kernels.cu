@@ -3,7 +3,7 @@
 //
 // The reference updates EVERY candidate row each step (inactive rows carry a
 // zero gradient, so their moments decay and weight decay still applies,
-// layers.py:429-433 + training.py:354-358); the kernel is therefore a plain
+// layers.py:159-163 + training.py:354-358); the kernel is therefore a plain
 // HBM-bound streaming update: per element it reads param, grad, m, v and
 // writes param, m, v (7 words).  Clipping never leaves the device: sumsq
 // partials -> clip_scale -> adamw reads *clip_scale.

@@ -97,7 +97,7 @@ def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype
     # activations and enough tokens the tensor cores run the dense-equivalent
     # product faster than the FMA pipe runs the diagonal one, and this branch
     # needs no host read of n_act; below that the reference's own switch
-    # (diagcore.py:226, layers.py:420): dense once the structural density of
+    # (diagcore.py:226, layers.py:150): dense once the structural density of
     # the active set reaches 1/4 (one host read of the device count).
     if act_dtype == torch.bfloat16 and B >= dense_route_min_tokens():
         return True

@@ -304,7 +304,7 @@ def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
 
 def gather_dense_grad(dW: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
                       need_soft: bool = True):
-    """g_values / g_soft from a dense dW (M, N) (the dense branch of layers.py:420-423)."""
+    """g_values / g_soft from a dense dW (M, N) (the dense branch of layers.py:150-153)."""
     _need_cuda(dW, values)
     C, L = geometry(M, N)
     dW = dW.to(values.dtype).contiguous()

@@ -124,7 +124,7 @@ class AdamW:
 def model_param_specs(model: torch.nn.Module) -> list[ParamSpec]:
     """ParamSpecs for a whole model: DiagLinear/DiagHeur specs, plus dense params
     (weights decay, biases / norms do not — the reference's DenseLayer rule,
-    layers.py:433-441)."""
+    layers.py:437-441)."""
     specs: list[ParamSpec] = []
     seen = set()
     for mod in model.modules():

@@ -404,3 +404,73 @@ def test_preselect_matches_layer_path():
     assert all(lyr._presel is None for lyr in layers)
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+class _Tensor:
+    """Minimal stand-in for the reference's autodiff.Tensor (autodiff.py:19-30)."""
+
+    def __init__(self, value, requires_grad=False):
+        self.value = np.asarray(value, dtype=np.float64)
+        self.grad = None
+
+
+class _Tape:
+    """Minimal stand-in for autodiff.Tape.record / backward (autodiff.py:43-50, 141-155)."""
+
+    def __init__(self):
+        self.ops = []
+
+    def record(self, out, inputs, backward):
+        self.ops.append((out, inputs, backward))
+        return out
+
+    def backward(self, out, up):
+        out.grad = up
+        for o, inputs, bw in reversed(self.ops):
+            if o.grad is None:
+                continue
+            for inp, g in zip(inputs, bw(o.grad)):
+                inp.grad = g if inp.grad is None else inp.grad + g
+
+
+class _Cache:
+    def __init__(self, rows, cols):
+        self.rows, self.cols = rows, cols
+
+
+@pytest.mark.parametrize("shape", [(64, 24), (24, 64), (40, 40)])
+@pytest.mark.parametrize("with_alpha", [False, True])
+def test_tape_adapter_matches_reference_op(shape, with_alpha):
+    """tape_adapter.record_diag_matmul has the reference op's contract
+    (layers.py:108-170): same forward, same (gx, g_values[, g_alpha])."""
+    from oracle import topk as otopk
+    from paper_2506_11449_b200.tape_adapter import record_diag_matmul
+
+    M, N = shape
+    C, L = max(M, N), min(M, N)
+    rng = np.random.default_rng(21)
+    k = max(1, C // 8)
+    alpha = rng.standard_normal(C)
+    T = 0.3
+    soft = otopk.soft_topk(alpha, k, T)
+    active = np.flatnonzero(soft >= 1e-3)
+    values = rng.standard_normal((C, L))
+    weights = soft[active, None] * values[active]
+    x = rng.standard_normal((7, N))
+    up = rng.standard_normal((7, M))
+    tape = _Tape()
+    xt, vt, at = _Tensor(x), _Tensor(values), _Tensor(alpha)
+    kw = dict(alpha=at, alpha_soft=soft, k=k, temperature=T) if with_alpha else {}
+    y = record_diag_matmul(tape, xt, vt, weights, active, _Cache(M, N), False, **kw)
+    y_ref = olayer.diag_matmul_forward(x, weights, active, M, N)
+    assert scaled_err(y.value, y_ref) < 1e-12
+    tape.backward(y, up)
+    ref = olayer.diag_matmul_backward(up, x, values, weights, active, M, N,
+                                      **({"alpha": alpha, "alpha_soft": soft, "k": k, "temperature": T}
+                                         if with_alpha else {}))
+    assert scaled_err(xt.grad, ref[0]) < 1e-12
+    assert scaled_err(vt.grad, ref[1]) < 1e-12
+    if with_alpha:
+        assert scaled_err(at.grad, ref[2]) < 1e-10
+    with pytest.raises(ShapeMismatch):
+        record_diag_matmul(tape, _Tensor(np.zeros((2, N + 1))), vt, weights, active, _Cache(M, N), False)
