@@ -216,6 +216,20 @@ DIAGMM_API int diagmm_sumsq_multi(int n, const diagmm_tensor* tensors, double* p
 DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_norm,
                                       double* norm, double* scale, void* stream);
 
+/* ---- fused LayerNorm for the bf16 activations of the ViT caller ----------
+ * Not a reference symbol: the caller's LayerNorm (vit.py) around DiagLinear.
+ * x, y, dy, dx: (M, D) bf16 row-major; w, b, dw, db: (D,) float; mean, rstd:
+ * (M,) float saved by the forward.  D % 8 == 0, D <= 1024.  The backward
+ * folds dgamma/dbeta in a fixed order (deterministic); workspace >=
+ * diagmm_layernorm_bwd_workspace(M, D) bytes. */
+DIAGMM_API int diagmm_layernorm_fwd(int M, int D, float eps, const void* x, const float* w,
+                                    const float* b, void* y, float* mean, float* rstd,
+                                    void* stream);
+DIAGMM_API size_t diagmm_layernorm_bwd_workspace(int M, int D);
+DIAGMM_API int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy, const float* w,
+                                    const float* mean, const float* rstd, void* dx, float* dw,
+                                    float* db, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- dense-equivalent route (reference's own BLAS switch) ---------------
  * The reference multiplies the materialized matrix with BLAS when the
  * structural density reaches 1/4 (diagcore.py:226-228) and computes dW

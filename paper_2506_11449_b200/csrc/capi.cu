@@ -35,6 +35,10 @@ int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, c
 int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
+int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
+size_t ln_bwd_workspace(int, int);
+int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
+               void*, size_t, cudaStream_t);
 constexpr int kSumsqScratch = 296;
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
@@ -164,6 +168,17 @@ int diagmm_clip_scale_tree(int n, const double* partial, double max_norm, double
                            void* stream) {
   if (n < 1) return DIAGMM_ESHAPE;
   return run_clip_scale_tree(n, partial, max_norm, norm, scale, S(stream));
+}
+
+int diagmm_layernorm_fwd(int M, int D, float eps, const void* x, const float* w, const float* b, void* y,
+                         float* mean, float* rstd, void* stream) {
+  return run_ln_fwd(M, D, eps, x, w, b, y, mean, rstd, S(stream));
+}
+size_t diagmm_layernorm_bwd_workspace(int M, int D) { return ln_bwd_workspace(M, D); }
+int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy, const float* w, const float* mean,
+                         const float* rstd, void* dx, float* dw, float* db, void* workspace, size_t ws_bytes,
+                         void* stream) {
+  return run_ln_bwd(M, D, x, dy, w, mean, rstd, dx, dw, db, workspace, ws_bytes, S(stream));
 }
 
 int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, const uint8_t* clamped,

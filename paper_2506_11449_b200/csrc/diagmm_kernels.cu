@@ -428,7 +428,6 @@ k_split_reduce(int B, int out_w, int nsplit, const typename Vec<T>::A* __restric
 constexpr int kDwPosWarps = 2;                         // warps along positions
 constexpr int kDwTile = kDwPosWarps * kWarpPos;        // 256 positions per CTA
 constexpr int kDwGroups = kWarps / kDwPosWarps;        // 4 diagonal groups
-constexpr int kJWMax = 16;                             // diagonals per warp (16, or 8 for small problems)
 constexpr int kDwNG = 2;                               // row groups per staged chunk
 
 template <typename T>
@@ -649,32 +648,123 @@ k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
 }
 
 // --------------------------------------------------------------------------- dense route
+// W_K (M, N) row-major in the activation type, written in ONE coalesced pass
+// (no memset): entry (r, c) belongs to offset o = (r - c) mod M (tall/square,
+// t = c) or (c - r) mod N (wide, t = r); a per-CTA offset -> slot table says
+// whether o is active.  8 consecutive columns per thread, 16-byte stores when
+// aligned.  (materialize, diagcore.py:153-159, with the weights of layers.py:235.)
+constexpr int kMatRows = 8;
 template <typename T>
-__global__ void k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals,
-                              const double* __restrict__ asoft, const int32_t* __restrict__ active,
-                              const int32_t* __restrict__ n_act_p, int max_act, T* __restrict__ w) {
-  using A = typename Traits<T>::A;
-  const int j = blockIdx.y;
+__global__ void __launch_bounds__(256)
+k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
+              const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+              T* __restrict__ w, int vec) {
+  extern __shared__ int s_slot[];  // C entries
+  const int C = max(M, N), L = min(M, N);
   const int n_act = min(*n_act_p, max_act);
-  if (j >= n_act) return;
-  const int L = min(M, N);
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= L) return;
-  const int o = active[j];
-  const A sc = asoft ? (A)asoft[o] : A(1);
-  int r, c;
-  if (M >= N) { r = o + t; r = r >= M ? r - M : r; c = t; } else { r = t; c = o + t; c = c >= N ? c - N : c; }
-  w[(size_t)r * N + c] = from_acc<T>(sc * (A)vals[(size_t)o * L + t]);
+  for (int i = threadIdx.x; i < C; i += blockDim.x) s_slot[i] = -1;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n_act; j += blockDim.x) s_slot[active[j]] = j;
+  __syncthreads();
+  const bool tall = M >= N;
+  const int r0 = blockIdx.x * kMatRows;
+  const int chunks = (N + 7) / 8;
+  for (int it = threadIdx.x; it < kMatRows * chunks; it += blockDim.x) {
+    const int rr = it / chunks, ch = it - rr * chunks;
+    const int r = r0 + rr;
+    if (r >= M) continue;
+    T outv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = ch * 8 + e;
+      float v = 0.f;
+      double vd = 0.0;
+      if (c < N) {
+        int o = tall ? r - c : c - r;
+        const int mod = tall ? M : N;
+        o = o < 0 ? o + mod : o;
+        const int t = tall ? c : r;
+        if (s_slot[o] >= 0) {
+          const double sc = asoft ? asoft[o] : 1.0;
+          vd = sc * (double)vals[(size_t)o * L + t];
+        }
+      }
+      v = (float)vd;
+      if constexpr (sizeof(T) == 8) outv[e] = (T)vd;
+      else outv[e] = from_acc<T>(v);
+    }
+    T* dst = w + (size_t)r * N + ch * 8;
+    if (vec && ch * 8 + 8 <= N) {
+      if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(outv);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; e += 16 / (int)sizeof(T))
+          *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(outv + e);
+      }
+    } else {
+      for (int e = 0; e < 8 && ch * 8 + e < N; ++e) dst[e] = outv[e];
+    }
+  }
 }
 
+// Dense dW -> per-diagonal rows, pass 1: a CTA stages a tile of dW (coalesced)
+// and writes, for every ACTIVE offset crossing the tile, the unscaled entries
+// gw[o, t] into row o of g_values (runs of consecutive t: coalesced).
+constexpr int kGTr = 32, kGTc = 128;  // tile along the "other" axis x along t
 template <typename P>
 __global__ void __launch_bounds__(256)
-k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ vals,
-               const double* __restrict__ asoft, const int32_t* __restrict__ slot,
-               const int32_t* __restrict__ n_act_p, P* __restrict__ g_values, double* __restrict__ g_soft) {
+k_gather_tiles(int M, int N, const P* __restrict__ dW, const int32_t* __restrict__ slot,
+               const int32_t* __restrict__ n_act_p, P* __restrict__ g_values) {
+  __shared__ P tile[kGTr][kGTc + 1];
+  const bool tall = M >= N;
+  const int L = min(M, N);
+  // t axis = columns (tall) or rows (wide); "u" axis = the other one
+  const int t0 = blockIdx.x * kGTc, u0 = blockIdx.y * kGTr;
+  const int Tn = tall ? N : M, Un = tall ? M : N;
+  for (int i = threadIdx.x; i < kGTr * kGTc; i += blockDim.x) {
+    int uu, tt;
+    if (tall) { uu = i / kGTc; tt = i - uu * kGTc; }   // rows = u, contiguous along t (cols)
+    else { tt = i / kGTr; uu = i - tt * kGTr; }        // rows = t, contiguous along u (cols)
+    const int u = u0 + uu, t = t0 + tt;
+    P v = P(0);
+    if (u < Un && t < Tn) v = tall ? dW[(size_t)u * N + t] : dW[(size_t)t * N + u];
+    tile[uu][tt] = v;
+  }
+  // diagonals crossing the tile: delta = uu - tt in (-(kGTc-1), kGTr-1]; offset o = (u - t) mod C
+  __shared__ int s_act[kGTr + kGTc];
+  const int C = max(M, N);
+  const int n_act = *n_act_p;
+  for (int dl = threadIdx.x; dl < kGTr + kGTc - 1; dl += blockDim.x) {
+    int o = (u0 - t0 + dl - (kGTc - 1)) % C;
+    o = o < 0 ? o + C : o;
+    const int sl = slot[o];
+    s_act[dl] = (sl >= 0 && sl < n_act) ? o : -1;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int dl = warp; dl < kGTr + kGTc - 1; dl += blockDim.x >> 5) {
+    const int delta = dl - (kGTc - 1);
+    const int o = s_act[dl];
+    if (o < 0) continue;
+    const int tt_lo = delta < 0 ? -delta : 0;
+    const int tt_hi = min(kGTc, kGTr - delta);
+    for (int tt = tt_lo + lane; tt < tt_hi; tt += 32) {
+      const int t = t0 + tt, u = u0 + tt + delta;
+      if (t < L && u < Un) g_values[(size_t)o * L + t] = tile[tt + delta][tt];
+    }
+  }
+}
+
+// pass 2 (per candidate row): inactive rows -> 0; active rows -> g_soft from the
+// unscaled gw, then scale by alpha_soft in place (layers.py:159-165).
+template <typename P>
+__global__ void __launch_bounds__(256)
+k_gather_finish(int C, int L, const P* __restrict__ vals, const double* __restrict__ asoft,
+                const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, P* __restrict__ g_values,
+                double* __restrict__ g_soft) {
   __shared__ double red[32];
   const int i = blockIdx.x;
-  const int L = min(M, N);
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
   if (s < 0 || s >= *n_act_p) {
@@ -685,11 +775,9 @@ k_gather_dense(int M, int N, const P* __restrict__ dW, const P* __restrict__ val
   const double sc = asoft ? asoft[i] : 1.0;
   double local = 0.0;
   for (int t = threadIdx.x; t < L; t += blockDim.x) {
-    int r, c;
-    if (M >= N) { r = i + t; r = r >= M ? r - M : r; c = t; } else { r = t; c = i + t; c = c >= N ? c - N : c; }
-    const double gw = (double)dW[(size_t)r * N + c];
-    grow[t] = (P)(sc * gw);
+    const double gw = (double)grow[t];
     local += gw * (double)vals[(size_t)i * L + t];
+    grow[t] = (P)(sc * gw);
   }
   if (g_soft) {
     double tot = block_sum(local, red);
@@ -930,23 +1018,27 @@ template <typename T>
 int run_materialize(int M, int N, const void* vals, const double* asoft, const int32_t* active,
                     const int32_t* n_act, int max_act, void* w, cudaStream_t st) {
   using P = typename Traits<T>::P;
-  const int L = M < N ? M : N;
-  cudaMemsetAsync(w, 0, (size_t)M * N * sizeof(T), st);
-  if (max_act > 0) {
-    dim3 grid(ceil_div(L, 256), max_act);
-    k_materialize<T><<<grid, 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, active, n_act, max_act,
-                                            static_cast<T*>(w));
-    note_launch();
-  }
+  const int C = M > N ? M : N;
+  const size_t sm = (size_t)C * sizeof(int);
+  if (sm > 200 * 1024) return DIAGMM_ETOOLARGE;
+  cudaFuncSetAttribute(k_materialize<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int vec = (N % 8 == 0) && aligned16(w);
+  k_materialize<T><<<ceil_div(M, kMatRows), 256, sm, st>>>(M, N, static_cast<const P*>(vals), asoft, active, n_act,
+                                                          max_act, static_cast<T*>(w), vec);
+  note_launch();
   return status_from_cuda();
 }
 
 template <typename P>
 int run_gather_dense(int M, int N, const void* dW, const void* vals, const double* asoft, const int32_t* slot,
                      const int32_t* n_act, void* g_values, double* g_soft, cudaStream_t st) {
-  const int C = M > N ? M : N;
-  k_gather_dense<P><<<C, 256, 0, st>>>(M, N, static_cast<const P*>(dW), static_cast<const P*>(vals), asoft, slot,
-                                       n_act, static_cast<P*>(g_values), g_soft);
+  const int C = M > N ? M : N, L = M < N ? M : N;
+  const bool tall = M >= N;
+  dim3 grid(ceil_div(L, kGTc), ceil_div(tall ? M : N, kGTr));
+  k_gather_tiles<P><<<grid, 256, 0, st>>>(M, N, static_cast<const P*>(dW), slot, n_act, static_cast<P*>(g_values));
+  note_launch();
+  k_gather_finish<P><<<C, 256, 0, st>>>(C, L, static_cast<const P*>(vals), asoft, slot, n_act,
+                                        static_cast<P*>(g_values), g_soft);
   note_launch();
   return status_from_cuda();
 }

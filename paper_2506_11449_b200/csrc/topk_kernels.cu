@@ -234,26 +234,41 @@ k_active_from_list(int C, int n, const int32_t* __restrict__ offs, int32_t* __re
   if (threadIdx.x == 0 && n_act) *n_act = n;
 }
 
-// Deterministic block reductions over per-thread partials.
+// Deterministic block reductions over per-thread partials: a fixed shuffle
+// tree inside each warp, then warp 0 folds the 32 warp results (2 barriers).
 __device__ double block_reduce_sum(double v, double* buf) {
-  buf[threadIdx.x] = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) buf[w] = v;
   __syncthreads();
-  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
-    if (threadIdx.x < s) buf[threadIdx.x] += buf[threadIdx.x + s];
-    __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) buf[32] = r;
   }
-  double r = buf[0];
+  __syncthreads();
+  r = buf[32];
   __syncthreads();
   return r;
 }
 __device__ double block_reduce_max(double v, double* buf) {
-  buf[threadIdx.x] = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) buf[w] = v;
   __syncthreads();
-  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
-    if (threadIdx.x < s) buf[threadIdx.x] = fmax(buf[threadIdx.x], buf[threadIdx.x + s]);
-    __syncthreads();
+  double r = -CUDART_INF;
+  if (w == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : -CUDART_INF;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) buf[32] = r;
   }
-  double r = buf[0];
+  __syncthreads();
+  r = buf[32];
   __syncthreads();
   return r;
 }

@@ -355,3 +355,42 @@ def clip_scale(partials: torch.Tensor, max_norm: float):
     _lib.call("diagmm_clip_scale", partials.numel(), _p(partials.contiguous()), float(max_norm), _p(norm),
               _p(scale), _stream(partials))
     return norm, scale
+
+
+class FusedLayerNorm(torch.autograd.Function):
+    """LayerNorm over the last dim for bf16 activations with float32 affine
+    parameters (csrc/norm_kernels.cu) — the ViT caller's norm around DiagLinear."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, eps):
+        _need_cuda(x, weight, bias)
+        D = x.shape[-1]
+        x2 = x.reshape(-1, D).to(torch.bfloat16).contiguous()
+        M = x2.shape[0]
+        y = torch.empty_like(x2)
+        mean = torch.empty(M, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(M, dtype=torch.float32, device=x.device)
+        w = weight.detach().float().contiguous()
+        b = bias.detach().float().contiguous()
+        _lib.call("diagmm_layernorm_fwd", M, D, float(eps), _p(x2), _p(w), _p(b), _p(y), _p(mean), _p(rstd),
+                  _stream(x2))
+        ctx.save_for_backward(x2, w, mean, rstd)
+        ctx.shape, ctx.in_dtype = x.shape, x.dtype
+        return y.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, w, mean, rstd = ctx.saved_tensors
+        M, D = x2.shape
+        g = dy.reshape(M, D).to(torch.bfloat16).contiguous()
+        dx = torch.empty_like(x2)
+        dw = torch.empty(D, dtype=torch.float32, device=x2.device)
+        db = torch.empty(D, dtype=torch.float32, device=x2.device)
+        ws = _workspace(x2.device, _lib.load().diagmm_layernorm_bwd_workspace(M, D))
+        _lib.call("diagmm_layernorm_bwd", M, D, _p(x2), _p(g), _p(w), _p(mean), _p(rstd), _p(dx), _p(dw), _p(db),
+                  _p(ws), ws.numel(), _stream(x2))
+        return dx.view(ctx.shape).to(ctx.in_dtype), dw, db, None
+
+
+def layer_norm_bf16(x, weight, bias, eps: float = 1e-5):
+    return FusedLayerNorm.apply(x, weight, bias, eps)

@@ -16,8 +16,28 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
+from . import ops
 from .layer import DiagLinear, preselect
 from .selection import TemperatureSchedule
+
+
+try:  # library attention kernel for the caller (not the DiagLinear hot path)
+    from flash_attn import flash_attn_qkvpacked_func as _flash_qkvpacked
+except Exception:  # noqa: BLE001 - optional: SDPA is used without it
+    _flash_qkvpacked = None
+
+
+class LayerNorm(nn.LayerNorm):
+    """nn.LayerNorm that runs the fused bf16 kernel (csrc/norm_kernels.cu) when
+    the activations are bf16 (directly or under CUDA autocast); float32 params."""
+
+    def forward(self, x):
+        bf16 = x.dtype == torch.bfloat16 or (torch.is_autocast_enabled("cuda")
+                                              and torch.get_autocast_dtype("cuda") == torch.bfloat16)
+        D = x.shape[-1]
+        if x.is_cuda and bf16 and self.elementwise_affine and D % 8 == 0 and D <= 1024:
+            return ops.layer_norm_bf16(x, self.weight, self.bias, self.eps)
+        return super().forward(x)
 
 
 @dataclass(frozen=True)
@@ -53,18 +73,22 @@ class Block(nn.Module):
         super().__init__()
         d = cfg.dim
         self.heads = cfg.heads
-        self.norm1 = nn.LayerNorm(d)
+        self.norm1 = LayerNorm(d)
         self.qkv = _sparse(d, 3 * d, cfg, 4 * idx, t_schedule, route, dense=not cfg.sparse_qkv)
         self.proj = _sparse(d, d, cfg, 4 * idx + 1, t_schedule, route)
-        self.norm2 = nn.LayerNorm(d)
+        self.norm2 = LayerNorm(d)
         self.fc1 = _sparse(d, cfg.mlp_ratio * d, cfg, 4 * idx + 2, t_schedule, route)
         self.fc2 = _sparse(cfg.mlp_ratio * d, d, cfg, 4 * idx + 3, t_schedule, route)
 
     def forward(self, x):
         B, T, D = x.shape
         h = self.qkv(self.norm1(x)).view(B, T, 3, self.heads, D // self.heads)
-        q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
-        a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
+        if _flash_qkvpacked is not None and h.dtype in (torch.bfloat16, torch.float16):
+            # packed q/k/v in, packed dq/dk/dv out: no unbind/stack copies
+            a = _flash_qkvpacked(h).reshape(B, T, D)
+        else:
+            q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
+            a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
         x = x + self.proj(a)
         return x + self.fc2(F.gelu(self.fc1(self.norm2(x)), approximate="tanh"))
 
@@ -82,7 +106,7 @@ class ViT(nn.Module):
             self.cls = nn.Parameter(torch.zeros(1, 1, cfg.dim))
             self.pos = nn.Parameter(torch.randn(1, cfg.tokens, cfg.dim) * 0.02)
             self.blocks = nn.ModuleList(Block(cfg, i, t_schedule, route) for i in range(cfg.depth))
-            self.norm = nn.LayerNorm(cfg.dim)
+            self.norm = LayerNorm(cfg.dim)
             self.head = nn.Linear(cfg.dim, cfg.classes)
 
     def diag_layers(self):

@@ -474,3 +474,23 @@ def test_tape_adapter_matches_reference_op(shape, with_alpha):
         assert scaled_err(at.grad, ref[2]) < 1e-10
     with pytest.raises(ShapeMismatch):
         record_diag_matmul(tape, _Tensor(np.zeros((2, N + 1))), vt, weights, active, _Cache(M, N), False)
+
+
+@pytest.mark.parametrize("M,D", [(1, 8), (37, 192), (2048, 768), (5, 1000)])
+def test_fused_layernorm_matches_torch_fp32(M, D):
+    """Caller kernel: fused bf16 LayerNorm vs a plain PyTorch fp32 reference."""
+    torch.manual_seed(0)
+    x = torch.randn(M, D, device=DEV).to(torch.bfloat16).requires_grad_(True)
+    w = (1 + 0.1 * torch.randn(D, device=DEV)).requires_grad_(True)
+    b = (0.1 * torch.randn(D, device=DEV)).requires_grad_(True)
+    g = torch.randn(M, D, device=DEV).to(torch.bfloat16)
+    y = ops.layer_norm_bf16(x, w, b, 1e-5)
+    y.backward(g)
+    xr = x.detach().float().requires_grad_(True)
+    wr, br = w.detach().clone().requires_grad_(True), b.detach().clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (D,), wr, br, 1e-5)
+    yr.backward(g.float())
+    assert (y.float() - yr).abs().max() <= 2e-2 * max(1.0, yr.abs().max().item())
+    assert (x.grad.float() - xr.grad).abs().max() <= 2e-2 * max(1.0, xr.grad.abs().max().item())
+    torch.testing.assert_close(w.grad, wr.grad, rtol=1e-3, atol=1e-3 * M ** 0.5)
+    torch.testing.assert_close(b.grad, br.grad, rtol=1e-3, atol=1e-3 * M ** 0.5)
