@@ -259,7 +259,8 @@ def main():
     per_fn = prof.totals_ms()
     # dominant = the C-ABI function (our kernels) with the most device time in a
     # step, among those whose algorithmic work is modelled (profiling.work)
-    modelled = {nm for nm, a, _, _ in prof.records if profiling.work(nm, a) is not None}
+    modelled = {nm for nm, a, _, _ in prof.records
+                if profiling.work(nm, a) is not None and nm in profiling.SECTION8_KERNELS}
     cands = {k: v for k, v in per_fn.items() if k in modelled}
     dominant = max(cands, key=cands.get) if cands else None
 
@@ -308,6 +309,9 @@ def main():
     nact_of = {(m.out_features, m.in_features): m.k for m in model.diag_layers()}
     roof = (profiling.roofline(dom_timer.records, peaks, peaks_kind, FMA_FP32_TFLOPS, nact_of)
             if dominant else None)
+    if roof is not None:
+        roof["traffic"] = profiling.measured_traffic(dominant)
+        roof["scope"] = "dominant SURVEY §8 kernel (C-ABI call) of the timed step, CUDA events on its stream"
 
     extras = {}
     if not args.no_extras and rank == 0:

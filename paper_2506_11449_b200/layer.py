@@ -254,7 +254,7 @@ class DiagLinear(nn.Module):
         a_soft = ops.soft_topk(self.alpha.detach(), self.k, self.t_schedule.t_final)
         vals = a_soft[sel].to(self.values.dtype)[:, None] * self.values.detach()[sel]
         w = DiagMatrix(self.out_features, self.in_features, sel, vals)
-        return FrozenDiagLinear(w, None if self.bias is None else self.bias.detach().clone())
+        return FrozenDiagLinear(w, None if self.bias is None else self.bias.detach().clone(), route=self.route)
 
     # ---- forward ----------------------------------------------------------------
     def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
@@ -284,22 +284,45 @@ class DiagLinear(nn.Module):
 
 
 class FrozenDiagLinear(nn.Module):
-    """Inference layer over a fixed diagonal matrix (layers.py:290-310)."""
+    """Inference layer over a fixed diagonal matrix (layers.py:290-310).
 
-    def __init__(self, weight: DiagMatrix, bias: torch.Tensor | None = None):
+    ``route`` as for DiagLinear: "auto" multiplies bf16 batches of >= 512 tokens
+    with the dense-equivalent matrix on the tensor cores (materialized once per
+    dtype and cached: the weights are frozen) and smaller batches with the
+    diagonal kernel (K1)."""
+
+    def __init__(self, weight: DiagMatrix, bias: torch.Tensor | None = None, route: str = "auto"):
         super().__init__()
+        if route not in ROUTES:
+            raise ValueError(f"route must be one of {ROUTES}")
         self.weight = weight
+        self.route = route
         self.in_features, self.out_features = weight.cols, weight.rows
         self.register_buffer("store", weight.store())
         self.register_buffer("bias", bias)
         self._sel = weight.selection()
+        self._dense = {}
+
+    def _dense_weight(self, dtype: torch.dtype) -> torch.Tensor:
+        W = self._dense.get(dtype)
+        if W is None:
+            W = ops.materialize(self.store, self._sel, self.out_features, self.in_features, dtype)
+            self._dense[dtype] = W
+        return W
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         lead = x.shape[:-1]
         x2 = _flatten(x, self.in_features)
         if self.store.dtype == torch.float64:
             x2 = x2.double()
-        y = ops.diag_forward(x2, self.store, self._sel, self.out_features, self.in_features, self.bias)
+        elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
+            x2 = x2.to(torch.get_autocast_dtype("cuda"))
+        dense = self.route == "dense" or (self.route == "auto" and x2.dtype == torch.bfloat16
+                                          and x2.shape[0] >= dense_route_min_tokens())
+        if dense:
+            y = F.linear(x2, self._dense_weight(x2.dtype), None if self.bias is None else self.bias.to(x2.dtype))
+        else:
+            y = ops.diag_forward(x2, self.store, self._sel, self.out_features, self.in_features, self.bias)
         return y.reshape(*lead, self.out_features)
 
 

@@ -19,6 +19,29 @@ from . import _lib
 
 _ELT = {0: 8, 1: 4, 2: 2}
 
+# C-ABI entry points that implement SURVEY §8 (a) rows (the roofline candidates)
+SECTION8_KERNELS = {
+    "diagmm_forward", "diagmm_backward_input", "diagmm_backward_weight", "diagmm_topk_waterfill",
+    "diagmm_topk_waterfill_batched", "diagmm_topk_grad", "diagmm_adamw", "diagmm_adamw_multi",
+    "diagmm_sumsq_multi", "diagmm_materialize", "diagmm_gather_dense_grad",
+}
+
+
+def measured_traffic(name: str):
+    """dram bytes (read + write) per launch of ``name`` from the committed ncu
+    --set full capture (profiles/*traffic*.json), or None."""
+    import json
+    from pathlib import Path
+
+    for f in sorted(Path(__file__).resolve().parents[1].glob("profiles/*traffic*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+        except (OSError, ValueError):
+            continue
+        if name in d:
+            return d[name]
+    return None
+
 
 class CallTimer:
     """Context manager: CUDA events around every C-ABI call (or only ``only``)."""
@@ -98,6 +121,9 @@ def work(name, args, nact_of=None):
         return 0.0, float(sum(25 * jobs[i].C for i in range(n)))
     if name == "diagmm_topk_waterfill":
         return 0.0, 25.0 * args[0]
+    if name == "diagmm_topk_grad":
+        # alpha, g_soft read and g_alpha written (f64), clamped (u8); + g_alpha read if accumulating
+        return 0.0, (25.0 + 8.0 * bool(args[8])) * args[0]
     if name == "diagmm_adamw":
         dt, n = args[0], args[1]
         return 0.0, 7 * (8 if dt == 0 else 4) * n
