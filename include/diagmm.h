@@ -234,13 +234,14 @@ DIAGMM_API int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy,
  * The reference multiplies the materialized matrix with BLAS when the
  * structural density reaches 1/4 (diagcore.py:226-228) and computes dW
  * densely then gathers (layers.py:150-153).  diagmm_materialize writes
- * W_K (M, N) row-major in `dtype` (zeros off the active diagonals);
+ * W_K (M, N) row-major in `dtype` (zeros off the active diagonals) in one
+ * coalesced pass, looking offsets up in `slot` (C,) from the selection;
  * diagmm_gather_dense_grad turns a dense dW (M, N, float32/float64 = param
  * type) into g_values / g_soft exactly like diagmm_backward_weight. */
 DIAGMM_API int diagmm_materialize(int dtype, int M, int N, const void* values,
                        const double* alpha_soft, const int32_t* active,
-                       const int32_t* n_act, int max_act, void* w_dense,
-                       void* stream);
+                       const int32_t* slot, const int32_t* n_act, int max_act,
+                       void* w_dense, void* stream);
 DIAGMM_API int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW,
                              const void* values, const double* alpha_soft,
                              const int32_t* active, const int32_t* slot,

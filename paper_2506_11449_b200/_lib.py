@@ -39,7 +39,7 @@ SIGNATURES = {
     "diagmm_sumsq_scratch_len": (_i, []),
     "diagmm_sumsq": (_i, [_i, _sz, _vp, _vp, _vp, _vp]),
     "diagmm_clip_scale": (_i, [_i, _vp, _d, _vp, _vp, _vp]),
-    "diagmm_materialize": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
+    "diagmm_materialize": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
     "diagmm_gather_dense_grad": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 

@@ -15,7 +15,7 @@ int run_dw(int, int, int, const void*, const void*, const void*, const double*, 
            const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
 template <typename T>
 int run_materialize(int, int, const void*, const double*, const int32_t*, const int32_t*, int, void*,
-                    cudaStream_t);
+                    cudaStream_t);  // (slot, n_act)
 template <typename P>
 int run_gather_dense(int, int, const void*, const void*, const double*, const int32_t*, const int32_t*,
                      void*, double*, cudaStream_t);
@@ -229,10 +229,12 @@ int diagmm_clip_scale(int n, const double* partial, double max_norm, double* nor
 }
 
 int diagmm_materialize(int dtype, int M, int N, const void* values, const double* alpha_soft,
-                       const int32_t* active, const int32_t* n_act, int max_act, void* w_dense,
-                       void* stream) {
+                       const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act,
+                       void* w_dense, void* stream) {
   if (int e = check_shape(M, N, 0, max_act)) return e;
-  DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, active, n_act, max_act, w_dense,
+  if (slot == nullptr) return DIAGMM_ESHAPE;
+  (void)active;
+  DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, slot, n_act, max_act, w_dense,
                   S(stream))
 }
 

@@ -409,6 +409,142 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
   }
 }
 
+// --------------------------------------------------------------------------- narrow batches
+// B <= kNarrowB: the weights dominate the traffic (HBM-bound regime), so they
+// are streamed ONCE in their stored fp32/fp64 form and scaled on the fly (no
+// prescale pass, no staging); the few input rows come through L1.  A CTA is
+// 128 positions (lane + 32u) x one chunk of the diagonal list; its 8 warps
+// interleave over the chunk and are folded in a fixed order; chunks (grid.y)
+// are folded by k_split_reduce in a fixed order.
+constexpr int kNarrowB = 8;
+template <typename T, int BT, bool GATHER>
+__global__ void __launch_bounds__(kThreads)
+k_product_narrow(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
+                 const double* __restrict__ asoft, const int32_t* __restrict__ active,
+                 const int32_t* __restrict__ n_act_p, int max_act, const typename Traits<T>::P* __restrict__ bias,
+                 T* __restrict__ out, typename Vec<T>::A* __restrict__ part, int nchunk) {
+  using A = typename Vec<T>::A;
+  __shared__ A red[kWarps][kWarpPos];
+  const int n_act = min(*n_act_p, max_act);
+  const int in_w = GATHER ? C : L, out_w = GATHER ? L : C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p0 = blockIdx.x * kWarpPos;
+  const int per = (n_act + nchunk - 1) / nchunk;
+  const int jb = min(n_act, (int)blockIdx.y * per), je = min(n_act, jb + per);
+  A acc[BT][kU];
+#pragma unroll
+  for (int b = 0; b < BT; ++b)
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[b][u] = A(0);
+  // this warp's diagonals: j = jb + warp + 8q.  Offsets/scales of 32 of them
+  // are fetched lane-parallel, then 4 diagonals' weights are loaded together
+  // (16 independent loads per lane in flight) before they are used.
+  const int nq = je - jb - warp > 0 ? (je - jb - warp + kWarps - 1) / kWarps : 0;
+  constexpr int UNR = 4;
+  for (int q0 = 0; q0 < nq; q0 += 32) {
+    int o_l = 0;
+    double s_l = 0.0;
+    if (q0 + lane < nq) {
+      o_l = __ldg(active + jb + warp + kWarps * (q0 + lane));
+      s_l = asoft ? asoft[o_l] : 1.0;
+    }
+    const int cnt = min(32, nq - q0);
+    for (int qq = 0; qq < cnt; qq += UNR) {
+      A wv[UNR][kU];
+      typename Traits<T>::P wraw[UNR][kU];
+      int xi[UNR][kU];
+      // raw weights first (they depend only on the offset), the scale after
+#pragma unroll
+      for (int r = 0; r < UNR; ++r) {
+        const int o = __shfl_sync(0xffffffffu, o_l, (qq + r) & 31);
+        const bool live = qq + r < cnt;
+        const typename Traits<T>::P* vr = vals + (size_t)o * L;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int p = p0 + lane + kWarp * u;
+          int c, xx;
+          bool ok;
+          if (GATHER) {
+            c = p; ok = p < L;
+            xx = p + o; xx = xx >= C ? xx - C : xx;
+          } else {
+            c = p - o; c = c < 0 ? c + C : c;
+            ok = p < C && c < L;
+            xx = c;
+          }
+          ok = ok && live;
+          wraw[r][u] = ok ? __ldg(vr + c) : typename Traits<T>::P(0);
+          xi[r][u] = ok ? xx : 0;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < UNR; ++r) {
+        const double sc = __shfl_sync(0xffffffffu, s_l, (qq + r) & 31);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) wv[r][u] = (A)(sc * (double)wraw[r][u]);
+      }
+#pragma unroll
+      for (int r = 0; r < UNR; ++r)
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int b = 0; b < BT; ++b)
+            if (b < B) acc[b][u] = fma(wv[r][u], to_acc<A>(__ldg(in + (size_t)b * in_w + xi[r][u])), acc[b][u]);
+    }
+  }
+  // fixed-order fold of the 8 warps, one batch row at a time
+#pragma unroll
+  for (int b = 0; b < BT; ++b) {
+    if (b >= B) break;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) red[warp][lane + kWarp * u] = acc[b][u];
+    __syncthreads();
+    for (int tt = threadIdx.x; tt < kWarpPos; tt += kThreads) {
+      const int p = p0 + tt;
+      if (p >= out_w) continue;
+      A s_ = A(0);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s_ += red[w][tt];
+      if (nchunk == 1) {
+        if (bias) s_ += (A)bias[p];
+        out[(size_t)b * out_w + p] = from_acc<T>(s_);
+      } else {
+        part[((size_t)blockIdx.y * B + b) * out_w + p] = s_;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// dW for narrow batches: one warp per diagonal, lanes over 128 positions, the
+// B-row contraction in registers; unscaled gw -> partial (finalized by
+// k_dw_finalize exactly like the wide path).
+template <typename T, int BT>
+__global__ void __launch_bounds__(kThreads)
+k_dw_narrow(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
+            const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+            typename Vec<T>::A* __restrict__ gw) {
+  using A = typename Vec<T>::A;
+  const int n_act = min(*n_act_p, max_act);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.y * kWarps + warp;
+  if (j >= n_act) return;
+  const int o = __ldg(active + j);
+  const int t0 = blockIdx.x * kWarpPos;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int t = t0 + lane + kWarp * u;
+    if (t >= L) continue;
+    int ca = o + t;
+    ca = ca >= C ? ca - C : ca;
+    A acc = A(0);
+#pragma unroll
+    for (int b = 0; b < BT; ++b)
+      if (b < B) acc = fma(to_acc<A>(__ldg(aop + (size_t)b * C + ca)), to_acc<A>(__ldg(bop + (size_t)b * L + t)), acc);
+    gw[(size_t)j * L + t] = acc;
+  }
+}
+
 // Fixed-order sum of the split partials (+ bias).
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -593,8 +729,14 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   const int n_act = min(*n_act_p, max_act);
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
+  constexpr int W = 16 / sizeof(P);
+  const bool vec = L % W == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0;
   if (s < 0 || s >= n_act) {
-    for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+    if (vec) {
+      for (int t = threadIdx.x; t < L / W; t += blockDim.x) reinterpret_cast<uint4*>(grow)[t] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+    }
     if (g_soft && threadIdx.x == 0) g_soft[i] = 0.0;
     return;
   }
@@ -653,55 +795,58 @@ k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
 // t = c) or (c - r) mod N (wide, t = r); a per-CTA offset -> slot table says
 // whether o is active.  8 consecutive columns per thread, 16-byte stores when
 // aligned.  (materialize, diagcore.py:153-159, with the weights of layers.py:235.)
-constexpr int kMatRows = 8;
+constexpr int kMatRows = 2;
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
-              const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+              const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
               T* __restrict__ w, int vec) {
-  extern __shared__ int s_slot[];  // C entries
-  const int C = max(M, N), L = min(M, N);
+  using P = typename Traits<T>::P;
+  const int L = min(M, N);
   const int n_act = min(*n_act_p, max_act);
-  for (int i = threadIdx.x; i < C; i += blockDim.x) s_slot[i] = -1;
-  __syncthreads();
-  for (int j = threadIdx.x; j < n_act; j += blockDim.x) s_slot[active[j]] = j;
-  __syncthreads();
   const bool tall = M >= N;
+  const int mod = tall ? M : N;
   const int r0 = blockIdx.x * kMatRows;
   const int chunks = (N + 7) / 8;
   for (int it = threadIdx.x; it < kMatRows * chunks; it += blockDim.x) {
     const int rr = it / chunks, ch = it - rr * chunks;
     const int r = r0 + rr;
     if (r >= M) continue;
-    T outv[8];
+    // branch-free: the 8 slot lookups, then the 8 value loads, all in flight
+    int oo[8];
+    bool on[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int c = ch * 8 + e;
-      float v = 0.f;
-      double vd = 0.0;
-      if (c < N) {
-        int o = tall ? r - c : c - r;
-        const int mod = tall ? M : N;
-        o = o < 0 ? o + mod : o;
-        const int t = tall ? c : r;
-        if (s_slot[o] >= 0) {
-          const double sc = asoft ? asoft[o] : 1.0;
-          vd = sc * (double)vals[(size_t)o * L + t];
-        }
-      }
-      v = (float)vd;
+      int o = tall ? r - c : c - r;
+      o = o < 0 ? o + mod : o;
+      oo[e] = c < N ? o : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int sl = __ldg(slot + oo[e]);
+      on[e] = ch * 8 + e < N && sl >= 0 && sl < n_act;
+    }
+    P raw[8];
+    double sc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = tall ? ch * 8 + e : r;
+      raw[e] = on[e] ? __ldg(vals + (size_t)oo[e] * L + t) : P(0);
+      sc[e] = on[e] ? (asoft ? __ldg(asoft + oo[e]) : 1.0) : 0.0;
+    }
+    T outv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const double vd = sc[e] * (double)raw[e];
       if constexpr (sizeof(T) == 8) outv[e] = (T)vd;
-      else outv[e] = from_acc<T>(v);
+      else outv[e] = from_acc<T>((float)vd);
     }
     T* dst = w + (size_t)r * N + ch * 8;
     if (vec && ch * 8 + 8 <= N) {
-      if constexpr (sizeof(T) == 2) {
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(outv);
-      } else {
 #pragma unroll
-        for (int e = 0; e < 8; e += 16 / (int)sizeof(T))
-          *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(outv + e);
-      }
+      for (int e = 0; e < 8; e += 16 / (int)sizeof(T))
+        *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(outv + e);
     } else {
       for (int e = 0; e < 8 && ch * 8 + e < N; ++e) dst[e] = outv[e];
     }
@@ -722,14 +867,24 @@ k_gather_tiles(int M, int N, const P* __restrict__ dW, const int32_t* __restrict
   // t axis = columns (tall) or rows (wide); "u" axis = the other one
   const int t0 = blockIdx.x * kGTc, u0 = blockIdx.y * kGTr;
   const int Tn = tall ? N : M, Un = tall ? M : N;
-  for (int i = threadIdx.x; i < kGTr * kGTc; i += blockDim.x) {
+  constexpr int kPer = kGTr * kGTc / 256;  // elements per thread; all loads in flight first
+  P v[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * 256;
     int uu, tt;
     if (tall) { uu = i / kGTc; tt = i - uu * kGTc; }   // rows = u, contiguous along t (cols)
     else { tt = i / kGTr; uu = i - tt * kGTr; }        // rows = t, contiguous along u (cols)
     const int u = u0 + uu, t = t0 + tt;
-    P v = P(0);
-    if (u < Un && t < Tn) v = tall ? dW[(size_t)u * N + t] : dW[(size_t)t * N + u];
-    tile[uu][tt] = v;
+    v[k] = (u < Un && t < Tn) ? (tall ? __ldg(dW + (size_t)u * N + t) : __ldg(dW + (size_t)t * N + u)) : P(0);
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * 256;
+    int uu, tt;
+    if (tall) { uu = i / kGTc; tt = i - uu * kGTc; }
+    else { tt = i / kGTr; uu = i - tt * kGTr; }
+    tile[uu][tt] = v[k];
   }
   // diagonals crossing the tile: delta = uu - tt in (-(kGTc-1), kGTr-1]; offset o = (u - t) mod C
   __shared__ int s_act[kGTr + kGTc];
@@ -767,8 +922,13 @@ k_gather_finish(int C, int L, const P* __restrict__ vals, const double* __restri
   const int i = blockIdx.x;
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
+  constexpr int W = 16 / sizeof(P);
   if (s < 0 || s >= *n_act_p) {
-    for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+    if (L % W == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0) {
+      for (int t = threadIdx.x; t < L / W; t += blockDim.x) reinterpret_cast<uint4*>(grow)[t] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+    }
     if (g_soft && threadIdx.x == 0) g_soft[i] = 0.0;
     return;
   }
@@ -860,6 +1020,45 @@ static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, 
   note_launch();
 }
 
+static int narrow_chunks(int out_w, int max_act) {
+  const int blocks = ceil_div(out_w, kWarpPos);
+  int nc = ceil_div(2 * num_sms(), blocks);
+  const int max_nc = max_act / 32 > 1 ? max_act / 32 : 1;  // >= 4 diagonals per warp
+  return nc < max_nc ? nc : max_nc;
+}
+
+template <typename T>
+static int run_product_narrow(bool gather, int B, int C, int L, const void* in, const void* vals, const double* asoft,
+                              const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
+                              typename Vec<T>::A* part, cudaStream_t st) {
+  using P = typename Traits<T>::P;
+  const int out_w = gather ? L : C;
+  const int nc = narrow_chunks(out_w, max_act);
+  dim3 grid(ceil_div(out_w, kWarpPos), nc);
+  auto tin = static_cast<const T*>(in);
+  auto tv = static_cast<const P*>(vals);
+  auto tb = static_cast<const P*>(bias);
+  auto to = static_cast<T*>(out);
+#define DIAGMM_NARROW(BT)                                                                                       \
+  if (B <= BT) {                                                                                                \
+    if (gather)                                                                                                 \
+      k_product_narrow<T, BT, true><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc);  \
+    else                                                                                                        \
+      k_product_narrow<T, BT, false><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc); \
+  } else
+  DIAGMM_NARROW(1) DIAGMM_NARROW(2) DIAGMM_NARROW(4) DIAGMM_NARROW(8) {}
+#undef DIAGMM_NARROW
+  note_launch();
+  if (nc > 1) {
+    const size_t n = (size_t)B * out_w;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    k_split_reduce<T><<<blocks, 256, 0, st>>>(B, out_w, nc, part, tb, to);
+    note_launch();
+  }
+  return status_from_cuda();
+}
+
 // workspace = [compact weights (max_act x ldw) | split partials]
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
@@ -867,7 +1066,9 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   const int out_w = gather ? L : C, cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
   const size_t wbytes = align16((size_t)(max_act > 0 ? max_act : 1) * w_ld<T>(out_w) * sizeof(typename WType<T>::type));
-  return wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
+  const size_t narrow = B <= kNarrowB ? (size_t)narrow_chunks(out_w, max_act) * B * out_w * sizeof(A) : 0;
+  const size_t wide = wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
+  return wide > narrow ? wide : narrow;
 }
 
 template <typename T>
@@ -880,6 +1081,8 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
   if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
+  if (B <= kNarrowB) return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
+                                                 static_cast<A*>(ws), st);
   const int out_w = gather ? L : C, in_w = gather ? C : L;
   const int cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
@@ -983,7 +1186,13 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   int* ctr = reinterpret_cast<int*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +
                                     align16((size_t)cparts * M * sizeof(A)));
-  if (B > 0 && max_act > 0) {
+  if (B > 0 && B <= 2 * kNarrowB && max_act > 0) {
+    parts = 1;
+    dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
+    if (B <= 4) k_dw_narrow<T, 4><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
+    else k_dw_narrow<T, 16><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
+    note_launch();
+  } else if (B > 0 && max_act > 0) {
     const int dwj = dw_diags(L, max_act);
     const int cap = dw_win_cap<T>(C, max_act, dwj);
     const size_t sm = dw_smem<T>(cap);
@@ -1015,16 +1224,12 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
 }
 
 template <typename T>
-int run_materialize(int M, int N, const void* vals, const double* asoft, const int32_t* active,
+int run_materialize(int M, int N, const void* vals, const double* asoft, const int32_t* slot,
                     const int32_t* n_act, int max_act, void* w, cudaStream_t st) {
   using P = typename Traits<T>::P;
-  const int C = M > N ? M : N;
-  const size_t sm = (size_t)C * sizeof(int);
-  if (sm > 200 * 1024) return DIAGMM_ETOOLARGE;
-  cudaFuncSetAttribute(k_materialize<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int vec = (N % 8 == 0) && aligned16(w);
-  k_materialize<T><<<ceil_div(M, kMatRows), 256, sm, st>>>(M, N, static_cast<const P*>(vals), asoft, active, n_act,
-                                                          max_act, static_cast<T*>(w), vec);
+  k_materialize<T><<<ceil_div(M, kMatRows), 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, slot, n_act,
+                                                         max_act, static_cast<T*>(w), vec);
   note_launch();
   return status_from_cuda();
 }

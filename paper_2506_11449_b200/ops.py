@@ -298,7 +298,7 @@ def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
         raise TypeError(f"cannot materialize {values.dtype} values as {dtype}")
     W = torch.empty(M, N, dtype=dtype, device=values.device)
     _lib.call("diagmm_materialize", _code(dtype), M, N, _p(values.contiguous()), _p(sel.alpha_soft),
-              _p(sel.active), _p(sel.n_act), C, _p(W), _stream(values))
+              _p(sel.active), _p(sel.slot), _p(sel.n_act), C, _p(W), _stream(values))
     return W
 
 

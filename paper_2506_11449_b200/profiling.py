@@ -102,7 +102,7 @@ def work(name, args, nact_of=None):
         return flops, byts
     if name == "diagmm_materialize":
         dt, M, N = args[0], args[1], args[2]
-        n = _n_act(args, name, nact_of) or args[7]
+        n = _n_act(args, name, nact_of) or args[8]
         return 0.0, _ELT[dt] * M * N + 4 * n * min(M, N)
     if name == "diagmm_gather_dense_grad":
         dt, M, N = args[0], args[1], args[2]
@@ -169,21 +169,24 @@ def roofline(records, peaks: dict, peaks_kind: str, fma_tflops: float, nact_of=N
 # ------------------------------------------------------------------ kernel section
 def _time_call(fn, reps: int, flush: torch.Tensor | None):
     """Device time of one call of ``fn`` (ms): ``reps`` calls, each preceded by an
-    L2 flush (a 256 MB write), captured in a CUDA graph and replayed, minus a
-    graph of the flushes alone — so neither Python/ctypes launch overhead nor the
-    flush is counted, and every call starts from a cold L2."""
+    L2 flush (a READ of a 256 MB buffer: it evicts L2 without leaving dirty lines
+    whose write-back would compete with the timed kernel), captured in a CUDA
+    graph and replayed, minus a graph of the flushes alone — so neither
+    Python/ctypes launch overhead nor the flush is counted, and every call
+    starts from a cold L2."""
     fn()
     torch.cuda.synchronize()
     g_work, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    sink = torch.empty(1, device=flush.device) if flush is not None else None
     with torch.cuda.graph(g_work):
         for _ in range(reps):
             if flush is not None:
-                flush.add_(1.0)
+                torch.amax(flush, dim=0, keepdim=True, out=sink)
             fn()
     with torch.cuda.graph(g_flush):
         for _ in range(reps):
             if flush is not None:
-                flush.add_(1.0)
+                torch.amax(flush, dim=0, keepdim=True, out=sink)
 
     def timed(g):
         g.replay()
@@ -261,4 +264,4 @@ def diagmm_config1(peaks, peaks_kind, fma_tflops):
         sweep.append(diag_case(dim, dim, B, s, torch.bfloat16, peaks, fma_tflops, reps=10, flush=flush))
     return {"config1": cfg1, "sweep_4096": sweep, "hbm_peak_gbs": peaks["hbm_gbs"],
             "fma_peak_tflops": fma_tflops, "peaks": peaks_kind,
-            "note": "L2 flushed (256 MB write) before every timed launch; median of reps"}
+            "note": "L2 flushed (256 MB read) before every timed launch; mean of reps, CUDA-graph replay minus flush-only replay"}

@@ -11,7 +11,8 @@ peaks = json.load(open("MEASURED_PEAKS.json")) if __import__("os").path.exists("
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
 cases = [(3072, 768, 256, 0.9, torch.float32), (768, 3072, 256, 0.9, torch.float32),
          (3072, 768, 256, 0.9, torch.bfloat16), (3072, 768, 4096, 0.9, torch.bfloat16),
-         (768, 3072, 4096, 0.9, torch.bfloat16), (4096, 4096, 1, 0.9, torch.bfloat16),
+         (768, 3072, 4096, 0.9, torch.bfloat16), (4096, 4096, 1, 0.9, torch.bfloat16), (4096, 4096, 8, 0.9, torch.bfloat16),
+         (4096, 4096, 16, 0.9, torch.bfloat16), (4096, 4096, 1, 0.99, torch.bfloat16),
          (4096, 4096, 64, 0.9, torch.bfloat16), (4096, 4096, 1024, 0.9, torch.bfloat16),
          (4096, 4096, 1024, 0.99, torch.bfloat16), (4096, 4096, 8192, 0.9, torch.bfloat16),
          (3072, 768, 50432, 0.9, torch.bfloat16)]
