@@ -216,6 +216,15 @@ DIAGMM_API int diagmm_sumsq_multi(int n, const diagmm_tensor* tensors, double* p
 DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_norm,
                                       double* norm, double* scale, void* stream);
 
+/* ---- tensor-core route (tcgen05 + TMEM + TMA) -----------------------------
+ * out[m, n] = sum_k A[m, k] * B[n, k] (+ bias[n]); A (Mdim, K), B (Ndim, K)
+ * bf16 row-major (k contiguous, 16-byte aligned, K % 8 == 0), fp32
+ * accumulation, out bf16 with row stride ldo.  The dense-equivalent DiagMM:
+ * forward with A = x, B = W_K (diagmm_materialize), input gradient with
+ * A = dy, B = W_K^T (the reference's dense switch, diagcore.py:226-228). */
+DIAGMM_API int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B,
+                                   const float* bias, void* out, int ldo, void* stream);
+
 /* ---- fused LayerNorm for the bf16 activations of the ViT caller ----------
  * Not a reference symbol: the caller's LayerNorm (vit.py) around DiagLinear.
  * x, y, dy, dx: (M, D) bf16 row-major; w, b, dw, db: (D,) float; mean, rstd:
@@ -242,6 +251,11 @@ DIAGMM_API int diagmm_materialize(int dtype, int M, int N, const void* values,
                        const double* alpha_soft, const int32_t* active,
                        const int32_t* slot, const int32_t* n_act, int max_act,
                        void* w_dense, void* stream);
+/* W_K^T (N, M) row-major: the B operand of the tensor-core input gradient. */
+DIAGMM_API int diagmm_materialize_transposed(int dtype, int M, int N, const void* values,
+                       const double* alpha_soft, const int32_t* active,
+                       const int32_t* slot, const int32_t* n_act, int max_act,
+                       void* w_dense_t, void* stream);
 DIAGMM_API int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW,
                              const void* values, const double* alpha_soft,
                              const int32_t* active, const int32_t* slot,

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libdiagmm.so"
-SOURCES = ["diagmm_kernels.cu", "topk_kernels.cu", "optim_kernels.cu", "norm_kernels.cu", "capi.cu"]
+SOURCES = ["diagmm_kernels.cu", "topk_kernels.cu", "optim_kernels.cu", "norm_kernels.cu", "tc_kernels.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -32,7 +32,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [CSRC / "common.cuh", ROOT / "include" / "diagmm.h"]
+    deps = [CSRC / s for s in SOURCES] + [CSRC / "common.cuh", CSRC / "tc_gemm.cuh", ROOT / "include" / "diagmm.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 

@@ -15,7 +15,7 @@ int run_dw(int, int, int, const void*, const void*, const void*, const double*, 
            const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
 template <typename T>
 int run_materialize(int, int, const void*, const double*, const int32_t*, const int32_t*, int, void*,
-                    cudaStream_t);  // (slot, n_act)
+                    cudaStream_t, bool);  // (slot, n_act, ..., transposed)
 template <typename P>
 int run_gather_dense(int, int, const void*, const void*, const double*, const int32_t*, const int32_t*,
                      void*, double*, cudaStream_t);
@@ -35,6 +35,7 @@ int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, c
 int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
+int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
@@ -170,6 +171,11 @@ int diagmm_clip_scale_tree(int n, const double* partial, double max_norm, double
   return run_clip_scale_tree(n, partial, max_norm, norm, scale, S(stream));
 }
 
+int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out,
+                        int ldo, void* stream) {
+  return run_tc_gemm_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, S(stream));
+}
+
 int diagmm_layernorm_fwd(int M, int D, float eps, const void* x, const float* w, const float* b, void* y,
                          float* mean, float* rstd, void* stream) {
   return run_ln_fwd(M, D, eps, x, w, b, y, mean, rstd, S(stream));
@@ -235,7 +241,17 @@ int diagmm_materialize(int dtype, int M, int N, const void* values, const double
   if (slot == nullptr) return DIAGMM_ESHAPE;
   (void)active;
   DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, slot, n_act, max_act, w_dense,
-                  S(stream))
+                  S(stream), false)
+}
+
+int diagmm_materialize_transposed(int dtype, int M, int N, const void* values, const double* alpha_soft,
+                                  const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act,
+                                  void* w_dense_t, void* stream) {
+  if (int e = check_shape(M, N, 0, max_act)) return e;
+  if (slot == nullptr) return DIAGMM_ESHAPE;
+  (void)active;
+  DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, slot, n_act, max_act, w_dense_t,
+                  S(stream), true)
 }
 
 int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW, const void* values,

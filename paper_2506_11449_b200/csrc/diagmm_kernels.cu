@@ -796,7 +796,8 @@ k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
 // whether o is active.  8 consecutive columns per thread, 16-byte stores when
 // aligned.  (materialize, diagcore.py:153-159, with the weights of layers.py:235.)
 constexpr int kMatRows = 2;
-template <typename T>
+// TRANS: write W_K^T (N, M) instead (the B operand of the tensor-core dX).
+template <typename T, bool TRANS>
 __global__ void __launch_bounds__(256)
 k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
               const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
@@ -806,33 +807,35 @@ k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, cons
   const int n_act = min(*n_act_p, max_act);
   const bool tall = M >= N;
   const int mod = tall ? M : N;
+  const int R = TRANS ? N : M, Cc = TRANS ? M : N;  // output rows / cols
   const int r0 = blockIdx.x * kMatRows;
-  const int chunks = (N + 7) / 8;
+  const int chunks = (Cc + 7) / 8;
   for (int it = threadIdx.x; it < kMatRows * chunks; it += blockDim.x) {
     const int rr = it / chunks, ch = it - rr * chunks;
-    const int r = r0 + rr;
-    if (r >= M) continue;
+    const int orow = r0 + rr;
+    if (orow >= R) continue;
     // branch-free: the 8 slot lookups, then the 8 value loads, all in flight
-    int oo[8];
+    int oo[8], tt[8];
     bool on[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int c = ch * 8 + e;
+      const int ocol = ch * 8 + e;
+      const int r = TRANS ? ocol : orow, c = TRANS ? orow : ocol;  // entry (r, c) of W_K
       int o = tall ? r - c : c - r;
       o = o < 0 ? o + mod : o;
-      oo[e] = c < N ? o : 0;
+      oo[e] = ocol < Cc ? o : 0;
+      tt[e] = tall ? c : r;
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int sl = __ldg(slot + oo[e]);
-      on[e] = ch * 8 + e < N && sl >= 0 && sl < n_act;
+      on[e] = ch * 8 + e < Cc && sl >= 0 && sl < n_act;
     }
     P raw[8];
     double sc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int t = tall ? ch * 8 + e : r;
-      raw[e] = on[e] ? __ldg(vals + (size_t)oo[e] * L + t) : P(0);
+      raw[e] = on[e] ? __ldg(vals + (size_t)oo[e] * L + tt[e]) : P(0);
       sc[e] = on[e] ? (asoft ? __ldg(asoft + oo[e]) : 1.0) : 0.0;
     }
     T outv[8];
@@ -842,13 +845,13 @@ k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, cons
       if constexpr (sizeof(T) == 8) outv[e] = (T)vd;
       else outv[e] = from_acc<T>((float)vd);
     }
-    T* dst = w + (size_t)r * N + ch * 8;
-    if (vec && ch * 8 + 8 <= N) {
+    T* dst = w + (size_t)orow * Cc + ch * 8;
+    if (vec && ch * 8 + 8 <= Cc) {
 #pragma unroll
       for (int e = 0; e < 8; e += 16 / (int)sizeof(T))
         *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(outv + e);
     } else {
-      for (int e = 0; e < 8 && ch * 8 + e < N; ++e) dst[e] = outv[e];
+      for (int e = 0; e < 8 && ch * 8 + e < Cc; ++e) dst[e] = outv[e];
     }
   }
 }
@@ -1225,11 +1228,13 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
 
 template <typename T>
 int run_materialize(int M, int N, const void* vals, const double* asoft, const int32_t* slot,
-                    const int32_t* n_act, int max_act, void* w, cudaStream_t st) {
+                    const int32_t* n_act, int max_act, void* w, cudaStream_t st, bool trans) {
   using P = typename Traits<T>::P;
-  const int vec = (N % 8 == 0) && aligned16(w);
-  k_materialize<T><<<ceil_div(M, kMatRows), 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, slot, n_act,
-                                                         max_act, static_cast<T*>(w), vec);
+  const int R = trans ? N : M, Cc = trans ? M : N;
+  const int vec = (Cc % 8 == 0) && aligned16(w);
+  auto k = trans ? k_materialize<T, true> : k_materialize<T, false>;
+  k<<<ceil_div(R, kMatRows), 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, slot, n_act, max_act,
+                                           static_cast<T*>(w), vec);
   note_launch();
   return status_from_cuda();
 }
@@ -1259,7 +1264,7 @@ int run_gather_dense(int M, int N, const void* dW, const void* vals, const doubl
                          const int32_t*, const int32_t*, const int32_t*, int, void*, double*, void*,      \
                          void*, size_t, cudaStream_t);                                                    \
   template int run_materialize<T>(int, int, const void*, const double*, const int32_t*, const int32_t*,   \
-                                  int, void*, cudaStream_t);
+                                  int, void*, cudaStream_t, bool);
 DIAGMM_INST(double)
 DIAGMM_INST(float)
 DIAGMM_INST(__nv_bfloat16)

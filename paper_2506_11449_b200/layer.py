@@ -105,6 +105,15 @@ def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype
     return 4 * sel.host_count() * L >= spec.M * spec.N
 
 
+def _tc_ok(x: torch.Tensor, M: int, N: int) -> bool:
+    """The tcgen05 route takes bf16 activations with 16-byte rows (M, N % 8 == 0).
+    DIAGMM_DENSE_BACKEND=cublas selects the library GEMM instead (A/B comparisons)."""
+    import os
+
+    return (x.dtype == torch.bfloat16 and M % 8 == 0 and N % 8 == 0
+            and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas")
+
+
 def dense_route_min_tokens() -> int:
     """Token count from which the bf16 tensor-core route beats the FMA route
     (measured on B200, profiles/r01_*; override with DIAGMM_DENSE_MIN_TOKENS)."""
@@ -126,13 +135,18 @@ class DiagMMFunction(torch.autograd.Function):
         dense = _use_dense(spec, sel, x.shape[0], x.dtype)
         vals = values.detach()
         W = None
-        if dense:
+        tc = dense and _tc_ok(x, M, N)
+        if tc:
+            # tensor-core route: our tcgen05 GEMM on the dense-equivalent W_K (bias fused)
+            y = ops.tc_gemm(x.contiguous(), ops.materialize(vals, sel, M, N, dtype=x.dtype),
+                            None if bias is None else bias.detach())
+        elif dense:
             W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
             y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
         else:
             y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach())
         ctx.save_for_backward(x, values, alpha)
-        ctx.sel, ctx.spec, ctx.W, ctx.has_bias = sel, spec, W, bias is not None
+        ctx.sel, ctx.spec, ctx.W, ctx.has_bias, ctx.tc = sel, spec, W, bias is not None, tc
         return y
 
     @staticmethod
@@ -144,10 +158,13 @@ class DiagMMFunction(torch.autograd.Function):
         vals = values.detach()
         dx = g_alpha = None
         need_soft = alpha is not None and ctx.needs_input_grad[2]
-        if W is not None:
-            dy = dy.to(W.dtype)
+        if W is not None or ctx.tc:
+            dy = dy.to(x.dtype)
             if ctx.needs_input_grad[0]:
-                dx = dy @ W
+                if ctx.tc:  # dx = dy @ W_K = tcgen05 GEMM against W_K^T
+                    dx = ops.tc_gemm(dy, ops.materialize(vals, sel, M, N, dtype=x.dtype, transposed=True))
+                else:
+                    dx = dy @ W
             out_dt = vals.dtype
             dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
                 else (dy.t() @ x.to(dy.dtype)).to(out_dt)
@@ -319,7 +336,9 @@ class FrozenDiagLinear(nn.Module):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))
         dense = self.route == "dense" or (self.route == "auto" and x2.dtype == torch.bfloat16
                                           and x2.shape[0] >= dense_route_min_tokens())
-        if dense:
+        if dense and _tc_ok(x2, self.out_features, self.in_features):
+            y = ops.tc_gemm(x2.contiguous(), self._dense_weight(x2.dtype), self.bias)
+        elif dense:
             y = F.linear(x2, self._dense_weight(x2.dtype), None if self.bias is None else self.bias.to(x2.dtype))
         else:
             y = ops.diag_forward(x2, self.store, self._sel, self.out_features, self.in_features, self.bias)

@@ -287,8 +287,9 @@ def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor
 
 
 def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
-                dtype: torch.dtype | None = None) -> torch.Tensor:
-    """Dense W_K (M, N) of the active diagonals (diagcore.py:153-159 + layers.py:235)."""
+                dtype: torch.dtype | None = None, transposed: bool = False) -> torch.Tensor:
+    """Dense W_K (M, N) — or W_K^T (N, M) — of the active diagonals
+    (diagcore.py:153-159 + layers.py:235)."""
     _need_cuda(values)
     C, L = geometry(M, N)
     if tuple(values.shape) != (C, L):
@@ -296,9 +297,10 @@ def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
     dtype = dtype or values.dtype
     if param_dtype_for(dtype) != values.dtype:
         raise TypeError(f"cannot materialize {values.dtype} values as {dtype}")
-    W = torch.empty(M, N, dtype=dtype, device=values.device)
-    _lib.call("diagmm_materialize", _code(dtype), M, N, _p(values.contiguous()), _p(sel.alpha_soft),
-              _p(sel.active), _p(sel.slot), _p(sel.n_act), C, _p(W), _stream(values))
+    W = torch.empty((N, M) if transposed else (M, N), dtype=dtype, device=values.device)
+    _lib.call("diagmm_materialize_transposed" if transposed else "diagmm_materialize", _code(dtype), M, N,
+              _p(values.contiguous()), _p(sel.alpha_soft), _p(sel.active), _p(sel.slot), _p(sel.n_act), C, _p(W),
+              _stream(values))
     return W
 
 
@@ -394,3 +396,18 @@ class FusedLayerNorm(torch.autograd.Function):
 
 def layer_norm_bf16(x, weight, bias, eps: float = 1e-5):
     return FusedLayerNorm.apply(x, weight, bias, eps)
+
+
+def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) -> torch.Tensor:
+    """out = a @ b.T (+ bias) on the tcgen05 tensor cores (bf16 in/out, fp32 accumulate)."""
+    _need_cuda(a, b)
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or a.dim() != 2 or b.dim() != 2:
+        raise TypeError("tc_gemm takes 2-D bfloat16 operands")
+    if a.shape[1] != b.shape[1]:
+        raise ShapeMismatch(f"inner dims differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty(a.shape[0], b.shape[0], dtype=torch.bfloat16, device=a.device)
+    bz = None if bias is None else bias.float().contiguous()
+    _lib.call("diagmm_tc_gemm_bf16", a.shape[0], b.shape[0], a.shape[1], _p(a), _p(b), _p(bz), _p(out), out.shape[1],
+              _stream(a))
+    return out

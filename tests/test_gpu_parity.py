@@ -494,3 +494,58 @@ def test_fused_layernorm_matches_torch_fp32(M, D):
     assert (x.grad.float() - xr.grad).abs().max() <= 2e-2 * max(1.0, xr.grad.abs().max().item())
     torch.testing.assert_close(w.grad, wr.grad, rtol=1e-3, atol=1e-3 * M ** 0.5)
     torch.testing.assert_close(b.grad, br.grad, rtol=1e-3, atol=1e-3 * M ** 0.5)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 200, 72), (1, 8, 8), (1000, 768, 3072), (4096, 2304, 768)])
+def test_tc_gemm_matches_fp32_reference(M, N, K):
+    """tcgen05 GEMM (TMA + TMEM): bf16 in, fp32 accumulate, bf16 out, fused bias."""
+    torch.manual_seed(M + N + K)
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = torch.randn(N, K, device=DEV).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV)
+    out = ops.tc_gemm(a, b, bias)
+    ref = a.float() @ b.float().t() + bias
+    assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 8e-3
+    out2 = ops.tc_gemm(a, b)
+    ref2 = a.float() @ b.float().t()
+    assert ((out2.float() - ref2).abs().max() / ref2.abs().max()).item() < 8e-3
+
+
+@pytest.mark.parametrize("shape", [(3072, 768), (768, 3072), (512, 512)])
+def test_materialize_transposed_is_exact_transpose(shape):
+    M, N = shape
+    C, L = max(M, N), min(M, N)
+    rng = np.random.default_rng(4)
+    offs = np.sort(rng.choice(C, max(1, C // 10), replace=False))
+    values = torch.randn(C, L, device=DEV)
+    sel = ops.selection_from_offsets(C, torch.as_tensor(offs, device=DEV))
+    for dt in (torch.bfloat16, torch.float32):
+        W = ops.materialize(values, sel, M, N, dtype=dt)
+        Wt = ops.materialize(values, sel, M, N, dtype=dt, transposed=True)
+        assert torch.equal(W.t().contiguous(), Wt)
+    ref = oracle.dense_matrix(M, N, [int(o) for o in offs], values[torch.as_tensor(offs, device=DEV)].double().cpu().numpy())
+    np.testing.assert_array_equal(ops.materialize(values.double(), sel, M, N).cpu().numpy(), ref)
+
+
+def test_tensor_core_route_matches_oracle():
+    """DiagLinear bf16 with >= 512 tokens runs the tcgen05 route (fwd, dX) and
+    matches the float64 oracle within the bf16 tolerance."""
+    n_in, n_out, B, T = 768, 3072, 1024, 0.05
+    ref = olayer.OracleDiagLayer(n_in, n_out, 0.9, t_kind="constant", t_init=T, t_final=T, t_total=1,
+                                 l1_coeff=0.0, seed=3)
+    rng = np.random.default_rng(9)
+    ref.alpha = ref.alpha + rng.standard_normal(ref.C)
+    x = rng.standard_normal((B, n_in))
+    up = rng.standard_normal((B, n_out))
+    y_ref, cache = ref.forward(x, 0)
+    g_ref = ref.backward(up, cache)
+    lyr = DiagLinear(n_in, n_out, 0.9, seed=3, l1_coeff=0.0, dtype=torch.float32, route="auto",
+                     t_schedule=TemperatureSchedule("constant", T, T, 1))
+    with torch.no_grad():
+        lyr.alpha.copy_(torch.as_tensor(ref.alpha, device=DEV))
+    xt = torch.as_tensor(x, dtype=torch.float32, device=DEV).to(torch.bfloat16).requires_grad_(True)
+    y = lyr(xt, step=0)
+    y.backward(torch.as_tensor(up, device=DEV).to(torch.bfloat16))
+    assert scaled_err(y.float().detach().cpu().numpy(), y_ref) < BF16_TOL
+    assert scaled_err(xt.grad.float().cpu().numpy(), g_ref["x"]) < BF16_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) < BF16_TOL
