@@ -36,6 +36,7 @@ int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
 int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, cudaStream_t);
+int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
@@ -174,6 +175,12 @@ int diagmm_clip_scale_tree(int n, const double* partial, double max_norm, double
 int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out,
                         int ldo, void* stream) {
   return run_tc_gemm_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, S(stream));
+}
+
+// internal (not in the header): 2:4 sparse tensor-core throughput probe
+DIAGMM_API int diagmm_internal_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void* B, void* out,
+                                               void* stream) {
+  return run_tc_sparse_probe(Mdim, Ndim, K, Acomp, B, out, S(stream));
 }
 
 int diagmm_layernorm_fwd(int M, int D, float eps, const void* x, const float* w, const float* b, void* y,

@@ -189,6 +189,205 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   }
 }
 
+template <int BN>
+struct SmemSp {  // 2:4-compressed A: half the K bytes
+  static constexpr size_t a_bytes = (size_t)BM * BK;
+  static constexpr size_t b_bytes = (size_t)BN * BK * 2;
+  static constexpr size_t stage = a_bytes + b_bytes;
+  static constexpr size_t c_bytes = (size_t)BM * BN;
+  static constexpr size_t bars = 128 + BN * 4;
+  static constexpr size_t total = 1024 + kStages * stage + c_bytes + bars;
+};
+
+__device__ __forceinline__ uint64_t smem_desc_sw64(const void* p) {  // K-major, 64-byte swizzle, SBO 512 B
+  const uint64_t a = (smem_u32(p) & 0x3FFFFu) >> 4;
+  return a | (1ull << 16) | (32ull << 32) | (1ull << 46) | (4ull << 61);
+}
+
+__device__ __forceinline__ void umma_sp_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t tmem_e,
+                                             uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(tmem_e), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_gemm_sp(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+          const __grid_constant__ CUtensorMap tc_out, int Mdim, int Ndim, int K, const float* __restrict__ bias) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using S = SmemSp<BN>;
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + kStages * S::a_bytes;
+  unsigned char* sC = smem + kStages * S::stage;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + S::c_bytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KB = (K + BK - 1) / BK;
+  const int nb = (Ndim + BN - 1) / BN;
+  const int tiles = ((Mdim + BM - 1) / BM) * nb;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])) : "memory");
+    }
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&tempty[i])) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+    prefetch_tmap(&tc_out);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= 2 && warp < 6) {  // probe metadata: idx (0,1) in every group of 4
+    const uint32_t taddr = *tslot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(2 * BN);
+    const uint32_t v = 0x44444444u;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer, running ahead across tiles
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kStages, round = it / kStages;
+          mbar_wait_parity(&empty[s], (round & 1) ^ 1);
+          mbar_expect_tx(&full[s], (uint32_t)S::stage);
+          tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
+          tma_load_2d(sB + s * S::b_bytes, &tb, kb * BK, n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer (one thread for the whole CTA)
+      constexpr uint32_t idesc = idesc_bf16(BM, BN) | (1u << 2);  // sparse
+      const uint32_t tmem_e = tmem + (uint32_t)(2 * BN);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int ab = i & 1;
+        mbar_wait_parity(&tempty[ab], ((i >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(ab * BN);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kStages, round = it / kStages;
+          mbar_wait_parity(&full[s], round & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc_sw64(sA + s * S::a_bytes);
+          const uint64_t db = smem_desc_sw128(sB + s * S::b_bytes);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)  // logical K = 32 per sparse MMA: A +32 B, B +64 B
+            umma_sp_bf16(acc, da + 2 * k, db + 4 * k, tmem_e, idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        umma_commit(&tfull[ab]);
+      }
+    }
+  } else {  // ---- epilogue: warps 2..9; warp w reads TMEM lanes 32*(w%4), column half (w-2)/4
+    // TMEM -> registers (32 columns at a time) -> +bias, bf16 -> the 128B-swizzled
+    // smem tile (one 64-column box per 16 KB) -> TMA bulk tensor store.
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int rl = q * 32 + lane;  // row within the tile
+    const int et = threadIdx.x - 64;  // epilogue thread id
+    const bool leader = et == 0;
+    float* sbias = reinterpret_cast<float*>(tslot + 4);  // BN floats after the barriers
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int ab = i & 1;
+      const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
+      // the previous tile's TMA store must have finished reading sC / sbias users done
+      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int c = et; c < BN; c += kEpiThreads) sbias[c] = (bias && n0 + c < Ndim) ? __ldg(bias + n0 + c) : 0.f;
+      mbar_wait_parity(&tfull[ab], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // two halves of BN/2 columns through the same 32 KB staging tile; the 8
+      // warps split each half (warps 2-5 the first BN/4 columns, 6-9 the next)
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        if (hh == 1) {
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 128; ++cc) {
+          const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float a = __uint_as_float(r[2 * j]) + sbias[c * 32 + 2 * j];
+            const float b = __uint_as_float(r[2 * j + 1]) + sbias[c * 32 + 2 * j + 1];
+            __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          const int cl = c - hh * (BN / 64);  // chunk within this half
+          unsigned char* box = sC + (size_t)(cl >> 1) * (BM * 128);
+          const int ch0 = (cl & 1) * 4;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int chunk = (ch0 + j) ^ (rl & 7);
+            *reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+        if (hh == 1) {  // accumulator consumed: hand it back to the MMA thread
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (leader) {
+#pragma unroll
+          for (int bx = 0; bx < BN / 128; ++bx) {
+            const int col = n0 + hh * (BN / 2) + bx * 64;
+            if (col >= Ndim) break;
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tc_out)),
+                         "r"(col), "r"(m0), "r"(smem_u32(sC + (size_t)bx * (BM * 128)))
+                         : "memory");
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -215,6 +414,36 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 }
 
 }  // namespace tc
+
+// Throughput probe of 2:4-sparse tcgen05.mma.sp (constant metadata; NOT a
+// correct product): A is (Mdim, K/2) compressed bf16.
+int run_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void* B, void* out, cudaStream_t st) {
+  using namespace tc;
+  constexpr int BN = 128;
+  CUtensorMap ta, tb, tco;
+  auto fn = encode_fn();
+  if (!fn) return DIAGMM_ECUDA;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)(K / 2), (cuuint64_t)Mdim};
+    cuuint64_t strides[1] = {(cuuint64_t)(K / 2) * 2};
+    cuuint32_t box[2] = {32, (cuuint32_t)BM};
+    cuuint32_t estr[2] = {1, 1};
+    if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(Acomp), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return DIAGMM_ECUDA;
+  }
+  if (!make_tmap_bf16(&tb, B, (uint64_t)Ndim, (uint64_t)K, BN, (uint64_t)K) ||
+      !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)Ndim))
+    return DIAGMM_ECUDA;
+  auto k = k_tc_gemm_sp<BN>;
+  const size_t sm = SmemSp<BN>::total;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k<<<grid, kThreads, sm, st>>>(ta, tb, tco, Mdim, Ndim, K, nullptr);
+  return status_from_cuda();
+}
 
 int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
                      cudaStream_t st) {
