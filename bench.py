@@ -225,7 +225,7 @@ def main():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = model(imgs)
         loss = F.cross_entropy(logits.float(), lbls, label_smoothing=0.1)
-        for pen in penalties(model):
+        for pen in penalties(model, fused=True):  # l1 gradient folded into K5
             loss = loss + pen
         loss.backward()
         if world > 1:

@@ -225,6 +225,20 @@ DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_n
 DIAGMM_API int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B,
                                    const float* bias, void* out, int ldo, void* stream);
 
+/* K3 on the tensor cores (bf16 activations): gw = diagonal entries of
+ * dy^T x computed by tcgen05 MMAs over token tiles (split-K across CTAs), the
+ * gather onto the active diagonals fused into the epilogue (the dense dW is
+ * never written), then finalized exactly like diagmm_backward_weight:
+ * g_values (C, L) float (active rows = alpha_soft * gw, others 0), g_soft
+ * (may be NULL).  Replaces the dense branch of layers.py:150-153 + 159-165.
+ * M, N multiples of 64; dy (B, M), x (B, N) bf16, 16-byte aligned. */
+DIAGMM_API size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act);
+DIAGMM_API int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x,
+                                         const void* values, const double* alpha_soft,
+                                         const int32_t* slot, const int32_t* n_act, int max_act,
+                                         void* g_values, double* g_soft, void* workspace,
+                                         size_t ws_bytes, void* stream);
+
 /* ---- fused LayerNorm for the bf16 activations of the ViT caller ----------
  * Not a reference symbol: the caller's LayerNorm (vit.py) around DiagLinear.
  * x, y, dy, dx: (M, D) bf16 row-major; w, b, dw, db: (D,) float; mean, rstd:

@@ -37,6 +37,9 @@ int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
 int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, cudaStream_t);
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
+size_t tc_dw_workspace(int, int, int, int);
+int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
+                   const int32_t*, int, void*, double*, void*, size_t, cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
@@ -175,6 +178,19 @@ int diagmm_clip_scale_tree(int n, const double* partial, double max_norm, double
 int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out,
                         int ldo, void* stream) {
   return run_tc_gemm_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, S(stream));
+}
+
+size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act) {
+  if (check_shape(M, N, B, max_act)) return 0;
+  return tc_dw_workspace(M, N, B, max_act);
+}
+
+int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x, const void* values,
+                              const double* alpha_soft, const int32_t* slot, const int32_t* n_act, int max_act,
+                              void* g_values, double* g_soft, void* workspace, size_t ws_bytes, void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, workspace,
+                        ws_bytes, S(stream));
 }
 
 // internal (not in the header): 2:4 sparse tensor-core throughput probe

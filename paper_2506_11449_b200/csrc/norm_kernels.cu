@@ -90,7 +90,7 @@ k_ln_fwd(int M, int D, float eps, const __nv_bfloat16* __restrict__ x, const flo
 
 // dx per row; per-CTA partial dgamma/dbeta over its rows -> part[blockIdx.x][2][D]
 template <int NV>
-__global__ void __launch_bounds__(kLnWarps * 32)
+__global__ void __launch_bounds__(kLnWarps * 32, 2)
 k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
          const float* __restrict__ w, const float* __restrict__ mean, const float* __restrict__ rstd,
          __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
@@ -105,29 +105,21 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
   for (int c = threadIdx.x; c < NV * 256; c += blockDim.x) s_w[c] = c < D ? w[c] : 0.f;
   __syncthreads();
   const int r0 = blockIdx.x * rows_per_cta, r1 = min(M, r0 + rows_per_cta);
-  // software pipeline: the next row's x / dy are in flight while this row is computed
-  uint4 nx[NV], ng[NV];
-  float nmu = 0.f, nrs = 0.f;
-  auto load_row = [&](int row) {
-    if (row >= r1) return;
+  // Two passes per row: statistics (s1, s2) and the dgamma/dbeta update, then
+  // dx — the second pass re-reads the row from L1 instead of holding it in
+  // registers, which keeps two CTAs (16 warps) resident per SM.
+#pragma unroll 1
+  for (int row = r0 + warp; row < r1; row += kLnWarps) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * D);
     const uint4* gr = reinterpret_cast<const uint4*>(dy + (size_t)row * D);
+    const float mu = mean[row], rs = rstd[row];
+    uint4 cx[NV], cg[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 8;
-      if (c < D) { nx[i] = xr[i * 32 + lane]; ng[i] = gr[i * 32 + lane]; }
-      else { nx[i] = make_uint4(0, 0, 0, 0); ng[i] = make_uint4(0, 0, 0, 0); }
+      cx[i] = c < D ? xr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
+      cg[i] = c < D ? gr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
     }
-    nmu = mean[row];
-    nrs = rstd[row];
-  };
-  load_row(r0 + warp);
-  for (int row = r0 + warp; row < r1; row += kLnWarps) {
-    uint4 cx[NV], cg[NV];  // this row, still packed (re-unpacked in the second pass)
-#pragma unroll
-    for (int i = 0; i < NV; ++i) { cx[i] = nx[i]; cg[i] = ng[i]; }
-    const float mu = nmu, rs = nrs;
-    load_row(row + kLnWarps);
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -153,8 +145,8 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
       const int c = (i * 32 + lane) * 8;
       if (c >= D) continue;
       float xh[8], g[8], o[8];
-      unpack8(cx[i], xh);
-      unpack8(cg[i], g);
+      unpack8(xr[i * 32 + lane], xh);  // L1 hit
+      unpack8(gr[i * 32 + lane], g);
       const float* wr = s_w + c;
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = rs * (g[e] * wr[e] - s1 - (xh[e] - mu) * rs * s2);

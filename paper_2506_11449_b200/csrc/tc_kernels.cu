@@ -4,6 +4,8 @@
 // (out x in); input gradient: A = dy, B = W_K^T.  See tc_gemm.cuh.
 #include <cudaTypedefs.h>
 
+#include <cmath>
+
 #include "tc_gemm.cuh"
 
 namespace diagmm {
@@ -388,6 +390,180 @@ k_tc_gemm_sp(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
   }
 }
 
+// ---------------------------------------------------------------------------
+// dW on the tensor cores with the diagonal gather fused into the epilogue.
+// D[m, n] = sum_tok dy[tok, m] * x[tok, n]: both operands MN-major (the token
+// dimension is K and is the strided one), staged as 64-element-wide TMA boxes
+// (2 for A's 128 rows, 4 for B's 256 columns) with the 128-byte swizzle.  The
+// epilogue keeps only the entries on ACTIVE diagonals and writes them, unscaled,
+// into the dW partial buffer [ksplit][slot][t] that k_dw_finalize folds (fixed
+// order), scales by alpha_soft and turns into g_values / g_soft — the dense dW
+// (M x N fp32) is never written.  K (tokens) is split across CTAs when the
+// output has fewer tiles than SMs.
+constexpr int kDwBN = 256;
+struct SmemDw {
+  static constexpr size_t a_bytes = (size_t)BM * BK * 2;      // 2 boxes of 64 x 64
+  static constexpr size_t b_bytes = (size_t)kDwBN * BK * 2;   // 4 boxes
+  static constexpr size_t stage = a_bytes + b_bytes;
+  static constexpr size_t total = 1024 + kStages * stage + 128 + 512 * 4;
+};
+
+// K-major? no: MN-major, 128-byte swizzle; LBO = next 64-element MN block (8 KB), SBO = 8 K-rows (1 KB)
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+  const uint64_t a = (smem_u32(p) & 0x3FFFFu) >> 4;
+  return a | (512ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N, int ntok,
+        int ksplit, const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
+        float* __restrict__ partial) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using S = SmemDw;
+  constexpr int BN = kDwBN;
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + kStages * S::a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::stage);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_slot = reinterpret_cast<int*>(smem + kStages * S::stage + 128);  // 384 offsets of the tile
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tall = M >= N;
+  const int C = tall ? M : N, L = tall ? N : M;
+  const int n_act = min(*n_act_p, max_act);
+  const int nb = (N + BN - 1) / BN;
+  const int otiles = ((M + BM - 1) / BM) * nb;
+  const int tiles = otiles * ksplit;
+  const int KBt = (ntok + BK - 1) / BK;                 // k-blocks in total
+  const int KBs = (KBt + ksplit - 1) / ksplit;          // per split
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])) : "memory");
+    }
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&tempty[i])) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(2 * BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int ot = t % otiles, z = t / otiles;
+        const int m0 = (ot / nb) * BM, n0 = (ot % nb) * BN;
+        const int kb0 = z * KBs, kb1 = min(KBt, kb0 + KBs);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % kStages, round = it / kStages;
+          mbar_wait_parity(&empty[s], (round & 1) ^ 1);
+          mbar_expect_tx(&full[s], (uint32_t)S::stage);
+#pragma unroll
+          for (int h = 0; h < BM / 64; ++h)
+            tma_load_2d(sA + s * S::a_bytes + h * 8192, &ta, m0 + h * 64, kb * BK, &full[s]);
+#pragma unroll
+          for (int h = 0; h < BN / 64; ++h)
+            tma_load_2d(sB + s * S::b_bytes + h * 8192, &tb, n0 + h * 64, kb * BK, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN) | (1u << 15) | (1u << 16);  // A, B MN-major
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int z = t / otiles;
+        const int kb0 = z * KBs, kb1 = min(KBt, kb0 + KBs);
+        const int ab = i & 1;
+        mbar_wait_parity(&tempty[ab], ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(ab * BN);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % kStages, round = it / kStages;
+          mbar_wait_parity(&full[s], round & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc_mn_sw128(sA + s * S::a_bytes);
+          const uint64_t db = smem_desc_mn_sw128(sB + s * S::b_bytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)  // +16 K-rows = +2048 bytes
+            umma_bf16(acc, da + 128 * k, db + 128 * k, idesc, (kb != kb0) || (k != 0));
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[ab]);
+      }
+    }
+  } else {  // ---- epilogue: gather the active diagonals out of the tile
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int ot = t % otiles, z = t / otiles;
+      const int m0 = (ot / nb) * BM, n0 = (ot % nb) * BN;
+      const int kb0 = z * KBs, kb1 = min(KBt, kb0 + KBs);
+      const int ab = i & 1;
+      // offsets crossing the tile: (m - n) or (n - m) over m0-n0+[-(BN-1), BM-1]
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int d = et; d < BM + BN - 1; d += kEpiThreads) {
+        const int delta = d - (BN - 1);  // (m - m0) - (n - n0)
+        int o = tall ? (m0 - n0 + delta) : (n0 - m0 - delta);
+        o %= C;
+        o = o < 0 ? o + C : o;
+        const int sl = slot[o];
+        s_slot[d] = (sl >= 0 && sl < n_act) ? sl : -1;
+      }
+      mbar_wait_parity(&tfull[ab], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int ml = q * 32 + lane;
+      const int m = m0 + ml;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 64; ++cc) {
+        const int c = half * (BN / 64) + cc;
+        uint32_t r[32];
+        tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int nl = c * 32 + j;
+          const int n = n0 + nl;
+          const int sl = s_slot[ml - nl + BN - 1];
+          if (sl < 0 || n >= N) continue;
+          const int tt = tall ? n : m;
+          partial[((size_t)z * max_act + sl) * L + tt] = __uint_as_float(r[j]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -442,6 +618,58 @@ int run_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void
   const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   k<<<grid, kThreads, sm, st>>>(ta, tb, tco, Mdim, Ndim, K, nullptr);
+  return status_from_cuda();
+}
+
+// dW via the tensor cores: returns the number of K splits written into
+// partial ([ksplit][max_act][L] fp32, unscaled gw by slot) or a negative status.
+int tc_dw_splits(int M, int N, int ntok) {
+  using namespace tc;
+  const int otiles = ceil_div(M, BM) * ceil_div(N, kDwBN);
+  const int kbt = ceil_div(ntok, BK);
+  const int sms = num_sms();
+  // split count with the best wave quantisation (ties: fewer splits = fewer partials)
+  int best = 1;
+  double best_eff = 0.0;
+  for (int ks = 1; ks <= 16 && ks <= kbt; ++ks) {
+    const int tiles = otiles * ks;
+    const double waves = (double)tiles / sms;
+    const double eff = waves / std::ceil(waves) * (tiles >= sms ? 1.0 : (double)tiles / sms);
+    if (eff > best_eff + 0.02) { best_eff = eff; best = ks; }
+  }
+  const int per = ceil_div(kbt, best);
+  return ceil_div(kbt, per);  // every split gets at least one k-block
+}
+
+int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
+              int max_act, float* partial, size_t partial_bytes, cudaStream_t st) {
+  using namespace tc;
+  const int L = M < N ? M : N;
+  if (M < 64 || N < 64 || M % 64 || N % 64 || ntok < 1) return DIAGMM_ESHAPE;
+  if ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x)) & 15) return DIAGMM_ESHAPE;
+  const int ks = tc_dw_splits(M, N, ntok);  // no empty split (see tc_dw_splits)
+  if (partial_bytes < (size_t)ks * max_act * L * sizeof(float)) return DIAGMM_EWORKSPACE;
+  auto fn = encode_fn();
+  if (!fn) return DIAGMM_ECUDA;
+  CUtensorMap ta, tb;
+  // MN-major boxes: 64 features (contiguous) x 64 tokens
+  auto mk = [&](CUtensorMap* map, const void* base, uint64_t cols) {
+    cuuint64_t dims[2] = {cols, (cuuint64_t)ntok};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)BK};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!mk(&ta, dy, (uint64_t)M) || !mk(&tb, x, (uint64_t)N)) return DIAGMM_ECUDA;
+  const size_t sm = SmemDw::total;
+  cudaFuncSetAttribute(k_tc_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int tiles = ceil_div(M, BM) * ceil_div(N, kDwBN) * ks;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  // partials of inactive slots are never read; active (slot, t) entries are all written
+  k_tc_dw<<<grid, kThreads, sm, st>>>(ta, tb, M, N, ntok, ks, slot, n_act, max_act, partial);
+  note_launch();
   return status_from_cuda();
 }
 

@@ -86,6 +86,7 @@ class _OpSpec:
     route: str
     fixed: ops.Selection | None = None
     presel: ops.Selection | None = None
+    l1: float = 0.0  # set by penalties(fused=True): the l1 gradient is added inside K5
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -166,9 +167,13 @@ class DiagMMFunction(torch.autograd.Function):
                 else:
                     dx = dy @ W
             out_dt = vals.dtype
-            dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
-                else (dy.t() @ x.to(dy.dtype)).to(out_dt)
-            g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
+            if ctx.tc and M % 64 == 0 and N % 64 == 0:
+                # tensor-core dW with the diagonal gather fused (no dense dW is written)
+                g_values, g_soft = ops.tc_backward_weight(dy, x.to(dy.dtype), vals, sel, M, N, need_soft=need_soft)
+            else:
+                dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
+                    else (dy.t() @ x.to(dy.dtype)).to(out_dt)
+                g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
             g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
         else:
             if ctx.needs_input_grad[0]:
@@ -177,7 +182,7 @@ class DiagMMFunction(torch.autograd.Function):
                 dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft)
         if need_soft:
             g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
-                                         clamped=sel.clamped)
+                                         clamped=sel.clamped, l1_coeff=spec.l1)
         return dx, g_values, g_alpha, g_bias, None
 
 
@@ -287,6 +292,7 @@ class DiagLinear(nn.Module):
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
                        presel=self._take_preselection(step, T))
         y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
+        self._last_spec = spec
         return y.reshape(*lead, self.out_features)
 
     def _take_preselection(self, step: int, T: float):
@@ -435,9 +441,29 @@ def preselect(layers, step: int) -> None:
         m._presel = ((step, m.k, T), sel)
 
 
-def penalties(model: nn.Module) -> list[torch.Tensor]:
-    """MLPModel.penalties (training.py:439-444) for any module tree."""
-    return [m.penalty() for m in model.modules() if isinstance(m, DiagLinear) and m.l1_coeff > 0]
+def penalties(model: nn.Module, fused: bool = False) -> list[torch.Tensor]:
+    """MLPModel.penalties (training.py:439-444) for any module tree.
+
+    ``fused=True`` (after the forward): returns ONE scalar, sum of l1_coeff * |alpha|_1
+    over the layers (the loss value is identical), computed without autograd;
+    its gradient l1_coeff * sign(alpha) (selection.py:217-222) is instead added
+    by each layer's soft-TopK gradient kernel (K5) in the backward of the
+    forward that just ran — one fused launch per layer instead of an autograd
+    chain of elementwise kernels."""
+    layers = [m for m in model.modules() if isinstance(m, DiagLinear) and m.l1_coeff > 0]
+    if not fused:
+        return [m.penalty() for m in layers]
+    if not layers:
+        return []
+    for m in layers:
+        spec = getattr(m, "_last_spec", None)
+        if spec is None:
+            raise RuntimeError("penalties(fused=True) must follow the forward of every DiagLinear")
+        spec.l1 = float(m.l1_coeff)
+    with torch.no_grad():
+        norms = torch._foreach_norm([m.alpha.detach() for m in layers], 1)
+        coeffs = torch.tensor([m.l1_coeff for m in layers], dtype=torch.float64, device=norms[0].device)
+        return [(torch.stack(norms) * coeffs).sum()]
 
 
 __all__ = [

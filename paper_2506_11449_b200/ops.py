@@ -411,3 +411,21 @@ def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) 
     _lib.call("diagmm_tc_gemm_bf16", a.shape[0], b.shape[0], a.shape[1], _p(a), _p(b), _p(bz), _p(out), out.shape[1],
               _stream(a))
     return out
+
+
+def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
+                       need_soft: bool = True, max_act: int | None = None):
+    """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None)."""
+    _check_product(dy, M, values, M, N)
+    _check_product(x, N, values, M, N)
+    C, L = geometry(M, N)
+    ma = C if max_act is None else int(max_act)
+    B = x.shape[0]
+    dy = dy.contiguous()
+    x = x.contiguous()
+    ws = _workspace(dy.device, _lib.load().diagmm_tc_backward_weight_workspace(M, N, B, ma))
+    g_values = torch.empty(C, L, dtype=values.dtype, device=dy.device)
+    g_soft = torch.empty(C, dtype=torch.float64, device=dy.device) if need_soft else None
+    _lib.call("diagmm_tc_backward_weight", M, N, B, _p(dy), _p(x), _p(values.contiguous()), _p(sel.alpha_soft),
+              _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(ws), ws.numel(), _stream(dy))
+    return g_values, g_soft

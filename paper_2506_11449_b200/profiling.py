@@ -23,7 +23,8 @@ _ELT = {0: 8, 1: 4, 2: 2}
 SECTION8_KERNELS = {
     "diagmm_forward", "diagmm_backward_input", "diagmm_backward_weight", "diagmm_topk_waterfill",
     "diagmm_topk_waterfill_batched", "diagmm_topk_grad", "diagmm_adamw", "diagmm_adamw_multi",
-    "diagmm_sumsq_multi", "diagmm_materialize", "diagmm_gather_dense_grad",
+    "diagmm_sumsq_multi", "diagmm_materialize", "diagmm_gather_dense_grad", "diagmm_tc_gemm_bf16",
+    "diagmm_tc_backward_weight",
 }
 
 
@@ -109,6 +110,12 @@ def work(name, args, nact_of=None):
         n = _n_act(args, name, nact_of) or max(M, N)
         p = 8 if dt == 0 else 4
         return 0.0, p * n * min(M, N) * 2 + p * max(M, N) * min(M, N)
+    if name == "diagmm_tc_gemm_bf16":  # dense-equivalent tensor-core product: 2 M N K flop
+        Md, Nd, K = args[0], args[1], args[2]
+        return 2.0 * Md * Nd * K, 2.0 * (Md * K + Nd * K + Md * Nd)
+    if name == "diagmm_tc_backward_weight":
+        M, N, B = args[0], args[1], args[2]
+        return 2.0 * M * N * B, 2.0 * B * (M + N) + 4.0 * max(M, N) * min(M, N)
     if name == "diagmm_adamw_multi":
         n, descs = args[0], args[1]
         return 0.0, float(sum(7 * (8 if descs[i].dtype == 0 else 4) * descs[i].n for i in range(n)))
@@ -150,6 +157,14 @@ def roofline(records, peaks: dict, peaks_kind: str, fma_tflops: float, nact_of=N
     n = len(records)
     sec = tot_ms / 1e3
     hbm = float(peaks["hbm_gbs"])
+    if name.startswith("diagmm_tc_"):  # tensor-core kernels: dense bf16 tcgen05 peak, sustained (inside a step)
+        tpk = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+        achieved = tot_f / sec / 1e12
+        if tot_f / (tpk * 1e12) >= tot_b / (hbm * 1e9):
+            return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s",
+                    "frac": achieved / tpk, "traffic": None, "launches": n, "avg_launch_us": tot_ms * 1e3 / n,
+                    "algorithmic_flops_per_launch": tot_f / n, "algorithmic_bytes_per_launch": tot_b / n,
+                    "peak_source": f"{peaks_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)"}
     t_fma = tot_f / (fma_tflops * 1e12)
     t_hbm = tot_b / (hbm * 1e9)
     if t_fma > t_hbm:

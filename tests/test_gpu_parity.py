@@ -549,3 +549,63 @@ def test_tensor_core_route_matches_oracle():
     assert scaled_err(y.float().detach().cpu().numpy(), y_ref) < BF16_TOL
     assert scaled_err(xt.grad.float().cpu().numpy(), g_ref["x"]) < BF16_TOL
     assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) < BF16_TOL
+
+
+@pytest.mark.parametrize("shape", [(3072, 768), (768, 3072), (512, 512), (2304, 768)])
+def test_tc_backward_weight_matches_oracle(shape):
+    """K3 on the tensor cores with the fused diagonal gather (split-K, MN-major
+    operands) vs the float64 oracle gradient on the same bf16 inputs."""
+    M, N = shape
+    C, L = max(M, N), min(M, N)
+    B = 1000
+    rng = np.random.default_rng(17)
+    k = max(1, C // 10)
+    alpha = rng.standard_normal(C)
+    T = 0.05
+    sel = ops.soft_topk_select(t(alpha), k, T)
+    soft = sel.alpha_soft.cpu().numpy()
+    act = sel.active[: sel.host_count()].cpu().numpy()
+    values = rng.standard_normal((C, L)) * 0.1
+    x = torch.randn(B, N, device=DEV).to(torch.bfloat16)
+    dy = torch.randn(B, M, device=DEV).to(torch.bfloat16)
+    vt = torch.as_tensor(values, dtype=torch.float32, device=DEV)
+    g_values, g_soft = ops.tc_backward_weight(dy, x, vt, sel, M, N)
+    xd, dyd = x.double().cpu().numpy(), dy.double().cpu().numpy()
+    weights = soft[act, None] * values[act]
+    ref = olayer.diag_matmul_backward(dyd, xd, vt.double().cpu().numpy(), weights, act, M, N,
+                                      alpha=alpha, alpha_soft=soft, k=k, temperature=T)
+    assert scaled_err(g_values.cpu().numpy(), ref[1]) < 1e-5
+    r_idx, c_idx = oracle.entry_coords(M, N, [int(o) for o in act])
+    gw = (dyd.T @ xd)[r_idx, c_idx]
+    gs = np.zeros(C)
+    gs[act] = (gw * vt.double().cpu().numpy()[act]).sum(axis=1)
+    assert scaled_err(g_soft.cpu().numpy(), gs) < 1e-5
+    inactive = np.setdiff1d(np.arange(C), act)
+    assert not g_values[torch.as_tensor(inactive, device=DEV)].any()
+
+
+def test_fused_l1_penalty_matches_autograd_penalty():
+    """penalties(fused=True): same loss value, and alpha.grad = K5 grad + l1*sign(alpha)
+    exactly as the autograd penalty gives it (selection.py:217-222)."""
+    from paper_2506_11449_b200 import penalties
+    from paper_2506_11449_b200.vit import MLPModel
+
+    grads = []
+    for fused in (False, True):
+        torch.manual_seed(0)
+        m = MLPModel(sizes=(64, 96, 32, 10), kinds=("dynadiag", "dynadiag", "dense"), dtype=torch.float64,
+                     t_schedule=TemperatureSchedule("constant", 0.05, 0.05, 1))
+        for lyr in m.layers:
+            if isinstance(lyr, DiagLinear):
+                lyr.l1_coeff = 1e-2
+        x = torch.randn(8, 64, device=DEV, dtype=torch.float64)
+        out = m(x, 0)
+        loss = out.square().mean()
+        pens = penalties(m, fused=fused)
+        for p in pens:
+            loss = loss + p
+        loss.backward()
+        grads.append((loss.item(), [l.alpha.grad.clone() for l in m.layers if isinstance(l, DiagLinear)]))
+    assert grads[0][0] == pytest.approx(grads[1][0], rel=1e-12)
+    for a, b in zip(grads[0][1], grads[1][1]):
+        torch.testing.assert_close(a, b, rtol=1e-12, atol=1e-14)

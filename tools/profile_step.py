@@ -33,7 +33,7 @@ def step(s):
     with torch.autocast("cuda", dtype=torch.bfloat16):
         logits = model(img)
     loss = F.cross_entropy(logits.float(), lbl, label_smoothing=0.1)
-    for pen in penalties(model):
+    for pen in penalties(model, fused=True):
         loss = loss + pen
     loss.backward()
     _, sc = clip.compute(specs)
