@@ -230,14 +230,17 @@ DIAGMM_API int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, con
  * gather onto the active diagonals fused into the epilogue (the dense dW is
  * never written), then finalized exactly like diagmm_backward_weight:
  * g_values (C, L) float (active rows = alpha_soft * gw, others 0), g_soft
- * (may be NULL).  Replaces the dense branch of layers.py:150-153 + 159-165.
- * M, N multiples of 64; dy (B, M), x (B, N) bf16, 16-byte aligned. */
+ * (may be NULL), g_bias (M,) float (may be NULL): the column sums of dy,
+ * accumulated by extra warps from the same dy tiles the MMAs consume
+ * (autodiff.py:77-79), so dy is read once.  Replaces the dense branch of
+ * layers.py:150-153 + 159-165.  M, N multiples of 64; dy (B, M), x (B, N)
+ * bf16, 16-byte aligned. */
 DIAGMM_API size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act);
 DIAGMM_API int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x,
                                          const void* values, const double* alpha_soft,
                                          const int32_t* slot, const int32_t* n_act, int max_act,
-                                         void* g_values, double* g_soft, void* workspace,
-                                         size_t ws_bytes, void* stream);
+                                         void* g_values, double* g_soft, void* g_bias,
+                                         void* workspace, size_t ws_bytes, void* stream);
 
 /* ---- fused LayerNorm for the bf16 activations of the ViT caller ----------
  * Not a reference symbol: the caller's LayerNorm (vit.py) around DiagLinear.

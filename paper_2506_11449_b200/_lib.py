@@ -66,7 +66,8 @@ SIGNATURES["diagmm_sumsq_multi_len"] = (_i, [_i, C.POINTER(TensorDesc)])
 SIGNATURES["diagmm_sumsq_multi"] = (_i, [_i, C.POINTER(TensorDesc), _vp, _i, _vp])
 SIGNATURES["diagmm_clip_scale_tree"] = (_i, [_i, _vp, _d, _vp, _vp, _vp])
 SIGNATURES["diagmm_tc_backward_weight_workspace"] = (_sz, [_i, _i, _i, _i])
-SIGNATURES["diagmm_tc_backward_weight"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp])
+SIGNATURES["diagmm_tc_backward_weight"] = (
+    _i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp])
 SIGNATURES["diagmm_layernorm_fwd"] = (_i, [_i, _i, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp])
 SIGNATURES["diagmm_layernorm_bwd_workspace"] = (_sz, [_i, _i])

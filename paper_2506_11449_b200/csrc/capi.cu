@@ -39,7 +39,7 @@ int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 size_t tc_dw_workspace(int, int, int, int);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
-                   const int32_t*, int, void*, double*, void*, size_t, cudaStream_t);
+                   const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
@@ -187,10 +187,11 @@ size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act) {
 
 int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x, const void* values,
                               const double* alpha_soft, const int32_t* slot, const int32_t* n_act, int max_act,
-                              void* g_values, double* g_soft, void* workspace, size_t ws_bytes, void* stream) {
+                              void* g_values, double* g_soft, void* g_bias, void* workspace, size_t ws_bytes,
+                              void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
-  return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, workspace,
-                        ws_bytes, S(stream));
+  return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
+                        workspace, ws_bytes, S(stream));
 }
 
 // internal (not in the header): 2:4 sparse tensor-core throughput probe

@@ -1256,25 +1256,39 @@ int run_gather_dense(int M, int N, const void* dW, const void* vals, const doubl
 // ---- dW on the tensor cores (tc_kernels.cu) + the same finalize
 int tc_dw_splits(int M, int N, int ntok);
 int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
-              int max_act, float* partial, size_t partial_bytes, cudaStream_t st);
+              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st);
 
 size_t tc_dw_workspace(int M, int N, int B, int max_act) {
   const int L = M < N ? M : N;
-  return align16((size_t)tc_dw_splits(M, N, B > 0 ? B : 1) * (max_act > 0 ? max_act : 1) * L * sizeof(float));
+  const int ks = tc_dw_splits(M, N, B > 0 ? B : 1);
+  return align16((size_t)ks * (max_act > 0 ? max_act : 1) * L * sizeof(float)) + align16((size_t)ks * M * sizeof(float));
 }
 
 int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const void* vals, const double* asoft,
-                   const int32_t* slot, const int32_t* n_act, int max_act, void* g_values, double* g_soft, void* ws,
-                   size_t ws_bytes, cudaStream_t st) {
+                   const int32_t* slot, const int32_t* n_act, int max_act, void* g_values, double* g_soft,
+                   void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
   using T = __nv_bfloat16;
   using P = typename Traits<T>::P;
   const int C = M > N ? M : N, L = M < N ? M : N;
   if (ws_bytes < tc_dw_workspace(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
   float* partial = static_cast<float*>(ws);
+  const int ks = tc_dw_splits(M, N, B > 0 ? B : 1);
+  const size_t pbytes = align16((size_t)ks * (max_act > 0 ? max_act : 1) * L * sizeof(float));
+  float* colsum = reinterpret_cast<float*>(static_cast<char*>(ws) + pbytes);
   int parts = 0;
-  if (B > 0 && max_act > 0) {
-    if (int e = run_tc_dw(M, N, B, dy, x, slot, n_act, max_act, partial, ws_bytes, st)) return e;
-    parts = tc_dw_splits(M, N, B);
+  if (B > 0 && (max_act > 0 || g_bias)) {
+    if (int e = run_tc_dw(M, N, B, dy, x, slot, n_act, max_act > 0 ? max_act : 1, partial, pbytes,
+                          g_bias ? colsum : nullptr, st))
+      return e;
+    parts = max_act > 0 ? ks : 0;
+  }
+  if (g_bias) {
+    if (B > 0) {
+      k_colsum_final<T><<<ceil_div(M, 32), 256, 0, st>>>(M, ks, colsum, static_cast<P*>(g_bias));
+      note_launch();
+    } else {
+      cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), st);
+    }
   }
   k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft);

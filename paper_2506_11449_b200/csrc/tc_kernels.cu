@@ -401,6 +401,7 @@ k_tc_gemm_sp(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
 // (M x N fp32) is never written.  K (tokens) is split across CTAs when the
 // output has fewer tiles than SMs.
 constexpr int kDwBN = 256;
+constexpr int kDwThreads = kThreads + 128;  // + 4 warps summing dy's columns (bias gradient) off the A stages
 struct SmemDw {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;      // 2 boxes of 64 x 64
   static constexpr size_t b_bytes = (size_t)kDwBN * BK * 2;   // 4 boxes
@@ -414,10 +415,10 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
   return a | (512ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDwThreads, 1)
 k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N, int ntok,
         int ksplit, const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
-        float* __restrict__ partial) {
+        float* __restrict__ partial, float* __restrict__ colsum) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -445,7 +446,7 @@ k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensor
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&empty[s])) : "memory");  // MMA + colsum
     }
     for (int i = 0; i < 2; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[i])) : "memory");
@@ -511,7 +512,57 @@ k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensor
         umma_commit(&tfull[ab]);
       }
     }
-  } else {  // ---- epilogue: gather the active diagonals out of the tile
+  } else if (warp >= 10) {  // ---- column sums of dy (bias gradient) from the A stages of n-block-0 tiles
+    // thread i: box h = i / 64, 16-byte chunk j = (i / 8) % 8 (8 columns), rows r = i % 8 + 8 m
+    const int ci = threadIdx.x - 320;
+    const int h = ci >> 6, j = (ci >> 3) & 7, rg = ci & 7;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int ot = t % otiles, z = t / otiles;
+      const int m0 = (ot / nb) * BM;
+      const bool sum = colsum != nullptr && (ot % nb) == 0;
+      const int kb0 = z * KBs, kb1 = min(KBt, kb0 + KBs);
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % kStages, round = it / kStages;
+        mbar_wait_parity(&full[s], round & 1);
+        if (sum) {
+          const unsigned char* box = sA + s * S::a_bytes + h * 8192;
+#pragma unroll
+          for (int mm = 0; mm < BK / 8; ++mm) {
+            const int r = rg + 8 * mm;
+            const uint4 u = *reinterpret_cast<const uint4*>(box + r * 128 + ((j ^ (r & 7)) << 4));
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              acc[2 * e] += __uint_as_float(w[e] << 16);
+              acc[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+            }
+          }
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // all 4 colsum warps done with stage s
+        if (threadIdx.x == 320)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      }
+      if (sum) {
+        // fold the 8 row groups (lanes rg = 0..7 of each 8-lane group), fixed order
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+        }
+        if (rg == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int m = m0 + h * 64 + j * 8 + e;
+            if (m < M) colsum[(size_t)z * M + m] = acc[e];
+          }
+        }
+      }
+    }
+  } else {  // ---- epilogue (warps 2..9): gather the active diagonals out of the tile
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int et = threadIdx.x - 64;
@@ -642,7 +693,7 @@ int tc_dw_splits(int M, int N, int ntok) {
 }
 
 int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
-              int max_act, float* partial, size_t partial_bytes, cudaStream_t st) {
+              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st) {
   using namespace tc;
   const int L = M < N ? M : N;
   if (M < 64 || N < 64 || M % 64 || N % 64 || ntok < 1) return DIAGMM_ESHAPE;
@@ -668,7 +719,7 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
   const int tiles = ceil_div(M, BM) * ceil_div(N, kDwBN) * ks;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   // partials of inactive slots are never read; active (slot, t) entries are all written
-  k_tc_dw<<<grid, kThreads, sm, st>>>(ta, tb, M, N, ntok, ks, slot, n_act, max_act, partial);
+  k_tc_dw<<<grid, kDwThreads, sm, st>>>(ta, tb, M, N, ntok, ks, slot, n_act, max_act, partial, colsum);
   note_launch();
   return status_from_cuda();
 }

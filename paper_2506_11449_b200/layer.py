@@ -168,13 +168,17 @@ class DiagMMFunction(torch.autograd.Function):
                     dx = dy @ W
             out_dt = vals.dtype
             if ctx.tc and M % 64 == 0 and N % 64 == 0:
-                # tensor-core dW with the diagonal gather fused (no dense dW is written)
-                g_values, g_soft = ops.tc_backward_weight(dy, x.to(dy.dtype), vals, sel, M, N, need_soft=need_soft)
+                # tensor-core dW with the diagonal gather and the bias gradient fused (dy read once,
+                # no dense dW written)
+                g_values, g_soft, g_bias = ops.tc_backward_weight(dy, x.to(dy.dtype), vals, sel, M, N,
+                                                                  need_soft=need_soft, need_bias=True)
+                if not ctx.has_bias:
+                    g_bias = None
             else:
                 dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
                     else (dy.t() @ x.to(dy.dtype)).to(out_dt)
                 g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
-            g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
+                g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
         else:
             if ctx.needs_input_grad[0]:
                 dx = ops.diag_backward_input(dy, vals, sel, M, N)

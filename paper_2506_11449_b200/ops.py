@@ -414,8 +414,8 @@ def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) 
 
 
 def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
-                       need_soft: bool = True, max_act: int | None = None):
-    """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None)."""
+                       need_soft: bool = True, max_act: int | None = None, need_bias: bool = False):
+    """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None[, g_bias (M,) f32])."""
     _check_product(dy, M, values, M, N)
     _check_product(x, N, values, M, N)
     C, L = geometry(M, N)
@@ -426,6 +426,7 @@ def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, 
     ws = _workspace(dy.device, _lib.load().diagmm_tc_backward_weight_workspace(M, N, B, ma))
     g_values = torch.empty(C, L, dtype=values.dtype, device=dy.device)
     g_soft = torch.empty(C, dtype=torch.float64, device=dy.device) if need_soft else None
+    g_bias = torch.empty(M, dtype=values.dtype, device=dy.device) if need_bias else None
     _lib.call("diagmm_tc_backward_weight", M, N, B, _p(dy), _p(x), _p(values.contiguous()), _p(sel.alpha_soft),
-              _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(ws), ws.numel(), _stream(dy))
-    return g_values, g_soft
+              _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(dy))
+    return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)

@@ -582,6 +582,10 @@ def test_tc_backward_weight_matches_oracle(shape):
     assert scaled_err(g_soft.cpu().numpy(), gs) < 1e-5
     inactive = np.setdiff1d(np.arange(C), act)
     assert not g_values[torch.as_tensor(inactive, device=DEV)].any()
+    # fused bias gradient (column sums of dy) from the same dy tiles
+    gv2, _, gb = ops.tc_backward_weight(dy, x, vt, sel, M, N, need_bias=True)
+    assert torch.equal(gv2, g_values)
+    np.testing.assert_allclose(gb.double().cpu().numpy(), dyd.sum(axis=0), rtol=1e-5, atol=1e-3)
 
 
 def test_fused_l1_penalty_matches_autograd_penalty():

@@ -23,5 +23,6 @@ for M, N, B, s, dt in cases:
     d = r.get("cublas_bf16_dense_us", {})
     print(f"{M}x{N} B={B} s={s} {str(dt)[6:]}: " + " ".join(
         f"{k}={r[k]['us']:.1f}us/{r[k]['tflops']:.1f}TF" for k in ("fwd", "dx", "dw")) +
-        f" | cublas bf16 fwd+bwd {d.get('total', 0):.1f}us, speedup {r.get('speedup_vs_cublas_bf16_fwd_bwd', 0):.2f}",
+        (f" | tc route {r['tc_route_us']['total']:.1f}us" if 'tc_route_us' in r else "") +
+        f" | cublas bf16 fwd+bwd {d.get('total', 0):.1f}us, best-route speedup {r.get('speedup_vs_cublas_bf16_fwd_bwd', 0):.2f}",
         flush=True)

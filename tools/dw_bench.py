@@ -22,10 +22,13 @@ for (M, N) in [(3072, 768), (768, 3072), (2304, 768), (768, 768)]:
     x = torch.randn(B, N, device="cuda").to(torch.bfloat16)
     dy = torch.randn(B, M, device="cuda").to(torch.bfloat16)
     t_tc = timeit(lambda: ops.tc_backward_weight(dy, x, vals, sel, M, N))
+    t_tcb = timeit(lambda: ops.tc_backward_weight(dy, x, vals, sel, M, N, need_bias=True))
+    t_bias = timeit(lambda: dy.sum(0, dtype=torch.float32))
     def ref():
         dW = torch.mm(dy.t(), x, out_dtype=torch.float32)
         return ops.gather_dense_grad(dW, vals, sel, M, N)
     t_cb = timeit(ref)
     t_mm = timeit(lambda: torch.mm(dy.t(), x, out_dtype=torch.float32))
     fl = 2.0 * M * N * B
-    print(f"{M}x{N} B={B}: tc dW {t_tc:.1f}us ({fl/t_tc/1e6:.0f} TF) | cublas+gather {t_cb:.1f}us (mm alone {t_mm:.1f}us, {fl/t_mm/1e6:.0f} TF)", flush=True)
+    print(f"{M}x{N} B={B}: tc dW {t_tc:.1f}us ({fl/t_tc/1e6:.0f} TF), +fused bias {t_tcb:.1f}us | cublas+gather {t_cb:.1f}us "
+          f"(mm alone {t_mm:.1f}us, {fl/t_mm/1e6:.0f} TF) + torch bias {t_bias:.1f}us", flush=True)
