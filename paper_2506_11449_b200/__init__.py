@@ -37,6 +37,7 @@ from .layer import (  # noqa: F401
     DiagLinear,
     DiagMatrix,
     DiagMMFunction,
+    DiagMLP,
     FrozenDiagLinear,
     ParamSpec,
     diagheur_update,

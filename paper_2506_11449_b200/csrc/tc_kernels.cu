@@ -11,13 +11,23 @@
 namespace diagmm {
 namespace tc {
 
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {  // d gelu_tanh / dx (PyTorch's formula)
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
 template <int BN>
 struct Smem {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;
   static constexpr size_t b_bytes = (size_t)BN * BK * 2;
   static constexpr size_t stage = a_bytes + b_bytes;
   static constexpr size_t c_bytes = (size_t)BM * BN;  // half the output tile (two 64-column swizzled boxes)
-  static constexpr size_t bars = 128 + BN * 4;  // barriers, TMEM slot, bias tile
+  static constexpr size_t bars = 128 + BN * 4;  // barriers, TMEM slot, aux barrier, bias tile
   static constexpr size_t total = 1024 /* alignment slack */ + kStages * stage + c_bytes + bars;
 };
 
@@ -28,7 +38,8 @@ struct Smem {
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-          const __grid_constant__ CUtensorMap tc_out, int Mdim, int Ndim, int K, const float* __restrict__ bias) {
+          const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
+          int K, const float* __restrict__ bias, int epi) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -41,6 +52,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* auxbar = tempty + 3;  // after tslot's 8 bytes
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (K + BK - 1) / BK;
@@ -56,10 +68,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[i])) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&tempty[i])) : "memory");
     }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(auxbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&ta);
     prefetch_tmap(&tb);
     prefetch_tmap(&tc_out);
+    if (epi) prefetch_tmap(&tc_aux);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -110,75 +124,109 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       }
     }
   } else {  // ---- epilogue: warps 2..9; warp w reads TMEM lanes 32*(w%4), column half (w-2)/4
-    // TMEM -> registers (32 columns at a time) -> +bias, bf16 -> the 128B-swizzled
-    // smem tile (one 64-column box per 16 KB) -> TMA bulk tensor store.
+    // TMEM -> registers (32 columns at a time) -> epilogue op, bf16 -> the 128B-
+    // swizzled smem tile (one 64-column box per 16 KB) -> TMA bulk tensor store.
+    //   epi 0: out = acc + bias
+    //   epi 1: aux = acc + bias (pre-activation), out = gelu_tanh(aux)
+    //   epi 2: out = acc * gelu_tanh'(aux)   (aux TMA-loaded into the staging tile)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int rl = q * 32 + lane;  // row within the tile
     const int et = threadIdx.x - 64;  // epilogue thread id
     const bool leader = et == 0;
     float* sbias = reinterpret_cast<float*>(tslot + 4);  // BN floats after the barriers
+    uint32_t aux_phase = 0;
+    auto wait_reads = [&]() {  // previous TMA store finished reading the staging tile
+      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    };
+    auto store_half = [&](const CUtensorMap* map, int m0, int col0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (leader) {
+#pragma unroll
+        for (int bx = 0; bx < BN / 128; ++bx) {
+          const int col = col0 + bx * 64;
+          if (col >= Ndim) break;
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                           reinterpret_cast<uint64_t>(map)),
+                       "r"(col), "r"(m0), "r"(smem_u32(sC + (size_t)bx * (BM * 128)))
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    };
+    // 8 bf16 of this thread's row in 16-byte chunk `ch` (0..7) of the box holding chunk cl
+    auto sc_addr = [&](int cl, int j) {
+      unsigned char* box = sC + (size_t)(cl >> 1) * (BM * 128);
+      const int chunk = ((cl & 1) * 4 + j) ^ (rl & 7);
+      return reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16);
+    };
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
       const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
-      // the previous tile's TMA store must have finished reading sC / sbias users done
-      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      wait_reads();
       for (int c = et; c < BN; c += kEpiThreads) sbias[c] = (bias && n0 + c < Ndim) ? __ldg(bias + n0 + c) : 0.f;
       mbar_wait_parity(&tfull[ab], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      // two halves of BN/2 columns through the same 32 KB staging tile; the 8
-      // warps split each half (warps 2-5 the first BN/4 columns, 6-9 the next)
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
-        if (hh == 1) {
-          if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (hh == 1) wait_reads();
+        if (epi == 2) {  // bring the pre-activation half tile into the staging buffer
+          if (leader) {
+            mbar_expect_tx(auxbar, (uint32_t)S::c_bytes);
+#pragma unroll
+            for (int bx = 0; bx < BN / 128; ++bx)
+              tma_load_2d(sC + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / 2) + bx * 64, m0, auxbar);
+          }
+          mbar_wait_parity(auxbar, aux_phase);
+          aux_phase ^= 1;
         }
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 128; ++cc) {
-          const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
-          uint32_t r[32];
-          tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
-          uint32_t pk[16];
+        for (int pass = 0; pass < (epi == 1 ? 2 : 1); ++pass) {
+          if (pass == 1) wait_reads();
+#pragma unroll 1
+          for (int cc = 0; cc < BN / 128; ++cc) {
+            const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
+            const int cl = c - hh * (BN / 64);                      // chunk within this half
+            uint32_t r[32];
+            tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+            uint32_t prev[16];
+            if (epi == 2) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float a = __uint_as_float(r[2 * j]) + sbias[c * 32 + 2 * j];
-            const float b = __uint_as_float(r[2 * j + 1]) + sbias[c * 32 + 2 * j + 1];
-            __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          const int cl = c - hh * (BN / 64);  // chunk within this half
-          unsigned char* box = sC + (size_t)(cl >> 1) * (BM * 128);
-          const int ch0 = (cl & 1) * 4;
+              for (int j = 0; j < 4; ++j) {
+                const uint4 u = *sc_addr(cl, j);
+                prev[4 * j] = u.x; prev[4 * j + 1] = u.y; prev[4 * j + 2] = u.z; prev[4 * j + 3] = u.w;
+              }
+            }
+            uint32_t pk[16];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int chunk = (ch0 + j) ^ (rl & 7);
-            *reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16) =
-                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          }
-        }
-        if (hh == 1) {  // accumulator consumed: hand it back to the MMA thread
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (leader) {
+            for (int j = 0; j < 16; ++j) {
+              float a = __uint_as_float(r[2 * j]), b = __uint_as_float(r[2 * j + 1]);
+              if (epi != 2) { a += sbias[c * 32 + 2 * j]; b += sbias[c * 32 + 2 * j + 1]; }
+              if (epi == 1 && pass == 1) {  // gelu of the bf16-rounded pre-activation (as stored)
+                a = gelu_tanh(__bfloat162float(__float2bfloat16_rn(a)));
+                b = gelu_tanh(__bfloat162float(__float2bfloat16_rn(b)));
+              } else if (epi == 2) {
+                a *= gelu_tanh_grad(__uint_as_float(prev[j] << 16));
+                b *= gelu_tanh_grad(__uint_as_float(prev[j] & 0xffff0000u));
+              }
+              __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
 #pragma unroll
-          for (int bx = 0; bx < BN / 128; ++bx) {
-            const int col = n0 + hh * (BN / 2) + bx * 64;
-            if (col >= Ndim) break;
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                             reinterpret_cast<uint64_t>(&tc_out)),
-                         "r"(col), "r"(m0), "r"(smem_u32(sC + (size_t)bx * (BM * 128)))
-                         : "memory");
+            for (int j = 0; j < 4; ++j) *sc_addr(cl, j) = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           }
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          const bool last = hh == 1 && pass == (epi == 1 ? 1 : 0);
+          if (last) {  // accumulator consumed: hand it back to the MMA thread
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
+          }
+          store_half((epi == 1 && pass == 0) ? &tc_aux : &tc_out, m0, n0 + hh * (BN / 2));
         }
       }
     }
@@ -725,23 +773,25 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
 }
 
 int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
-                     cudaStream_t st) {
+                     void* aux, int epi, cudaStream_t st) {
   using namespace tc;
   constexpr int BN = 256;
   if (Mdim < 1 || Ndim < 1 || K < 1 || K % 8 || ldo < Ndim) return DIAGMM_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return DIAGMM_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo % 8)) return DIAGMM_ESHAPE;
-  CUtensorMap ta, tb, tco;
+  if (epi < 0 || epi > 2 || (epi && (aux == nullptr || (reinterpret_cast<uintptr_t>(aux) & 15)))) return DIAGMM_ESHAPE;
+  CUtensorMap ta, tb, tco, taux;
   if (!make_tmap_bf16(&ta, A, (uint64_t)Mdim, (uint64_t)K, BM, (uint64_t)K) ||
       !make_tmap_bf16(&tb, B, (uint64_t)Ndim, (uint64_t)K, BN, (uint64_t)K) ||
-      !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo))
+      !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo) ||
+      !make_tmap_bf16(&taux, epi ? aux : out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo))
     return DIAGMM_ECUDA;
   auto k = k_tc_gemm<BN>;
   const size_t sm = Smem<BN>::total;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k<<<grid, kThreads, sm, st>>>(ta, tb, tco, Mdim, Ndim, K, bias);
+  k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
   note_launch();
   return status_from_cuda();
 }

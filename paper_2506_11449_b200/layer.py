@@ -190,6 +190,49 @@ class DiagMMFunction(torch.autograd.Function):
         return dx, g_values, g_alpha, g_bias, None
 
 
+class DiagMLPFunction(torch.autograd.Function):
+    """fc2(gelu_tanh(fc1(x))) for two DiagLinear layers on the tensor-core route
+    with the GELU fused into the GEMM epilogues: fc1's epilogue writes the
+    pre-activation and gelu(pre); fc2's input-gradient epilogue multiplies by
+    gelu'(pre) — no separate GELU kernels, forward or backward.  Gradients per
+    layer are exactly those of DiagMMFunction (layers.py:143-167)."""
+
+    @staticmethod
+    def forward(ctx, x, v1, a1, b1, v2, a2, b2, s1: _OpSpec, s2: _OpSpec, fuse_fwd: bool = True):
+        sel1 = s1.presel or ops.soft_topk_select(a1.detach(), s1.k, s1.temperature)
+        sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature)
+        x = x.contiguous()
+        W1 = ops.materialize(v1.detach(), sel1, s1.M, s1.N, dtype=x.dtype)
+        if fuse_fwd:
+            act, pre = ops.tc_gemm_ex(x, W1, None if b1 is None else b1.detach(), epilogue=1)
+        else:
+            pre = ops.tc_gemm(x, W1, None if b1 is None else b1.detach())
+            act = F.gelu(pre, approximate="tanh")
+        W2 = ops.materialize(v2.detach(), sel2, s2.M, s2.N, dtype=x.dtype)
+        y = ops.tc_gemm(act, W2, None if b2 is None else b2.detach())
+        ctx.save_for_backward(x, pre, act, v1, a1, v2, a2)
+        ctx.sels, ctx.specs, ctx.has_bias = (sel1, sel2), (s1, s2), (b1 is not None, b2 is not None)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, pre, act, v1, a1, v2, a2 = ctx.saved_tensors
+        (sel1, sel2), (s1, s2) = ctx.sels, ctx.specs
+        dy = dy.to(x.dtype).contiguous()
+        v1d, v2d = v1.detach(), v2.detach()
+        # fc2: input gradient straight to d(pre) through gelu', then dW2 (+ bias) from act
+        d_pre, _ = ops.tc_gemm_ex(dy, ops.materialize(v2d, sel2, s2.M, s2.N, dtype=x.dtype, transposed=True),
+                                  None, epilogue=2, aux=pre)
+        gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True)
+        ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1)
+        # fc1
+        dx = ops.tc_gemm(d_pre, ops.materialize(v1d, sel1, s1.M, s1.N, dtype=x.dtype, transposed=True))
+        gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True)
+        ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1)
+        hb1, hb2 = ctx.has_bias
+        return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None)
+
+
 def _flatten(x: torch.Tensor, width: int) -> torch.Tensor:
     if x.dim() < 1 or x.shape[-1] != width:
         raise ShapeMismatch(f"input has shape {tuple(x.shape)}, expected (..., {width})")
@@ -292,12 +335,16 @@ class DiagLinear(nn.Module):
             x2 = x2.double()
         elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))  # like nn.Linear under autocast
+        spec = self._make_spec(step)
+        y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
+        return y.reshape(*lead, self.out_features)
+
+    def _make_spec(self, step: int) -> "_OpSpec":
         T = self.temperature(step)
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
                        presel=self._take_preselection(step, T))
-        y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
         self._last_spec = spec
-        return y.reshape(*lead, self.out_features)
+        return spec
 
     def _take_preselection(self, step: int, T: float):
         ps, self._presel = self._presel, None
@@ -308,6 +355,52 @@ class DiagLinear(nn.Module):
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, k={self.k}, "
                 f"candidates={self.candidates}, route={self.route}")
+
+
+class DiagMLP(nn.Module):
+    """fc1 -> GELU (tanh) -> fc2 with two DiagLinear layers (the ViT / GPT MLP).
+
+    With DIAGMM_FUSE_MLP=bwd|1 on the tensor-core route (bf16, >= dense_route_min_tokens
+    tokens, dims multiple of 64) the GELU is fused into the GEMM epilogues
+    (DiagMLPFunction: "bwd" = gelu' in fc2's input-gradient epilogue, "1" = also
+    gelu in fc1's epilogue).  Measured on B200 the extra epilogue work makes the
+    short-K (768) GEMMs epilogue-bound and the step 0.4 / 1.9 ms slower, so the
+    default is the unfused fc2(gelu(fc1(x)))."""
+
+    def __init__(self, fc1: "DiagLinear", fc2: "DiagLinear"):
+        super().__init__()
+        if fc1.out_features != fc2.in_features:
+            raise ShapeMismatch("fc1.out_features must equal fc2.in_features")
+        self.fc1, self.fc2 = fc1, fc2
+
+    def _fusable(self, x2: torch.Tensor) -> bool:
+        import os
+
+        layers = (self.fc1, self.fc2)
+        return (x2.dtype == torch.bfloat16 and x2.shape[0] >= dense_route_min_tokens()
+                and all(m.route == "auto" and m.out_features % 64 == 0 and m.in_features % 64 == 0 for m in layers)
+                and all(m.values.dtype == torch.float32 for m in layers)
+                and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas"
+                and os.environ.get("DIAGMM_FUSE_MLP", "0") != "0")
+
+    def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
+        f1, f2 = self.fc1, self.fc2
+        lead = x.shape[:-1]
+        x2 = _flatten(x, f1.in_features)
+        if x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
+            x2 = x2.to(torch.get_autocast_dtype("cuda"))
+        if not self._fusable(x2):
+            h = F.gelu(f1(x2, step), approximate="tanh")
+            return f2(h, step).reshape(*lead, f2.out_features)
+        step1 = f1.step if step is None else int(step)
+        step2 = f2.step if step is None else int(step)
+        f1.last_step, f2.last_step = step1, step2
+        import os
+
+        fuse_fwd = os.environ.get("DIAGMM_FUSE_MLP", "0") in ("1", "both", "fwd")
+        y = DiagMLPFunction.apply(x2, f1.values, f1.alpha, f1.bias, f2.values, f2.alpha, f2.bias,
+                                  f1._make_spec(step1), f2._make_spec(step2), fuse_fwd)
+        return y.reshape(*lead, f2.out_features)
 
 
 class FrozenDiagLinear(nn.Module):
@@ -471,6 +564,6 @@ def penalties(model: nn.Module, fused: bool = False) -> list[torch.Tensor]:
 
 
 __all__ = [
-    "DiagLinear", "DiagMMFunction", "FrozenDiagLinear", "DiagHeurLinear", "DiagMatrix",
+    "DiagLinear", "DiagMMFunction", "DiagMLP", "DiagMLPFunction", "FrozenDiagLinear", "DiagHeurLinear", "DiagMatrix",
     "ParamSpec", "diagheur_update", "penalties", "preselect", "EPS_ACTIVE",
 ]

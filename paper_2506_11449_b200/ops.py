@@ -430,3 +430,27 @@ def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, 
     _lib.call("diagmm_tc_backward_weight", M, N, B, _p(dy), _p(x), _p(values.contiguous()), _p(sel.alpha_soft),
               _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(dy))
     return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)
+
+
+def tc_gemm_ex(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None, epilogue: int = 1,
+               aux: torch.Tensor | None = None):
+    """Tensor-core GEMM with a fused GELU (tanh) epilogue (diagmm_tc_gemm_bf16_ex):
+    epilogue 1 -> (gelu(a b^T + bias), pre-activation);  epilogue 2 (aux = pre) ->
+    ((a b^T) * gelu'(aux), aux)."""
+    _need_cuda(a, b)
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or a.shape[1] != b.shape[1]:
+        raise ShapeMismatch("tc_gemm_ex takes bf16 operands with equal inner dims")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty(a.shape[0], b.shape[0], dtype=torch.bfloat16, device=a.device)
+    if epilogue == 1:
+        aux = torch.empty_like(out)
+    elif epilogue == 2:
+        if aux is None or tuple(aux.shape) != tuple(out.shape) or aux.dtype != torch.bfloat16:
+            raise ShapeMismatch("epilogue 2 needs the (M, N) bf16 pre-activation as aux")
+        aux = aux.contiguous()
+    else:
+        raise ValueError("epilogue must be 1 or 2")
+    bz = None if bias is None else bias.float().contiguous()
+    _lib.call("diagmm_tc_gemm_bf16_ex", a.shape[0], b.shape[0], a.shape[1], _p(a), _p(b), _p(bz), _p(out),
+              out.shape[1], _p(aux), int(epilogue), _stream(a))
+    return out, aux

@@ -290,6 +290,8 @@ def diagmm_config1(peaks, peaks_kind, fma_tflops):
     for (dim, s, B) in [(4096, 0.9, 1), (4096, 0.9, 64), (4096, 0.9, 1024), (4096, 0.99, 1024),
                         (4096, 0.9, 8192)]:
         sweep.append(diag_case(dim, dim, B, s, torch.bfloat16, peaks, fma_tflops, reps=10, flush=flush))
-    return {"config1": cfg1, "sweep_4096": sweep, "hbm_peak_gbs": peaks["hbm_gbs"],
+    # the ViT-B/16 MLP shape at its per-step token count (256 images x 197 tokens)
+    vit = diag_case(3072, 768, 50432, 0.9, torch.bfloat16, peaks, fma_tflops, reps=5, flush=flush)
+    return {"config1": cfg1, "sweep_4096": sweep, "vit_fc1_50432_tokens": vit, "hbm_peak_gbs": peaks["hbm_gbs"],
             "fma_peak_tflops": fma_tflops, "peaks": peaks_kind,
             "note": "L2 flushed (256 MB read) before every timed launch; mean of reps, CUDA-graph replay minus flush-only replay"}

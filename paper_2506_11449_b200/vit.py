@@ -17,7 +17,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from . import ops
-from .layer import DiagLinear, preselect
+from .layer import DiagLinear, DiagMLP, preselect
 from .selection import TemperatureSchedule
 
 
@@ -79,6 +79,7 @@ class Block(nn.Module):
         self.norm2 = LayerNorm(d)
         self.fc1 = _sparse(d, cfg.mlp_ratio * d, cfg, 4 * idx + 2, t_schedule, route)
         self.fc2 = _sparse(cfg.mlp_ratio * d, d, cfg, 4 * idx + 3, t_schedule, route)
+        self.mlp = DiagMLP(self.fc1, self.fc2)  # GELU fused into the tensor-core epilogues
 
     def forward(self, x):
         B, T, D = x.shape
@@ -90,7 +91,7 @@ class Block(nn.Module):
             q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
         x = x + self.proj(a)
-        return x + self.fc2(F.gelu(self.fc1(self.norm2(x)), approximate="tanh"))
+        return x + self.mlp(self.norm2(x))
 
 
 class ViT(nn.Module):

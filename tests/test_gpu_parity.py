@@ -613,3 +613,51 @@ def test_fused_l1_penalty_matches_autograd_penalty():
     assert grads[0][0] == pytest.approx(grads[1][0], rel=1e-12)
     for a, b in zip(grads[0][1], grads[1][1]):
         torch.testing.assert_close(a, b, rtol=1e-12, atol=1e-14)
+
+
+def test_tc_gemm_gelu_epilogues_match_torch():
+    torch.manual_seed(1)
+    M, N, K = 700, 512, 256
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=DEV) * 0.1).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV)
+    act, pre = ops.tc_gemm_ex(a, b, bias, epilogue=1)
+    ref_pre = (a.float() @ b.float().t() + bias).to(torch.bfloat16)
+    assert ((pre.float() - ref_pre.float()).abs().max() / ref_pre.float().abs().max()).item() < 1e-2
+    ref_act = torch.nn.functional.gelu(pre.float(), approximate="tanh")
+    torch.testing.assert_close(act.float(), ref_act, rtol=1e-2, atol=1e-2)
+    g = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    # epilogue 2: out = (g @ W^T) * gelu'(pre), with W (N, K)
+    W = (torch.randn(N, K, device=DEV) * 0.1).to(torch.bfloat16)
+    d, _ = ops.tc_gemm_ex(g, W, None, epilogue=2, aux=pre)
+    ref_d = torch.ops.aten.gelu_backward((g.float() @ W.float().t()).to(torch.bfloat16).float(), pre.float(),
+                                         approximate="tanh")
+    assert ((d.float() - ref_d).abs().max() / ref_d.abs().max()).item() < 2e-2
+
+
+def test_diag_mlp_fused_matches_unfused(monkeypatch):
+    """DiagMLP with the GELU fused into the tensor-core epilogues == fc2(gelu(fc1(x)))."""
+    from paper_2506_11449_b200 import DiagMLP
+
+    T = TemperatureSchedule("constant", 0.05, 0.05, 1)
+    res = []
+    for fuse in ("1", "0", "bwd"):
+        monkeypatch.setenv("DIAGMM_FUSE_MLP", fuse)
+        torch.manual_seed(3)
+        f1 = DiagLinear(256, 1024, 0.9, seed=5, t_schedule=T, route="auto")
+        f2 = DiagLinear(1024, 256, 0.9, seed=6, t_schedule=T, route="auto")
+        with torch.no_grad():
+            f1.bias.normal_(0, 0.1)
+            f2.bias.normal_(0, 0.1)
+        mlp = DiagMLP(f1, f2)
+        x = torch.randn(1024, 256, device=DEV, generator=torch.Generator(device=DEV).manual_seed(7))
+        x = x.to(torch.bfloat16).requires_grad_(True)
+        y = mlp(x, step=0)
+        y.float().square().mean().backward()
+        res.append((y.float().detach(), x.grad.float(), f1.values.grad, f1.alpha.grad, f1.bias.grad,
+                    f2.values.grad, f2.alpha.grad, f2.bias.grad))
+    names = ["y", "dx", "dv1", "da1", "db1", "dv2", "da2", "db2"]
+    for other in (res[0], res[2]):
+        for nm, a, b in zip(names, other, res[1]):
+            scale = max(1e-6, b.abs().max().item())
+            assert ((a - b).abs().max().item() / scale) < 3e-2, nm
