@@ -40,6 +40,7 @@
 //    overlap one CTA's staging with another's FMAs.
 #include "common.cuh"
 #include <cmath>
+#include <cstdlib>
 
 namespace diagmm {
 
@@ -416,7 +417,7 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
 // 128 positions (lane + 32u) x one chunk of the diagonal list; its 8 warps
 // interleave over the chunk and are folded in a fixed order; chunks (grid.y)
 // are folded by k_split_reduce in a fixed order.
-constexpr int kNarrowB = 8;
+constexpr int kNarrowB = 8;  // rows per CTA (grid.z walks row blocks)
 template <typename T, int BT, bool GATHER>
 __global__ void __launch_bounds__(kThreads)
 k_product_narrow(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
@@ -429,6 +430,11 @@ k_product_narrow(int B, int C, int L, const T* __restrict__ in, const typename T
   const int in_w = GATHER ? C : L, out_w = GATHER ? L : C;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p0 = blockIdx.x * kWarpPos;
+  const int b0 = blockIdx.z * BT;
+  const int Bt = B;  // total rows (partials are indexed by global row)
+  B = min(BT, Bt - b0);  // rows of this block
+  in += (size_t)b0 * in_w;
+  out += (size_t)b0 * out_w;
   const int per = (n_act + nchunk - 1) / nchunk;
   const int jb = min(n_act, (int)blockIdx.y * per), je = min(n_act, jb + per);
   A acc[BT][kU];
@@ -509,7 +515,7 @@ k_product_narrow(int B, int C, int L, const T* __restrict__ in, const typename T
         if (bias) s_ += (A)bias[p];
         out[(size_t)b * out_w + p] = from_acc<T>(s_);
       } else {
-        part[((size_t)blockIdx.y * B + b) * out_w + p] = s_;
+        part[((size_t)blockIdx.y * Bt + b0 + b) * out_w + p] = s_;
       }
     }
     __syncthreads();
@@ -531,18 +537,36 @@ k_dw_narrow(int B, int C, int L, const T* __restrict__ aop, const T* __restrict_
   if (j >= n_act) return;
   const int o = __ldg(active + j);
   const int t0 = blockIdx.x * kWarpPos;
+  int ca[kU];
+  bool ok[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int t = t0 + lane + kWarp * u;
-    if (t >= L) continue;
-    int ca = o + t;
-    ca = ca >= C ? ca - C : ca;
-    A acc = A(0);
-#pragma unroll
-    for (int b = 0; b < BT; ++b)
-      if (b < B) acc = fma(to_acc<A>(__ldg(aop + (size_t)b * C + ca)), to_acc<A>(__ldg(bop + (size_t)b * L + t)), acc);
-    gw[(size_t)j * L + t] = acc;
+    ok[u] = t < L;
+    int c = o + t;
+    c = c >= C ? c - C : c;
+    ca[u] = ok[u] ? c : 0;
   }
+  A acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u] = A(0);
+  // the B-row contraction: BT rows unrolled per step (fixed order, deterministic)
+  for (int b0 = 0; b0 < B; b0 += BT) {
+#pragma unroll
+    for (int bb = 0; bb < BT; ++bb) {
+      const int b = b0 + bb;
+      if (b >= B) break;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = t0 + lane + kWarp * u;
+        if (ok[u])
+          acc[u] = fma(to_acc<A>(__ldg(aop + (size_t)b * C + ca[u])), to_acc<A>(__ldg(bop + (size_t)b * L + t)), acc[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u)
+    if (ok[u]) gw[(size_t)j * L + t0 + lane + kWarp * u] = acc[u];
 }
 
 // Fixed-order sum of the split partials (+ bias).
@@ -1023,8 +1047,18 @@ static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, 
   note_launch();
 }
 
-static int narrow_chunks(int out_w, int max_act) {
-  const int blocks = ceil_div(out_w, kWarpPos);
+// largest batch the narrow (staging-free) product kernels take (row blocks of 8)
+static int narrow_max_b() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIAGMM_NARROW_MAX_B");
+    v = e ? atoi(e) : 8;
+  }
+  return v;
+}
+
+static int narrow_chunks(int out_w, int max_act, int B = 1) {
+  const int blocks = ceil_div(out_w, kWarpPos) * ceil_div(B > 0 ? B : 1, kNarrowB);
   int nc = ceil_div(2 * num_sms(), blocks);
   const int max_nc = max_act / 32 > 1 ? max_act / 32 : 1;  // >= 4 diagonals per warp
   return nc < max_nc ? nc : max_nc;
@@ -1036,20 +1070,21 @@ static int run_product_narrow(bool gather, int B, int C, int L, const void* in, 
                               typename Vec<T>::A* part, cudaStream_t st) {
   using P = typename Traits<T>::P;
   const int out_w = gather ? L : C;
-  const int nc = narrow_chunks(out_w, max_act);
-  dim3 grid(ceil_div(out_w, kWarpPos), nc);
+  const int nc = narrow_chunks(out_w, max_act, B);
+  dim3 grid(ceil_div(out_w, kWarpPos), nc, ceil_div(B, kNarrowB));
   auto tin = static_cast<const T*>(in);
   auto tv = static_cast<const P*>(vals);
   auto tb = static_cast<const P*>(bias);
   auto to = static_cast<T*>(out);
 #define DIAGMM_NARROW(BT)                                                                                       \
-  if (B <= BT) {                                                                                                \
-    if (gather)                                                                                                 \
-      k_product_narrow<T, BT, true><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc);  \
-    else                                                                                                        \
-      k_product_narrow<T, BT, false><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc); \
-  } else
-  DIAGMM_NARROW(1) DIAGMM_NARROW(2) DIAGMM_NARROW(4) DIAGMM_NARROW(8) {}
+  if (gather)                                                                                                   \
+    k_product_narrow<T, BT, true><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc);  \
+  else                                                                                                          \
+    k_product_narrow<T, BT, false><<<grid, kThreads, 0, st>>>(B, C, L, tin, tv, asoft, active, n_act, max_act, tb, to, part, nc);
+  if (B <= 1) { DIAGMM_NARROW(1) }
+  else if (B <= 2) { DIAGMM_NARROW(2) }
+  else if (B <= 4) { DIAGMM_NARROW(4) }
+  else { DIAGMM_NARROW(8) }  // B > 8: row blocks of 8 along grid.z
 #undef DIAGMM_NARROW
   note_launch();
   if (nc > 1) {
@@ -1069,7 +1104,8 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   const int out_w = gather ? L : C, cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
   const size_t wbytes = align16((size_t)(max_act > 0 ? max_act : 1) * w_ld<T>(out_w) * sizeof(typename WType<T>::type));
-  const size_t narrow = B <= kNarrowB ? (size_t)narrow_chunks(out_w, max_act) * B * out_w * sizeof(A) : 0;
+  const size_t narrow = B <= (narrow_max_b() > kNarrowB ? narrow_max_b() : kNarrowB)
+                            ? (size_t)narrow_chunks(out_w, max_act, B) * B * out_w * sizeof(A) : 0;
   const size_t wide = wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
   return wide > narrow ? wide : narrow;
 }
@@ -1084,8 +1120,9 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
   if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
-  if (B <= kNarrowB) return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
-                                                 static_cast<A*>(ws), st);
+  if (B <= (narrow_max_b() > kNarrowB ? narrow_max_b() : kNarrowB))
+    return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
+                                 static_cast<A*>(ws), st);
   const int out_w = gather ? L : C, in_w = gather ? C : L;
   const int cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
@@ -1123,6 +1160,15 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
 }
 
 // ---- dW
+static int narrow_dw_max_b() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIAGMM_NARROW_DW_MAX_B");
+    v = e ? atoi(e) : 16;
+  }
+  return v;
+}
+
 template <typename T>
 static int dw_win_cap(int C, int max_act, int dwj) {
   constexpr int V = vec_rows<T>();
@@ -1189,11 +1235,11 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   int* ctr = reinterpret_cast<int*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +
                                     align16((size_t)cparts * M * sizeof(A)));
-  if (B > 0 && B <= 2 * kNarrowB && max_act > 0) {
+  if (B > 0 && B <= (narrow_dw_max_b() > 2 * kNarrowB ? narrow_dw_max_b() : 2 * kNarrowB) && max_act > 0) {
     parts = 1;
     dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
     if (B <= 4) k_dw_narrow<T, 4><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
-    else k_dw_narrow<T, 16><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
+    else k_dw_narrow<T, 8><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
     note_launch();
   } else if (B > 0 && max_act > 0) {
     const int dwj = dw_diags(L, max_act);

@@ -27,6 +27,41 @@ except Exception:  # noqa: BLE001 - optional: SDPA is used without it
     _flash_qkvpacked = None
 
 
+class PackedQKVAttention(torch.autograd.Function):
+    """Attention on a packed (B, T, 3, H, hd) qkv tensor through cuDNN's fused
+    SDPA kernels (library), with the three input gradients written straight
+    back into one packed (B, T, 3, H, hd) gradient — the caller's attention
+    around the qkv DiagLinear, without autograd's unbind/stack copies."""
+
+    @staticmethod
+    def forward(ctx, h):
+        # q, k, v: strided views of h made autograd leaves of their own, so the
+        # library op's registered backward gives dq, dk, dv and nothing else
+        qkv = [t.detach().requires_grad_(True) for t in h.permute(2, 0, 3, 1, 4).unbind(0)]
+        with torch.enable_grad():
+            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True)[0]
+        ctx.graph = (out, qkv)
+        ctx.h_shape = h.shape
+        return out.detach()
+
+    @staticmethod
+    def backward(ctx, g):
+        out, qkv = ctx.graph
+        grads = torch.autograd.grad(out, qkv, g)
+        ctx.graph = None
+        dh = torch.empty(ctx.h_shape, dtype=g.dtype, device=g.device)
+        dhv = dh.permute(2, 0, 3, 1, 4)  # (3, B, H, T, hd) view of the packed gradient
+        for i in range(3):
+            dhv[i].copy_(grads[i])
+        return dh
+
+
+def _attention_backend() -> str:
+    import os
+
+    return os.environ.get("DIAGMM_VIT_ATTENTION", "cudnn")
+
+
 class LayerNorm(nn.LayerNorm):
     """nn.LayerNorm that runs the fused bf16 kernel (csrc/norm_kernels.cu) when
     the activations are bf16 (directly or under CUDA autocast); float32 params."""
@@ -84,7 +119,10 @@ class Block(nn.Module):
     def forward(self, x):
         B, T, D = x.shape
         h = self.qkv(self.norm1(x)).view(B, T, 3, self.heads, D // self.heads)
-        if _flash_qkvpacked is not None and h.dtype in (torch.bfloat16, torch.float16):
+        backend = _attention_backend()
+        if backend == "cudnn" and h.is_cuda and h.dtype in (torch.bfloat16, torch.float16):
+            a = PackedQKVAttention.apply(h).transpose(1, 2).reshape(B, T, D)
+        elif backend != "sdpa" and _flash_qkvpacked is not None and h.dtype in (torch.bfloat16, torch.float16):
             # packed q/k/v in, packed dq/dk/dv out: no unbind/stack copies
             a = _flash_qkvpacked(h).reshape(B, T, D)
         else:
