@@ -43,8 +43,9 @@ def _worker(rank, world, port, q):
     shard = slice(rank * 4, rank * 4 + 4)
     _loss(m, x[shard], y[shard]).backward()
     GradientAllReducer(m.parameters())()
-    q.put((rank, {n: p.grad.clone() for n, p in m.named_parameters()},
-           {n: p.detach().clone() for n, p in m.named_parameters()}))
+    # numpy copies: pickled by value (tensors would be shared by fd and vanish with this process)
+    q.put((rank, {n: p.grad.detach().numpy().copy() for n, p in m.named_parameters()},
+           {n: p.detach().numpy().copy() for n, p in m.named_parameters()}))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -70,6 +71,6 @@ def test_allreduce_matches_full_batch_gradient():
     loss.backward()
     for n, p in m.named_parameters():
         for r in (0, 1):
-            torch.testing.assert_close(res[r][0][n], p.grad, rtol=1e-6, atol=1e-7)
-            torch.testing.assert_close(res[r][1][n], p.detach())
-        assert torch.equal(res[0][0][n], res[1][0][n])  # replicas bit-identical
+            torch.testing.assert_close(torch.from_numpy(res[r][0][n]), p.grad, rtol=1e-6, atol=1e-7)
+            torch.testing.assert_close(torch.from_numpy(res[r][1][n]), p.detach())
+        assert (res[0][0][n] == res[1][0][n]).all()  # replicas bit-identical
