@@ -155,11 +155,23 @@ class ViT(nn.Module):
         for m in self.diag_layers():
             m.step = step
 
+    def _patchify(self, images):
+        """Patch embedding as a GEMM: non-overlapping 16x16 patches are a pure
+        reshape/permute of the image, so conv2d(stride=kernel) == unfold @ W^T
+        (cuDNN's conv spends ~3 ms per step on layout transposes here)."""
+        B, Cin, H, W = images.shape
+        p = self.cfg.patch
+        x = images.reshape(B, Cin, H // p, p, W // p, p).permute(0, 2, 4, 1, 3, 5).reshape(B, -1, Cin * p * p)
+        w, b = self.patch.weight.reshape(self.cfg.dim, -1), self.patch.bias
+        if not torch.is_autocast_enabled(x.device.type):
+            w, b = w.to(x.dtype), None if b is None else b.to(x.dtype)
+        return torch.nn.functional.linear(x, w, b)
+
     def forward(self, images):
         diag = self.diag_layers()
         if diag:
             preselect(diag, diag[0].step)  # one batched soft-TopK launch for all layers
-        x = self.patch(images).flatten(2).transpose(1, 2)
+        x = self._patchify(images)
         x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
         for blk in self.blocks:
             x = blk(x)

@@ -114,3 +114,15 @@ def test_vit_layer_k_values():
     assert required_diagonals(768, 3072, 0.9) == 307
     assert required_diagonals(576, 192, 0.9) == 58
     assert required_diagonals(192, 192, 0.9) == 19
+
+
+def test_vit_patchify_equals_conv():
+    """The ViT caller's GEMM patch embedding equals the stride-16 convolution (CPU, fp64)."""
+    import torch
+    from paper_2506_11449_b200.vit import ViT, ViTConfig
+
+    cfg = ViTConfig(image=32, patch=16, dim=24, depth=0, heads=2, classes=5)
+    m = ViT(cfg, device="cpu").double()
+    img = torch.randn(3, 3, 32, 32, dtype=torch.float64)
+    ref = m.patch(img).flatten(2).transpose(1, 2)
+    torch.testing.assert_close(m._patchify(img), ref, rtol=1e-12, atol=1e-12)
