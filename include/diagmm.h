@@ -263,6 +263,13 @@ DIAGMM_API int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy,
                                     const float* mean, const float* rstd, void* dx, float* dw,
                                     float* db, void* workspace, size_t ws_bytes, void* stream);
 
+/* Packed attention-input gradient for the ViT caller: dqkv (B, T, 3, H, hd)
+ * bf16 contiguous <- dq, dk, dv (B, H, T, hd) bf16 sharing the element
+ * strides (stride_b, stride_h, stride_t; hd contiguous, all multiples of 8). */
+DIAGMM_API int diagmm_pack_qkv_grad(int B, int T, int H, int hd, const void* dq, const void* dk,
+                                    const void* dv, long long stride_b, long long stride_h,
+                                    long long stride_t, void* dqkv, void* stream);
+
 /* ---- dense-equivalent route (reference's own BLAS switch) ---------------
  * The reference multiplies the materialized matrix with BLAS when the
  * structural density reaches 1/4 (diagcore.py:226-228) and computes dW

@@ -40,6 +40,8 @@ int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStre
 size_t tc_dw_workspace(int, int, int, int);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
                    const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
+int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long long, long long, long long, void*,
+                 cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
@@ -203,6 +205,11 @@ int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x
 DIAGMM_API int diagmm_internal_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void* B, void* out,
                                                void* stream) {
   return run_tc_sparse_probe(Mdim, Ndim, K, Acomp, B, out, S(stream));
+}
+
+int diagmm_pack_qkv_grad(int B, int T, int H, int hd, const void* dq, const void* dk, const void* dv,
+                         long long stride_b, long long stride_h, long long stride_t, void* dqkv, void* stream) {
+  return run_pack_qkv(B, T, H, hd, dq, dk, dv, stride_b, stride_h, stride_t, dqkv, S(stream));
 }
 
 int diagmm_layernorm_fwd(int M, int D, float eps, const void* x, const float* w, const float* b, void* y,

@@ -201,6 +201,42 @@ k_ln_fold(int D, int nparts, const float* __restrict__ part, float* __restrict__
   }
 }
 
+// ---- packed qkv gradient: dh (B, T, 3, H, hd) <- dq, dk, dv (B, H, T, hd) with
+// arbitrary (b, h, t) strides and unit hd stride; one pass, 16-byte accesses.
+__global__ void __launch_bounds__(256)
+k_pack_qkv(int B, int T, int H, int hd, const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
+           const __nv_bfloat16* __restrict__ dv, long long sb, long long sh, long long st,
+           __nv_bfloat16* __restrict__ dh) {
+  const int v8 = hd / 8;
+  const long long total = (long long)B * T * 3 * H * v8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    long long r = i;
+    const int c = (int)(r % v8); r /= v8;
+    const int h = (int)(r % H); r /= H;
+    const int w = (int)(r % 3); r /= 3;
+    const int t = (int)(r % T);
+    const int b = (int)(r / T);
+    const __nv_bfloat16* src = w == 0 ? dq : (w == 1 ? dk : dv);
+    const uint4 u = *reinterpret_cast<const uint4*>(src + b * sb + h * sh + t * st + c * 8);
+    reinterpret_cast<uint4*>(dh)[i] = u;
+  }
+}
+
+int run_pack_qkv(int B, int T, int H, int hd, const void* dq, const void* dk, const void* dv, long long sb,
+                 long long sh, long long st, void* dh, cudaStream_t stream) {
+  if (B < 0 || T < 0 || H < 1 || hd < 8 || hd % 8) return DIAGMM_ESHAPE;
+  if ((sb | sh | st) % 8) return DIAGMM_ESHAPE;
+  const long long total = (long long)B * T * 3 * H * (hd / 8);
+  if (total == 0) return DIAGMM_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 16LL * num_sms()) blocks = 16LL * num_sms();
+  k_pack_qkv<<<(int)blocks, 256, 0, stream>>>(B, T, H, hd, static_cast<const __nv_bfloat16*>(dq),
+                                             static_cast<const __nv_bfloat16*>(dk), static_cast<const __nv_bfloat16*>(dv),
+                                             sb, sh, st, static_cast<__nv_bfloat16*>(dh));
+  note_launch();
+  return status_from_cuda();
+}
+
 static int ln_nv(int D) { return (D + 255) / 256; }
 
 int run_ln_fwd(int M, int D, float eps, const void* x, const float* w, const float* b, void* y, float* mean,

@@ -16,7 +16,7 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
-from . import ops
+from . import _lib, ops
 from .layer import DiagLinear, DiagMLP, preselect
 from .selection import TemperatureSchedule
 
@@ -50,9 +50,17 @@ class PackedQKVAttention(torch.autograd.Function):
         grads = torch.autograd.grad(out, qkv, g)
         ctx.graph = None
         dh = torch.empty(ctx.h_shape, dtype=g.dtype, device=g.device)
-        dhv = dh.permute(2, 0, 3, 1, 4)  # (3, B, H, T, hd) view of the packed gradient
-        for i in range(3):
-            dhv[i].copy_(grads[i])
+        st = grads[0].stride()
+        if (g.dtype == torch.bfloat16 and all(x.stride() == st and x.is_cuda for x in grads)
+                and grads[0].stride(-1) == 1):
+            B, T, _, H, hd = ctx.h_shape
+            _lib.call("diagmm_pack_qkv_grad", B, T, H, hd, grads[0].data_ptr(), grads[1].data_ptr(),
+                      grads[2].data_ptr(), st[0], st[1], st[2], dh.data_ptr(),
+                      torch.cuda.current_stream(g.device).cuda_stream)
+        else:
+            dhv = dh.permute(2, 0, 3, 1, 4)  # (3, B, H, T, hd) view of the packed gradient
+            for i in range(3):
+                dhv[i].copy_(grads[i])
         return dh
 
 

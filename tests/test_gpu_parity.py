@@ -661,3 +661,20 @@ def test_diag_mlp_fused_matches_unfused(monkeypatch):
         for nm, a, b in zip(names, other, res[1]):
             scale = max(1e-6, b.abs().max().item())
             assert ((a - b).abs().max().item() / scale) < 3e-2, nm
+
+
+def test_packed_qkv_attention_matches_sdpa():
+    """The ViT caller's packed-qkv attention (cuDNN SDPA + one-pass gradient pack)."""
+    from paper_2506_11449_b200.vit import PackedQKVAttention
+
+    B, T, H, hd = 4, 197, 12, 64
+    h = torch.randn(B, T, 3, H, hd, device=DEV, dtype=torch.bfloat16, requires_grad=True)
+    out = PackedQKVAttention.apply(h)
+    g = torch.randn_like(out)
+    out.backward(g)
+    h2 = h.detach().clone().requires_grad_(True)
+    q, k, v = h2.permute(2, 0, 3, 1, 4).unbind(0)
+    o2 = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
+    o2.backward(g.float())
+    assert (out.float() - o2).abs().max().item() < 2e-2
+    assert (h.grad.float() - h2.grad).abs().max().item() < 3e-2 * max(1.0, h2.grad.abs().max().item())
