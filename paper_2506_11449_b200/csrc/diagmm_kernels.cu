@@ -41,6 +41,7 @@
 #include "common.cuh"
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 namespace diagmm {
 
@@ -163,31 +164,44 @@ __device__ __forceinline__ void transpose_store<double>(double2 (&r)[2], double2
 // takes source column sc = (c0 + col) mod `mod` if sc < `limit`, else zero;
 // rows >= B are zero.  `vec_ok`: mod, limit, c0 multiples of VEC and src
 // 16-byte aligned (then every VEC-chunk is one aligned load).
-template <typename T>
+template <typename T, int UNR = 1>
 __device__ void stage_t(typename Vec<T>::U* __restrict__ dst, int ld, int ncols, const T* __restrict__ src, int B,
                         int W, int b0, int NG, int c0, int mod, int limit, bool vec_ok) {
   using U = typename Vec<T>::U;
   constexpr int VEC = vec_rows<T>();
   if (vec_ok) {
+    // UNR items per thread per pass: all their loads are issued before the
+    // first transpose, so a pass costs one memory latency, not UNR of them
     const int chunks = (ncols + VEC - 1) / VEC;
-    for (int it = threadIdx.x; it < NG * chunks; it += blockDim.x) {
-      const int g = it / chunks, ch = it - g * chunks;
-      const int sc = (c0 + ch * VEC) % mod;
-      const bool valid = sc < limit;
-      U r[VEC];
+    const int total = NG * chunks;
+    for (int base = threadIdx.x; base < total; base += blockDim.x * UNR) {
+      U r[UNR][VEC];
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        const int b = b0 + g * VEC + i;
-        if (valid && b < B) r[i] = *reinterpret_cast<const U*>(src + (size_t)b * W + sc);
-        else r[i] = U{};
+      for (int k = 0; k < UNR; ++k) {
+        const int it = base + k * blockDim.x;
+        const int g = it / chunks, ch = it - g * chunks;
+        const int sc = (c0 + ch * VEC) % mod;
+        const bool valid = it < total && sc < limit;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          const int b = b0 + g * VEC + i;
+          if (valid && b < B) r[k][i] = *reinterpret_cast<const U*>(src + (size_t)b * W + sc);
+          else r[k][i] = U{};
+        }
       }
-      U* d = dst + (size_t)g * ld + ch * VEC;
-      if (ch * VEC + VEC <= ncols) {
-        transpose_store<T>(r, d, 1);
-      } else {  // ragged last chunk: store the columns that fit
-        U tmp[VEC];
-        transpose_store<T>(r, tmp, 1);
-        for (int j = 0; ch * VEC + j < ncols; ++j) d[j] = tmp[j];
+#pragma unroll
+      for (int k = 0; k < UNR; ++k) {
+        const int it = base + k * blockDim.x;
+        if (it >= total) break;
+        const int g = it / chunks, ch = it - g * chunks;
+        U* d = dst + (size_t)g * ld + ch * VEC;
+        if (ch * VEC + VEC <= ncols) {
+          transpose_store<T>(r[k], d, 1);
+        } else {  // ragged last chunk: store the columns that fit
+          U tmp[VEC];
+          transpose_store<T>(r[k], tmp, 1);
+          for (int j = 0; ch * VEC + j < ncols; ++j) d[j] = tmp[j];
+        }
       }
     }
   } else {
@@ -268,6 +282,14 @@ k_prescale(int C, int L, int out_w, int ldw, int gather, const typename Traits<T
 // grid.z) take interleaved slices of its diagonal list and are folded in a
 // fixed order (deterministic).  PW = 8 is the pure position tiling (large
 // batches), PW = 1 with nsplit > 1 the pure diagonal split (B = 1).
+// bytes of the staged tile / fold buffer of k_product (the active list follows)
+template <typename T>
+__host__ __device__ inline size_t product_tile_bytes(int g, int cols) {
+  const size_t tile = (size_t)g * cols * 16;
+  const size_t red = (size_t)kWarps * g * vec_rows<T>() * kWarpPos * sizeof(typename Vec<T>::A);
+  return align16(tile > red ? tile : red);
+}
+
 template <typename T, int G, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 2)
 k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>::type* __restrict__ wts, int ldw,
@@ -293,11 +315,16 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
   const int pw = warp % PW, dw = warp / PW;
   const int p0 = t0 + pw * kWarpPos;  // this warp's first position
 
-  stage_t<T>(xs, cols, cols, in, B, in_w, b0, G, 0, GATHER ? C : 0x7fffffff, in_w, vec_ok != 0);
+  // the active offsets live in shared memory behind the tile: the scatter-form
+  // range search and the per-diagonal offset reads then cost no L2 round trips
+  int32_t* s_act = reinterpret_cast<int32_t*>(smem + product_tile_bytes<T>(G, cols));
+  for (int i = threadIdx.x; i < n_act; i += kThreads) s_act[i] = __ldg(active + i);
+  stage_t<T, 16 / vec_rows<T>()>(xs, cols, cols, in, B, in_w, b0, G, 0, GATHER ? C : 0x7fffffff, in_w, vec_ok != 0);
+  __syncthreads();
 
   int lo1, hi1, lo2, hi2;
   if (GATHER) { lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0; }
-  else scatter_ranges(active, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
+  else scatter_ranges(s_act, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
   const int len1 = hi1 - lo1;
   const int total = p0 < out_w ? len1 + (hi2 - lo2) : 0;
   const int per = (total + nsplit - 1) / nsplit;
@@ -323,7 +350,7 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
     if (q < nq) {
       const int v = vb + DW * q;
       const int j = v < len1 ? lo1 + v : lo2 + (v - len1);
-      const int o = __ldg(active + j);
+      const int o = s_act[j];
       const int base = p0 + lane + (GATHER ? o : C - o);
       ci = base >= C ? base - C : base;  // < C
       const typename WType<T>::type* wr = wts + (size_t)j * ldw + p0 + lane;
@@ -589,6 +616,7 @@ constexpr int kDwPosWarps = 2;                         // warps along positions
 constexpr int kDwTile = kDwPosWarps * kWarpPos;        // 256 positions per CTA
 constexpr int kDwGroups = kWarps / kDwPosWarps;        // 4 diagonal groups
 constexpr int kDwNG = 2;                               // row groups per staged chunk
+template <typename T> __host__ __device__ constexpr int kDwUnr() { return 8 / vec_rows<T>() > 1 ? 8 / vec_rows<T>() : 1; }
 
 template <typename T>
 __host__ __device__ inline size_t dw_smem(int win_cap) {
@@ -601,7 +629,7 @@ template <typename T, int JW>
 __global__ void __launch_bounds__(kThreads, 2)
 k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
      const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act, int win_cap,
-     int rows_per_part, typename Vec<T>::A* __restrict__ partial, int* __restrict__ tile_ctr, int vec_ok) {
+     int rows_per_part, typename Vec<T>::A* __restrict__ partial, int vec_ok) {
   using U = typename Vec<T>::U;
   using A = typename Vec<T>::A;
   constexpr int VEC = vec_rows<T>();
@@ -640,8 +668,8 @@ k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
   const int rb = blockIdx.z * rows_per_part, re = min(B, rb + rows_per_part);
   for (int r0 = rb; r0 < re; r0 += RB) {
     __syncthreads();  // previous chunk consumed
-    if (!direct) stage_t<T>(as, win_cap, wcols, aop, re, C, r0, kDwNG, aws, C, C, vec_ok != 0);
-    stage_t<T>(bs, kDwTile, kDwTile, bop, re, L, r0, kDwNG, t0, 0x7fffffff, L, vec_ok != 0);
+    if (!direct) stage_t<T, kDwUnr<T>()>(as, win_cap, wcols, aop, re, C, r0, kDwNG, aws, C, C, vec_ok != 0);
+    stage_t<T, kDwUnr<T>()>(bs, kDwTile, kDwTile, bop, re, L, r0, kDwNG, t0, 0x7fffffff, L, vec_ok != 0);
     __syncthreads();
 #pragma unroll
     for (int g = 0; g < kDwNG; ++g) {
@@ -689,38 +717,6 @@ k_dw(int B, int C, int L, const T* __restrict__ aop, const T* __restrict__ bop,
       if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
     }
   }
-  if (gridDim.z == 1) return;
-  // The last row part to finish folds all parts of this tile in a fixed order
-  // (deterministic) into part 0, so the partials only ever live in L2.
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* ctr = tile_ctr + blockIdx.y * gridDim.x + blockIdx.x;
-    const int prev = atomicAdd(ctr, 1);
-    s_last = prev == (int)gridDim.z - 1;
-    if (s_last) *ctr = 0;  // ready for the next launch
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int i = threadIdx.x; i < nj * kDwTile; i += kThreads) {
-    const int jj = i / kDwTile, t = t0 + (i - jj * kDwTile);
-    if (t >= L) continue;
-    const size_t off = (size_t)(j0 + jj) * L + t;
-    const size_t zs = (size_t)max_act * L;
-    A sum = A(0);
-    int z = 0;
-    for (; z + 8 <= (int)gridDim.z; z += 8) {  // 8 loads in flight, summed in z order
-      A v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcg(partial + (size_t)(z + k) * zs + off);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum += v[k];
-    }
-    for (; z < (int)gridDim.z; ++z) sum += __ldcg(partial + (size_t)z * zs + off);
-    partial[off] = sum;
-  }
 }
 
 // Deterministic block sum of one double per thread (fixed tree order).
@@ -739,7 +735,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // Reduce dW partials over parts (fixed order), scale into g_values rows,
-// zero inactive rows, and form g_soft.
+// zero inactive rows, and form g_soft.  One CTA per candidate row.  The row is
+// walked in 16-byte vectors with every load of the (usually single) pass
+// issued before its first use, so an active row costs ~one memory latency and
+// the ~90 % inactive rows are a vectorised zero fill.  g_soft: per-thread sums
+// in a fixed order, then a fixed shuffle/warp tree (deterministic).
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
@@ -748,16 +748,21 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
               typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
-  __shared__ double red[32];
+  static_assert(sizeof(A) == sizeof(P), "partials and values share the vector width");
+  constexpr int VW = 16 / sizeof(P);
+  using V = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
+  using VA = typename std::conditional<sizeof(A) == 8, double2, float4>::type;
+  __shared__ double red[kWarps];
   const int i = blockIdx.x;
   const int n_act = min(*n_act_p, max_act);
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
-  constexpr int W = 16 / sizeof(P);
-  const bool vec = L % W == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0;
+  const bool vec = L % VW == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   if (s < 0 || s >= n_act) {
     if (vec) {
-      for (int t = threadIdx.x; t < L / W; t += blockDim.x) reinterpret_cast<uint4*>(grow)[t] = make_uint4(0, 0, 0, 0);
+      V* g4 = reinterpret_cast<V*>(grow);
+      for (int t = threadIdx.x; t < L / VW; t += blockDim.x) g4[t] = V{};
     } else {
       for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
     }
@@ -765,16 +770,58 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
     return;
   }
   const double sc = asoft ? asoft[i] : 1.0;
+  const P* vrow = vals + (size_t)i * L;
   double local = 0.0;
-  for (int t = threadIdx.x; t < L; t += blockDim.x) {
-    A gw = A(0);
-    for (int p = 0; p < nparts; ++p) gw += partial[((size_t)p * max_act + s) * L + t];
-    grow[t] = (P)(sc * (double)gw);
-    local += (double)gw * (double)vals[(size_t)i * L + t];
+  if (vec) {
+    // parts are summed in index order; up to 8 of their loads are in flight
+    const int nv = L / VW;
+    const size_t zs = (size_t)max_act * L / VW;
+    const VA* pbase = reinterpret_cast<const VA*>(partial + (size_t)s * L);
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+      const V v = reinterpret_cast<const V*>(vrow)[c];
+      VA gw = nparts > 0 ? pbase[c] : VA{};
+      A* ge = reinterpret_cast<A*>(&gw);
+      for (int p0 = 1; p0 < nparts; p0 += 8) {
+        VA x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (p0 + k < nparts) x[k] = __ldcg(pbase + (size_t)(p0 + k) * zs + c);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (p0 + k >= nparts) break;
+          const A* xe = reinterpret_cast<const A*>(&x[k]);
+#pragma unroll
+          for (int e = 0; e < VW; ++e) ge[e] += xe[e];
+        }
+      }
+      const P* ve = reinterpret_cast<const P*>(&v);
+      V o;
+      P* oe = reinterpret_cast<P*>(&o);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        oe[e] = (P)(sc * (double)ge[e]);
+        local += (double)ge[e] * (double)ve[e];
+      }
+      reinterpret_cast<V*>(grow)[c] = o;
+    }
+  } else {
+    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+      A gw = A(0);
+      for (int p = 0; p < nparts; ++p) gw += partial[((size_t)p * max_act + s) * L + t];
+      grow[t] = (P)(sc * (double)gw);
+      local += (double)gw * (double)vrow[t];
+    }
   }
   if (g_soft) {
-    double tot = block_sum(local, red);
-    if (threadIdx.x == 0) g_soft[i] = tot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      g_soft[i] = tot;
+    }
   }
 }
 
@@ -982,11 +1029,7 @@ struct ProductPlan {
 
 template <typename T>
 static size_t product_smem(int g, int cols, int max_act) {
-  using A = typename Vec<T>::A;
-  const size_t tile = (size_t)g * cols * 16;
-  const size_t red = (size_t)kWarps * g * vec_rows<T>() * kWarpPos * sizeof(A);  // fold buffer
-  (void)max_act;
-  return align16(tile > red ? tile : red);
+  return product_tile_bytes<T>(g, cols) + align16((size_t)(max_act > 0 ? max_act : 1) * sizeof(int32_t));
 }
 
 template <typename T>
@@ -1188,8 +1231,10 @@ static int dw_diags(int L, int max_act) {
 }
 
 static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_per_part) {
+  // as many row parts as keep the grid within ONE wave at two resident CTAs
+  // per SM (a second, partial wave would double the kernel time)
   const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, dw_diags(L, max_act));
-  long long p = ceil_div(3LL * num_sms(), tiles);
+  long long p = 2LL * num_sms() / tiles;
   if (p < 1) p = 1;
   const long long max_p = ceil_div(B, rb);
   if (p > max_p) p = max_p;
@@ -1210,9 +1255,7 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
   const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
-  const size_t tiles = (size_t)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwGroups * 8);
-  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A)) +
-                    align16(tiles * sizeof(int));
+  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
   size_t w = dw > prod_f ? dw : prod_f;
   return w > prod_b ? w : prod_b;
 }
@@ -1233,8 +1276,6 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
-  int* ctr = reinterpret_cast<int*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +
-                                    align16((size_t)cparts * M * sizeof(A)));
   if (B > 0 && B <= (narrow_dw_max_b() > 2 * kNarrowB ? narrow_dw_max_b() : 2 * kNarrowB) && max_act > 0) {
     parts = 1;
     dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
@@ -1249,13 +1290,12 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
     auto k = dwj == kDwGroups * 16 ? k_dw<T, 16> : k_dw<T, 8>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid(ceil_div(L, kDwTile), ceil_div(max_act, dwj), parts);
-    if (parts > 1) cudaMemsetAsync(ctr, 0, (size_t)grid.x * grid.y * sizeof(int), st);
-    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, ctr, vec_ok);
+    k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, vec_ok);
     note_launch();
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts > 0 ? 1 : 0, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft);
   note_launch();
   if (g_bias) {
