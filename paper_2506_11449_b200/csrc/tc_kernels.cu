@@ -5,37 +5,53 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "tc_gemm.cuh"
 
 namespace diagmm {
 namespace tc {
 
+// GELU (tanh form) in the GEMM epilogues.  tanh comes from the SFU
+// (tanh.approx.f32, |rel err| < 2^-10.9): the results are rounded to bf16
+// (2^-8) right after, and a full-precision tanhf made the epilogue warps,
+// not the tensor cores, the bottleneck of the fused fc1/fc2 tiles.
+__device__ __forceinline__ float tanh_sfu(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_sfu(k0 * fmaf(k1 * x, x * x, x)), hx);
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {  // d gelu_tanh / dx (PyTorch's formula)
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanhf(k0 * (x + k1 * x * x * x));
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+  const float x2 = x * x;
+  const float t = tanh_sfu(k0 * fmaf(k1 * x, x2, x));
+  const float hx = 0.5f * x;
+  return fmaf(hx * (1.f - t * t), k0 * fmaf(3.f * k1, x2, 1.f), 0.5f * (1.f + t));
 }
 
-template <int BN>
+template <int BN, int NST = kStages, int NC = 1>
 struct Smem {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;
   static constexpr size_t b_bytes = (size_t)BN * BK * 2;
   static constexpr size_t stage = a_bytes + b_bytes;
   static constexpr size_t c_bytes = (size_t)BM * BN;  // half the output tile (two 64-column swizzled boxes)
   static constexpr size_t bars = 128 + BN * 4;  // barriers, TMEM slot, aux barrier, bias tile
-  static constexpr size_t total = 1024 /* alignment slack */ + kStages * stage + c_bytes + bars;
+  static constexpr size_t total = 1024 /* alignment slack */ + NST * stage + NC * c_bytes + bars;
 };
 
 // Persistent: grid = min(tiles, SMs); CTA c takes tiles c, c + grid, ...
 // (n-block fastest).  The TMA warp runs ahead across tile boundaries, the
 // MMA thread alternates between two TMEM accumulators (2 x BN columns) so the
 // epilogue of tile i overlaps the main loop of tile i+1.
-template <int BN>
+// NST smem pipeline stages, NC half-tile staging buffers: the GELU-forward
+// variant (two outputs per tile) trades one stage for a second staging buffer
+// so the pre-activation and the activation leave in the same store round.
+template <int BN, int NST, int NC>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
@@ -43,13 +59,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  using S = Smem<BN>;
+  using S = Smem<BN, NST, NC>;
   unsigned char* sA = smem;
-  unsigned char* sB = smem + kStages * S::a_bytes;
-  unsigned char* sC = smem + kStages * S::stage;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(sC + S::c_bytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // [2]
+  unsigned char* sB = smem + NST * S::a_bytes;
+  unsigned char* sC = smem + NST * S::stage;  // 1024-aligned
+  unsigned char* sC2 = sC + (NC > 1 ? S::c_bytes : 0);  // pre-activation staging (epi 1)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + NC * S::c_bytes);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* auxbar = tempty + 3;  // after tslot's 8 bytes
@@ -60,7 +77,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   const int tiles = ((Mdim + BM - 1) / BM) * nb;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])) : "memory");
     }
@@ -92,7 +109,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % kStages, round = it / kStages;
+          const int s = it % NST, round = it / NST;
           mbar_wait_parity(&empty[s], (round & 1) ^ 1);
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
           tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
@@ -110,7 +127,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)(ab * BN);
         for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % kStages, round = it / kStages;
+          const int s = it % NST, round = it / NST;
           mbar_wait_parity(&full[s], round & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t da = smem_desc_sw128(sA + s * S::a_bytes);
@@ -127,7 +144,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     // TMEM -> registers (32 columns at a time) -> epilogue op, bf16 -> the 128B-
     // swizzled smem tile (one 64-column box per 16 KB) -> TMA bulk tensor store.
     //   epi 0: out = acc + bias
-    //   epi 1: aux = acc + bias (pre-activation), out = gelu_tanh(aux)
+    //   epi 1: aux = acc + bias (pre-activation), out = gelu_tanh(aux): one TMEM
+    //          read, both halves staged (sC2 / sC) and stored in one round (NC = 2)
     //   epi 2: out = acc * gelu_tanh'(aux)   (aux TMA-loaded into the staging tile)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -136,11 +154,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     const bool leader = et == 0;
     float* sbias = reinterpret_cast<float*>(tslot + 4);  // BN floats after the barriers
     uint32_t aux_phase = 0;
-    auto wait_reads = [&]() {  // previous TMA store finished reading the staging tile
-      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    // epi 0 with two staging buffers ping-pongs the halves (sC, sC2), so a
+    // store round only waits for the one issued a round earlier
+    const bool pingpong = NC > 1 && epi == 0;
+    auto wait_reads = [&]() {  // the store that last used the next staging buffer finished reading it
+      if (leader) {
+        if (pingpong) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     };
-    auto store_half = [&](const CUtensorMap* map, int m0, int col0) {
+    auto store_half = [&](int m0, int col0, bool with_aux, unsigned char* obuf) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (leader) {
@@ -149,16 +173,21 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           const int col = col0 + bx * 64;
           if (col >= Ndim) break;
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                           reinterpret_cast<uint64_t>(map)),
-                       "r"(col), "r"(m0), "r"(smem_u32(sC + (size_t)bx * (BM * 128)))
+                           reinterpret_cast<uint64_t>(&tc_out)),
+                       "r"(col), "r"(m0), "r"(smem_u32(obuf + (size_t)bx * (BM * 128)))
                        : "memory");
+          if (with_aux)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tc_aux)),
+                         "r"(col), "r"(m0), "r"(smem_u32(sC2 + (size_t)bx * (BM * 128)))
+                         : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
     // 8 bf16 of this thread's row in 16-byte chunk `ch` (0..7) of the box holding chunk cl
-    auto sc_addr = [&](int cl, int j) {
-      unsigned char* box = sC + (size_t)(cl >> 1) * (BM * 128);
+    auto sc_addr = [&](int cl, int j, unsigned char* buf) {
+      unsigned char* box = buf + (size_t)(cl >> 1) * (BM * 128);
       const int chunk = ((cl & 1) * 4 + j) ^ (rl & 7);
       return reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16);
     };
@@ -166,7 +195,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
       const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
+      // epi 2: the pre-activation half tile comes in by TMA — into sC2, issued
+      // ahead (half 0 before the accumulator wait, half 1 right after half 0's
+      // store round) when there are two staging buffers, else into sC in turn
+      auto load_aux = [&](int hh, unsigned char* buf) {
+        mbar_expect_tx(auxbar, (uint32_t)S::c_bytes);
+#pragma unroll
+        for (int bx = 0; bx < BN / 128; ++bx)
+          tma_load_2d(buf + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / 2) + bx * 64, m0, auxbar);
+      };
       wait_reads();
+      if (NC > 1 && epi == 2 && leader) load_aux(0, sC2);
       for (int c = et; c < BN; c += kEpiThreads) sbias[c] = (bias && n0 + c < Ndim) ? __ldg(bias + n0 + c) : 0.f;
       mbar_wait_parity(&tfull[ab], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -174,60 +213,60 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         if (hh == 1) wait_reads();
-        if (epi == 2) {  // bring the pre-activation half tile into the staging buffer
-          if (leader) {
-            mbar_expect_tx(auxbar, (uint32_t)S::c_bytes);
-#pragma unroll
-            for (int bx = 0; bx < BN / 128; ++bx)
-              tma_load_2d(sC + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / 2) + bx * 64, m0, auxbar);
-          }
+        if (epi == 2) {
+          if (NC == 1 && leader) load_aux(hh, sC);
           mbar_wait_parity(auxbar, aux_phase);
           aux_phase ^= 1;
         }
+        unsigned char* obuf = (pingpong && hh == 1) ? sC2 : sC;
 #pragma unroll 1
-        for (int pass = 0; pass < (epi == 1 ? 2 : 1); ++pass) {
-          if (pass == 1) wait_reads();
-#pragma unroll 1
-          for (int cc = 0; cc < BN / 128; ++cc) {
-            const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
-            const int cl = c - hh * (BN / 64);                      // chunk within this half
-            uint32_t r[32];
-            tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
-            uint32_t prev[16];
-            if (epi == 2) {
+        for (int cc = 0; cc < BN / 128; ++cc) {
+          const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
+          const int cl = c - hh * (BN / 64);                      // chunk within this half
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+          uint32_t prev[16];
+          if (epi == 2) {
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const uint4 u = *sc_addr(cl, j);
-                prev[4 * j] = u.x; prev[4 * j + 1] = u.y; prev[4 * j + 2] = u.z; prev[4 * j + 3] = u.w;
-              }
+            for (int j = 0; j < 4; ++j) {
+              const uint4 u = *sc_addr(cl, j, NC > 1 ? sC2 : sC);
+              prev[4 * j] = u.x; prev[4 * j + 1] = u.y; prev[4 * j + 2] = u.z; prev[4 * j + 3] = u.w;
             }
-            uint32_t pk[16];
+          }
+          uint32_t pk[16], pre[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float a = __uint_as_float(r[2 * j]), b = __uint_as_float(r[2 * j + 1]);
-              if (epi != 2) { a += sbias[c * 32 + 2 * j]; b += sbias[c * 32 + 2 * j + 1]; }
-              if (epi == 1 && pass == 1) {  // gelu of the bf16-rounded pre-activation (as stored)
-                a = gelu_tanh(__bfloat162float(__float2bfloat16_rn(a)));
-                b = gelu_tanh(__bfloat162float(__float2bfloat16_rn(b)));
-              } else if (epi == 2) {
-                a *= gelu_tanh_grad(__uint_as_float(prev[j] << 16));
-                b *= gelu_tanh_grad(__uint_as_float(prev[j] & 0xffff0000u));
-              }
-              __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          for (int j = 0; j < 16; ++j) {
+            float a = __uint_as_float(r[2 * j]), b = __uint_as_float(r[2 * j + 1]);
+            if (epi != 2) { a += sbias[c * 32 + 2 * j]; b += sbias[c * 32 + 2 * j + 1]; }
+            if (epi == 1) {  // gelu of the bf16-rounded pre-activation (as stored)
+              __nv_bfloat162 hp = __floats2bfloat162_rn(a, b);
+              pre[j] = *reinterpret_cast<uint32_t*>(&hp);
+              a = gelu_tanh(__low2float(hp));
+              b = gelu_tanh(__high2float(hp));
+            } else if (epi == 2) {
+              a *= gelu_tanh_grad(__uint_as_float(prev[j] << 16));
+              b *= gelu_tanh_grad(__uint_as_float(prev[j] & 0xffff0000u));
             }
+            __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          if (NC > 1 && epi == 1) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) *sc_addr(cl, j) = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            for (int j = 0; j < 4; ++j)
+              *sc_addr(cl, j, sC2) = make_uint4(pre[4 * j], pre[4 * j + 1], pre[4 * j + 2], pre[4 * j + 3]);
           }
-          const bool last = hh == 1 && pass == (epi == 1 ? 1 : 0);
-          if (last) {  // accumulator consumed: hand it back to the MMA thread
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0)
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
-          }
-          store_half((epi == 1 && pass == 0) ? &tc_aux : &tc_out, m0, n0 + hh * (BN / 2));
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *sc_addr(cl, j, obuf) = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
+        if (hh == 1) {  // accumulator consumed: hand it back to the MMA thread
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
+        }
+        store_half(m0, n0 + hh * (BN / 2), NC > 1 && epi == 1, obuf);
+        if (NC > 1 && epi == 2 && hh == 0 && leader) load_aux(1, sC2);  // sC2 read by all (barrier above)
       }
     }
     if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -786,12 +825,20 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
       !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo) ||
       !make_tmap_bf16(&taux, epi ? aux : out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo))
     return DIAGMM_ECUDA;
-  auto k = k_tc_gemm<BN>;
-  const size_t sm = Smem<BN>::total;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+  static const bool pp0 = [] { const char* e = getenv("DIAGMM_TC_PINGPONG"); return e && atoi(e) != 0; }();
+  if (epi != 0 || pp0) {  // a second half-tile buffer (pre-activation out / aux in / ping-pong): 3 stages
+    auto k = k_tc_gemm<BN, kStages - 1, 2>;
+    const size_t sm = Smem<BN, kStages - 1, 2>::total;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+  } else {
+    auto k = k_tc_gemm<BN, kStages, 1>;
+    const size_t sm = Smem<BN, kStages, 1>::total;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+  }
   note_launch();
   return status_from_cuda();
 }

@@ -360,12 +360,14 @@ class DiagLinear(nn.Module):
 class DiagMLP(nn.Module):
     """fc1 -> GELU (tanh) -> fc2 with two DiagLinear layers (the ViT / GPT MLP).
 
-    With DIAGMM_FUSE_MLP=bwd|1 on the tensor-core route (bf16, >= dense_route_min_tokens
-    tokens, dims multiple of 64) the GELU is fused into the GEMM epilogues
-    (DiagMLPFunction: "bwd" = gelu' in fc2's input-gradient epilogue, "1" = also
-    gelu in fc1's epilogue).  Measured on B200 the extra epilogue work makes the
-    short-K (768) GEMMs epilogue-bound and the step 0.4 / 1.9 ms slower, so the
-    default is the unfused fc2(gelu(fc1(x)))."""
+    On the tensor-core route (bf16, >= dense_route_min_tokens tokens, dims multiple
+    of 64) the GELU is fused into the GEMM epilogues (DiagMLPFunction): gelu in
+    fc1's epilogue (which also stores the pre-activation) and gelu' in fc2's
+    input-gradient epilogue, so the two elementwise GELU passes over the
+    (tokens x 4d) activation disappear.  DIAGMM_FUSE_MLP selects it: "1" (default)
+    both, "bwd" backward only, "0" the unfused fc2(gelu(fc1(x))).  The epilogues
+    take tanh from the SFU; with a full-precision tanhf the short-K (768) GEMMs
+    were epilogue-bound and the fused step was slower."""
 
     def __init__(self, fc1: "DiagLinear", fc2: "DiagLinear"):
         super().__init__()
@@ -381,7 +383,7 @@ class DiagMLP(nn.Module):
                 and all(m.route == "auto" and m.out_features % 64 == 0 and m.in_features % 64 == 0 for m in layers)
                 and all(m.values.dtype == torch.float32 for m in layers)
                 and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas"
-                and os.environ.get("DIAGMM_FUSE_MLP", "0") != "0")
+                and os.environ.get("DIAGMM_FUSE_MLP", "1") != "0")
 
     def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
         f1, f2 = self.fc1, self.fc2
@@ -397,7 +399,7 @@ class DiagMLP(nn.Module):
         f1.last_step, f2.last_step = step1, step2
         import os
 
-        fuse_fwd = os.environ.get("DIAGMM_FUSE_MLP", "0") in ("1", "both", "fwd")
+        fuse_fwd = os.environ.get("DIAGMM_FUSE_MLP", "1") in ("1", "both", "fwd")
         y = DiagMLPFunction.apply(x2, f1.values, f1.alpha, f1.bias, f2.values, f2.alpha, f2.bias,
                                   f1._make_spec(step1), f2._make_spec(step2), fuse_fwd)
         return y.reshape(*lead, f2.out_features)

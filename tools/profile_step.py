@@ -50,6 +50,15 @@ step(3)
 s1.record()
 torch.cuda.synchronize()
 print(f"step ms (events, unprofiled) {s0.elapsed_time(s1):.2f}")
+import time
+for _ in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    step(3)
+    t_host = (time.perf_counter() - t0) * 1e3
+    torch.cuda.synchronize()
+    t_all = (time.perf_counter() - t0) * 1e3
+    print(f"host enqueue ms {t_host:.2f}  enqueue+drain ms {t_all:.2f}")
 from torch.profiler import ProfilerActivity, profile
 
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
