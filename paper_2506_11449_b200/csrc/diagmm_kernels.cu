@@ -43,6 +43,8 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 namespace diagmm {
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -200,7 +202,9 @@ __device__ void stage_t(typename Vec<T>::U* __restrict__ dst, int ld, int ncols,
         } else {  // ragged last chunk: store the columns that fit
           U tmp[VEC];
           transpose_store<T>(r[k], tmp, 1);
-          for (int j = 0; ch * VEC + j < ncols; ++j) d[j] = tmp[j];
+#pragma unroll
+          for (int j = 0; j < VEC; ++j)
+            if (ch * VEC + j < ncols) d[j] = tmp[j];
         }
       }
     }
@@ -249,22 +253,44 @@ __host__ __device__ inline int scatter_cols(int L) {
 //   scatter form: w[j, p] = s_j * values[o_j, c], c = (p - o_j) mod C,  0 if c >= L
 // s_j = alpha_soft[o_j] (the reference's `weights`, layers.py:235); one
 // rounding from the float64 product.  Columns [out_w, ldw) are zero.
+// Each thread writes 4 consecutive positions of one diagonal row (one 16-byte
+// load in the aligned gather form, 4 independent loads otherwise), so the
+// HBM-bound pass keeps enough bytes in flight.
+constexpr int kPreVec = 4;
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_prescale(int C, int L, int out_w, int ldw, int gather, const typename Traits<T>::P* __restrict__ vals,
            const double* __restrict__ asoft, const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p,
            int max_act, typename WType<T>::type* __restrict__ w) {
+  using P = typename Traits<T>::P;
   using WT = typename WType<T>::type;
   const int n_act = min(*n_act_p, max_act);
+  const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * kPreVec;
+  if (p0 >= ldw) return;
+  const bool vec = gather && (L % 4 == 0) && p0 + kPreVec <= L && (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   for (int j = blockIdx.y; j < n_act; j += gridDim.y) {
     const int o = active[j];
     const double s = asoft ? asoft[o] : 1.0;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < ldw; p += gridDim.x * blockDim.x) {
-      int c = p;
-      if (!gather) { c = p - o; c = c < 0 ? c + C : c; }
-      const double v = (p < out_w && c < L) ? s * (double)vals[(size_t)o * L + c] : 0.0;
-      if constexpr (sizeof(WT) == 2) w[(size_t)j * ldw + p] = __double2bfloat16(v);
-      else w[(size_t)j * ldw + p] = (WT)v;
+    const P* vr = vals + (size_t)o * L;
+    P v[kPreVec];
+    if (vec && sizeof(P) == 4) {
+      const float4 f = *reinterpret_cast<const float4*>(vr + p0);
+      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < kPreVec; ++e) {
+        const int p = p0 + e;
+        int c = p;
+        if (!gather) { c = p - o; c = c < 0 ? c + C : c; }
+        v[e] = (p < out_w && c < L) ? vr[c] : P(0);
+      }
+    }
+    WT* wr = w + (size_t)j * ldw + p0;
+#pragma unroll
+    for (int e = 0; e < kPreVec; ++e) {
+      const double x = s * (double)v[e];
+      if constexpr (sizeof(WT) == 2) wr[e] = __double2bfloat16(x);
+      else wr[e] = (WT)x;
     }
   }
 }
@@ -284,21 +310,44 @@ k_prescale(int C, int L, int out_w, int ldw, int gather, const typename Traits<T
 // batches), PW = 1 with nsplit > 1 the pure diagonal split (B = 1).
 // bytes of the staged tile / fold buffer of k_product (the active list follows)
 template <typename T>
-__host__ __device__ inline size_t product_tile_bytes(int g, int cols) {
+__host__ __device__ inline size_t product_tile_bytes(int g, int cols, bool cluster = false) {
   const size_t tile = (size_t)g * cols * 16;
-  const size_t red = (size_t)kWarps * g * vec_rows<T>() * kWarpPos * sizeof(typename Vec<T>::A);
+  const size_t row = (size_t)g * vec_rows<T>() * kWarpPos * sizeof(typename Vec<T>::A);
+  const size_t red = kWarps * row + (cluster ? row : 0);  // + the folded tile (cluster fold, PW = 1)
   return align16(tile > red ? tile : red);
 }
 
-template <typename T, int G, bool GATHER>
+// Weight of the compute type formed in the kernel (FW): s_j * values in fp32
+// for bf16 / fp32 (a float64 product plus its F2F conversions costs more than
+// the FMAs it feeds at these batch sizes; the fp32 product is within 2 ulp of
+// k_prescale's single rounding), in fp64 for fp64.
+template <typename T> struct FwScale { using S = float; };
+template <> struct FwScale<double> { using S = double; };
+template <typename T> __device__ __forceinline__ typename Vec<T>::W weight_from(typename FwScale<T>::S s,
+                                                                               typename Traits<T>::P v);
+template <> __device__ __forceinline__ uint32_t weight_from<__nv_bfloat16>(float s, float v) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(s * v));
+}
+template <> __device__ __forceinline__ float weight_from<float>(float s, float v) { return s * v; }
+template <> __device__ __forceinline__ double weight_from<double>(double s, double v) { return s * v; }
+
+// FW (fused weights, small batches): the ring fetches the stored values and
+// alpha_soft and forms the weight at use time — no k_prescale pass.  With
+// nsplit > 1 the grid.z CTAs of a tile form one thread-block cluster and fold
+// their partial tiles through distributed shared memory (fixed rank order),
+// so there is no partial buffer and no second kernel either.
+template <typename T, int G, bool GATHER, bool FW>
 __global__ void __launch_bounds__(kThreads, 2)
 k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>::type* __restrict__ wts, int ldw,
+          const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
           const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
           const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out, typename Vec<T>::A* __restrict__ part,
           int PW, int nsplit, int vec_ok) {
   using U = typename Vec<T>::U;
   using A = typename Vec<T>::A;
   using Wt = typename Vec<T>::W;
+  using P = typename Traits<T>::P;
+  using RW = typename std::conditional<FW, P, Wt>::type;  // what the ring holds
   constexpr int VEC = vec_rows<T>();
   constexpr int RT = G * VEC;  // rows per CTA
   extern __shared__ __align__(128) unsigned char smem[];
@@ -317,7 +366,7 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
 
   // the active offsets live in shared memory behind the tile: the scatter-form
   // range search and the per-diagonal offset reads then cost no L2 round trips
-  int32_t* s_act = reinterpret_cast<int32_t*>(smem + product_tile_bytes<T>(G, cols));
+  int32_t* s_act = reinterpret_cast<int32_t*>(smem + product_tile_bytes<T>(G, cols, FW && nsplit > 1));
   for (int i = threadIdx.x; i < n_act; i += kThreads) s_act[i] = __ldg(active + i);
   stage_t<T, 16 / vec_rows<T>()>(xs, cols, cols, in, B, in_w, b0, G, 0, GATHER ? C : 0x7fffffff, in_w, vec_ok != 0);
   __syncthreads();
@@ -346,38 +395,58 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
 
   // Diagonal q+D is fetched (weights + staged-row index) while diagonal q is
   // multiplied: a D-deep register ring hides the L2 latency of the weights.
-  auto fetch = [&](int q, Wt (&wv)[kU], int& ci) {
+  using SC = typename FwScale<T>::S;
+  auto fetch = [&](int q, RW (&wv)[kU], SC& sc, int& ci) {
     if (q < nq) {
       const int v = vb + DW * q;
       const int j = v < len1 ? lo1 + v : lo2 + (v - len1);
       const int o = s_act[j];
       const int base = p0 + lane + (GATHER ? o : C - o);
       ci = base >= C ? base - C : base;  // < C
-      const typename WType<T>::type* wr = wts + (size_t)j * ldw + p0 + lane;
+      if constexpr (FW) {
+        sc = asoft ? (SC)__ldg(asoft + o) : SC(1);
+        const P* vr = vals + (size_t)o * L;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) wv[u] = pok[u] ? Vec<T>::load_w(wr + kWarp * u) : Wt(0);
+        for (int u = 0; u < kU; ++u) {
+          int c = GATHER ? p0 + lane + kWarp * u : ci + kWarp * u;
+          if (!GATHER) c = c >= C ? c - C : c;
+          wv[u] = (pok[u] && c < L) ? __ldg(vr + c) : P(0);
+        }
+      } else {
+        const typename WType<T>::type* wr = wts + (size_t)j * ldw + p0 + lane;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) wv[u] = pok[u] ? Vec<T>::load_w(wr + kWarp * u) : Wt(0);
+      }
     }
   };
   constexpr int D = (sizeof(Wt) == 8 || RT > 8) ? 4 : 8;
-  Wt wb[D][kU];
+  RW wb[D][kU];
+  SC sb[D];
   int cb_[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) wb[d][u] = Wt(0);
+    for (int u = 0; u < kU; ++u) wb[d][u] = RW(0);
+    sb[d] = SC(0);
     cb_[d] = 0;
-    fetch(d, wb[d], cb_[d]);
+    fetch(d, wb[d], sb[d], cb_[d]);
   }
   for (int q0 = 0; q0 < nq; q0 += D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       if (q0 + d < nq) {  // warp-uniform
+        Wt w[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if constexpr (FW) w[u] = weight_from<T>(sb[d], wb[d][u]);
+          else w[u] = wb[d][u];
+        }
         if (GATHER) {
           const U* xr = xs + cb_[d];
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
 #pragma unroll
-            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xr[(size_t)g * cols + kWarp * u], wb[d][u]);
+            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xr[(size_t)g * cols + kWarp * u], w[u]);
           }
         } else {
 #pragma unroll
@@ -386,11 +455,11 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
             c = c >= C ? c - C : c;
             c = c < L ? c : L;  // column L is zero
 #pragma unroll
-            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xs[(size_t)g * cols + c], wb[d][u]);
+            for (int g = 0; g < G; ++g) fma_vec(acc[g][u], xs[(size_t)g * cols + c], w[u]);
           }
         }
       }
-      fetch(q0 + d + D, wb[d], cb_[d]);
+      fetch(q0 + d + D, wb[d], sb[d], cb_[d]);
     }
   }
 
@@ -413,6 +482,7 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
   // fixed-order fold of the DW diagonal slices through shared memory:
   // red[dw][row][pos] with pos over the CTA's PW*128 positions
   const int TT = PW * kWarpPos;
+  const int tt_shift = 31 - __clz(TT);  // TT is 128 * a power of two
   __syncthreads();
 #pragma unroll
   for (int g = 0; g < G; ++g)
@@ -422,17 +492,45 @@ k_product(int B, int C, int L, const T* __restrict__ in, const typename WType<T>
       for (int u = 0; u < kU; ++u)
         red[((size_t)dw * RT + g * VEC + r) * TT + pw * kWarpPos + lane + kWarp * u] = acc[g][u][r];
   __syncthreads();
+  const bool cluster_fold = FW && nsplit > 1;
+  A* fin = red + (size_t)DW * RT * TT;  // this CTA's folded tile (cluster fold only)
   for (int i = threadIdx.x; i < RT * TT; i += kThreads) {
-    const int b = i / TT, tt = i - b * TT;
+    const int b = i >> tt_shift, tt = i & (TT - 1);
     const int p = t0 + tt;
-    if (b0 + b >= B || p >= out_w) continue;
     A s = A(0);
     for (int w = 0; w < DW; ++w) s += red[((size_t)w * RT + b) * TT + tt];
-    if (nsplit == 1) {
-      if (bias) s += (A)bias[p];
-      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
-    } else {
-      part[((size_t)blockIdx.z * B + b0 + b) * out_w + p] = s;
+    if (cluster_fold) {
+      fin[i] = s;
+    } else if (b0 + b < B && p < out_w) {
+      if (nsplit == 1) {
+        if (bias) s += (A)bias[p];
+        out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+      } else {
+        part[((size_t)blockIdx.z * B + b0 + b) * out_w + p] = s;
+      }
+    }
+  }
+  if constexpr (FW) {
+    if (cluster_fold) {
+      // every rank folds one slice of the tile, reading the partial tiles of all
+      // ranks in rank order (deterministic), then the cluster waits so no CTA
+      // leaves while its shared memory is still being read
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();
+      const int rank = (int)cl.block_rank(), nr = (int)cl.num_blocks();
+      const int per_r = (RT * TT + nr - 1) / nr;
+      const int i0 = rank * per_r, i1 = min(RT * TT, i0 + per_r);
+      for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+        const int b = i >> tt_shift, tt = i & (TT - 1);
+        const int p = t0 + tt;
+        if (b0 + b >= B || p >= out_w) continue;
+        A s = A(0);
+        for (int r = 0; r < nr; ++r) s += cl.map_shared_rank(fin, r)[i];
+        if (bias) s += (A)bias[p];
+        out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+      }
+      cl.sync();
     }
   }
 }
@@ -605,10 +703,28 @@ k_split_reduce(int B, int out_w, int nsplit, const typename Vec<T>::A* __restric
   const size_t n = (size_t)B * out_w;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     A s = A(0);
-    for (int z = 0; z < nsplit; ++z) s += part[(size_t)z * n + i];
+    for (int z0 = 0; z0 < nsplit; z0 += 8) {  // 8 loads in flight, summed in split order
+      A v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = z0 + k < nsplit ? __ldcg(part + (size_t)(z0 + k) * n + i) : A(0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (z0 + k < nsplit) s += v[k];
+    }
     if (bias) s += (A)bias[i % out_w];
     out[i] = from_acc<T>(s);
   }
+}
+
+// small outputs use 64-thread blocks so the fold spreads over more SMs
+template <typename T>
+static void launch_split_reduce(int B, int out_w, int nsplit, const typename Vec<T>::A* part,
+                                const typename Traits<T>::P* bias, T* out, cudaStream_t st) {
+  const size_t n = (size_t)B * out_w;
+  const int threads = n < (size_t)256 * num_sms() ? 64 : 256;
+  long long blocks = (long long)((n + threads - 1) / threads);
+  if (blocks > 4LL * num_sms()) blocks = 4LL * num_sms();
+  k_split_reduce<T><<<(int)blocks, threads, 0, st>>>(B, out_w, nsplit, part, bias, out);
 }
 
 // --------------------------------------------------------------------------- K3
@@ -1025,11 +1141,11 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 struct ProductPlan {
   int g, pw, gx, gy, nsplit;
   size_t smem;
+  bool fw;  // fused weights (no k_prescale); nsplit > 1 then means a cluster fold
 };
-
 template <typename T>
-static size_t product_smem(int g, int cols, int max_act) {
-  return product_tile_bytes<T>(g, cols) + align16((size_t)(max_act > 0 ? max_act : 1) * sizeof(int32_t));
+static size_t product_smem(int g, int cols, int max_act, bool cluster = false) {
+  return product_tile_bytes<T>(g, cols, cluster) + align16((size_t)(max_act > 0 ? max_act : 1) * sizeof(int32_t));
 }
 
 template <typename T>
@@ -1049,7 +1165,7 @@ static ProductPlan plan_product(int B, int out_w, int cols, int max_act) {
   const int sms = num_sms();
   const double slots = 2.0 * sms;
   const int pw_max = ceil_div(out_w, kWarpPos);
-  ProductPlan best{0, 0, 0, 0, 1, 0};
+  ProductPlan best{0, 0, 0, 0, 1, 0, false};
   double best_eff = -1.0;
   for (int g : {2, 1}) {
     const size_t sm = product_smem<T>(g, cols, max_act);
@@ -1062,31 +1178,51 @@ static ProductPlan plan_product(int B, int out_w, int cols, int max_act) {
       const double eff = waves / std::ceil(waves) - 0.02 * (g == 1) - 0.01 * (pw < 4);
       if (eff > best_eff + 1e-9) {
         best_eff = eff;
-        best = {g, pw, ceil_div(out_w, pw * kWarpPos), ceil_div(B, g * VEC), 1, sm};
+        best = {g, pw, ceil_div(out_w, pw * kWarpPos), ceil_div(B, g * VEC), 1, sm, false};
       }
     }
   }
-  if (best.g) return best;
-  // few rows: PW = 1, split the diagonal list across CTAs
-  const size_t sm = product_smem<T>(1, cols, max_act);
-  if (sm > 220 * 1024) return best;
-  ProductPlan p{1, 1, ceil_div(out_w, kWarpPos), ceil_div(B, VEC), 1, sm};
+  if (best.g) return best;  // row-tiled: pre-scaled weights (measured faster than FW here)
+  // few rows: PW = 1, the diagonal list split over a cluster of at most 8 CTAs
+  // that fold through distributed shared memory, weights formed in the kernel
+  // (FW): one launch, no prescale pass, no partial buffer (B = 8 at 4096^2:
+  // 15 us vs 28 us with prescale + split partials + k_split_reduce)
+  const bool fw = true;
+  ProductPlan p{1, 1, ceil_div(out_w, kWarpPos), ceil_div(B, VEC), 1, 0, fw};
   const long long ctas = (long long)p.gx * p.gy;
-  const int ns = (int)ceil_div((long long)slots, ctas);
-  const int max_ns = max_act / 16 > 1 ? max_act / 16 : 1;
+  // as many splits as fit ONE wave (a second, nearly empty wave doubles the time)
+  const int ns = ctas >= (long long)slots ? 1 : (int)((long long)slots / ctas);
+  int max_ns = max_act / 16 > 1 ? max_act / 16 : 1;
+  if (fw && max_ns > 8) max_ns = 8;
   p.nsplit = ns < max_ns ? ns : max_ns;
+  p.smem = product_smem<T>(1, cols, max_act, fw && p.nsplit > 1);
+  if (p.smem > 220 * 1024) return best;
   return p;
 }
 
-template <typename T, int G, bool GA>
+template <typename T, int G, bool GA, bool FW>
 static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, int L, const T* in,
-                           const typename WType<T>::type* w, int ldw, const int32_t* active, const int32_t* n_act,
-                           int max_act, const typename Traits<T>::P* bias, T* out, typename Vec<T>::A* part,
-                           int vec_ok) {
-  auto k = k_product<T, G, GA>;
+                           const typename WType<T>::type* w, int ldw, const typename Traits<T>::P* vals,
+                           const double* asoft, const int32_t* active, const int32_t* n_act, int max_act,
+                           const typename Traits<T>::P* bias, T* out, typename Vec<T>::A* part, int vec_ok) {
+  auto k = k_product<T, G, GA, FW>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-  k<<<dim3(p.gx, p.gy, p.nsplit), kThreads, p.smem, st>>>(B, C, L, in, w, ldw, active, n_act, max_act, bias,
-                                                          out, part, p.pw, p.nsplit, vec_ok);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.gx, p.gy, p.nsplit);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (FW && p.nsplit > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = p.nsplit;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, k, B, C, L, in, w, ldw, vals, asoft, active, n_act, max_act, bias, out, part, p.pw,
+                     p.nsplit, vec_ok);
   note_launch();
 }
 
@@ -1094,8 +1230,10 @@ static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, 
 static int narrow_max_b() {
   static int v = -1;
   if (v < 0) {
+    // measured (4096^2, 90 %): the staging-free kernel wins at B <= 4, the
+    // staged k_product from B = 8 (28 vs 52 us)
     const char* e = getenv("DIAGMM_NARROW_MAX_B");
-    v = e ? atoi(e) : 8;
+    v = e ? atoi(e) : 4;
   }
   return v;
 }
@@ -1131,10 +1269,7 @@ static int run_product_narrow(bool gather, int B, int C, int L, const void* in, 
 #undef DIAGMM_NARROW
   note_launch();
   if (nc > 1) {
-    const size_t n = (size_t)B * out_w;
-    int blocks = (int)((n + 255) / 256);
-    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-    k_split_reduce<T><<<blocks, 256, 0, st>>>(B, out_w, nc, part, tb, to);
+    launch_split_reduce<T>(B, out_w, nc, part, tb, to, st);
     note_launch();
   }
   return status_from_cuda();
@@ -1147,7 +1282,7 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   const int out_w = gather ? L : C, cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B > 0 ? B : 1, out_w, cols, max_act);
   const size_t wbytes = align16((size_t)(max_act > 0 ? max_act : 1) * w_ld<T>(out_w) * sizeof(typename WType<T>::type));
-  const size_t narrow = B <= (narrow_max_b() > kNarrowB ? narrow_max_b() : kNarrowB)
+  const size_t narrow = B <= narrow_max_b()
                             ? (size_t)narrow_chunks(out_w, max_act, B) * B * out_w * sizeof(A) : 0;
   const size_t wide = wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
   return wide > narrow ? wide : narrow;
@@ -1163,7 +1298,7 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
   if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
-  if (B <= (narrow_max_b() > kNarrowB ? narrow_max_b() : kNarrowB))
+  if (B <= narrow_max_b())
     return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
                                  static_cast<A*>(ws), st);
   const int out_w = gather ? L : C, in_w = gather ? C : L;
@@ -1173,30 +1308,30 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   const int ldw = w_ld<T>(out_w);
   WT* w = static_cast<WT*>(ws);
   A* part = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)(max_act > 0 ? max_act : 1) * ldw * sizeof(WT)));
-  if (max_act > 0) {
-    dim3 grid(ceil_div(ldw, 256), max_act < 4096 ? max_act : 4096);
+  if (max_act > 0 && !p.fw) {
+    dim3 grid(ceil_div(ldw, 256 * kPreVec), max_act < 65535 ? max_act : 65535);
     k_prescale<T><<<grid, 256, 0, st>>>(C, L, out_w, ldw, gather ? 1 : 0, static_cast<const P*>(vals), asoft, active,
                                         n_act, max_act, w);
     note_launch();
   }
   const int vec_ok = in_w % VEC == 0 && C % VEC == 0 && aligned16(in);
   auto tin = static_cast<const T*>(in);
+  auto tv = static_cast<const P*>(vals);
   auto tb = static_cast<const P*>(bias);
   auto to = static_cast<T*>(out);
-#define DIAGMM_GO(G)                                                                                     \
-  if (p.g == G) {                                                                                        \
-    if (gather)                                                                                          \
-      launch_product<T, G, true>(p, st, B, C, L, tin, w, ldw, active, n_act, max_act, tb, to, part, vec_ok);  \
-    else                                                                                                 \
-      launch_product<T, G, false>(p, st, B, C, L, tin, w, ldw, active, n_act, max_act, tb, to, part, vec_ok); \
+#define DIAGMM_GO(G, FW)                                                                                          \
+  if (p.g == G && p.fw == FW) {                                                                                   \
+    if (gather)                                                                                                   \
+      launch_product<T, G, true, FW>(p, st, B, C, L, tin, w, ldw, tv, asoft, active, n_act, max_act, tb, to, part, \
+                                     vec_ok);                                                                     \
+    else                                                                                                          \
+      launch_product<T, G, false, FW>(p, st, B, C, L, tin, w, ldw, tv, asoft, active, n_act, max_act, tb, to, part,\
+                                      vec_ok);                                                                    \
   }
-  DIAGMM_GO(2) DIAGMM_GO(1)
+  DIAGMM_GO(2, false) DIAGMM_GO(1, false) DIAGMM_GO(2, true) DIAGMM_GO(1, true)
 #undef DIAGMM_GO
-  if (p.nsplit > 1) {
-    const size_t n = (size_t)B * out_w;
-    int blocks = (int)((n + 255) / 256);
-    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-    k_split_reduce<T><<<blocks, 256, 0, st>>>(B, out_w, p.nsplit, part, tb, to);
+  if (p.nsplit > 1 && !p.fw) {
+    launch_split_reduce<T>(B, out_w, p.nsplit, part, tb, to, st);
     note_launch();
   }
   return status_from_cuda();
@@ -1207,7 +1342,7 @@ static int narrow_dw_max_b() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DIAGMM_NARROW_DW_MAX_B");
-    v = e ? atoi(e) : 16;
+    v = e ? atoi(e) : 8;
   }
   return v;
 }
@@ -1276,7 +1411,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
-  if (B > 0 && B <= (narrow_dw_max_b() > 2 * kNarrowB ? narrow_dw_max_b() : 2 * kNarrowB) && max_act > 0) {
+  if (B > 0 && B <= narrow_dw_max_b() && max_act > 0) {
     parts = 1;
     dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
     if (B <= 4) k_dw_narrow<T, 4><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || tail -20 gpurun_out/build.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+python tools/bench_kernels.py 5 6 7 8 9 2
