@@ -34,12 +34,12 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {  // d gelu_tanh / dx 
   return fmaf(hx * (1.f - t * t), k0 * fmaf(3.f * k1, x2, 1.f), 0.5f * (1.f + t));
 }
 
-template <int BN, int NST = kStages, int NC = 1>
+template <int BN, int NST = kStages, int NC = 1, int R = 2>
 struct Smem {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;
   static constexpr size_t b_bytes = (size_t)BN * BK * 2;
   static constexpr size_t stage = a_bytes + b_bytes;
-  static constexpr size_t c_bytes = (size_t)BM * BN;  // half the output tile (two 64-column swizzled boxes)
+  static constexpr size_t c_bytes = (size_t)BM * (BN / R) * 2;  // one store round: (BN/R)/64 swizzled 64-col boxes
   static constexpr size_t bars = 128 + BN * 4;  // barriers, TMEM slot, aux barrier, bias tile
   static constexpr size_t total = 1024 /* alignment slack */ + NST * stage + NC * c_bytes + bars;
 };
@@ -48,10 +48,11 @@ struct Smem {
 // (n-block fastest).  The TMA warp runs ahead across tile boundaries, the
 // MMA thread alternates between two TMEM accumulators (2 x BN columns) so the
 // epilogue of tile i overlaps the main loop of tile i+1.
-// NST smem pipeline stages, NC half-tile staging buffers: the GELU-forward
-// variant (two outputs per tile) trades one stage for a second staging buffer
-// so the pre-activation and the activation leave in the same store round.
-template <int BN, int NST, int NC>
+// NST smem pipeline stages, NC staging buffers of one store round, R store
+// rounds per tile.  The GELU variants (a second output / an aux input per
+// tile) need a second buffer: 4 stages + two quarter-tile buffers (R = 4) fit
+// next to each other in the 227 KB, 3 stages + two half-tile buffers too.
+template <int BN, int NST, int NC, int R>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
@@ -59,7 +60,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  using S = Smem<BN, NST, NC>;
+  using S = Smem<BN, NST, NC, R>;
+  constexpr int CPR = (BN / R) / 32;  // 32-column TMEM chunks per store round
+  constexpr int BPR = (BN / R) / 64;  // 64-column swizzled boxes per store round
   unsigned char* sA = smem;
   unsigned char* sB = smem + NST * S::a_bytes;
   unsigned char* sC = smem + NST * S::stage;  // 1024-aligned
@@ -169,7 +172,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (leader) {
 #pragma unroll
-        for (int bx = 0; bx < BN / 128; ++bx) {
+        for (int bx = 0; bx < BPR; ++bx) {
           const int col = col0 + bx * 64;
           if (col >= Ndim) break;
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -201,8 +204,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       auto load_aux = [&](int hh, unsigned char* buf) {
         mbar_expect_tx(auxbar, (uint32_t)S::c_bytes);
 #pragma unroll
-        for (int bx = 0; bx < BN / 128; ++bx)
-          tma_load_2d(buf + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / 2) + bx * 64, m0, auxbar);
+        for (int bx = 0; bx < BPR; ++bx)
+          tma_load_2d(buf + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / R) + bx * 64, m0, auxbar);
       };
       wait_reads();
       if (NC > 1 && epi == 2 && leader) load_aux(0, sC2);
@@ -211,18 +214,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        if (hh == 1) wait_reads();
+      for (int hh = 0; hh < R; ++hh) {
+        if (hh > 0) wait_reads();
         if (epi == 2) {
           if (NC == 1 && leader) load_aux(hh, sC);
           mbar_wait_parity(auxbar, aux_phase);
           aux_phase ^= 1;
         }
-        unsigned char* obuf = (pingpong && hh == 1) ? sC2 : sC;
+        unsigned char* obuf = (pingpong && (hh & 1)) ? sC2 : sC;
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 128; ++cc) {
-          const int c = hh * (BN / 64) + half * (BN / 128) + cc;  // 32-column chunk index in the tile
-          const int cl = c - hh * (BN / 64);                      // chunk within this half
+        for (int cc = 0; cc < CPR / 2; ++cc) {
+          const int c = hh * CPR + half * (CPR / 2) + cc;  // 32-column chunk index in the tile
+          const int cl = c - hh * CPR;                      // chunk within this round
           uint32_t r[32];
           tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
           uint32_t prev[16];
@@ -259,14 +262,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           for (int j = 0; j < 4; ++j)
             *sc_addr(cl, j, obuf) = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
-        if (hh == 1) {  // accumulator consumed: hand it back to the MMA thread
+        if (hh == R - 1) {  // accumulator consumed: hand it back to the MMA thread
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
         }
-        store_half(m0, n0 + hh * (BN / 2), NC > 1 && epi == 1, obuf);
-        if (NC > 1 && epi == 2 && hh == 0 && leader) load_aux(1, sC2);  // sC2 read by all (barrier above)
+        store_half(m0, n0 + hh * (BN / R), NC > 1 && epi == 1, obuf);
+        if (NC > 1 && epi == 2 && hh + 1 < R && leader) load_aux(hh + 1, sC2);  // sC2 read by all (barrier above)
       }
     }
     if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -828,16 +831,16 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   static const bool pp0 = [] { const char* e = getenv("DIAGMM_TC_PINGPONG"); return e && atoi(e) != 0; }();
-  if (epi != 0 || pp0) {  // a second half-tile buffer (pre-activation out / aux in / ping-pong): 3 stages
-    auto k = k_tc_gemm<BN, kStages - 1, 2>;
-    const size_t sm = Smem<BN, kStages - 1, 2>::total;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+  auto go = [&](auto kern, size_t sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+  };
+  // (4 stages + two quarter-tile buffers, R = 4, measured: fc1-shaped gelu 276 /
+  // gelu' 291 us vs 272 / 277 us for 3 stages + two half-tile buffers)
+  if (epi != 0 || pp0) {  // 3 stages + two half-tile buffers (GELU / ping-pong)
+    go(k_tc_gemm<BN, kStages - 1, 2, 2>, Smem<BN, kStages - 1, 2, 2>::total);
   } else {
-    auto k = k_tc_gemm<BN, kStages, 1>;
-    const size_t sm = Smem<BN, kStages, 1>::total;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+    go(k_tc_gemm<BN, kStages, 1, 2>, Smem<BN, kStages, 1, 2>::total);
   }
   note_launch();
   return status_from_cuda();
