@@ -34,25 +34,28 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {  // d gelu_tanh / dx 
   return fmaf(hx * (1.f - t * t), k0 * fmaf(3.f * k1, x2, 1.f), 0.5f * (1.f + t));
 }
 
-template <int BN, int NST = kStages, int NC = 1, int R = 2>
+template <int BN, int NST = kStages, int NC = 1, int R = 2, int PP = 1>
 struct Smem {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;
   static constexpr size_t b_bytes = (size_t)BN * BK * 2;
   static constexpr size_t stage = a_bytes + b_bytes;
   static constexpr size_t c_bytes = (size_t)BM * (BN / R) * 2;  // one store round: (BN/R)/64 swizzled 64-col boxes
   static constexpr size_t bars = 128 + BN * 4;  // barriers, TMEM slot, aux barrier, bias tile
-  static constexpr size_t total = 1024 /* alignment slack */ + NST * stage + NC * c_bytes + bars;
+  static constexpr size_t total = 1024 /* alignment slack */ + NST * stage + PP * NC * c_bytes + bars;
 };
 
 // Persistent: grid = min(tiles, SMs); CTA c takes tiles c, c + grid, ...
 // (n-block fastest).  The TMA warp runs ahead across tile boundaries, the
 // MMA thread alternates between two TMEM accumulators (2 x BN columns) so the
 // epilogue of tile i overlaps the main loop of tile i+1.
-// NST smem pipeline stages, NC staging buffers of one store round, R store
-// rounds per tile.  The GELU variants (a second output / an aux input per
-// tile) need a second buffer: 4 stages + two quarter-tile buffers (R = 4) fit
-// next to each other in the 227 KB, 3 stages + two half-tile buffers too.
-template <int BN, int NST, int NC, int R>
+// NST smem pipeline stages; R store rounds per tile; NC staging buffers per
+// round (the output, plus the pre-activation out (epi 1) / aux in (epi 2));
+// PP buffer sets used round-robin, so with PP = 2 a round only waits for the
+// store issued two rounds earlier.  The GELU variants use 3 stages + 2 sets x
+// 2 quarter-tile buffers (208 KB): their epilogue was the accumulator-release
+// bottleneck (the MMA warp spun on the TMEM-empty barrier) while each store
+// round waited for the previous round's bulk store to leave shared memory.
+template <int BN, int NST, int NC, int R, int PP>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
@@ -60,14 +63,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  using S = Smem<BN, NST, NC, R>;
+  using S = Smem<BN, NST, NC, R, PP>;
   constexpr int CPR = (BN / R) / 32;  // 32-column TMEM chunks per store round
   constexpr int BPR = (BN / R) / 64;  // 64-column swizzled boxes per store round
   unsigned char* sA = smem;
   unsigned char* sB = smem + NST * S::a_bytes;
-  unsigned char* sC = smem + NST * S::stage;  // 1024-aligned
-  unsigned char* sC2 = sC + (NC > 1 ? S::c_bytes : 0);  // pre-activation staging (epi 1)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sC + NC * S::c_bytes);
+  unsigned char* sC = smem + NST * S::stage;  // 1024-aligned staging buffers [PP][NC]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + PP * NC * S::c_bytes);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -148,7 +150,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     // swizzled smem tile (one 64-column box per 16 KB) -> TMA bulk tensor store.
     //   epi 0: out = acc + bias
     //   epi 1: aux = acc + bias (pre-activation), out = gelu_tanh(aux): one TMEM
-    //          read, both halves staged (sC2 / sC) and stored in one round (NC = 2)
+    //          read, both staged (out / aux buffer of the round's set) and stored in one round
     //   epi 2: out = acc * gelu_tanh'(aux)   (aux TMA-loaded into the staging tile)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -157,17 +159,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     const bool leader = et == 0;
     float* sbias = reinterpret_cast<float*>(tslot + 4);  // BN floats after the barriers
     uint32_t aux_phase = 0;
-    // epi 0 with two staging buffers ping-pongs the halves (sC, sC2), so a
-    // store round only waits for the one issued a round earlier
-    const bool pingpong = NC > 1 && epi == 0;
-    auto wait_reads = [&]() {  // the store that last used the next staging buffer finished reading it
+    auto buf = [&](int set, int which) { return sC + (size_t)(set * NC + which) * S::c_bytes; };
+    auto wait_reads = [&]() {  // the store that last used this round's buffer set has left smem
       if (leader) {
-        if (pingpong) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (PP > 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     };
-    auto store_half = [&](int m0, int col0, bool with_aux, unsigned char* obuf) {
+    auto store_round = [&](int m0, int col0, int set, bool with_aux) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (leader) {
@@ -177,51 +177,53 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           if (col >= Ndim) break;
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                            reinterpret_cast<uint64_t>(&tc_out)),
-                       "r"(col), "r"(m0), "r"(smem_u32(obuf + (size_t)bx * (BM * 128)))
+                       "r"(col), "r"(m0), "r"(smem_u32(buf(set, 0) + (size_t)bx * (BM * 128)))
                        : "memory");
           if (with_aux)
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                              reinterpret_cast<uint64_t>(&tc_aux)),
-                         "r"(col), "r"(m0), "r"(smem_u32(sC2 + (size_t)bx * (BM * 128)))
+                         "r"(col), "r"(m0), "r"(smem_u32(buf(set, 1) + (size_t)bx * (BM * 128)))
                          : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
     // 8 bf16 of this thread's row in 16-byte chunk `ch` (0..7) of the box holding chunk cl
-    auto sc_addr = [&](int cl, int j, unsigned char* buf) {
-      unsigned char* box = buf + (size_t)(cl >> 1) * (BM * 128);
+    auto sc_addr = [&](int cl, int j, unsigned char* base) {
+      unsigned char* box = base + (size_t)(cl >> 1) * (BM * 128);
       const int chunk = ((cl & 1) * 4 + j) ^ (rl & 7);
       return reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16);
     };
-    int i = 0;
+    int i = 0, rc = 0;  // rc: store rounds so far (buffer set = rc % PP)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
       const int m0 = (t / nb) * BM, n0 = (t % nb) * BN;
-      // epi 2: the pre-activation half tile comes in by TMA — into sC2, issued
-      // ahead (half 0 before the accumulator wait, half 1 right after half 0's
-      // store round) when there are two staging buffers, else into sC in turn
-      auto load_aux = [&](int hh, unsigned char* buf) {
+      // epi 2: the pre-activation for each round comes in by TMA into the aux
+      // buffer of that round's set — round 0's before the accumulator wait,
+      // round hh+1's right after round hh's store round
+      auto load_aux = [&](int hh, unsigned char* dst) {
         mbar_expect_tx(auxbar, (uint32_t)S::c_bytes);
 #pragma unroll
         for (int bx = 0; bx < BPR; ++bx)
-          tma_load_2d(buf + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / R) + bx * 64, m0, auxbar);
+          tma_load_2d(dst + (size_t)bx * (BM * 128), &tc_aux, n0 + hh * (BN / R) + bx * 64, m0, auxbar);
       };
       wait_reads();
-      if (NC > 1 && epi == 2 && leader) load_aux(0, sC2);
+      if (NC > 1 && epi == 2 && leader) load_aux(0, buf(rc % PP, 1));
       for (int c = et; c < BN; c += kEpiThreads) sbias[c] = (bias && n0 + c < Ndim) ? __ldg(bias + n0 + c) : 0.f;
       mbar_wait_parity(&tfull[ab], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll 1
-      for (int hh = 0; hh < R; ++hh) {
+      for (int hh = 0; hh < R; ++hh, ++rc) {
+        const int set = rc % PP;
         if (hh > 0) wait_reads();
         if (epi == 2) {
-          if (NC == 1 && leader) load_aux(hh, sC);
+          if (NC == 1 && leader) load_aux(hh, buf(set, 0));
           mbar_wait_parity(auxbar, aux_phase);
           aux_phase ^= 1;
         }
-        unsigned char* obuf = (pingpong && (hh & 1)) ? sC2 : sC;
+        unsigned char* obuf = buf(set, 0);
+        unsigned char* abuf = buf(set, NC - 1);  // aux in (epi 2) / pre-activation out (epi 1)
 #pragma unroll 1
         for (int cc = 0; cc < CPR / 2; ++cc) {
           const int c = hh * CPR + half * (CPR / 2) + cc;  // 32-column chunk index in the tile
@@ -232,7 +234,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           if (epi == 2) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint4 u = *sc_addr(cl, j, NC > 1 ? sC2 : sC);
+              const uint4 u = *sc_addr(cl, j, abuf);
               prev[4 * j] = u.x; prev[4 * j + 1] = u.y; prev[4 * j + 2] = u.z; prev[4 * j + 3] = u.w;
             }
           }
@@ -256,7 +258,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           if (NC > 1 && epi == 1) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              *sc_addr(cl, j, sC2) = make_uint4(pre[4 * j], pre[4 * j + 1], pre[4 * j + 2], pre[4 * j + 3]);
+              *sc_addr(cl, j, abuf) = make_uint4(pre[4 * j], pre[4 * j + 1], pre[4 * j + 2], pre[4 * j + 3]);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -268,8 +270,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           if (lane == 0)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
         }
-        store_half(m0, n0 + hh * (BN / R), NC > 1 && epi == 1, obuf);
-        if (NC > 1 && epi == 2 && hh + 1 < R && leader) load_aux(hh + 1, sC2);  // sC2 read by all (barrier above)
+        store_round(m0, n0 + hh * (BN / R), set, NC > 1 && epi == 1);
+        if (NC > 1 && epi == 2 && hh + 1 < R && leader) load_aux(hh + 1, buf((rc + 1) % PP, 1));
       }
     }
     if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -830,17 +832,19 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
     return DIAGMM_ECUDA;
   const int tiles = ceil_div(Mdim, BM) * ceil_div(Ndim, BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  static const bool pp0 = [] { const char* e = getenv("DIAGMM_TC_PINGPONG"); return e && atoi(e) != 0; }();
   auto go = [&](auto kern, size_t sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
   };
-  // (4 stages + two quarter-tile buffers, R = 4, measured: fc1-shaped gelu 276 /
-  // gelu' 291 us vs 272 / 277 us for 3 stages + two half-tile buffers)
-  if (epi != 0 || pp0) {  // 3 stages + two half-tile buffers (GELU / ping-pong)
-    go(k_tc_gemm<BN, kStages - 1, 2, 2>, Smem<BN, kStages - 1, 2, 2>::total);
+  // measured at the fc1 / fc2 shapes (50 432 tokens, N = 3072, K = 768):
+  //   gelu (epi 1):  3 stages + 2 sets x 2 quarter-tile buffers 254 us, one set of half tiles 274 us
+  //   gelu' (epi 2): one set of half tiles 278 us, 2 sets of quarter tiles 287 us
+  if (epi == 0) {
+    go(k_tc_gemm<BN, kStages, 1, 2, 1>, Smem<BN, kStages, 1, 2, 1>::total);
+  } else if (epi == 1) {
+    go(k_tc_gemm<BN, kStages - 1, 2, 4, 2>, Smem<BN, kStages - 1, 2, 4, 2>::total);
   } else {
-    go(k_tc_gemm<BN, kStages, 1, 2>, Smem<BN, kStages, 1, 2>::total);
+    go(k_tc_gemm<BN, kStages - 1, 2, 2, 1>, Smem<BN, kStages - 1, 2, 2, 1>::total);
   }
   note_launch();
   return status_from_cuda();
