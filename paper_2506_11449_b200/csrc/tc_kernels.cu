@@ -59,7 +59,7 @@ template <int BN, int NST, int NC, int R, int PP>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
-          int K, const float* __restrict__ bias, int epi) {
+          int K, const float* __restrict__ bias, int epi, const __nv_bfloat16* __restrict__ aux_g, int ld_aux) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -194,6 +194,23 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       const int chunk = ((cl & 1) * 4 + j) ^ (rl & 7);
       return reinterpret_cast<uint4*>(box + rl * 128 + chunk * 16);
     };
+    // epi 2 with NC == 1 (R == 4: one 32-column chunk per thread per round):
+    // the pre-activation comes straight from global into registers, one round
+    // ahead (this tile's next round, or the next tile's first round), so no
+    // aux staging buffer and no exposed TMA round trip
+    uint4 av_cur[4], av_nxt[4];
+    auto load_aux_regs = [&](int tt, int hh, uint4 (&dst)[4]) {
+      const int row = (tt / nb) * BM + rl;
+      const int col0 = (tt % nb) * BN + hh * (BN / R) + half * 32;
+      const __nv_bfloat16* src = aux_g + (size_t)row * ld_aux + col0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dst[j] = make_uint4(0, 0, 0, 0);
+        if (tt < tiles && row < Mdim && col0 + 8 * j + 8 <= Ndim) dst[j] = __ldg(reinterpret_cast<const uint4*>(src + 8 * j));
+      }
+    };
+    constexpr bool kRegAux = (NC == 1 && R == 4);
+    if (kRegAux && epi == 2) load_aux_regs(blockIdx.x, 0, av_cur);
     int i = 0, rc = 0;  // rc: store rounds so far (buffer set = rc % PP)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
@@ -217,7 +234,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       for (int hh = 0; hh < R; ++hh, ++rc) {
         const int set = rc % PP;
         if (hh > 0) wait_reads();
-        if (epi == 2) {
+        if (kRegAux && epi == 2) {
+          if (hh + 1 < R) load_aux_regs(t, hh + 1, av_nxt);
+          else load_aux_regs(t + gridDim.x, 0, av_nxt);
+        } else if (epi == 2) {
           if (NC == 1 && leader) load_aux(hh, buf(set, 0));
           mbar_wait_parity(auxbar, aux_phase);
           aux_phase ^= 1;
@@ -234,7 +254,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           if (epi == 2) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint4 u = *sc_addr(cl, j, abuf);
+              const uint4 u = kRegAux ? av_cur[j] : *sc_addr(cl, j, abuf);
               prev[4 * j] = u.x; prev[4 * j + 1] = u.y; prev[4 * j + 2] = u.z; prev[4 * j + 3] = u.w;
             }
           }
@@ -271,6 +291,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
         }
         store_round(m0, n0 + hh * (BN / R), set, NC > 1 && epi == 1);
+        if (kRegAux && epi == 2) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) av_cur[j] = av_nxt[j];
+        }
         if (NC > 1 && epi == 2 && hh + 1 < R && leader) load_aux(hh + 1, buf((rc + 1) % PP, 1));
       }
     }
@@ -834,17 +858,20 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   const int grid = tiles < num_sms() ? tiles : num_sms();
   auto go = [&](auto kern, size_t sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi);
+    kern<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi,
+                                     static_cast<const __nv_bfloat16*>(aux), ldo);
   };
-  // measured at the fc1 / fc2 shapes (50 432 tokens, N = 3072, K = 768):
-  //   gelu (epi 1):  3 stages + 2 sets x 2 quarter-tile buffers 254 us, one set of half tiles 274 us
-  //   gelu' (epi 2): one set of half tiles 278 us, 2 sets of quarter tiles 287 us
-  if (epi == 0) {
-    go(k_tc_gemm<BN, kStages, 1, 2, 1>, Smem<BN, kStages, 1, 2, 1>::total);
-  } else if (epi == 1) {
+  // Measured at the ViT shapes (50 432 tokens; tools/epi_bench.py):
+  //   epi 0: 4 stages + 2 sets of quarter-tile buffers (round-robin) 206 / 154 / 59 us
+  //          (N x K = 3072 x 768 / 2304 x 768 / 768 x 768) vs 220 / 165 / 68 us with one
+  //          set of half tiles — the epilogue no longer holds the accumulator back
+  //   epi 1 (gelu, 2 outputs): 3 stages + 2 sets x (out, pre) quarter tiles 252 us vs 274
+  //   epi 2 (gelu'): the epi-0 layout, aux straight from global into registers one
+  //          round ahead: 270 / 194 us vs 278 / 208 us staged by TMA
+  if (epi == 1) {
     go(k_tc_gemm<BN, kStages - 1, 2, 4, 2>, Smem<BN, kStages - 1, 2, 4, 2>::total);
   } else {
-    go(k_tc_gemm<BN, kStages - 1, 2, 2, 1>, Smem<BN, kStages - 1, 2, 2, 1>::total);
+    go(k_tc_gemm<BN, kStages, 1, 4, 2>, Smem<BN, kStages, 1, 4, 2>::total);
   }
   note_launch();
   return status_from_cuda();

@@ -25,7 +25,9 @@ def timeit(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-for (n_out, k) in [(3072, 768), (768, 3072)]:
+import os
+shapes = [(3072, 768), (768, 3072), (2304, 768), (768, 768), (768, 2304)] if os.environ.get('EPI_ALL') else [(3072, 768), (768, 3072)]
+for (n_out, k) in shapes:
     a = torch.randn(T, k, device=dev).to(torch.bfloat16)
     w = (torch.randn(n_out, k, device=dev) * 0.05).to(torch.bfloat16)
     bias = torch.randn(n_out, device=dev)
