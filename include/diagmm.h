@@ -231,6 +231,12 @@ DIAGMM_API int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, con
 DIAGMM_API int diagmm_tc_gemm_bf16_ex(int Mdim, int Ndim, int K, const void* A, const void* B,
                                       const float* bias, void* out, int ldo, void* aux,
                                       int epilogue, void* stream);
+/* out = A B (+ bias) with B given as (K, Ndim) row-major (Ndim % 8 == 0), staged
+ * MN-major: the dense-equivalent input gradient dx = dy W_K reads the forward's
+ * W_K (diagmm_materialize) directly, no W_K^T (epilogue 0, or 2 as above). */
+DIAGMM_API int diagmm_tc_gemm_bf16_nn(int Mdim, int Ndim, int K, const void* A, const void* B,
+                                      const float* bias, void* out, int ldo, void* aux,
+                                      int epilogue, void* stream);
 
 /* K3 on the tensor cores (bf16 activations): gw = diagonal entries of
  * dy^T x computed by tcgen05 MMAs over token tiles (split-K across CTAs), the

@@ -35,7 +35,8 @@ int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, c
 int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
-int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, void*, int, cudaStream_t);
+int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, void*, int, cudaStream_t,
+                     bool b_kn = false);
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 size_t tc_dw_workspace(int, int, int, int);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
@@ -185,6 +186,11 @@ int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B,
 int diagmm_tc_gemm_bf16_ex(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out,
                            int ldo, void* aux, int epilogue, void* stream) {
   return run_tc_gemm_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, aux, epilogue, S(stream));
+}
+
+int diagmm_tc_gemm_bf16_nn(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out,
+                           int ldo, void* aux, int epilogue, void* stream) {
+  return run_tc_gemm_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, aux, epilogue, S(stream), true);
 }
 
 size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act) {

@@ -34,6 +34,13 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {  // d gelu_tanh / dx 
   return fmaf(hx * (1.f - t * t), k0 * fmaf(3.f * k1, x2, 1.f), 0.5f * (1.f + t));
 }
 
+// MN-major operand, 128-byte swizzle: 64-element MN boxes 8 KB apart (LBO),
+// 8 K-rows 1 KB apart (SBO); one UMMA K step (16 rows) = +2 KB (+128 encoded)
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+  const uint64_t a = (smem_u32(p) & 0x3FFFFu) >> 4;
+  return a | (512ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
 template <int BN, int NST = kStages, int NC = 1, int R = 2, int PP = 1>
 struct Smem {
   static constexpr size_t a_bytes = (size_t)BM * BK * 2;
@@ -55,7 +62,10 @@ struct Smem {
 // 2 quarter-tile buffers (208 KB): their epilogue was the accumulator-release
 // bottleneck (the MMA warp spun on the TMEM-empty barrier) while each store
 // round waited for the previous round's bulk store to leave shared memory.
-template <int BN, int NST, int NC, int R, int PP>
+// BMN: B given as (K, N) row-major (out = A @ B) and staged MN-major (four
+// 64-column boxes per stage), so the input-gradient product reads W_K itself
+// instead of a materialized W_K^T.
+template <int BN, int NST, int NC, int R, int PP, bool BMN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
@@ -118,13 +128,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           mbar_wait_parity(&empty[s], (round & 1) ^ 1);
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
           tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
-          tma_load_2d(sB + s * S::b_bytes, &tb, kb * BK, n0, &full[s]);
+          if constexpr (BMN) {
+#pragma unroll
+            for (int h = 0; h < BN / 64; ++h) tma_load_2d(sB + s * S::b_bytes + h * 8192, &tb, n0 + h * 64, kb * BK, &full[s]);
+          } else {
+            tma_load_2d(sB + s * S::b_bytes, &tb, kb * BK, n0, &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer (one thread for the whole CTA)
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      constexpr uint32_t idesc = idesc_bf16(BM, BN) | (BMN ? (1u << 16) : 0u);  // B MN-major
       int it = 0, i = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
         const int ab = i & 1;
@@ -136,10 +151,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           mbar_wait_parity(&full[s], round & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t da = smem_desc_sw128(sA + s * S::a_bytes);
-          const uint64_t db = smem_desc_sw128(sB + s * S::b_bytes);
+          const uint64_t db = BMN ? smem_desc_mn_sw128(sB + s * S::b_bytes) : smem_desc_sw128(sB + s * S::b_bytes);
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)  // +32 bytes along K inside the swizzle atom
-            umma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / UK; ++k)  // K-major: +32 bytes inside the swizzle atom; MN-major: +16 rows
+            umma_bf16(acc, da + 2 * k, db + (BMN ? 128 : 2) * k, idesc, (kb | k) != 0);
           umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
         umma_commit(&tfull[ab]);
@@ -525,11 +540,6 @@ struct SmemDw {
   static constexpr size_t total = 1024 + kStages * stage + 128 + 512 * 4;
 };
 
-// K-major? no: MN-major, 128-byte swizzle; LBO = next 64-element MN block (8 KB), SBO = 8 K-rows (1 KB)
-__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
-  const uint64_t a = (smem_u32(p) & 0x3FFFFu) >> 4;
-  return a | (512ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
-}
 
 __global__ void __launch_bounds__(kDwThreads, 1)
 k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N, int ntok,
@@ -756,6 +766,20 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MN-major staging of a (rows = K, cols = N) row-major matrix: boxes of 64
+// columns (128 bytes, contiguous) x BK rows, 128-byte swizzle.
+bool make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace tc
 
 // Throughput probe of 2:4-sparse tcgen05.mma.sp (constant metadata; NOT a
@@ -841,16 +865,18 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
 }
 
 int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
-                     void* aux, int epi, cudaStream_t st) {
+                     void* aux, int epi, cudaStream_t st, bool b_kn) {
   using namespace tc;
   constexpr int BN = 256;
   if (Mdim < 1 || Ndim < 1 || K < 1 || K % 8 || ldo < Ndim) return DIAGMM_ESHAPE;
+  if (b_kn && Ndim % 8) return DIAGMM_ESHAPE;  // B (K, N) rows must be 16-byte multiples
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return DIAGMM_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo % 8)) return DIAGMM_ESHAPE;
   if (epi < 0 || epi > 2 || (epi && (aux == nullptr || (reinterpret_cast<uintptr_t>(aux) & 15)))) return DIAGMM_ESHAPE;
   CUtensorMap ta, tb, tco, taux;
   if (!make_tmap_bf16(&ta, A, (uint64_t)Mdim, (uint64_t)K, BM, (uint64_t)K) ||
-      !make_tmap_bf16(&tb, B, (uint64_t)Ndim, (uint64_t)K, BN, (uint64_t)K) ||
+      !(b_kn ? make_tmap_bf16_mn(&tb, B, (uint64_t)K, (uint64_t)Ndim)
+             : make_tmap_bf16(&tb, B, (uint64_t)Ndim, (uint64_t)K, BN, (uint64_t)K)) ||
       !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo) ||
       !make_tmap_bf16(&taux, epi ? aux : out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo))
     return DIAGMM_ECUDA;
@@ -869,9 +895,11 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   //   epi 2 (gelu'): the epi-0 layout, aux straight from global into registers one
   //          round ahead: 270 / 194 us vs 278 / 208 us staged by TMA
   if (epi == 1) {
-    go(k_tc_gemm<BN, kStages - 1, 2, 4, 2>, Smem<BN, kStages - 1, 2, 4, 2>::total);
+    if (b_kn) go(k_tc_gemm<BN, kStages - 1, 2, 4, 2, true>, Smem<BN, kStages - 1, 2, 4, 2>::total);
+    else go(k_tc_gemm<BN, kStages - 1, 2, 4, 2>, Smem<BN, kStages - 1, 2, 4, 2>::total);
   } else {
-    go(k_tc_gemm<BN, kStages, 1, 4, 2>, Smem<BN, kStages, 1, 4, 2>::total);
+    if (b_kn) go(k_tc_gemm<BN, kStages, 1, 4, 2, true>, Smem<BN, kStages, 1, 4, 2>::total);
+    else go(k_tc_gemm<BN, kStages, 1, 4, 2>, Smem<BN, kStages, 1, 4, 2>::total);
   }
   note_launch();
   return status_from_cuda();

@@ -138,9 +138,10 @@ class DiagMMFunction(torch.autograd.Function):
         W = None
         tc = dense and _tc_ok(x, M, N)
         if tc:
-            # tensor-core route: our tcgen05 GEMM on the dense-equivalent W_K (bias fused)
-            y = ops.tc_gemm(x.contiguous(), ops.materialize(vals, sel, M, N, dtype=x.dtype),
-                            None if bias is None else bias.detach())
+            # tensor-core route: our tcgen05 GEMM on the dense-equivalent W_K (bias fused);
+            # W_K is kept for the input gradient (read MN-major there: no W_K^T is built)
+            W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+            y = ops.tc_gemm(x.contiguous(), W, None if bias is None else bias.detach())
         elif dense:
             W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
             y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
@@ -154,6 +155,7 @@ class DiagMMFunction(torch.autograd.Function):
     def backward(ctx, dy):
         x, values, alpha = ctx.saved_tensors
         sel, spec, W = ctx.sel, ctx.spec, ctx.W
+        ctx.W = None
         M, N = spec.M, spec.N
         dy = dy.contiguous()
         vals = values.detach()
@@ -162,8 +164,8 @@ class DiagMMFunction(torch.autograd.Function):
         if W is not None or ctx.tc:
             dy = dy.to(x.dtype)
             if ctx.needs_input_grad[0]:
-                if ctx.tc:  # dx = dy @ W_K = tcgen05 GEMM against W_K^T
-                    dx = ops.tc_gemm(dy, ops.materialize(vals, sel, M, N, dtype=x.dtype, transposed=True))
+                if ctx.tc:  # dx = dy @ W_K on the tensor cores, W_K staged MN-major
+                    dx = ops.tc_gemm_nn(dy, W)
                 else:
                     dx = dy @ W
             out_dt = vals.dtype
@@ -212,6 +214,7 @@ class DiagMLPFunction(torch.autograd.Function):
         y = ops.tc_gemm(act, W2, None if b2 is None else b2.detach())
         ctx.save_for_backward(x, pre, act, v1, a1, v2, a2)
         ctx.sels, ctx.specs, ctx.has_bias = (sel1, sel2), (s1, s2), (b1 is not None, b2 is not None)
+        ctx.W = (W1, W2)  # read MN-major by the input-gradient products (no W^T materialized)
         return y
 
     @staticmethod
@@ -221,12 +224,13 @@ class DiagMLPFunction(torch.autograd.Function):
         dy = dy.to(x.dtype).contiguous()
         v1d, v2d = v1.detach(), v2.detach()
         # fc2: input gradient straight to d(pre) through gelu', then dW2 (+ bias) from act
-        d_pre, _ = ops.tc_gemm_ex(dy, ops.materialize(v2d, sel2, s2.M, s2.N, dtype=x.dtype, transposed=True),
-                                  None, epilogue=2, aux=pre)
+        W1, W2 = ctx.W
+        ctx.W = None
+        d_pre = ops.tc_gemm_nn(dy, W2, None, epilogue=2, aux=pre)
         gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True)
         ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1)
         # fc1
-        dx = ops.tc_gemm(d_pre, ops.materialize(v1d, sel1, s1.M, s1.N, dtype=x.dtype, transposed=True))
+        dx = ops.tc_gemm_nn(d_pre, W1)
         gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True)
         ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1)
         hb1, hb2 = ctx.has_bias

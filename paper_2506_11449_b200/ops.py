@@ -413,6 +413,29 @@ def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) 
     return out
 
 
+def tc_gemm_nn(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None, epilogue: int = 0,
+               aux: torch.Tensor | None = None):
+    """out = a @ b (+ bias) with b (K, N) row-major, staged MN-major (diagmm_tc_gemm_bf16_nn):
+    the dense-equivalent input gradient dx = dy @ W_K straight from the forward's W_K.
+    epilogue 2 (aux = pre-activation) returns (a @ b) * gelu'(aux)."""
+    _need_cuda(a, b)
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or a.dim() != 2 or b.dim() != 2:
+        raise TypeError("tc_gemm_nn takes 2-D bfloat16 operands")
+    if a.shape[1] != b.shape[0] or b.shape[1] % 8:
+        raise ShapeMismatch(f"tc_gemm_nn: {tuple(a.shape)} @ {tuple(b.shape)} (N must be a multiple of 8)")
+    if epilogue not in (0, 2):
+        raise ValueError("tc_gemm_nn supports epilogue 0 or 2")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty(a.shape[0], b.shape[1], dtype=torch.bfloat16, device=a.device)
+    if epilogue == 2 and (aux is None or tuple(aux.shape) != tuple(out.shape) or aux.dtype != torch.bfloat16):
+        raise ShapeMismatch("epilogue 2 needs the (M, N) bf16 pre-activation as aux")
+    ax = None if epilogue == 0 else aux.contiguous()
+    bz = None if bias is None else bias.float().contiguous()
+    _lib.call("diagmm_tc_gemm_bf16_nn", a.shape[0], b.shape[1], a.shape[1], _p(a), _p(b), _p(bz), _p(out),
+              out.shape[1], _p(ax), int(epilogue), _stream(a))
+    return out
+
+
 def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
                        need_soft: bool = True, max_act: int | None = None, need_bias: bool = False):
     """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None[, g_bias (M,) f32])."""

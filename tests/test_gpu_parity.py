@@ -635,6 +635,24 @@ def test_tc_gemm_gelu_epilogues_match_torch():
     assert ((d.float() - ref_d).abs().max() / ref_d.abs().max()).item() < 2e-2
 
 
+@pytest.mark.parametrize("M,N,K", [(700, 512, 256), (300, 320, 192), (1024, 768, 3072)])
+def test_tc_gemm_nn_matches_torch(M, N, K):
+    """out = a @ b with b (K, N) staged MN-major (the input gradient straight from W_K)."""
+    torch.manual_seed(2)
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = (torch.randn(K, N, device=DEV) * 0.1).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV)
+    ref = a.float() @ b.float() + bias
+    out = ops.tc_gemm_nn(a, b, bias)
+    assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 1e-2
+    # same as the K-major GEMM against the transpose, bit for bit (same tiles, same k order)
+    torch.testing.assert_close(out, ops.tc_gemm(a, b.t().contiguous(), bias), rtol=0, atol=0)
+    pre = (torch.randn(M, N, device=DEV)).to(torch.bfloat16)
+    d = ops.tc_gemm_nn(a, b, None, epilogue=2, aux=pre)
+    d_ref, _ = ops.tc_gemm_ex(a, b.t().contiguous(), None, epilogue=2, aux=pre)
+    torch.testing.assert_close(d, d_ref, rtol=0, atol=0)
+
+
 def test_diag_mlp_fused_matches_unfused(monkeypatch):
     """DiagMLP with the GELU fused into the tensor-core epilogues == fc2(gelu(fc1(x)))."""
     from paper_2506_11449_b200 import DiagMLP
