@@ -224,10 +224,11 @@ DIAGMM_API int diagmm_clip_scale_tree(int n, const double* partial, double max_n
  * A = dy, B = W_K^T (the reference's dense switch, diagcore.py:226-228). */
 DIAGMM_API int diagmm_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B,
                                    const float* bias, void* out, int ldo, void* stream);
-/* Same GEMM with a fused activation epilogue (aux: (Mdim, Ndim) bf16, row
- * stride ldo):  epilogue 1: aux = A B^T + bias (pre-activation), out =
- * gelu_tanh(aux);  epilogue 2: out = (A B^T) * gelu_tanh'(aux) — the MLP's
- * GELU forward fused into fc1 and its backward into fc2's input gradient. */
+/* Same GEMM with a fused epilogue (aux: (Mdim, Ndim) bf16, row stride ldo):
+ * epilogue 1: aux = A B^T + bias (pre-activation), out = gelu_tanh(aux);
+ * epilogue 2: out = (A B^T) * gelu_tanh'(aux) — the MLP's GELU forward fused
+ * into fc1 and its backward into fc2's input gradient;  epilogue 3: out =
+ * A B^T + bias + aux — the caller's residual add fused into proj / fc2. */
 DIAGMM_API int diagmm_tc_gemm_bf16_ex(int Mdim, int Ndim, int K, const void* A, const void* B,
                                       const float* bias, void* out, int ldo, void* aux,
                                       int epilogue, void* stream);

@@ -166,7 +166,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     //   epi 0: out = acc + bias
     //   epi 1: aux = acc + bias (pre-activation), out = gelu_tanh(aux): one TMEM
     //          read, both staged (out / aux buffer of the round's set) and stored in one round
-    //   epi 2: out = acc * gelu_tanh'(aux)   (aux TMA-loaded into the staging tile)
+    //   epi 2: out = acc * gelu_tanh'(aux)   (aux prefetched into registers, or TMA-staged)
+    //   epi 3: out = acc + bias + aux          (the residual add of the block, same aux path)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int rl = q * 32 + lane;  // row within the tile
@@ -225,7 +226,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       }
     };
     constexpr bool kRegAux = (NC == 1 && R == 4);
-    if (kRegAux && epi == 2) load_aux_regs(blockIdx.x, 0, av_cur);
+    const bool reg_aux = kRegAux && (epi == 2 || epi == 3);
+    if (reg_aux) load_aux_regs(blockIdx.x, 0, av_cur);
     int i = 0, rc = 0;  // rc: store rounds so far (buffer set = rc % PP)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
@@ -249,7 +251,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
       for (int hh = 0; hh < R; ++hh, ++rc) {
         const int set = rc % PP;
         if (hh > 0) wait_reads();
-        if (kRegAux && epi == 2) {
+        if (reg_aux) {
           if (hh + 1 < R) load_aux_regs(t, hh + 1, av_nxt);
           else load_aux_regs(t + gridDim.x, 0, av_nxt);
         } else if (epi == 2) {
@@ -266,7 +268,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           uint32_t r[32];
           tmem_ld32(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
           uint32_t prev[16];
-          if (epi == 2) {
+          if (epi >= 2) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const uint4 u = kRegAux ? av_cur[j] : *sc_addr(cl, j, abuf);
@@ -286,6 +288,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             } else if (epi == 2) {
               a *= gelu_tanh_grad(__uint_as_float(prev[j] << 16));
               b *= gelu_tanh_grad(__uint_as_float(prev[j] & 0xffff0000u));
+            } else if (epi == 3) {  // residual: one rounding of acc + bias + r
+              a += __uint_as_float(prev[j] << 16);
+              b += __uint_as_float(prev[j] & 0xffff0000u);
             }
             __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
@@ -306,7 +311,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[ab])) : "memory");
         }
         store_round(m0, n0 + hh * (BN / R), set, NC > 1 && epi == 1);
-        if (kRegAux && epi == 2) {
+        if (reg_aux) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) av_cur[j] = av_nxt[j];
         }
@@ -872,7 +877,7 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   if (b_kn && Ndim % 8) return DIAGMM_ESHAPE;  // B (K, N) rows must be 16-byte multiples
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return DIAGMM_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo % 8)) return DIAGMM_ESHAPE;
-  if (epi < 0 || epi > 2 || (epi && (aux == nullptr || (reinterpret_cast<uintptr_t>(aux) & 15)))) return DIAGMM_ESHAPE;
+  if (epi < 0 || epi > 3 || (epi && (aux == nullptr || (reinterpret_cast<uintptr_t>(aux) & 15)))) return DIAGMM_ESHAPE;
   CUtensorMap ta, tb, tco, taux;
   if (!make_tmap_bf16(&ta, A, (uint64_t)Mdim, (uint64_t)K, BM, (uint64_t)K) ||
       !(b_kn ? make_tmap_bf16_mn(&tb, B, (uint64_t)K, (uint64_t)Ndim)

@@ -127,7 +127,7 @@ class DiagMMFunction(torch.autograd.Function):
     """y = x @ W_K^T + bias for the soft-selected diagonals (layers.py:108-170, 230-251)."""
 
     @staticmethod
-    def forward(ctx, x, values, alpha, bias, spec: _OpSpec):
+    def forward(ctx, x, values, alpha, bias, spec: _OpSpec, residual=None):
         M, N = spec.M, spec.N
         if alpha is not None:
             sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
@@ -141,12 +141,20 @@ class DiagMMFunction(torch.autograd.Function):
             # tensor-core route: our tcgen05 GEMM on the dense-equivalent W_K (bias fused);
             # W_K is kept for the input gradient (read MN-major there: no W_K^T is built)
             W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
-            y = ops.tc_gemm(x.contiguous(), W, None if bias is None else bias.detach())
+            bz = None if bias is None else bias.detach()
+            if residual is not None and residual.dtype == x.dtype:
+                # the caller's residual add fused into the epilogue (one rounding)
+                y, _ = ops.tc_gemm_ex(x.contiguous(), W, bz, epilogue=3, aux=residual.detach())
+                residual = None
+            else:
+                y = ops.tc_gemm(x.contiguous(), W, bz)
         elif dense:
             W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
             y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
         else:
             y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach())
+        if residual is not None:
+            y = y + residual.detach()
         ctx.save_for_backward(x, values, alpha)
         ctx.sel, ctx.spec, ctx.W, ctx.has_bias, ctx.tc = sel, spec, W, bias is not None, tc
         return y
@@ -156,6 +164,7 @@ class DiagMMFunction(torch.autograd.Function):
         x, values, alpha = ctx.saved_tensors
         sel, spec, W = ctx.sel, ctx.spec, ctx.W
         ctx.W = None
+        d_res = dy if ctx.needs_input_grad[5] else None
         M, N = spec.M, spec.N
         dy = dy.contiguous()
         vals = values.detach()
@@ -189,7 +198,7 @@ class DiagMMFunction(torch.autograd.Function):
         if need_soft:
             g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
                                          clamped=sel.clamped, l1_coeff=spec.l1)
-        return dx, g_values, g_alpha, g_bias, None
+        return dx, g_values, g_alpha, g_bias, None, d_res
 
 
 class DiagMLPFunction(torch.autograd.Function):
@@ -200,7 +209,7 @@ class DiagMLPFunction(torch.autograd.Function):
     layer are exactly those of DiagMMFunction (layers.py:143-167)."""
 
     @staticmethod
-    def forward(ctx, x, v1, a1, b1, v2, a2, b2, s1: _OpSpec, s2: _OpSpec, fuse_fwd: bool = True):
+    def forward(ctx, x, v1, a1, b1, v2, a2, b2, s1: _OpSpec, s2: _OpSpec, fuse_fwd: bool = True, residual=None):
         sel1 = s1.presel or ops.soft_topk_select(a1.detach(), s1.k, s1.temperature)
         sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature)
         x = x.contiguous()
@@ -211,7 +220,13 @@ class DiagMLPFunction(torch.autograd.Function):
             pre = ops.tc_gemm(x, W1, None if b1 is None else b1.detach())
             act = F.gelu(pre, approximate="tanh")
         W2 = ops.materialize(v2.detach(), sel2, s2.M, s2.N, dtype=x.dtype)
-        y = ops.tc_gemm(act, W2, None if b2 is None else b2.detach())
+        bz2 = None if b2 is None else b2.detach()
+        if residual is not None and residual.dtype == x.dtype:  # residual add fused into fc2's epilogue
+            y, _ = ops.tc_gemm_ex(act, W2, bz2, epilogue=3, aux=residual.detach())
+        else:
+            y = ops.tc_gemm(act, W2, bz2)
+            if residual is not None:
+                y = y + residual.detach()
         ctx.save_for_backward(x, pre, act, v1, a1, v2, a2)
         ctx.sels, ctx.specs, ctx.has_bias = (sel1, sel2), (s1, s2), (b1 is not None, b2 is not None)
         ctx.W = (W1, W2)  # read MN-major by the input-gradient products (no W^T materialized)
@@ -221,6 +236,7 @@ class DiagMLPFunction(torch.autograd.Function):
     def backward(ctx, dy):
         x, pre, act, v1, a1, v2, a2 = ctx.saved_tensors
         (sel1, sel2), (s1, s2) = ctx.sels, ctx.specs
+        dy0 = dy
         dy = dy.to(x.dtype).contiguous()
         v1d, v2d = v1.detach(), v2.detach()
         # fc2: input gradient straight to d(pre) through gelu', then dW2 (+ bias) from act
@@ -234,7 +250,8 @@ class DiagMLPFunction(torch.autograd.Function):
         gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True)
         ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1)
         hb1, hb2 = ctx.has_bias
-        return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None)
+        d_res = dy0 if ctx.needs_input_grad[10] else None
+        return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None, d_res)
 
 
 def _flatten(x: torch.Tensor, width: int) -> torch.Tensor:
@@ -330,7 +347,9 @@ class DiagLinear(nn.Module):
         return FrozenDiagLinear(w, None if self.bias is None else self.bias.detach().clone(), route=self.route)
 
     # ---- forward ----------------------------------------------------------------
-    def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, step: int | None = None, residual: torch.Tensor | None = None) -> torch.Tensor:
+        """y = x W_K^T + bias (+ residual: the caller's skip connection, fused into the
+        tensor-core epilogue when it can be)."""
         step = self.step if step is None else int(step)
         self.last_step = step
         lead = x.shape[:-1]
@@ -340,7 +359,8 @@ class DiagLinear(nn.Module):
         elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))  # like nn.Linear under autocast
         spec = self._make_spec(step)
-        y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec)
+        r2 = None if residual is None else _flatten(residual, self.out_features)
+        y = DiagMMFunction.apply(x2, self.values, self.alpha, self.bias, spec, r2)
         return y.reshape(*lead, self.out_features)
 
     def _make_spec(self, step: int) -> "_OpSpec":
@@ -389,15 +409,16 @@ class DiagMLP(nn.Module):
                 and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas"
                 and os.environ.get("DIAGMM_FUSE_MLP", "1") != "0")
 
-    def forward(self, x: torch.Tensor, step: int | None = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, step: int | None = None, residual: torch.Tensor | None = None) -> torch.Tensor:
         f1, f2 = self.fc1, self.fc2
         lead = x.shape[:-1]
         x2 = _flatten(x, f1.in_features)
         if x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))
+        r2 = None if residual is None else _flatten(residual, f2.out_features)
         if not self._fusable(x2):
             h = F.gelu(f1(x2, step), approximate="tanh")
-            return f2(h, step).reshape(*lead, f2.out_features)
+            return f2(h, step, residual=r2).reshape(*lead, f2.out_features)
         step1 = f1.step if step is None else int(step)
         step2 = f2.step if step is None else int(step)
         f1.last_step, f2.last_step = step1, step2
@@ -405,7 +426,7 @@ class DiagMLP(nn.Module):
 
         fuse_fwd = os.environ.get("DIAGMM_FUSE_MLP", "1") in ("1", "both", "fwd")
         y = DiagMLPFunction.apply(x2, f1.values, f1.alpha, f1.bias, f2.values, f2.alpha, f2.bias,
-                                  f1._make_spec(step1), f2._make_spec(step2), fuse_fwd)
+                                  f1._make_spec(step1), f2._make_spec(step2), fuse_fwd, r2)
         return y.reshape(*lead, f2.out_features)
 
 

@@ -459,7 +459,7 @@ def tc_gemm_ex(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = Non
                aux: torch.Tensor | None = None):
     """Tensor-core GEMM with a fused GELU (tanh) epilogue (diagmm_tc_gemm_bf16_ex):
     epilogue 1 -> (gelu(a b^T + bias), pre-activation);  epilogue 2 (aux = pre) ->
-    ((a b^T) * gelu'(aux), aux)."""
+    ((a b^T) * gelu'(aux), aux);  epilogue 3 (aux = residual) -> (a b^T + bias + aux, aux)."""
     _need_cuda(a, b)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or a.shape[1] != b.shape[1]:
         raise ShapeMismatch("tc_gemm_ex takes bf16 operands with equal inner dims")
@@ -467,12 +467,12 @@ def tc_gemm_ex(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = Non
     out = torch.empty(a.shape[0], b.shape[0], dtype=torch.bfloat16, device=a.device)
     if epilogue == 1:
         aux = torch.empty_like(out)
-    elif epilogue == 2:
+    elif epilogue in (2, 3):
         if aux is None or tuple(aux.shape) != tuple(out.shape) or aux.dtype != torch.bfloat16:
-            raise ShapeMismatch("epilogue 2 needs the (M, N) bf16 pre-activation as aux")
+            raise ShapeMismatch(f"epilogue {epilogue} needs an (M, N) bf16 aux tensor")
         aux = aux.contiguous()
     else:
-        raise ValueError("epilogue must be 1 or 2")
+        raise ValueError("epilogue must be 1, 2 or 3")
     bz = None if bias is None else bias.float().contiguous()
     _lib.call("diagmm_tc_gemm_bf16_ex", a.shape[0], b.shape[0], a.shape[1], _p(a), _p(b), _p(bz), _p(out),
               out.shape[1], _p(aux), int(epilogue), _stream(a))

@@ -136,8 +136,9 @@ class Block(nn.Module):
         else:
             q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
-        x = x + self.proj(a)
-        return x + self.mlp(self.norm2(x))
+        # skip connections fused into the proj / fc2 epilogues (DiagLinear residual=)
+        x = self.proj(a, residual=x) if isinstance(self.proj, DiagLinear) else x + self.proj(a)
+        return self.mlp(self.norm2(x), residual=x)
 
 
 class ViT(nn.Module):

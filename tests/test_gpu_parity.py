@@ -653,6 +653,43 @@ def test_tc_gemm_nn_matches_torch(M, N, K):
     torch.testing.assert_close(d, d_ref, rtol=0, atol=0)
 
 
+def test_tc_gemm_residual_epilogue():
+    """epilogue 3: out = a b^T + bias + residual in one rounding."""
+    torch.manual_seed(4)
+    M, N, K = 900, 768, 512
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=DEV) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV)
+    r = torch.randn(M, N, device=DEV).to(torch.bfloat16)
+    out, _ = ops.tc_gemm_ex(a, b, bias, epilogue=3, aux=r)
+    ref = a.float() @ b.float().t() + bias + r.float()
+    assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 1e-2
+
+
+def test_diaglinear_residual_fused_matches_add():
+    """DiagLinear(x, residual=r) == DiagLinear(x) + r on the tensor-core route (bf16 tolerance),
+    gradients included (d residual = dy)."""
+    T = TemperatureSchedule("constant", 0.05, 0.05, 1)
+    lyr = DiagLinear(512, 768, 0.9, seed=9, t_schedule=T, route="auto")
+    with torch.no_grad():
+        lyr.bias.normal_(0, 0.1)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = torch.randn(1024, 512, device=DEV, generator=g).to(torch.bfloat16)
+    r = torch.randn(1024, 768, device=DEV, generator=g).to(torch.bfloat16)
+    dy = torch.randn(1024, 768, device=DEV, generator=g).to(torch.bfloat16)
+    res = []
+    for fused in (True, False):
+        xi, ri = x.clone().requires_grad_(True), r.clone().requires_grad_(True)
+        lyr.values.grad = lyr.alpha.grad = lyr.bias.grad = None
+        y = lyr(xi, step=0, residual=ri) if fused else lyr(xi, step=0) + ri
+        y.backward(dy)
+        res.append((y.float().detach(), xi.grad.float(), ri.grad.float(), lyr.values.grad.clone(),
+                    lyr.alpha.grad.clone(), lyr.bias.grad.clone()))
+    for nm, a, b in zip(["y", "dx", "dr", "dv", "da", "db"], *res):
+        scale = max(1e-6, b.abs().max().item())
+        assert ((a - b).abs().max().item() / scale) < 1e-2, nm
+
+
 def test_diag_mlp_fused_matches_unfused(monkeypatch):
     """DiagMLP with the GELU fused into the tensor-core epilogues == fc2(gelu(fc1(x)))."""
     from paper_2506_11449_b200 import DiagMLP
