@@ -230,6 +230,28 @@ def test_config1_fp32_vs_oracle(shape, T):
     assert scaled_err(lyr.bias.grad.cpu().numpy(), g_ref["bias"]) <= F32_TOL
 
 
+@pytest.mark.parametrize("shape", [(768, 3072), (3072, 768)])
+@pytest.mark.parametrize("B", [1, 3, 5, 8, 16, 32, 48])
+def test_small_batch_plans_fp32_vs_oracle(shape, B):
+    """Every small-batch plan against the oracle: narrow kernels (B <= 4), the
+    cluster-split products with in-kernel weights and the DSMEM fold, and the
+    row-tiled plans with the prescaled store (the plan switches with B)."""
+    n_in, n_out = shape
+    ref, lyr, x, up = _cfg1_case(n_in, n_out, 0.05, B, torch.float32)
+    y_ref, cache = ref.forward(x, 0)
+    g_ref = ref.backward(up, cache)
+    xt = t(x, torch.float32).requires_grad_(True)
+    y = lyr(xt, step=0)
+    (y * t(up, torch.float32)).sum().backward()
+    assert scaled_err(y.detach().cpu().numpy(), y_ref) <= F32_TOL
+    assert scaled_err(xt.grad.cpu().numpy(), g_ref["x"]) <= F32_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) <= F32_TOL
+    assert scaled_err(lyr.alpha.grad.cpu().numpy(), g_ref["alpha"]) <= F32_TOL
+    # deterministic: the same call again is bit-identical
+    y2 = lyr(t(x, torch.float32), step=0)
+    torch.testing.assert_close(y.detach(), y2.detach(), rtol=0, atol=0)
+
+
 @pytest.mark.parametrize("route", ["dense", "auto"])
 def test_dense_route_matches_oracle(route):
     ref, lyr, x, up = _cfg1_case(768, 3072, 0.05, 64, torch.float32, route=route)
@@ -249,6 +271,22 @@ def test_bf16_activations_vs_oracle():
     xb = t(x, torch.bfloat16)
     upb = t(up, torch.bfloat16)
     # oracle on the same (bf16-rounded) inputs
+    y_ref, cache = ref.forward(xb.double().cpu().numpy(), 0)
+    g_ref = ref.backward(upb.double().cpu().numpy(), cache)
+    xt = xb.clone().requires_grad_(True)
+    y = lyr(xt, step=0)
+    y.backward(upb)
+    assert scaled_err(y.detach().double().cpu().numpy(), y_ref) <= BF16_TOL
+    assert scaled_err(xt.grad.double().cpu().numpy(), g_ref["x"]) <= BF16_TOL
+    assert scaled_err(lyr.values.grad.cpu().numpy(), g_ref["values"]) <= BF16_TOL
+
+
+@pytest.mark.parametrize("B", [3, 8, 16, 40])
+def test_small_batch_bf16_vs_oracle(B):
+    """bf16 activations through the small-batch plans (narrow / cluster split with
+    in-kernel bf16 weights / row-tiled) against the oracle on the same rounded inputs."""
+    ref, lyr, x, up = _cfg1_case(3072, 768, 0.05, B, torch.float32)
+    xb, upb = t(x, torch.bfloat16), t(up, torch.bfloat16)
     y_ref, cache = ref.forward(xb.double().cpu().numpy(), 0)
     g_ref = ref.backward(upb.double().cpu().numpy(), cache)
     xt = xb.clone().requires_grad_(True)
