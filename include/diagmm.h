@@ -249,6 +249,22 @@ DIAGMM_API int diagmm_tc_gemm_bf16_nn(int Mdim, int Ndim, int K, const void* A, 
  * (autodiff.py:77-79), so dy is read once.  Replaces the dense branch of
  * layers.py:150-153 + 159-165.  M, N multiples of 64; dy (B, M), x (B, N)
  * bf16, 16-byte aligned. */
+/* The same two products with the (B, M)/(B, K) left operand given as 2-3
+ * separate row-major column blocks A0 | A1 | A2 of `ks` / `ms` columns each
+ * (multiple of 64 / 128): the qkv layer's input and weight gradients read the
+ * attention's dq, dk, dv directly — no packed (B, 3*d) gradient is built.
+ * diagmm_tc_gemm_bf16_nn_split: out = [A0|A1|A2] B, B (K, Ndim) row-major.
+ * diagmm_tc_backward_weight_split: as diagmm_tc_backward_weight with
+ * dy = [dy0|dy1|dy2]; workspace from diagmm_tc_backward_weight_workspace. */
+DIAGMM_API int diagmm_tc_gemm_bf16_nn_split(int Mdim, int Ndim, int K, const void* A0, const void* A1,
+                                            const void* A2, int ks, const void* B, const float* bias,
+                                            void* out, int ldo, void* stream);
+DIAGMM_API int diagmm_tc_backward_weight_split(int M, int N, int B, const void* dy0, const void* dy1,
+                                               const void* dy2, int ms, const void* x, const void* values,
+                                               const double* alpha_soft, const int32_t* slot,
+                                               const int32_t* n_act, int max_act, void* g_values,
+                                               double* g_soft, void* g_bias, void* workspace,
+                                               size_t ws_bytes, void* stream);
 DIAGMM_API size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act);
 DIAGMM_API int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x,
                                          const void* values, const double* alpha_soft,

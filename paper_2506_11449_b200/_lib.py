@@ -71,6 +71,9 @@ SIGNATURES["diagmm_tc_backward_weight"] = (
 SIGNATURES["diagmm_tc_gemm_bf16"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16_ex"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16_nn"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp])
+SIGNATURES["diagmm_tc_gemm_bf16_nn_split"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp])
+SIGNATURES["diagmm_tc_backward_weight_split"] = (
+    _i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp])
 SIGNATURES["diagmm_pack_qkv_grad"] = (_i, [_i, _i, _i, _i, _vp, _vp, _vp, C.c_longlong, C.c_longlong, C.c_longlong,
                                            _vp, _vp])
 SIGNATURES["diagmm_layernorm_fwd"] = (_i, [_i, _i, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp])

@@ -36,11 +36,12 @@ int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
 int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void*, int, void*, int, cudaStream_t,
-                     bool b_kn = false);
+                     bool b_kn = false, const void* A1 = nullptr, const void* A2 = nullptr, int a_ks = 0);
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 size_t tc_dw_workspace(int, int, int, int);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
-                   const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
+                   const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, const void* dy1 = nullptr,
+                   const void* dy2 = nullptr, int a_ms = 0);
 int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long long, long long, long long, void*,
                  cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
@@ -205,6 +206,22 @@ int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x
   if (int e = check_shape(M, N, B, max_act)) return e;
   return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
                         workspace, ws_bytes, S(stream));
+}
+
+int diagmm_tc_gemm_bf16_nn_split(int Mdim, int Ndim, int K, const void* A0, const void* A1, const void* A2, int ks,
+                                 const void* B, const float* bias, void* out, int ldo, void* stream) {
+  if (ks < 1) return DIAGMM_ESHAPE;
+  return run_tc_gemm_bf16(Mdim, Ndim, K, A0, B, bias, out, ldo, nullptr, 0, S(stream), true, A1, A2, ks);
+}
+
+int diagmm_tc_backward_weight_split(int M, int N, int B, const void* dy0, const void* dy1, const void* dy2, int ms,
+                                    const void* x, const void* values, const double* alpha_soft,
+                                    const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
+                                    double* g_soft, void* g_bias, void* workspace, size_t ws_bytes, void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  if (ms < 1) return DIAGMM_ESHAPE;
+  return run_tc_dw_full(M, N, B, dy0, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
+                        workspace, ws_bytes, S(stream), dy1, dy2, ms);
 }
 
 // internal (not in the header): 2:4 sparse tensor-core throughput probe

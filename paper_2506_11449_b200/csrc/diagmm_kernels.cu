@@ -1479,7 +1479,8 @@ int run_gather_dense(int M, int N, const void* dW, const void* vals, const doubl
 // ---- dW on the tensor cores (tc_kernels.cu) + the same finalize
 int tc_dw_splits(int M, int N, int ntok);
 int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
-              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st);
+              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st, const void* dy1,
+              const void* dy2, int a_ms);
 
 size_t tc_dw_workspace(int M, int N, int B, int max_act) {
   const int L = M < N ? M : N;
@@ -1489,7 +1490,8 @@ size_t tc_dw_workspace(int M, int N, int B, int max_act) {
 
 int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const void* vals, const double* asoft,
                    const int32_t* slot, const int32_t* n_act, int max_act, void* g_values, double* g_soft,
-                   void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+                   void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st, const void* dy1, const void* dy2,
+                   int a_ms) {
   using T = __nv_bfloat16;
   using P = typename Traits<T>::P;
   const int C = M > N ? M : N, L = M < N ? M : N;
@@ -1501,7 +1503,7 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
   int parts = 0;
   if (B > 0 && (max_act > 0 || g_bias)) {
     if (int e = run_tc_dw(M, N, B, dy, x, slot, n_act, max_act > 0 ? max_act : 1, partial, pbytes,
-                          g_bias ? colsum : nullptr, st))
+                          g_bias ? colsum : nullptr, st, dy1, dy2, a_ms))
       return e;
     parts = max_act > 0 ? ks : 0;
   }

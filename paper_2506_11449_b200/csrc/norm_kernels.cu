@@ -185,9 +185,16 @@ k_ln_fold(int D, int nparts, const float* __restrict__ part, float* __restrict__
   const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
   if (c < D)
-    for (int p = w; p < nparts; p += 8) {
-      a += part[((size_t)p * 2 + 0) * D + c];
-      b += part[((size_t)p * 2 + 1) * D + c];
+    for (int p0 = w; p0 < nparts; p0 += 32) {  // 4 parts' loads in flight, summed in part order
+      float va[4], vb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = p0 + 8 * k;
+        va[k] = p < nparts ? part[((size_t)p * 2 + 0) * D + c] : 0.f;
+        vb[k] = p < nparts ? part[((size_t)p * 2 + 1) * D + c] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { a += va[k]; b += vb[k]; }
     }
   red[0][w][lane] = a;
   red[1][w][lane] = b;
@@ -256,8 +263,11 @@ int run_ln_fwd(int M, int D, float eps, const void* x, const float* w, const flo
   return status_from_cuda();
 }
 
+// one wave at 2 CTAs/SM: half the dgamma/dbeta partials of 4 per SM, same dx time
+static int ln_bwd_ctas() { return 2 * num_sms(); }
+
 size_t ln_bwd_workspace(int M, int D) {
-  const int ctas = 4 * num_sms();
+  const int ctas = ln_bwd_ctas();
   return (size_t)ctas * 2 * D * sizeof(float);
 }
 
@@ -265,7 +275,7 @@ int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, cons
                void* dx, float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (M < 0 || D < 8 || D % 8 || D > kLnMaxV * 256) return DIAGMM_ESHAPE;
   if (ws_bytes < ln_bwd_workspace(M, D)) return DIAGMM_EWORKSPACE;
-  int ctas = 4 * num_sms();
+  int ctas = ln_bwd_ctas();
   const int rpc = ceil_div(M > 0 ? M : 1, ctas);
   ctas = ceil_div(M > 0 ? M : 1, rpc);
   float* part = static_cast<float*>(ws);

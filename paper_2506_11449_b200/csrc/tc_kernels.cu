@@ -69,7 +69,8 @@ template <int BN, int NST, int NC, int R, int PP, bool BMN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
           const __grid_constant__ CUtensorMap tc_out, const __grid_constant__ CUtensorMap tc_aux, int Mdim, int Ndim,
-          int K, const float* __restrict__ bias, int epi, const __nv_bfloat16* __restrict__ aux_g, int ld_aux) {
+          int K, const float* __restrict__ bias, int epi, const __nv_bfloat16* __restrict__ aux_g, int ld_aux,
+          const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap ta2, int a_ks) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -103,6 +104,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(auxbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&ta);
+    if (a_ks) { prefetch_tmap(&ta1); prefetch_tmap(&ta2); }
     prefetch_tmap(&tb);
     prefetch_tmap(&tc_out);
     if (epi) prefetch_tmap(&tc_aux);
@@ -127,7 +129,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           const int s = it % NST, round = it / NST;
           mbar_wait_parity(&empty[s], (round & 1) ^ 1);
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
-          tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
+          if (a_ks) {  // A = [A0 | A1 | A2] along K, a_ks columns each (a multiple of BK)
+            const int part = kb * BK / a_ks;
+            const CUtensorMap* am = part == 0 ? &ta : part == 1 ? &ta1 : &ta2;
+            tma_load_2d(sA + s * S::a_bytes, am, kb * BK - part * a_ks, m0, &full[s]);
+          } else {
+            tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
+          }
           if constexpr (BMN) {
 #pragma unroll
             for (int h = 0; h < BN / 64; ++h) tma_load_2d(sB + s * S::b_bytes + h * 8192, &tb, n0 + h * 64, kb * BK, &full[s]);
@@ -549,7 +557,8 @@ struct SmemDw {
 __global__ void __launch_bounds__(kDwThreads, 1)
 k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N, int ntok,
         int ksplit, const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
-        float* __restrict__ partial, float* __restrict__ colsum) {
+        float* __restrict__ partial, float* __restrict__ colsum, const __grid_constant__ CUtensorMap ta1,
+        const __grid_constant__ CUtensorMap ta2, int a_ms) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -585,6 +594,7 @@ k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensor
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&ta);
+    if (a_ms) { prefetch_tmap(&ta1); prefetch_tmap(&ta2); }
     prefetch_tmap(&tb);
   }
   if (warp == 1) {
@@ -610,8 +620,11 @@ k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensor
           mbar_wait_parity(&empty[s], (round & 1) ^ 1);
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
 #pragma unroll
-          for (int h = 0; h < BM / 64; ++h)
-            tma_load_2d(sA + s * S::a_bytes + h * 8192, &ta, m0 + h * 64, kb * BK, &full[s]);
+          for (int h = 0; h < BM / 64; ++h) {  // dy = [dy0 | dy1 | dy2] along M (a_ms columns each)
+            const int row = m0 + h * 64, part = a_ms ? row / a_ms : 0;
+            const CUtensorMap* am = part == 0 ? &ta : part == 1 ? &ta1 : &ta2;
+            tma_load_2d(sA + s * S::a_bytes + h * 8192, am, row - part * a_ms, kb * BK, &full[s]);
+          }
 #pragma unroll
           for (int h = 0; h < BN / 64; ++h)
             tma_load_2d(sB + s * S::b_bytes + h * 8192, &tb, n0 + h * 64, kb * BK, &full[s]);
@@ -838,7 +851,8 @@ int tc_dw_splits(int M, int N, int ntok) {
 }
 
 int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
-              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st) {
+              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st, const void* dy1,
+              const void* dy2, int a_ms) {
   using namespace tc;
   const int L = M < N ? M : N;
   if (M < 64 || N < 64 || M % 64 || N % 64 || ntok < 1) return DIAGMM_ESHAPE;
@@ -858,19 +872,29 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  if (!mk(&ta, dy, (uint64_t)M) || !mk(&tb, x, (uint64_t)N)) return DIAGMM_ECUDA;
+  CUtensorMap ta1, ta2;
+  if (a_ms) {  // dy given as column blocks of a_ms (a multiple of 128) in 2 or 3 separate matrices
+    if (a_ms % 128 || M % a_ms || M / a_ms > 3 || (M / a_ms > 1 && !dy1) || (M / a_ms > 2 && !dy2)) return DIAGMM_ESHAPE;
+    if ((reinterpret_cast<uintptr_t>(dy1) | reinterpret_cast<uintptr_t>(dy2)) & 15) return DIAGMM_ESHAPE;
+    if (!mk(&ta, dy, (uint64_t)a_ms) || !mk(&ta1, dy1 ? dy1 : dy, (uint64_t)a_ms) ||
+        !mk(&ta2, dy2 ? dy2 : dy, (uint64_t)a_ms) || !mk(&tb, x, (uint64_t)N))
+      return DIAGMM_ECUDA;
+  } else {
+    if (!mk(&ta, dy, (uint64_t)M) || !mk(&tb, x, (uint64_t)N)) return DIAGMM_ECUDA;
+    ta1 = ta2 = ta;
+  }
   const size_t sm = SmemDw::total;
   cudaFuncSetAttribute(k_tc_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int tiles = ceil_div(M, BM) * ceil_div(N, kDwBN) * ks;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   // partials of inactive slots are never read; active (slot, t) entries are all written
-  k_tc_dw<<<grid, kDwThreads, sm, st>>>(ta, tb, M, N, ntok, ks, slot, n_act, max_act, partial, colsum);
+  k_tc_dw<<<grid, kDwThreads, sm, st>>>(ta, tb, M, N, ntok, ks, slot, n_act, max_act, partial, colsum, ta1, ta2, a_ms);
   note_launch();
   return status_from_cuda();
 }
 
 int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
-                     void* aux, int epi, cudaStream_t st, bool b_kn) {
+                     void* aux, int epi, cudaStream_t st, bool b_kn, const void* A1, const void* A2, int a_ks) {
   using namespace tc;
   constexpr int BN = 256;
   if (Mdim < 1 || Ndim < 1 || K < 1 || K % 8 || ldo < Ndim) return DIAGMM_ESHAPE;
@@ -878,8 +902,15 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return DIAGMM_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo % 8)) return DIAGMM_ESHAPE;
   if (epi < 0 || epi > 3 || (epi && (aux == nullptr || (reinterpret_cast<uintptr_t>(aux) & 15)))) return DIAGMM_ESHAPE;
-  CUtensorMap ta, tb, tco, taux;
-  if (!make_tmap_bf16(&ta, A, (uint64_t)Mdim, (uint64_t)K, BM, (uint64_t)K) ||
+  CUtensorMap ta, tb, tco, taux, ta1, ta2;
+  if (a_ks) {  // A given as column blocks of a_ks (a multiple of BK) in 2 or 3 separate (Mdim, a_ks) matrices
+    if (a_ks % BK || K % a_ks || K / a_ks > 3 || (K / a_ks > 1 && !A1) || (K / a_ks > 2 && !A2)) return DIAGMM_ESHAPE;
+    if ((reinterpret_cast<uintptr_t>(A1) | reinterpret_cast<uintptr_t>(A2)) & 15) return DIAGMM_ESHAPE;
+    if (!make_tmap_bf16(&ta1, A1 ? A1 : A, (uint64_t)Mdim, (uint64_t)a_ks, BM, (uint64_t)a_ks) ||
+        !make_tmap_bf16(&ta2, A2 ? A2 : A, (uint64_t)Mdim, (uint64_t)a_ks, BM, (uint64_t)a_ks))
+      return DIAGMM_ECUDA;
+  }
+  if (!make_tmap_bf16(&ta, A, (uint64_t)Mdim, (uint64_t)(a_ks ? a_ks : K), BM, (uint64_t)(a_ks ? a_ks : K)) ||
       !(b_kn ? make_tmap_bf16_mn(&tb, B, (uint64_t)K, (uint64_t)Ndim)
              : make_tmap_bf16(&tb, B, (uint64_t)Ndim, (uint64_t)K, BN, (uint64_t)K)) ||
       !make_tmap_bf16(&tco, out, (uint64_t)Mdim, (uint64_t)Ndim, BM, (uint64_t)ldo) ||
@@ -890,7 +921,8 @@ int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, co
   auto go = [&](auto kern, size_t sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, kThreads, sm, st>>>(ta, tb, tco, taux, Mdim, Ndim, K, bias, epi,
-                                     static_cast<const __nv_bfloat16*>(aux), ldo);
+                                     static_cast<const __nv_bfloat16*>(aux), ldo, a_ks ? ta1 : ta, a_ks ? ta2 : ta,
+                                     a_ks);
   };
   // Measured at the ViT shapes (50 432 tokens; tools/epi_bench.py):
   //   epi 0: 4 stages + 2 sets of quarter-tile buffers (round-robin) 206 / 154 / 59 us

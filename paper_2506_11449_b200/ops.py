@@ -455,6 +455,49 @@ def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, 
     return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)
 
 
+def tc_gemm_nn_split(parts: list[torch.Tensor], b: torch.Tensor) -> torch.Tensor:
+    """out = cat(parts, dim=1) @ b without the concatenation (diagmm_tc_gemm_bf16_nn_split):
+    2-3 row-major (M, ks) bf16 blocks, b (len(parts)*ks, N)."""
+    if not 2 <= len(parts) <= 3:
+        raise ValueError("tc_gemm_nn_split takes 2 or 3 column blocks")
+    _need_cuda(b, *parts)
+    M, ks = parts[0].shape
+    if any(p.shape != (M, ks) or p.dtype != torch.bfloat16 for p in parts) or b.dtype != torch.bfloat16:
+        raise ShapeMismatch("tc_gemm_nn_split: equal (M, ks) bf16 blocks")
+    if b.shape[0] != ks * len(parts) or b.shape[1] % 8 or ks % 64:
+        raise ShapeMismatch(f"tc_gemm_nn_split: blocks of {ks} columns against b {tuple(b.shape)}")
+    ps = [p.contiguous() for p in parts] + [None] * (3 - len(parts))
+    b = b.contiguous()
+    out = torch.empty(M, b.shape[1], dtype=torch.bfloat16, device=b.device)
+    _lib.call("diagmm_tc_gemm_bf16_nn_split", M, b.shape[1], b.shape[0], _p(ps[0]), _p(ps[1]), _p(ps[2]), ks,
+              _p(b), None, _p(out), out.shape[1], _stream(b))
+    return out
+
+
+def tc_backward_weight_split(dy_parts: list[torch.Tensor], x: torch.Tensor, values: torch.Tensor, sel: Selection,
+                             M: int, N: int, need_soft: bool = True, max_act: int | None = None,
+                             need_bias: bool = False):
+    """tc_backward_weight with dy = cat(dy_parts, dim=1) read block by block (no concatenation)."""
+    if not 2 <= len(dy_parts) <= 3:
+        raise ValueError("tc_backward_weight_split takes 2 or 3 column blocks")
+    B, ms = dy_parts[0].shape
+    if any(p.shape != (B, ms) for p in dy_parts) or ms * len(dy_parts) != M or ms % 128:
+        raise ShapeMismatch("tc_backward_weight_split: equal (B, ms) blocks with ms*len == M, ms % 128 == 0")
+    _check_product(x, N, values, M, N)
+    C, L = geometry(M, N)
+    ma = C if max_act is None else int(max_act)
+    ps = [p.contiguous() for p in dy_parts] + [None] * (3 - len(dy_parts))
+    x = x.contiguous()
+    ws = _workspace(x.device, _lib.load().diagmm_tc_backward_weight_workspace(M, N, B, ma))
+    g_values = torch.empty(C, L, dtype=values.dtype, device=x.device)
+    g_soft = torch.empty(C, dtype=torch.float64, device=x.device) if need_soft else None
+    g_bias = torch.empty(M, dtype=values.dtype, device=x.device) if need_bias else None
+    _lib.call("diagmm_tc_backward_weight_split", M, N, B, _p(ps[0]), _p(ps[1]), _p(ps[2]), ms, _p(x),
+              _p(values.contiguous()), _p(sel.alpha_soft), _p(sel.slot), _p(sel.n_act), ma, _p(g_values),
+              _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(x))
+    return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)
+
+
 def tc_gemm_ex(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None, epilogue: int = 1,
                aux: torch.Tensor | None = None):
     """Tensor-core GEMM with a fused GELU (tanh) epilogue (diagmm_tc_gemm_bf16_ex):

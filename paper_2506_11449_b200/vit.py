@@ -64,6 +64,68 @@ class PackedQKVAttention(torch.autograd.Function):
         return dh
 
 
+class QKVAttentionFunction(torch.autograd.Function):
+    """qkv DiagLinear (tensor-core route) + cuDNN attention as one autograd node.
+
+    Forward: W_K materialized once, h = x W_K^T + b on our tcgen05 GEMM, cuDNN
+    SDPA on the packed (B, T, 3, H, hd) h.  Backward: the attention gradients
+    dq, dk, dv come back as three (B*T, d) row-major blocks (BSHD); the qkv
+    input gradient (dx = [dq|dk|dv] W_K, W_K read MN-major) and the qkv weight
+    gradient (diagonal gather + bias fused) read the three blocks directly, so
+    the packed (B*T, 3d) gradient is never built.  Gradients are exactly those
+    of DiagMMFunction (layers.py:143-167) for the qkv layer."""
+
+    @staticmethod
+    def forward(ctx, x, values, alpha, bias, spec, B, T, H):
+        M, N = spec.M, spec.N
+        sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+        vals = values.detach()
+        W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+        h = ops.tc_gemm(x.contiguous(), W, None if bias is None else bias.detach())
+        hd = N // H
+        qkv = [t_.detach().requires_grad_(True) for t_ in h.view(B, T, 3, H, hd).permute(2, 0, 3, 1, 4).unbind(0)]
+        with torch.enable_grad():
+            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True)[0]
+        ctx.graph = (out, qkv)
+        ctx.save_for_backward(x, values, alpha)
+        ctx.sel, ctx.spec, ctx.W, ctx.has_bias, ctx.bth = sel, spec, W, bias is not None, (B, T, H)
+        return out.detach()
+
+    @staticmethod
+    def backward(ctx, g):
+        out, qkv = ctx.graph
+        ctx.graph = None
+        x, values, alpha = ctx.saved_tensors
+        sel, spec, W = ctx.sel, ctx.spec, ctx.W
+        ctx.W = None
+        B, T, H = ctx.bth
+        M, N = spec.M, spec.N
+        grads = torch.autograd.grad(out, qkv, g)
+        # (B, H, T, hd) with BSHD memory -> (B*T, d) views; copies only if cuDNN changes layout
+        parts = [d.permute(0, 2, 1, 3).reshape(B * T, N) for d in grads]
+        dx = ops.tc_gemm_nn_split(parts, W) if ctx.needs_input_grad[0] else None
+        need_soft = alpha is not None and ctx.needs_input_grad[2]
+        gv, gs, gb = ops.tc_backward_weight_split(parts, x, values.detach(), sel, M, N, need_soft=need_soft,
+                                                  need_bias=True)
+        ga = None
+        if need_soft:
+            ga = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, gs, clamped=sel.clamped,
+                                    l1_coeff=spec.l1)
+        return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None
+
+
+def _qkv_fusable(qkv, x2: torch.Tensor, H: int) -> bool:
+    import os
+
+    from .layer import dense_route_min_tokens
+
+    return (isinstance(qkv, DiagLinear) and qkv.route == "auto" and x2.is_cuda and x2.dtype == torch.bfloat16
+            and x2.shape[0] >= dense_route_min_tokens() and qkv.values.dtype == torch.float32
+            and qkv.in_features % 128 == 0 and qkv.out_features == 3 * qkv.in_features
+            and qkv.in_features % H == 0 and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas"
+            and os.environ.get("DIAGMM_FUSE_QKV", "1") != "0")
+
+
 def _attention_backend() -> str:
     import os
 
@@ -126,8 +188,20 @@ class Block(nn.Module):
 
     def forward(self, x):
         B, T, D = x.shape
-        h = self.qkv(self.norm1(x)).view(B, T, 3, self.heads, D // self.heads)
         backend = _attention_backend()
+        xn = self.norm1(x)
+        x2 = xn.reshape(B * T, D)
+        if x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
+            x2 = x2.to(torch.get_autocast_dtype("cuda"))
+        if backend == "cudnn" and _qkv_fusable(self.qkv, x2, self.heads):
+            q = self.qkv
+            step = q.step
+            q.last_step = step
+            a = QKVAttentionFunction.apply(x2, q.values, q.alpha, q.bias, q._make_spec(step), B, T, self.heads)
+            a = a.transpose(1, 2).reshape(B, T, D)
+            x = self.proj(a, residual=x) if isinstance(self.proj, DiagLinear) else x + self.proj(a)
+            return self.mlp(self.norm2(x), residual=x)
+        h = self.qkv(xn).view(B, T, 3, self.heads, D // self.heads)
         if backend == "cudnn" and h.is_cuda and h.dtype in (torch.bfloat16, torch.float16):
             a = PackedQKVAttention.apply(h).transpose(1, 2).reshape(B, T, D)
         elif backend != "sdpa" and _flash_qkvpacked is not None and h.dtype in (torch.bfloat16, torch.float16):

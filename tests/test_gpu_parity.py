@@ -756,6 +756,29 @@ def test_diag_mlp_fused_matches_unfused(monkeypatch):
             assert ((a - b).abs().max().item() / scale) < 3e-2, nm
 
 
+def test_fused_qkv_attention_block_matches_unfused(monkeypatch):
+    """The qkv DiagLinear + attention autograd node (dq/dk/dv read as three column
+    blocks by the input- and weight-gradient products) == the unfused block."""
+    from paper_2506_11449_b200.vit import ViT, ViTConfig
+
+    cfg = ViTConfig(dim=256, depth=1, heads=4, classes=10)
+    res = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("DIAGMM_FUSE_QKV", fuse)
+        torch.manual_seed(0)
+        model = ViT(cfg, device=DEV)
+        img = torch.randn(4, 3, 224, 224, device=DEV, generator=torch.Generator(device=DEV).manual_seed(1))
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = model(img)
+        out.float().square().mean().backward()
+        q = model.blocks[0].qkv
+        res.append((out.float().detach(), q.values.grad.clone(), q.alpha.grad.clone(), q.bias.grad.clone(),
+                    model.patch.weight.grad.float().clone()))
+    for nm, a, b in zip(["out", "dv_qkv", "da_qkv", "db_qkv", "d_patch"], *res):
+        scale = max(1e-6, b.abs().max().item())
+        assert ((a - b).abs().max().item() / scale) < 3e-2, nm
+
+
 def test_packed_qkv_attention_matches_sdpa():
     """The ViT caller's packed-qkv attention (cuDNN SDPA + one-pass gradient pack)."""
     from paper_2506_11449_b200.vit import PackedQKVAttention
