@@ -130,9 +130,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           mbar_wait_parity(&empty[s], (round & 1) ^ 1);
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
           if (a_ks) {  // A = [A0 | A1 | A2] along K, a_ks columns each (a multiple of BK)
-            const int part = kb * BK / a_ks;
-            const CUtensorMap* am = part == 0 ? &ta : part == 1 ? &ta1 : &ta2;
-            tma_load_2d(sA + s * S::a_bytes, am, kb * BK - part * a_ks, m0, &full[s]);
+            const int part = kb * BK / a_ks, kc = kb * BK - part * a_ks;
+            if (part == 0) tma_load_2d(sA + s * S::a_bytes, &ta, kc, m0, &full[s]);
+            else if (part == 1) tma_load_2d(sA + s * S::a_bytes, &ta1, kc, m0, &full[s]);
+            else tma_load_2d(sA + s * S::a_bytes, &ta2, kc, m0, &full[s]);
           } else {
             tma_load_2d(sA + s * S::a_bytes, &ta, kb * BK, m0, &full[s]);
           }
@@ -621,9 +622,10 @@ k_tc_dw(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensor
           mbar_expect_tx(&full[s], (uint32_t)S::stage);
 #pragma unroll
           for (int h = 0; h < BM / 64; ++h) {  // dy = [dy0 | dy1 | dy2] along M (a_ms columns each)
-            const int row = m0 + h * 64, part = a_ms ? row / a_ms : 0;
-            const CUtensorMap* am = part == 0 ? &ta : part == 1 ? &ta1 : &ta2;
-            tma_load_2d(sA + s * S::a_bytes + h * 8192, am, row - part * a_ms, kb * BK, &full[s]);
+            const int row = m0 + h * 64, part = a_ms ? row / a_ms : 0, rc = row - part * a_ms;
+            if (part == 0) tma_load_2d(sA + s * S::a_bytes + h * 8192, &ta, rc, kb * BK, &full[s]);
+            else if (part == 1) tma_load_2d(sA + s * S::a_bytes + h * 8192, &ta1, rc, kb * BK, &full[s]);
+            else tma_load_2d(sA + s * S::a_bytes + h * 8192, &ta2, rc, kb * BK, &full[s]);
           }
 #pragma unroll
           for (int h = 0; h < BN / 64; ++h)
