@@ -28,6 +28,19 @@ SECTION8_KERNELS = {
 }
 
 
+# C-ABI entry points that launch the same kernel with another epilogue / operand
+# layout are one kernel family for the roofline (k_tc_gemm, k_tc_dw)
+FAMILY = {
+    "diagmm_tc_gemm_bf16_ex": "diagmm_tc_gemm_bf16", "diagmm_tc_gemm_bf16_nn": "diagmm_tc_gemm_bf16",
+    "diagmm_tc_gemm_bf16_nn_split": "diagmm_tc_gemm_bf16",
+    "diagmm_tc_backward_weight_split": "diagmm_tc_backward_weight",
+}
+
+
+def family(name: str) -> str:
+    return FAMILY.get(name, name)
+
+
 def measured_traffic(name: str):
     """dram bytes (read + write) per launch of ``name`` from the committed ncu
     --set full capture (profiles/*traffic*.json), or None."""
@@ -47,12 +60,12 @@ def measured_traffic(name: str):
 class CallTimer:
     """Context manager: CUDA events around every C-ABI call (or only ``only``)."""
 
-    def __init__(self, only: str | None = None):
-        self.only = only
+    def __init__(self, only=None):
+        self.only = {only} if isinstance(only, str) else (set(only) if only is not None else None)
         self.records = []
 
     def _hook(self, name, args, fn):
-        if self.only is not None and name != self.only:
+        if self.only is not None and name not in self.only:
             return fn(*args)
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
@@ -110,10 +123,12 @@ def work(name, args, nact_of=None):
         n = _n_act(args, name, nact_of) or max(M, N)
         p = 8 if dt == 0 else 4
         return 0.0, p * n * min(M, N) * 2 + p * max(M, N) * min(M, N)
-    if name == "diagmm_tc_gemm_bf16":  # dense-equivalent tensor-core product: 2 M N K flop
+    if name in ("diagmm_tc_gemm_bf16", "diagmm_tc_gemm_bf16_ex", "diagmm_tc_gemm_bf16_nn",
+                "diagmm_tc_gemm_bf16_nn_split"):  # dense-equivalent tensor-core product: 2 M N K flop
         Md, Nd, K = args[0], args[1], args[2]
-        return 2.0 * Md * Nd * K, 2.0 * (Md * K + Nd * K + Md * Nd)
-    if name == "diagmm_tc_backward_weight":
+        aux = 2.0 * Md * Nd if name in ("diagmm_tc_gemm_bf16_ex", "diagmm_tc_gemm_bf16_nn") and args[9] else 0.0
+        return 2.0 * Md * Nd * K, 2.0 * (Md * K + Nd * K + Md * Nd) + aux
+    if name in ("diagmm_tc_backward_weight", "diagmm_tc_backward_weight_split"):
         M, N, B = args[0], args[1], args[2]
         return 2.0 * M * N * B, 2.0 * B * (M + N) + 4.0 * max(M, N) * min(M, N)
     if name == "diagmm_adamw_multi":
@@ -157,6 +172,7 @@ def roofline(records, peaks: dict, peaks_kind: str, fma_tflops: float, nact_of=N
     n = len(records)
     sec = tot_ms / 1e3
     hbm = float(peaks["hbm_gbs"])
+    name = family(name)
     if name.startswith("diagmm_tc_"):  # tensor-core kernels: dense bf16 tcgen05 peak, sustained (inside a step)
         tpk = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
         achieved = tot_f / sec / 1e12
