@@ -273,9 +273,11 @@ def diag_case(M, N, B, sparsity, act_dtype, peaks, fma_tflops, seed=0, reps=20, 
            **out, "fwd_bwd_us": tot}
     if act_dtype == torch.bfloat16 and M % 64 == 0 and N % 64 == 0:
         # the tensor-core route of the same framework (materialize + tcgen05 GEMMs, fused-gather dW)
+        # the layer's route: W_K materialized once in the forward and read MN-major by dX
+        W = ops.materialize(values, sel, M, N, dtype=act_dtype)
         tc = {
             "fwd": lambda: ops.tc_gemm(x, ops.materialize(values, sel, M, N, dtype=act_dtype)),
-            "dx": lambda: ops.tc_gemm(dy, ops.materialize(values, sel, M, N, dtype=act_dtype, transposed=True)),
+            "dx": lambda: ops.tc_gemm_nn(dy, W),
             "dw": lambda: ops.tc_backward_weight(dy, x, values, sel, M, N, need_soft=False, max_act=k),
         }
         res["tc_route_us"] = {}

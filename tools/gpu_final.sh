@@ -7,4 +7,4 @@ timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo benchref=$?
 timeout 600 python tools/bench_kernels.py > gpurun_out/kern.log 2>&1; echo kern=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1; echo ncul=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gather_tiles|k_gather_finish|k_adamw_multi|k_materialize|k_tc_gemm" -c 6 -o gpurun_out/dominant_full python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1; echo ncuf=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_materialize|k_tc_gemm" -c 6 -o gpurun_out/dominant_full python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1; echo ncuf=$?
