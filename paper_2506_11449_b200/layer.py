@@ -416,6 +416,8 @@ class DiagMLP(nn.Module):
         if x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))
         r2 = None if residual is None else _flatten(residual, f2.out_features)
+        if isinstance(f1, FrozenDiagLinear) and isinstance(f2, FrozenDiagLinear):  # inference (freeze())
+            return f2(f1.forward_gelu(x2), residual=r2).reshape(*lead, f2.out_features)
         if not self._fusable(x2):
             h = F.gelu(f1(x2, step), approximate="tanh")
             return f2(h, step, residual=r2).reshape(*lead, f2.out_features)
@@ -457,22 +459,50 @@ class FrozenDiagLinear(nn.Module):
             self._dense[dtype] = W
         return W
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
-        lead = x.shape[:-1]
+    def _prep(self, x: torch.Tensor) -> torch.Tensor:
         x2 = _flatten(x, self.in_features)
         if self.store.dtype == torch.float64:
             x2 = x2.double()
         elif x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))
+        return x2
+
+    def _tc(self, x2: torch.Tensor) -> bool:
         dense = self.route == "dense" or (self.route == "auto" and x2.dtype == torch.bfloat16
                                           and x2.shape[0] >= dense_route_min_tokens())
-        if dense and _tc_ok(x2, self.out_features, self.in_features):
-            y = ops.tc_gemm(x2.contiguous(), self._dense_weight(x2.dtype), self.bias)
+        return dense and _tc_ok(x2, self.out_features, self.in_features)
+
+    def forward(self, x: torch.Tensor, step: int | None = None, residual: torch.Tensor | None = None) -> torch.Tensor:
+        """y = x W^T + bias (+ residual, fused into the tensor-core epilogue); ``step``
+        is accepted for call compatibility with DiagLinear and ignored (frozen)."""
+        lead = x.shape[:-1]
+        x2 = self._prep(x)
+        r2 = None if residual is None else _flatten(residual, self.out_features)
+        dense = self.route == "dense" or (self.route == "auto" and x2.dtype == torch.bfloat16
+                                          and x2.shape[0] >= dense_route_min_tokens())
+        if self._tc(x2):
+            if r2 is not None and r2.dtype == x2.dtype:
+                y, _ = ops.tc_gemm_ex(x2.contiguous(), self._dense_weight(x2.dtype), self.bias, epilogue=3, aux=r2)
+                r2 = None
+            else:
+                y = ops.tc_gemm(x2.contiguous(), self._dense_weight(x2.dtype), self.bias)
         elif dense:
             y = F.linear(x2, self._dense_weight(x2.dtype), None if self.bias is None else self.bias.to(x2.dtype))
         else:
             y = ops.diag_forward(x2, self.store, self._sel, self.out_features, self.in_features, self.bias)
+        if r2 is not None:
+            y = y + r2
         return y.reshape(*lead, self.out_features)
+
+    def forward_gelu(self, x: torch.Tensor) -> torch.Tensor:
+        """gelu_tanh(x W^T + bias), fused into the tensor-core epilogue when it can be
+        (the frozen MLP's fc1)."""
+        lead = x.shape[:-1]
+        x2 = self._prep(x)
+        if self._tc(x2):
+            act, _ = ops.tc_gemm_ex(x2.contiguous(), self._dense_weight(x2.dtype), self.bias, epilogue=1)
+            return act.reshape(*lead, self.out_features)
+        return F.gelu(self.forward(x), approximate="tanh")
 
 
 class DiagHeurLinear(nn.Module):

@@ -17,7 +17,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from . import _lib, ops
-from .layer import DiagLinear, DiagMLP, preselect
+from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, preselect
 from .selection import TemperatureSchedule
 
 
@@ -199,7 +199,7 @@ class Block(nn.Module):
             q.last_step = step
             a = QKVAttentionFunction.apply(x2, q.values, q.alpha, q.bias, q._make_spec(step), B, T, self.heads)
             a = a.transpose(1, 2).reshape(B, T, D)
-            x = self.proj(a, residual=x) if isinstance(self.proj, DiagLinear) else x + self.proj(a)
+            x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
             return self.mlp(self.norm2(x), residual=x)
         h = self.qkv(xn).view(B, T, 3, self.heads, D // self.heads)
         if backend == "cudnn" and h.is_cuda and h.dtype in (torch.bfloat16, torch.float16):
@@ -211,7 +211,7 @@ class Block(nn.Module):
             q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
         # skip connections fused into the proj / fc2 epilogues (DiagLinear residual=)
-        x = self.proj(a, residual=x) if isinstance(self.proj, DiagLinear) else x + self.proj(a)
+        x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
         return self.mlp(self.norm2(x), residual=x)
 
 

@@ -779,6 +779,27 @@ def test_fused_qkv_attention_block_matches_unfused(monkeypatch):
         assert ((a - b).abs().max().item() / scale) < 3e-2, nm
 
 
+def test_frozen_fused_epilogues_match_unfused():
+    """FrozenDiagLinear on the tensor-core route: gelu and residual fused in the
+    epilogue == the separate ops (inference path of bench.py's infer number)."""
+    T = TemperatureSchedule("constant", 1e-9, 1e-9, 1)
+    lyr = DiagLinear(512, 1024, 0.9, seed=3, t_schedule=T, route="auto")
+    with torch.no_grad():
+        lyr.bias.normal_(0, 0.1)
+    fz = lyr.freeze()
+    g = torch.Generator(device=DEV).manual_seed(8)
+    x = torch.randn(1024, 512, device=DEV, generator=g).to(torch.bfloat16)
+    r = torch.randn(1024, 1024, device=DEV, generator=g).to(torch.bfloat16)
+    with torch.no_grad():
+        y = fz(x)
+        a = fz.forward_gelu(x)
+        a_ref = torch.nn.functional.gelu(y.float(), approximate="tanh")
+        yr = fz(x, residual=r)
+        yr_ref = y.float() + r.float()
+    assert ((a.float() - a_ref).abs().max() / a_ref.abs().max()).item() < 2e-2
+    assert ((yr.float() - yr_ref).abs().max() / yr_ref.abs().max()).item() < 2e-2
+
+
 def test_packed_qkv_attention_matches_sdpa():
     """The ViT caller's packed-qkv attention (cuDNN SDPA + one-pass gradient pack)."""
     from paper_2506_11449_b200.vit import PackedQKVAttention
