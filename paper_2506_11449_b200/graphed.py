@@ -1,0 +1,58 @@
+"""Forward + backward of a training step as one CUDA graph (the step's launch-bound
+chain of ~400 kernels replayed without host work or inter-launch gaps).
+
+The captured part is everything up to the gradients: TopK re-selection, DiagLinear
+products, the caller's attention / LayerNorm / loss and the backward.  The optimizer
+stays eager because the Adam step count (bias corrections) changes every step.  The
+capture is valid while the per-step host arguments it bakes in stay fixed: the soft
+TopK temperature (a constant schedule) and the l1 coefficients; inputs are copied into
+the captured buffers before each replay."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class GraphedStep:
+    """``fwd_bwd(inputs...) -> loss`` captured once; ``step(*inputs)`` copies the inputs
+    into the captured buffers (when they are other tensors), replays, returns the
+    captured loss tensor.  Gradients stay in the graph's static tensors (``.grad`` of
+    the parameters), overwritten by every replay."""
+
+    def __init__(self, fwd_bwd, params, *static_inputs: torch.Tensor, warmup: int = 1):
+        self.inputs = static_inputs
+        dev = static_inputs[0].device
+        for p in params:
+            p.grad = None
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm the side stream's allocator pool
+            for _ in range(warmup):
+                fwd_bwd(*static_inputs)
+                for p in params:
+                    p.grad = None
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = _lib.load().diagmm_launch_count()
+        with torch.cuda.graph(self.graph):
+            self.loss = fwd_bwd(*static_inputs)
+        self.launches = _lib.load().diagmm_launch_count() - n0  # our kernels per replay
+        torch.cuda.synchronize(dev)
+
+    def step(self, *inputs: torch.Tensor) -> torch.Tensor:
+        for dst, src in zip(self.inputs, inputs):
+            if src is not dst:
+                dst.copy_(src, non_blocking=True)
+        self.graph.replay()
+        return self.loss
+
+
+def schedules_constant(model: torch.nn.Module) -> bool:
+    """True when every DiagLinear's temperature is the same at every step."""
+    from .layer import DiagLinear
+
+    return all(m.t_schedule.kind == "constant" or m.t_schedule.t_init == m.t_schedule.t_final
+               for m in model.modules() if isinstance(m, DiagLinear))

@@ -616,8 +616,9 @@ def penalties(model: nn.Module, fused: bool = False) -> list[torch.Tensor]:
         spec.l1 = float(m.l1_coeff)
     with torch.no_grad():
         norms = torch._foreach_norm([m.alpha.detach() for m in layers], 1)
-        coeffs = torch.tensor([m.l1_coeff for m in layers], dtype=torch.float64, device=norms[0].device)
-        return [(torch.stack(norms) * coeffs).sum()]
+        # scalar coefficients (no host-to-device copy: the step stays CUDA-graph capturable)
+        scaled = torch._foreach_mul(norms, [float(m.l1_coeff) for m in layers])
+        return [torch.stack(scaled).sum()]
 
 
 __all__ = [

@@ -800,6 +800,54 @@ def test_frozen_fused_epilogues_match_unfused():
     assert ((yr.float() - yr_ref).abs().max() / yr_ref.abs().max()).item() < 2e-2
 
 
+def test_graphed_training_step_matches_eager():
+    """Forward + backward captured as one CUDA graph (bench.py's step): three steps of
+    replay + eager AdamW move the parameters exactly like three eager steps (up to the
+    library attention's own run-to-run noise)."""
+    import torch.nn.functional as F
+
+    from paper_2506_11449_b200 import AdamW, GlobalNormClipper, model_param_specs, penalties
+    from paper_2506_11449_b200.graphed import GraphedStep
+    from paper_2506_11449_b200.vit import ViT, ViTConfig
+
+    cfg = ViTConfig(dim=256, depth=2, heads=4, classes=10)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    img = torch.randn(4, 3, 224, 224, device=DEV, generator=g).to(torch.bfloat16)
+    lbl = torch.randint(0, 10, (4,), device=DEV, generator=g)
+    finals = []
+    for graphed in (False, True):
+        torch.manual_seed(0)
+        model = ViT(cfg, device=DEV)
+        specs = model_param_specs(model)
+        opt, clip = AdamW(specs, lr=1e-3), GlobalNormClipper(1.0)
+
+        def fwd_bwd(i, l):
+            model.set_step(0)
+            with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+                logits = model(i)
+            loss = F.cross_entropy(logits.float(), l)
+            for pen in penalties(model, fused=True):
+                loss = loss + pen
+            loss.backward()
+            return loss
+
+        init = [s_.tensor.detach().clone() for s_ in specs]
+        gs = GraphedStep(fwd_bwd, [s_.tensor for s_ in specs], img.clone(), lbl.clone()) if graphed else None
+        for _ in range(3):
+            if gs is not None:
+                gs.step(img, lbl)
+            else:
+                fwd_bwd(img, lbl)
+            _, sc = clip.compute(specs)
+            opt.step(clip_scale=sc)
+            if gs is None:
+                opt.zero_grad()
+        finals.append([s_.tensor.detach().clone() for s_ in specs])
+    moved = torch.stack([(b.double() - a.double()).norm() for a, b in zip(init, finals[0])]).norm()
+    diff = torch.stack([(a.double() - b.double()).norm() for a, b in zip(*finals)]).norm()
+    assert moved > 0 and (diff / moved).item() < 1e-2, (diff.item(), moved.item())
+
+
 def test_packed_qkv_attention_matches_sdpa():
     """The ViT caller's packed-qkv attention (cuDNN SDPA + one-pass gradient pack)."""
     from paper_2506_11449_b200.vit import PackedQKVAttention
