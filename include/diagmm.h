@@ -285,6 +285,13 @@ DIAGMM_API size_t diagmm_layernorm_bwd_workspace(int M, int D);
 DIAGMM_API int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy, const float* w,
                                     const float* mean, const float* rstd, void* dx, float* dw,
                                     float* db, void* workspace, size_t ws_bytes, void* stream);
+/* Same backward with the skip connection's gradient dres ((M, D) bf16, may be
+ * NULL) added into dx: x feeds both the norm and the block's residual, so its
+ * two gradient contributions are summed inside the kernel. */
+DIAGMM_API int diagmm_layernorm_bwd_res(int M, int D, const void* x, const void* dy, const void* dres,
+                                        const float* w, const float* mean, const float* rstd, void* dx,
+                                        float* dw, float* db, void* workspace, size_t ws_bytes,
+                                        void* stream);
 
 /* Packed attention-input gradient for the ViT caller: dqkv (B, T, 3, H, hd)
  * bf16 contiguous <- dq, dk, dv (B, H, T, hd) bf16 sharing the element

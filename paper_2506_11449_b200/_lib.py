@@ -79,6 +79,7 @@ SIGNATURES["diagmm_pack_qkv_grad"] = (_i, [_i, _i, _i, _i, _vp, _vp, _vp, C.c_lo
 SIGNATURES["diagmm_layernorm_fwd"] = (_i, [_i, _i, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp])
 SIGNATURES["diagmm_layernorm_bwd_workspace"] = (_sz, [_i, _i])
 SIGNATURES["diagmm_layernorm_bwd"] = (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp])
+SIGNATURES["diagmm_layernorm_bwd_res"] = (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp])
 
 _LIB = None
 

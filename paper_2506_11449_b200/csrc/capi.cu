@@ -47,7 +47,7 @@ int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
-               void*, size_t, cudaStream_t);
+               void*, size_t, cudaStream_t, const void* dres = nullptr);
 constexpr int kSumsqScratch = 296;
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
@@ -244,6 +244,13 @@ int diagmm_layernorm_bwd(int M, int D, const void* x, const void* dy, const floa
                          const float* rstd, void* dx, float* dw, float* db, void* workspace, size_t ws_bytes,
                          void* stream) {
   return run_ln_bwd(M, D, x, dy, w, mean, rstd, dx, dw, db, workspace, ws_bytes, S(stream));
+}
+
+int diagmm_layernorm_bwd_res(int M, int D, const void* x, const void* dy, const void* dres, const float* w,
+                             const float* mean, const float* rstd, void* dx, float* dw, float* db, void* workspace,
+                             size_t ws_bytes, void* stream) {
+  if (dres && (reinterpret_cast<uintptr_t>(dres) & 15)) return DIAGMM_ESHAPE;
+  return run_ln_bwd(M, D, x, dy, w, mean, rstd, dx, dw, db, workspace, ws_bytes, S(stream), dres);
 }
 
 int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, const uint8_t* clamped,

@@ -93,7 +93,7 @@ template <int NV>
 __global__ void __launch_bounds__(kLnWarps * 32, 2)
 k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
          const float* __restrict__ w, const float* __restrict__ mean, const float* __restrict__ rstd,
-         __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
+         __nv_bfloat16* __restrict__ dx, float* __restrict__ part, const __nv_bfloat16* __restrict__ dres) {
   __shared__ float s_acc[2][kLnMaxV * 256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float dg[NV][8], db[NV][8];
@@ -150,6 +150,12 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
       const float* wr = s_w + c;
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = rs * (g[e] * wr[e] - s1 - (xh[e] - mu) * rs * s2);
+      if (dres) {  // the skip connection's gradient, summed here instead of by a separate add
+        float rr[8];
+        unpack8(reinterpret_cast<const uint4*>(dres + (size_t)row * D)[i * 32 + lane], rr);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] += rr[e];
+      }
       dr[i * 32 + lane] = pack8(o);
     }
   }
@@ -272,7 +278,7 @@ size_t ln_bwd_workspace(int M, int D) {
 }
 
 int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, const float* mean, const float* rstd,
-               void* dx, float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t st) {
+               void* dx, float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t st, const void* dres) {
   if (M < 0 || D < 8 || D % 8 || D > kLnMaxV * 256) return DIAGMM_ESHAPE;
   if (ws_bytes < ln_bwd_workspace(M, D)) return DIAGMM_EWORKSPACE;
   int ctas = ln_bwd_ctas();
@@ -282,11 +288,12 @@ int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, cons
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto G = static_cast<const __nv_bfloat16*>(dy);
   auto DX = static_cast<__nv_bfloat16*>(dx);
+  auto R = static_cast<const __nv_bfloat16*>(dres);
   switch (ln_nv(D)) {
-    case 1: k_ln_bwd<1><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part); break;
-    case 2: k_ln_bwd<2><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part); break;
-    case 3: k_ln_bwd<3><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part); break;
-    default: k_ln_bwd<4><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part); break;
+    case 1: k_ln_bwd<1><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
+    case 2: k_ln_bwd<2><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
+    case 3: k_ln_bwd<3><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
+    default: k_ln_bwd<4><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
   }
   note_launch();
   k_ln_fold<<<ceil_div(D, 32), 256, 0, st>>>(D, ctas, part, dw, db);

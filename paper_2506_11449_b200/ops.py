@@ -398,6 +398,48 @@ def layer_norm_bf16(x, weight, bias, eps: float = 1e-5):
     return FusedLayerNorm.apply(x, weight, bias, eps)
 
 
+class FusedLayerNormSkip(torch.autograd.Function):
+    """(LayerNorm(x), x) as ONE autograd node: when x also feeds the block's skip
+    connection, both of its gradient contributions arrive in this backward and the
+    kernel sums them (diagmm_layernorm_bwd_res) — no separate gradient add."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, eps):
+        _need_cuda(x, weight, bias)
+        D = x.shape[-1]
+        x2 = x.reshape(-1, D).to(torch.bfloat16).contiguous()
+        M = x2.shape[0]
+        y = torch.empty_like(x2)
+        mean = torch.empty(M, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(M, dtype=torch.float32, device=x.device)
+        w = weight.detach().float().contiguous()
+        b = bias.detach().float().contiguous()
+        _lib.call("diagmm_layernorm_fwd", M, D, float(eps), _p(x2), _p(w), _p(b), _p(y), _p(mean), _p(rstd),
+                  _stream(x2))
+        ctx.save_for_backward(x2, w, mean, rstd)
+        ctx.shape, ctx.in_dtype = x.shape, x.dtype
+        return y.view(x.shape), x
+
+    @staticmethod
+    def backward(ctx, dy, dskip):
+        x2, w, mean, rstd = ctx.saved_tensors
+        M, D = x2.shape
+        g = dy.reshape(M, D).to(torch.bfloat16).contiguous()
+        r = None if dskip is None else dskip.reshape(M, D).to(torch.bfloat16).contiguous()
+        dx = torch.empty_like(x2)
+        dw = torch.empty(D, dtype=torch.float32, device=x2.device)
+        db = torch.empty(D, dtype=torch.float32, device=x2.device)
+        ws = _workspace(x2.device, _lib.load().diagmm_layernorm_bwd_workspace(M, D))
+        _lib.call("diagmm_layernorm_bwd_res", M, D, _p(x2), _p(g), _p(r), _p(w), _p(mean), _p(rstd), _p(dx),
+                  _p(dw), _p(db), _p(ws), ws.numel(), _stream(x2))
+        return dx.view(ctx.shape).to(ctx.in_dtype), dw, db, None
+
+
+def layer_norm_skip_bf16(x, weight, bias, eps: float = 1e-5):
+    """(layer_norm(x), x) with the skip connection's gradient summed in the LN backward."""
+    return FusedLayerNormSkip.apply(x, weight, bias, eps)
+
+
 def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) -> torch.Tensor:
     """out = a @ b.T (+ bias) on the tcgen05 tensor cores (bf16 in/out, fp32 accumulate)."""
     _need_cuda(a, b)

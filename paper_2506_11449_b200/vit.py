@@ -136,13 +136,23 @@ class LayerNorm(nn.LayerNorm):
     """nn.LayerNorm that runs the fused bf16 kernel (csrc/norm_kernels.cu) when
     the activations are bf16 (directly or under CUDA autocast); float32 params."""
 
-    def forward(self, x):
+    def _fused(self, x) -> bool:
         bf16 = x.dtype == torch.bfloat16 or (torch.is_autocast_enabled("cuda")
                                               and torch.get_autocast_dtype("cuda") == torch.bfloat16)
         D = x.shape[-1]
-        if x.is_cuda and bf16 and self.elementwise_affine and D % 8 == 0 and D <= 1024:
+        return x.is_cuda and bf16 and self.elementwise_affine and D % 8 == 0 and D <= 1024
+
+    def forward(self, x):
+        if self._fused(x):
             return ops.layer_norm_bf16(x, self.weight, self.bias, self.eps)
         return super().forward(x)
+
+    def forward_skip(self, x):
+        """(norm(x), x) where x also feeds the block's skip connection: the two
+        gradients of x are summed inside the LayerNorm backward kernel."""
+        if self._fused(x) and x.dtype == torch.bfloat16:
+            return ops.layer_norm_skip_bf16(x, self.weight, self.bias, self.eps)
+        return self.forward(x), x
 
 
 @dataclass(frozen=True)
@@ -189,7 +199,7 @@ class Block(nn.Module):
     def forward(self, x):
         B, T, D = x.shape
         backend = _attention_backend()
-        xn = self.norm1(x)
+        xn, x = self.norm1.forward_skip(x)  # x's skip and norm gradients meet in the LN backward
         x2 = xn.reshape(B * T, D)
         if x2.dtype == torch.float32 and torch.is_autocast_enabled("cuda"):
             x2 = x2.to(torch.get_autocast_dtype("cuda"))
@@ -200,7 +210,8 @@ class Block(nn.Module):
             a = QKVAttentionFunction.apply(x2, q.values, q.alpha, q.bias, q._make_spec(step), B, T, self.heads)
             a = a.transpose(1, 2).reshape(B, T, D)
             x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
-            return self.mlp(self.norm2(x), residual=x)
+            xn2, x = self.norm2.forward_skip(x)
+            return self.mlp(xn2, residual=x)
         h = self.qkv(xn).view(B, T, 3, self.heads, D // self.heads)
         if backend == "cudnn" and h.is_cuda and h.dtype in (torch.bfloat16, torch.float16):
             a = PackedQKVAttention.apply(h).transpose(1, 2).reshape(B, T, D)
@@ -212,7 +223,8 @@ class Block(nn.Module):
             a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
         # skip connections fused into the proj / fc2 epilogues (DiagLinear residual=)
         x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
-        return self.mlp(self.norm2(x), residual=x)
+        xn2, x = self.norm2.forward_skip(x)
+        return self.mlp(xn2, residual=x)
 
 
 class ViT(nn.Module):

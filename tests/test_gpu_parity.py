@@ -848,6 +848,27 @@ def test_graphed_training_step_matches_eager():
     assert moved > 0 and (diff / moved).item() < 1e-2, (diff.item(), moved.item())
 
 
+def test_layernorm_skip_matches_separate_add():
+    """(LN(x), x) as one node: dx = LN backward + the skip gradient, summed in the kernel."""
+    g = torch.Generator(device=DEV).manual_seed(11)
+    x = torch.randn(777, 768, device=DEV, generator=g).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(768, device=DEV, generator=g)).requires_grad_(True)
+    b = (0.1 * torch.randn(768, device=DEV, generator=g)).requires_grad_(True)
+    dy = torch.randn(777, 768, device=DEV, generator=g).to(torch.bfloat16)
+    dr = torch.randn(777, 768, device=DEV, generator=g).to(torch.bfloat16)
+    x1 = x.clone().requires_grad_(True)
+    y, skip = ops.layer_norm_skip_bf16(x1, w, b)
+    torch.autograd.backward([y, skip], [dy, dr])
+    x2 = x.clone().requires_grad_(True)
+    w2, b2 = w.detach().clone().requires_grad_(True), b.detach().clone().requires_grad_(True)
+    y2 = ops.layer_norm_bf16(x2, w2, b2)
+    torch.autograd.backward([y2, x2], [dy, dr])
+    torch.testing.assert_close(y, y2, rtol=0, atol=0)
+    assert ((x1.grad.float() - x2.grad.float()).abs().max() / x2.grad.float().abs().max()).item() < 1e-2
+    torch.testing.assert_close(w.grad, w2.grad, rtol=0, atol=0)
+    torch.testing.assert_close(b.grad, b2.grad, rtol=0, atol=0)
+
+
 def test_packed_qkv_attention_matches_sdpa():
     """The ViT caller's packed-qkv attention (cuDNN SDPA + one-pass gradient pack)."""
     from paper_2506_11449_b200.vit import PackedQKVAttention
