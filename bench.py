@@ -464,21 +464,28 @@ def infer_images_per_s(model, images, args, dev):
             for parent, attr, mod in self.saved:
                 setattr(parent, attr, mod)
 
-    with _Swap(), torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+    with _Swap(), torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
         for _ in range(3):
             model(images)
+        torch.cuda.synchronize()
+        # the forward replayed as one CUDA graph (frozen weights: every argument is static)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            model(images)
+        g.replay()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 5
         s.record()
         for _ in range(reps):
-            model(images)
+            g.replay()
         e.record()
         torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
     _ = FrozenDiagLinear
     return {"value": images.shape[0] / (ms / 1e3), "unit": "images/s", "ms_per_batch": ms,
-            "route": "frozen (hard top-K, α̃ baked in), tensor-core route, GELU + residual fused in the epilogues"}
+            "route": "frozen (hard top-K, α̃ baked in), tensor-core route, GELU + residual fused in the epilogues, "
+                     "forward replayed as one CUDA graph"}
 
 
 def diagmm_kernel_section(peaks, peaks_kind):
