@@ -1043,6 +1043,75 @@ k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, cons
   }
 }
 
+// Tiled materialize (W_K, bf16 / fp32): a CTA owns a 32 x 256 output tile,
+// finds the active offsets crossing it (287 candidates, slot lookups, compacted
+// in shared memory), writes their entries into a zeroed shared tile — for one
+// diagonal consecutive threads read consecutive stored values — and stores the
+// tile with 16-byte writes.  The per-element kernel above does a slot lookup
+// and a scattered value load for every output element.
+constexpr int kMTR = 32, kMTC = 256;
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_materialize_tiles(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
+                    const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
+                    T* __restrict__ w, int vec) {
+  static_assert(sizeof(T) <= 4, "tile kernel for bf16 / fp32");
+  __shared__ __align__(16) T tile[kMTR][kMTC];
+  __shared__ int s_list[kMTR + kMTC];
+  __shared__ double s_sc[kMTR + kMTC];
+  __shared__ int s_cnt;
+  const int n_act = min(*n_act_p, max_act);
+  const bool tall = M >= N;
+  const int mod = tall ? M : N, L = tall ? N : M;
+  const int r0 = blockIdx.y * kMTR, c0 = blockIdx.x * kMTC;
+  constexpr int VW = 16 / sizeof(T);
+  for (int i = threadIdx.x; i < kMTR * kMTC / VW; i += blockDim.x)
+    reinterpret_cast<uint4*>(&tile[0][0])[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  int lo = tall ? r0 - c0 - kMTC + 1 : c0 - r0 - kMTR + 1;
+  int width = kMTR + kMTC - 1;
+  if (width >= mod) { lo = 0; width = mod; }
+  lo %= mod;
+  lo = lo < 0 ? lo + mod : lo;
+  for (int k = threadIdx.x; k < width; k += blockDim.x) {
+    int o = lo + k;
+    o = o >= mod ? o - mod : o;
+    const int sl = __ldg(slot + o);
+    if (sl >= 0 && sl < n_act) {  // order of the list is irrelevant: every entry has one writer
+      const int idx = atomicAdd(&s_cnt, 1);
+      s_list[idx] = o;
+      s_sc[idx] = asoft ? __ldg(asoft + o) : 1.0;
+    }
+  }
+  __syncthreads();
+  const int nd = s_cnt;
+  for (int it = threadIdx.x; it < nd * kMTR; it += blockDim.x) {
+    const int di = it / kMTR, i = it - di * kMTR;
+    const int o = s_list[di], r = r0 + i;
+    if (r >= M) continue;
+    int c, t;
+    if (tall) { c = r - o; c = c < 0 ? c + mod : c; t = c; }
+    else { c = r + o; c = c >= mod ? c - mod : c; t = r; }
+    if (c < c0 || c >= c0 + kMTC || c >= N) continue;
+    const double v = s_sc[di] * (double)__ldg(vals + (size_t)o * L + t);
+    tile[i][c - c0] = from_acc<T>((float)v);
+  }
+  __syncthreads();
+  const int chunks = kMTC / VW;
+  for (int it = threadIdx.x; it < kMTR * chunks; it += blockDim.x) {
+    const int i = it / chunks, ch = it - i * chunks;
+    const int r = r0 + i, cb = c0 + ch * VW;
+    if (r >= M || cb >= N) continue;
+    T* dst = w + (size_t)r * N + cb;
+    if (vec && cb + VW <= N) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&tile[i][ch * VW]);
+    } else {
+      for (int e = 0; e < VW && cb + e < N; ++e) dst[e] = tile[i][ch * VW + e];
+    }
+  }
+}
+
 // Dense dW -> per-diagonal rows, pass 1: a CTA stages a tile of dW (coalesced)
 // and writes, for every ACTIVE offset crossing the tile, the unscaled entries
 // gw[o, t] into row o of g_values (runs of consecutive t: coalesced).
@@ -1455,6 +1524,15 @@ int run_materialize(int M, int N, const void* vals, const double* asoft, const i
   using P = typename Traits<T>::P;
   const int R = trans ? N : M, Cc = trans ? M : N;
   const int vec = (Cc % 8 == 0) && aligned16(w);
+  if constexpr (sizeof(T) <= 4) {
+    if (!trans) {
+      const int vt = (N % (16 / (int)sizeof(T)) == 0) && aligned16(w);
+      k_materialize_tiles<T><<<dim3(ceil_div(N, kMTC), ceil_div(M, kMTR)), 256, 0, st>>>(
+          M, N, static_cast<const P*>(vals), asoft, slot, n_act, max_act, static_cast<T*>(w), vt);
+      note_launch();
+      return status_from_cuda();
+    }
+  }
   auto k = trans ? k_materialize<T, true> : k_materialize<T, false>;
   k<<<ceil_div(R, kMatRows), 256, 0, st>>>(M, N, static_cast<const P*>(vals), asoft, slot, n_act, max_act,
                                            static_cast<T*>(w), vec);
