@@ -61,6 +61,15 @@ class DiagMatrix:
     offsets: torch.Tensor
     values: torch.Tensor
 
+    def __post_init__(self):
+        """DiagonalPattern's checks (diagcore.py:71-88): offsets in [0, max(M, N)),
+        no duplicates; stored ascending (values permuted with them)."""
+        offs = ops.validate_offsets(max(self.rows, self.cols), self.offsets)
+        if not torch.equal(offs, self.offsets.to(offs.dtype)):
+            order = torch.argsort(self.offsets)
+            self.values = self.values[order]
+        self.offsets = offs.to(self.offsets.dtype)
+
     def store(self) -> torch.Tensor:
         """Candidate-store layout (C, L) with zeros on unused offsets."""
         C, L = ops.geometry(self.rows, self.cols)
@@ -164,7 +173,7 @@ class DiagMMFunction(torch.autograd.Function):
         x, values, alpha = ctx.saved_tensors
         sel, spec, W = ctx.sel, ctx.spec, ctx.W
         ctx.W = None
-        d_res = dy if ctx.needs_input_grad[5] else None
+        d_res = dy if len(ctx.needs_input_grad) > 5 and ctx.needs_input_grad[5] else None
         M, N = spec.M, spec.N
         dy = dy.contiguous()
         vals = values.detach()
@@ -542,7 +551,7 @@ class DiagHeurLinear(nn.Module):
         if self.values.dtype == torch.float64:
             x2 = x2.double()
         spec = _OpSpec(self.out_features, self.in_features, self.k, 1.0, "diag", self._selection())
-        y = DiagMMFunction.apply(x2, self.values, None, self.bias, spec)
+        y = DiagMMFunction.apply(x2, self.values, None, self.bias, spec, None)
         return y.reshape(*lead, self.out_features)
 
     def param_specs(self) -> list[ParamSpec]:

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .errors import ShapeMismatch
+from .errors import DuplicateOffset, OffsetOutOfRange, ShapeMismatch
 
 _ACT_CODES = {torch.float64: _lib.F64, torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
 
@@ -183,11 +183,27 @@ def select_hard(alpha: torch.Tensor, k: int) -> torch.Tensor:
     return idx.long()
 
 
+def validate_offsets(C: int, offsets: torch.Tensor) -> torch.Tensor:
+    """DiagonalPattern's checks (diagcore.py:71-88), one host read at construction
+    time: every offset in [0, C) (OffsetOutOfRange), none twice (DuplicateOffset).
+    Returns the offsets sorted ascending (the reference stores them sorted)."""
+    h = offsets.detach().to("cpu", torch.int64).reshape(-1)
+    if h.numel() and (int(h.min()) < 0 or int(h.max()) >= C):
+        bad = int(h[(h < 0) | (h >= C)][0])
+        raise OffsetOutOfRange(f"offset {bad} outside [0, {C})")
+    s = torch.sort(h).values
+    if s.numel() > 1 and bool((s[1:] == s[:-1]).any()):
+        dup = int(s[1:][s[1:] == s[:-1]][0])
+        raise DuplicateOffset(f"offset {dup} given twice")
+    return s.to(offsets.device)
+
+
 def selection_from_offsets(C: int, offsets: torch.Tensor, alpha_soft: torch.Tensor | None = None
                            ) -> Selection:
-    """Selection for an explicit ascending offset list (DiagHeur / frozen layers)."""
+    """Selection for an explicit offset list (DiagHeur / frozen layers): validated
+    like the reference's DiagonalPattern and sorted ascending."""
     _need_cuda(offsets)
-    offs = offsets.to(torch.int32).contiguous()
+    offs = validate_offsets(C, offsets).to(torch.int32).contiguous()
     n = offs.numel()
     dev = offs.device
     sel = new_selection(C, dev, k=n)
@@ -481,6 +497,8 @@ def tc_gemm_nn(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = Non
 def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
                        need_soft: bool = True, max_act: int | None = None, need_bias: bool = False):
     """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None[, g_bias (M,) f32])."""
+    if dy.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
+        raise TypeError("tc_backward_weight takes bfloat16 dy and x (the TMA maps are bf16)")
     _check_product(dy, M, values, M, N)
     _check_product(x, N, values, M, N)
     C, L = geometry(M, N)
@@ -522,6 +540,8 @@ def tc_backward_weight_split(dy_parts: list[torch.Tensor], x: torch.Tensor, valu
     """tc_backward_weight with dy = cat(dy_parts, dim=1) read block by block (no concatenation)."""
     if not 2 <= len(dy_parts) <= 3:
         raise ValueError("tc_backward_weight_split takes 2 or 3 column blocks")
+    if any(p.dtype != torch.bfloat16 for p in dy_parts) or x.dtype != torch.bfloat16:
+        raise TypeError("tc_backward_weight_split takes bfloat16 dy blocks and x (the TMA maps are bf16)")
     B, ms = dy_parts[0].shape
     if any(p.shape != (B, ms) for p in dy_parts) or ms * len(dy_parts) != M or ms % 128:
         raise ShapeMismatch("tc_backward_weight_split: equal (B, ms) blocks with ms*len == M, ms % 128 == 0")

@@ -4,7 +4,8 @@ Bars (BASELINE.json north star): TopK offsets / masks / clamped sets and hard
 selections bit-exact; float64 instantiation at the reference's own
 tolerances (1e-12 products, 1e-10 layer gradients); float32 within 1e-5
 relative (scaled by max(1, max|ref|), bench._validate's convention); bf16
-activations within 2e-2 of the same scale (8-bit mantissa inputs, fp32
+activations within 5e-3 of the same scale against the oracle evaluated on the
+same bf16-rounded inputs (8-bit mantissa outputs and weights, fp32
 accumulation).
 """
 
@@ -25,7 +26,7 @@ if torch.cuda.is_available():
     )
 
 F32_TOL = 1e-5
-BF16_TOL = 2e-2
+BF16_TOL = 5e-3  # bf16 outputs: 2^-9 output rounding + bf16 weights, measured <= 3.2e-3 (r01 smoke)
 DEV = "cuda"
 
 
@@ -62,12 +63,21 @@ def test_products_vs_reference_golden(act):
         st = _store(M, N, offs, g[f"c{i}_values"], pdt)
         sel = ops.selection_from_offsets(max(M, N), t(offs, torch.int64))
         x = t(g[f"c{i}_X"].T.copy(), act)
-        y = ops.diag_forward(x, st, sel, M, N)
-        assert scaled_err(y.double().cpu().numpy().T, g[f"c{i}_Y"]) <= tol, (i, act)
-        # K2: dx = dy @ W equals the reference's transpose product (diagcore.py:162-191)
         dy = t(g[f"c{i}_U"].T.copy(), act)
+        y_want, dx_want = g[f"c{i}_Y"], g[f"c{i}_TU"]
+        if act == torch.bfloat16:  # the oracle on the same rounded inputs
+            vals = np.asarray(g[f"c{i}_values"], dtype=np.float64)
+            y_want = oracle.diag_spmm(M, N, [int(o) for o in offs], vals, x.double().cpu().numpy().T)
+            y_gold = oracle.diag_spmm(M, N, [int(o) for o in offs], vals, g[f"c{i}_X"])
+            assert scaled_err(y_gold, g[f"c{i}_Y"]) < 1e-12  # the oracle itself is pinned to golden
+            dx_want = olayer.diag_matmul_backward(dy.double().cpu().numpy(), x.double().cpu().numpy(),
+                                                  _store(M, N, offs, vals, torch.float64).cpu().numpy(),
+                                                  vals, offs, M, N)[0].T
+        y = ops.diag_forward(x, st, sel, M, N)
+        assert scaled_err(y.double().cpu().numpy().T, y_want) <= tol, (i, act)
+        # K2: dx = dy @ W equals the reference's transpose product (diagcore.py:162-191)
         dx = ops.diag_backward_input(dy, st, sel, M, N)
-        assert scaled_err(dx.double().cpu().numpy().T, g[f"c{i}_TU"]) <= tol, (i, act)
+        assert scaled_err(dx.double().cpu().numpy().T, dx_want) <= tol, (i, act)
         W = ops.materialize(st, sel, M, N, dtype=pdt)
         assert scaled_err(W.double().cpu().numpy(), g[f"c{i}_dense"]) <= (0 if act == torch.float64 else 1e-6)
 
@@ -884,3 +894,29 @@ def test_packed_qkv_attention_matches_sdpa():
     o2.backward(g.float())
     assert (out.float() - o2).abs().max().item() < 2e-2
     assert (h.grad.float() - h2.grad).abs().max().item() < 3e-2 * max(1.0, h2.grad.abs().max().item())
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("shape", [(64, 96), (96, 64), (80, 80)])
+def test_diagheur_forward_backward_vs_oracle(dtype, shape):
+    """DiagHeurLinear (fixed active set, no alpha) through DiagMMFunction: forward and
+    (gx, g_values) against the oracle op with alpha=None (layers.py:355-363, 143-158)."""
+    from paper_2506_11449_b200 import DiagHeurLinear
+
+    n_in, n_out = shape
+    lyr = DiagHeurLinear(n_in, n_out, 0.8, seed=4, dtype=dtype)
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((13, n_in))
+    up = rng.standard_normal((13, n_out))
+    xt = t(x, dtype).requires_grad_(True)
+    y = lyr(xt)
+    (y * t(up, dtype)).sum().backward()
+    act = lyr.active
+    vals = lyr.values.detach().double().cpu().numpy()
+    tol = 1e-10 if dtype == torch.float64 else F32_TOL
+    y_ref = olayer.diag_matmul_forward(x, vals[act], act, n_out, n_in)
+    gx, gv = olayer.diag_matmul_backward(up, x, vals, vals[act], act, n_out, n_in)
+    assert scaled_err(y.detach().cpu().numpy(), y_ref) <= tol
+    assert scaled_err(xt.grad.cpu().numpy(), gx) <= tol
+    assert scaled_err(lyr.values.grad.cpu().numpy(), gv) <= tol
+    assert scaled_err(lyr.bias.grad.cpu().numpy(), up.sum(0)) <= tol

@@ -126,3 +126,23 @@ def test_vit_patchify_equals_conv():
     img = torch.randn(3, 3, 32, 32, dtype=torch.float64)
     ref = m.patch(img).flatten(2).transpose(1, 2)
     torch.testing.assert_close(m._patchify(img), ref, rtol=1e-12, atol=1e-12)
+
+
+def test_diag_matrix_validates_offsets_like_the_reference():
+    """DiagonalPattern's checks (diagcore.py:71-88) on the device matrix type:
+    OffsetOutOfRange, DuplicateOffset, and unsorted offsets stored ascending."""
+    import torch
+
+    from paper_2506_11449_b200.errors import DuplicateOffset, OffsetOutOfRange
+    from paper_2506_11449_b200.layer import DiagMatrix
+
+    v = torch.arange(12, dtype=torch.float64).reshape(3, 4)
+    with pytest.raises(OffsetOutOfRange):
+        DiagMatrix(6, 4, torch.tensor([0, 2, 6]), v)
+    with pytest.raises(OffsetOutOfRange):
+        DiagMatrix(6, 4, torch.tensor([-1, 2, 3]), v)
+    with pytest.raises(DuplicateOffset):
+        DiagMatrix(6, 4, torch.tensor([1, 3, 1]), v)
+    m = DiagMatrix(6, 4, torch.tensor([5, 0, 2]), v)
+    assert m.offsets.tolist() == [0, 2, 5]
+    assert m.values[:, 0].tolist() == [4.0, 8.0, 0.0]
