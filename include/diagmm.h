@@ -61,6 +61,8 @@ enum diagmm_status {
 /* Library identity: "diagmm <version> sm_100a". */
 DIAGMM_API const char* diagmm_version(void);
 DIAGMM_API const char* diagmm_status_string(int status);
+/* The CUDA runtime's message for the last DIAGMM_ECUDA returned on this host thread. */
+DIAGMM_API const char* diagmm_last_error(void);
 /* Kernels launched by this library since load (for launch accounting). */
 DIAGMM_API unsigned long long diagmm_launch_count(void);
 

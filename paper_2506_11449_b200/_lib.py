@@ -23,6 +23,7 @@ _vp, _i, _d, _sz = C.c_void_p, C.c_int, C.c_double, C.c_size_t
 SIGNATURES = {
     "diagmm_version": (C.c_char_p, []),
     "diagmm_status_string": (C.c_char_p, [_i]),
+    "diagmm_last_error": (C.c_char_p, []),
     "diagmm_launch_count": (C.c_ulonglong, []),
     "diagmm_forward_workspace": (_sz, [_i, _i, _i, _i, _i]),
     "diagmm_forward": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
@@ -113,6 +114,8 @@ def check(status: int, what: str) -> None:
         return
     lib = load()
     msg = lib.diagmm_status_string(status).decode()
+    if status == 6:  # DIAGMM_ECUDA: name the CUDA error behind it
+        msg += f" ({lib.diagmm_last_error().decode()})"
     exc = STATUS_EXCEPTIONS.get(status, NativeLibraryError)
     raise exc(f"{what}: {msg}")
 

@@ -76,6 +76,8 @@ extern "C" {
 
 const char* diagmm_version(void) { return "diagmm 0.1.0 sm_100a"; }
 
+const char* diagmm_last_error(void) { return diagmm::last_cuda_error(); }
+
 unsigned long long diagmm_launch_count(void) { return g_launches.load(); }
 
 const char* diagmm_status_string(int status) {

@@ -85,9 +85,17 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// the CUDA error behind the last DIAGMM_ECUDA of this host thread (diagmm_last_error)
+inline const char*& last_cuda_error() {
+  static thread_local const char* msg = "no error";
+  return msg;
+}
+
 inline int status_from_cuda() {
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? DIAGMM_OK : DIAGMM_ECUDA;
+  if (e == cudaSuccess) return DIAGMM_OK;
+  last_cuda_error() = cudaGetErrorString(e);
+  return DIAGMM_ECUDA;
 }
 
 inline int num_sms() {

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "tc_gemm.cuh"
@@ -773,17 +774,44 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled with the failure recorded for diagmm_last_error()
+static bool encode_2d(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[2], const cuuint64_t (&strides)[1],
+                      const cuuint32_t (&box)[2], CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) {
+    last_cuda_error() = "cuTensorMapEncodeTiled entry point unavailable";
+    return false;
+  }
+  // the driver call needs the device's context current on THIS host thread (autograd
+  // runs backward on its own thread; before its first runtime call nothing is bound)
+  static thread_local bool bound = false;
+  if (!bound) {
+    cudaFree(nullptr);
+    bound = true;
+  }
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    static thread_local char msg[256];
+    snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled=%d base=%p dims=(%llu,%llu) stride=%llu box=(%u,%u)", (int)r,
+             base, (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)strides[0], box[0],
+             box[1]);
+    last_cuda_error() = msg;
+    return false;
+  }
+  return true;
+}
+
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                     uint64_t ld) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  return encode_2d(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // MN-major staging of a (rows = K, cols = N) row-major matrix: boxes of 64
@@ -791,13 +819,10 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 bool make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)BK};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  return encode_2d(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace tc
@@ -866,13 +891,10 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
   CUtensorMap ta, tb;
   // MN-major boxes: 64 features (contiguous) x 64 tokens
   auto mk = [&](CUtensorMap* map, const void* base, uint64_t cols) {
-    cuuint64_t dims[2] = {cols, (cuuint64_t)ntok};
-    cuuint64_t strides[1] = {cols * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)BK};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const cuuint64_t dims[2] = {cols, (cuuint64_t)ntok};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)BK};
+    return encode_2d(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
   };
   CUtensorMap ta1, ta2;
   if (a_ms) {  // dy given as column blocks of a_ms (a multiple of 128) in 2 or 3 separate matrices

@@ -100,6 +100,42 @@ def _n_act(args, name, nact_of):
     return nact_of.get((M, N)) if nact_of else None
 
 
+TC_FORWARD = ("diagmm_tc_gemm_bf16", "diagmm_tc_gemm_bf16_ex")
+TC_PRODUCTS = TC_FORWARD + ("diagmm_tc_gemm_bf16_nn", "diagmm_tc_gemm_bf16_nn_split")
+TC_DW = ("diagmm_tc_backward_weight", "diagmm_tc_backward_weight_split")
+
+
+def tc_layer_shape(name, args):
+    """(M, N) of the DiagLinear layer a tensor-core call belongs to: the forward
+    GEMM is (tokens x M) = (tokens x N) W_K^T, the input gradient (tokens x N) =
+    (tokens x M) W_K, dW takes (M, N) directly."""
+    if name in TC_DW:
+        return args[0], args[1]
+    Md, Nd, K = args[0], args[1], args[2]
+    return (Nd, K) if name in TC_FORWARD else (K, Nd)
+
+
+def tc_work(name, args, nact_of=None, dense_equivalent=False):
+    """(flops, bytes) of one tensor-core call.  Default: SURVEY §8(d)'s algorithmic
+    work of the DiagLinear op the call implements — 2 nnz B FLOP with nnz = n_act L,
+    bytes s B (M + N) + s_w nnz (+ the fused epilogue's extra (B x M) tensor, + the
+    full fp32 candidate gradient C L written by dW).  ``dense_equivalent``: the
+    dense GEMM the tensor cores actually execute (2 M N B) — reported separately,
+    never as the roofline."""
+    M, N = tc_layer_shape(name, args)
+    C, L = max(M, N), min(M, N)
+    if name in TC_DW:
+        B = args[2]
+        n = (nact_of or {}).get((M, N), C)
+        flops = 2.0 * (M * N if dense_equivalent else n * L) * B
+        return flops, 2.0 * B * (M + N) + 4.0 * C * L + 4.0 * n * L
+    B = args[0]
+    n = (nact_of or {}).get((M, N), C)
+    aux = 2.0 * B * args[1] if name in ("diagmm_tc_gemm_bf16_ex", "diagmm_tc_gemm_bf16_nn") and args[9] else 0.0
+    flops = 2.0 * (M * N if dense_equivalent else n * L) * B
+    return flops, 2.0 * B * (M + N) + 2.0 * n * L + 8.0 * n + aux
+
+
 def work(name, args, nact_of=None):
     """(flops, bytes) of one call, or None when not modelled."""
     if name in ("diagmm_forward", "diagmm_backward_input", "diagmm_backward_weight"):
@@ -123,14 +159,8 @@ def work(name, args, nact_of=None):
         n = _n_act(args, name, nact_of) or max(M, N)
         p = 8 if dt == 0 else 4
         return 0.0, p * n * min(M, N) * 2 + p * max(M, N) * min(M, N)
-    if name in ("diagmm_tc_gemm_bf16", "diagmm_tc_gemm_bf16_ex", "diagmm_tc_gemm_bf16_nn",
-                "diagmm_tc_gemm_bf16_nn_split"):  # dense-equivalent tensor-core product: 2 M N K flop
-        Md, Nd, K = args[0], args[1], args[2]
-        aux = 2.0 * Md * Nd if name in ("diagmm_tc_gemm_bf16_ex", "diagmm_tc_gemm_bf16_nn") and args[9] else 0.0
-        return 2.0 * Md * Nd * K, 2.0 * (Md * K + Nd * K + Md * Nd) + aux
-    if name in ("diagmm_tc_backward_weight", "diagmm_tc_backward_weight_split"):
-        M, N, B = args[0], args[1], args[2]
-        return 2.0 * M * N * B, 2.0 * B * (M + N) + 4.0 * max(M, N) * min(M, N)
+    if name in TC_PRODUCTS or name in TC_DW:
+        return tc_work(name, args, nact_of)
     if name == "diagmm_adamw_multi":
         n, descs = args[0], args[1]
         return 0.0, float(sum(7 * (8 if descs[i].dtype == 0 else 4) * descs[i].n for i in range(n)))
@@ -173,14 +203,28 @@ def roofline(records, peaks: dict, peaks_kind: str, fma_tflops: float, nact_of=N
     sec = tot_ms / 1e3
     hbm = float(peaks["hbm_gbs"])
     name = family(name)
-    if name.startswith("diagmm_tc_"):  # tensor-core kernels: dense bf16 tcgen05 peak, sustained (inside a step)
+    if name.startswith("diagmm_tc_"):
+        # tensor-core family: the roofline is SURVEY §8(d)'s algorithmic work (2 nnz B
+        # FLOP at the bf16 tensor peak vs the algorithmic bytes at HBM bandwidth); the
+        # dense-equivalent rate the tensor cores run at is reported beside it
         tpk = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
-        achieved = tot_f / sec / 1e12
-        if tot_f / (tpk * 1e12) >= tot_b / (hbm * 1e9):
-            return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s",
-                    "frac": achieved / tpk, "traffic": None, "launches": n, "avg_launch_us": tot_ms * 1e3 / n,
-                    "algorithmic_flops_per_launch": tot_f / n, "algorithmic_bytes_per_launch": tot_b / n,
+        dense_f = sum(tc_work(nm, a, nact_of, dense_equivalent=True)[0] for nm, a, _, _ in records)
+        t_tc, t_hbm = tot_f / (tpk * 1e12), tot_b / (hbm * 1e9)
+        common = {"kernel": name, "traffic": None, "launches": n, "avg_launch_us": tot_ms * 1e3 / n,
+                  "algorithmic_flops_per_launch": tot_f / n, "algorithmic_bytes_per_launch": tot_b / n,
+                  "work_model": "SURVEY 8(d): 2*n_act*L*B FLOP; s*B*(M+N) + s_w*nnz (+ fused epilogue tensor) bytes",
+                  "dense_equivalent": {"flops_per_launch": dense_f / n, "tflops": dense_f / sec / 1e12,
+                                       "frac_of_bf16_peak": dense_f / sec / 1e12 / tpk,
+                                       "note": "the dense GEMM the tcgen05 route executes (W_K materialized); "
+                                               "not the roofline"}}
+        if t_tc >= t_hbm:
+            achieved = tot_f / sec / 1e12
+            return {**common, "bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s",
+                    "frac": achieved / tpk,
                     "peak_source": f"{peaks_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)"}
+        achieved = tot_b / sec / 1e9
+        return {**common, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": f"{peaks_kind} hbm_gbs (MEASURED_PEAKS.json)"}
     t_fma = tot_f / (fma_tflops * 1e12)
     t_hbm = tot_b / (hbm * 1e9)
     if t_fma > t_hbm:
