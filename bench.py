@@ -79,7 +79,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -124,7 +124,39 @@ def vit_layer_shapes(model: str):
     return cfg, per_block * cfg.depth
 
 
-def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int):
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+class _Threads:
+    """Limit BLAS / OpenMP threads of the numpy oracle (threadpoolctl) for the 1-core run."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def __enter__(self):
+        try:
+            from threadpoolctl import threadpool_limits
+
+            self.ctx = threadpool_limits(limits=self.n)
+        except ImportError:  # pragma: no cover
+            self.ctx = None
+        return self
+
+    def __exit__(self, *a):
+        if self.ctx is not None:
+            self.ctx.restore_original_limits()
+
+
+def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int, threads: int | None = None):
     """The reference's CPU DiagLinear path (oracle port, float64) on a bounded sample:
     ``images`` images' tokens through every DiagLinear layer of the model, one
     training step each (forward, backward + l1, clip, AdamW) in the post-anneal
@@ -148,16 +180,55 @@ def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int)
         for lyr, st, shp in zip(layers, states, shapes):
             olayer.layer_train_step(lyr, xs[shp], ups[shp], step, st)
 
-    for s in range(warmup):
-        one_step(s)
-    times = []
-    for s in range(steps):
-        t0 = time.perf_counter()
-        one_step(warmup + s)
-        times.append(time.perf_counter() - t0)
+    cores = threads or len(os.sched_getaffinity(0))
+    with _Threads(cores):
+        for s in range(warmup):
+            one_step(s)
+        times = []
+        for s in range(steps):
+            t0 = time.perf_counter()
+            one_step(warmup + s)
+            times.append(time.perf_counter() - t0)
     sec = statistics.median(times)
-    cores = len(os.sched_getaffinity(0))
     return images / sec, sec, cores, tokens
+
+
+def cpu_config1_ms(threads: int, reps: int = 3):
+    """BASELINE config 1 on the reference's CPU algorithm (oracle port, float64):
+    DiagLinear 768 -> 3072 at 90 %, batch 256, forward + backward + TopK update +
+    clip + AdamW (layer_train_step), median of ``reps`` after one warm-up."""
+    import numpy as np
+
+    from oracle import layer as olayer  # checker / CPU baseline only
+
+    rng = np.random.default_rng(0)
+    lyr = olayer.OracleDiagLayer(768, 3072, 0.9, t_kind="constant", t_init=1e-3, t_final=1e-3, t_total=1,
+                                 l1_coeff=1e-4, seed=0)
+    lyr.alpha = lyr.alpha + rng.standard_normal(lyr.C)
+    x, up = rng.standard_normal((256, 768)), rng.standard_normal((256, 3072))
+    st: dict = {}
+    with _Threads(threads):
+        olayer.layer_train_step(lyr, x, up, 0, st)
+        ts = []
+        for i in range(reps):
+            t0 = time.perf_counter()
+            olayer.layer_train_step(lyr, x, up, i + 1, st)
+            ts.append(time.perf_counter() - t0)
+    return statistics.median(ts) * 1e3
+
+
+def cpu_baseline_block(model: str, images: int):
+    """cpu_baseline for the bench line: all host cores and 1 core."""
+    allc = len(os.sched_getaffinity(0))
+    ips_all, sec_all, _, tokens = cpu_reference_images_per_s(model, images, 1, 1, threads=allc)
+    ips_one, sec_one, _, _ = cpu_reference_images_per_s(model, images, 1, 0, threads=1)
+    return {"value": ips_all, "unit": UNIT, "cores": allc, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"{images} image(s) = {tokens} tokens through all DiagLinear layers of {model} (fwd + bwd + "
+                      f"l1 + clip + AdamW, float64 oracle of the reference algorithm, post-anneal T = 1e-9); "
+                      f"attention, LayerNorm, patch embedding and head are NOT timed",
+            "all_cores": {"value": ips_all, "cores": allc, "sec_per_sample": sec_all},
+            "one_core": {"value": ips_one, "cores": 1, "sec_per_sample": sec_one}}
 
 
 def run_reference(args):
@@ -171,32 +242,238 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers (48) training step, CPU oracle port",
+        "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers training step, CPU oracle port",
                    "global_batch": args.cpu_sample_images, "seq_len": tokens // max(1, args.cpu_sample_images),
                    "parallelism": "none (host threads via BLAS)"},
-        "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{args.cpu_sample_images} image(s) = {tokens} tokens through all DiagLinear "
-                                   f"layers (fwd+bwd+clip+AdamW), float64, median of {steps}"},
+                                   f"layers (fwd+bwd+clip+AdamW), float64, median of {steps}; attention / LayerNorm "
+                                   f"not timed"},
         "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm
+class TrainHarness:
+    """One model's training step (forward, backward, DP all-reduce, clip, AdamW)
+    on a fixed synthetic batch, with CUDA-graph capture of forward + backward."""
+
+    def __init__(self, model, batch, dev, world, args):
+        import torch
+
+        from paper_2506_11449_b200 import AdamW, GlobalNormClipper, model_param_specs
+        from paper_2506_11449_b200.dp import GradientAllReducer, broadcast_parameters
+
+        self.model, self.dev, self.world, self.args = model, dev, world, args
+        broadcast_parameters(model)  # identical replicas
+        self.specs = model_param_specs(model)
+        self.opt = AdamW(self.specs, lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
+        self.clip = GlobalNormClipper(1.0)
+        self.inputs, self.labels = batch
+        self.allreduce = GradientAllReducer([s.tensor for s in self.specs])
+        self.graph = None
+        self.graph_note = "off"
+        self.step_no = 0
+        self._torch = torch
+
+    def fwd_bwd(self, step, inp, lbl):
+        import torch.nn.functional as F
+
+        from paper_2506_11449_b200 import penalties
+
+        torch = self._torch
+        if hasattr(self.model, "set_step"):
+            self.model.set_step(step)
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+            logits = self.model(inp)
+        loss = F.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), lbl.reshape(-1), label_smoothing=0.1)
+        for pen in penalties(self.model, fused=True):  # l1 gradient folded into K5
+            loss = loss + pen
+        loss.backward()
+        return loss
+
+    def update(self):
+        if self.world > 1:
+            self.allreduce()
+        _, scale = self.clip.compute(self.specs)
+        self.opt.step(clip_scale=scale)
+
+    def train_step(self, inp=None, lbl=None):
+        inp = self.inputs if inp is None else inp
+        lbl = self.labels if lbl is None else lbl
+        if self.graph is not None:
+            loss = self.graph.step(inp, lbl)  # inputs copied into the captured buffers, replay
+            self.update()  # clip + AdamW eager: the Adam step count / bias corrections change every step
+        else:
+            loss = self.fwd_bwd(self.step_no, inp, lbl)
+            self.update()
+            self.opt.zero_grad()
+        self.step_no += 1
+        return loss
+
+    def warm(self, n):
+        for _ in range(n):
+            self.train_step()
+        self._torch.cuda.synchronize()
+
+    def capture(self, mode="auto"):
+        from paper_2506_11449_b200.graphed import GraphedStep, schedules_constant
+
+        if not (mode == "on" or (mode == "auto" and schedules_constant(self.model))):
+            return self.graph_note
+        step = self.step_no
+        try:
+            self.graph = GraphedStep(lambda i, l: self.fwd_bwd(step, i, l), [s_.tensor for s_ in self.specs],
+                                     self.inputs, self.labels)
+            self.graph_note = "forward+backward replayed as one CUDA graph; clip + AdamW eager"
+        except Exception as exc:  # noqa: BLE001 - a capture failure must not cost the measurement
+            if mode == "on":
+                raise
+            self.graph = None
+            self.opt.zero_grad()
+            self._torch.cuda.synchronize()
+            self.graph_note = f"capture failed ({type(exc).__name__}), eager steps"
+        for _ in range(2):
+            self.train_step()
+        return self.graph_note
+
+    def timed(self, steps, sampler=None):
+        """Device time per step (ms) over ``steps`` steps, max over ranks; launches of our kernels."""
+        from paper_2506_11449_b200 import _lib
+
+        torch = self._torch
+        barrier(self.world)
+        torch.cuda.synchronize()
+        l0 = _lib.load().diagmm_launch_count()
+        stream = torch.cuda.current_stream(self.dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            s.record(stream)
+            for _ in range(steps):
+                self.train_step()
+            e.record(stream)
+            torch.cuda.synchronize()
+        barrier(self.world)
+        launches = _lib.load().diagmm_launch_count() - l0 + (steps * self.graph.launches if self.graph else 0)
+        return max_over_ranks(s.elapsed_time(e) / steps, self.world, self.dev), int(launches)
+
+    def e2e(self, steps):
+        """The same step through the public API with host buffers: every step's inputs
+        go host->device from pinned memory on a copy stream (prefetched one step ahead
+        into a double buffer) and every step's loss comes back device->host (pinned,
+        non-blocking; read one step later), so the copies overlap compute instead of
+        draining the pipeline.  The timed region (wall clock and device events) covers
+        all copies of all steps."""
+        torch = self._torch
+        inputs, labels, dev = self.inputs, self.labels, self.dev
+        h_in = [inputs.cpu().pin_memory() for _ in range(2)]
+        h_lb = [labels.cpu().pin_memory() for _ in range(2)]
+        d_in = [torch.empty_like(inputs) for _ in range(2)]
+        d_lb = [torch.empty_like(labels) for _ in range(2)]
+        h_loss = torch.empty(steps, dtype=torch.float32, pin_memory=True)
+        copy_stream = torch.cuda.Stream(dev)
+        stream = torch.cuda.current_stream(dev)
+        ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        loss_evt = [torch.cuda.Event() for _ in range(steps)]
+
+        def h2d(i):
+            b = i % 2
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(done[b])  # the step that used this buffer has finished
+                d_in[b].copy_(h_in[b], non_blocking=True)
+                d_lb[b].copy_(h_lb[b], non_blocking=True)
+                ready[b].record(copy_stream)
+
+        barrier(self.world)
+        torch.cuda.synchronize()
+        for ev in done:
+            ev.record(stream)
+        t0 = time.perf_counter()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record(stream)
+        h2d(0)
+        losses = []
+        for i in range(steps):
+            b = i % 2
+            stream.wait_event(ready[b])
+            if i + 1 < steps:
+                h2d(i + 1)
+            loss = self.train_step(d_in[b], d_lb[b])
+            done[b].record(stream)
+            h_loss[i].copy_(loss.detach().float(), non_blocking=True)  # D2H of the step's result
+            loss_evt[i].record(stream)
+            if i > 0:
+                loss_evt[i - 1].synchronize()
+                losses.append(float(h_loss[i - 1]))
+        loss_evt[-1].synchronize()
+        losses.append(float(h_loss[steps - 1]))
+        ee.record(stream)
+        torch.cuda.synchronize()
+        assert all(v == v for v in losses), "non-finite loss"
+        ms = max_over_ranks(es.elapsed_time(ee) / steps, self.world, dev)
+        wall = max_over_ranks((time.perf_counter() - t0) * 1e3 / steps, self.world, dev)
+        h2d_bytes = inputs.numel() * inputs.element_size() + labels.numel() * labels.element_size()
+        return max(ms, wall), h2d_bytes
+
+    def release(self):
+        self.graph = None
+        self.opt = None
+        self.specs = None
+        self.model = None
+        self._torch.cuda.synchronize()
+        self._torch.cuda.empty_cache()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_batch(cfg, B, dev, rank):
+    import torch
+
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    images = torch.randn(B, 3, cfg.image, cfg.image, device=dev, generator=g).to(torch.bfloat16)
+    labels = torch.randint(0, cfg.classes, (B,), device=dev, generator=g)
+    return images, labels
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
 
-    import numpy as np
+    import dataclasses
+
     import torch
     import torch.distributed as dist
-    import torch.nn.functional as F
 
-    from paper_2506_11449_b200 import AdamW, GlobalNormClipper, _lib, model_param_specs, penalties
     from paper_2506_11449_b200 import profiling
-    from paper_2506_11449_b200.graphed import GraphedStep, schedules_constant
     from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16, ViT
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,72 +491,17 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    torch.backends.cuda.matmul.allow_tf32 = True
-    torch.backends.cudnn.allow_tf32 = True
 
     cfg = VIT_B16 if args.model == "vit_b16" else VIT_TINY16
     torch.manual_seed(1234)  # dense params; DiagLinear init is seeded per layer (numpy stream)
     model = ViT(cfg, route=args.route, device=dev)
-    from paper_2506_11449_b200.dp import GradientAllReducer, broadcast_parameters
-
-    broadcast_parameters(model)  # identical replicas
-    specs = model_param_specs(model)
-    opt = AdamW(specs, lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
-    clip = GlobalNormClipper(1.0)
     B = args.batch
-    g = torch.Generator(device=dev).manual_seed(100 + rank)
-    images = torch.randn(B, 3, cfg.image, cfg.image, device=dev, generator=g).to(torch.bfloat16)
-    labels = torch.randint(0, cfg.classes, (B,), device=dev, generator=g)
-    allreduce_grads = GradientAllReducer([s.tensor for s in specs])
+    h = TrainHarness(model, make_batch(cfg, B, dev, rank), dev, world, args)
 
-    def fwd_bwd(step, imgs, lbls):
-        model.set_step(step)
-        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
-            logits = model(imgs)
-        loss = F.cross_entropy(logits.float(), lbls, label_smoothing=0.1)
-        for pen in penalties(model, fused=True):  # l1 gradient folded into K5
-            loss = loss + pen
-        loss.backward()
-        return loss
-
-    def update():
-        if world > 1:
-            allreduce_grads()
-        _, scale = clip.compute(specs)
-        opt.step(clip_scale=scale)
-
-    graph = {}  # {"g": GraphedStep} once forward + backward are captured
-
-    def train_step(step, imgs, lbls):
-        if graph:
-            loss = graph["g"].step(imgs, lbls)  # inputs copied into the captured buffers, replay
-            update()  # clip + AdamW eager: the Adam step count / bias corrections change every step
-            return loss
-        loss = fwd_bwd(step, imgs, lbls)
-        update()
-        opt.zero_grad()
-        return loss
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    step = 0
     # warm-up (also profiles every C-ABI call once to find our dominant kernel)
-    for _ in range(max(args.warmup, 3)):
-        train_step(step, images, labels)
-        step += 1
-    torch.cuda.synchronize()
+    h.warm(max(args.warmup, 3))
     with profiling.CallTimer() as prof:
-        train_step(step, images, labels)
-        step += 1
+        h.train_step()
     torch.cuda.synchronize()
     per_fn = prof.totals_ms()
     # dominant = the C-ABI function (our kernels) with the most device time in a
@@ -292,108 +514,24 @@ def main():
             cands[profiling.family(k)] = cands.get(profiling.family(k), 0.0) + v
     dominant = max(cands, key=cands.get) if cands else None
     dominant_fns = {k for k in per_fn if profiling.family(k) == dominant} if dominant else None
-
     # roofline of the dominant kernel family: CUDA events around each of its C-ABI calls
     # over args.steps eager steps of this run (inside a graph replay there are no
     # per-call events; the kernels and shapes are the same)
     with profiling.CallTimer(only=dominant_fns) as dom_timer:
         for _ in range(args.steps):
-            train_step(step, images, labels)
-            step += 1
+            h.train_step()
         torch.cuda.synchronize()
-    graph_note = "off"
-    if args.graph == "on" or (args.graph == "auto" and schedules_constant(model)):
-        try:
-            graph["g"] = GraphedStep(lambda i, l: fwd_bwd(step, i, l), [s_.tensor for s_ in specs], images, labels)
-            graph_note = "forward+backward replayed as one CUDA graph; clip + AdamW eager"
-        except Exception as exc:  # noqa: BLE001 - a capture failure must not cost the measurement
-            if args.graph == "on":
-                raise
-            graph.clear()
-            opt.zero_grad()
-            torch.cuda.synchronize()
-            graph_note = f"capture failed ({type(exc).__name__}), eager steps"
-        for _ in range(2):
-            train_step(step, images, labels)
-            step += 1
+    graph_note = h.capture(args.graph)
 
-    # ---- timed region: inputs resident in HBM
-    barrier()
-    torch.cuda.synchronize()
-    launches0 = _lib.load().diagmm_launch_count()
-    stream = torch.cuda.current_stream(dev)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---- timed region: inputs resident in HBM (clocks sampled every 100 ms during it
+    # and during the e2e steps that follow)
     with ClockSampler(local) as clocks:
-        start.record(stream)
-        for _ in range(args.steps):
-            train_step(step, images, labels)
-            step += 1
-        end.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    # our kernel launches in the timed region: the eager ones (clip, AdamW) counted at
-    # launch, plus the captured ones once per replay
-    launches = _lib.load().diagmm_launch_count() - launches0 + (args.steps * graph["g"].launches if graph else 0)
-    ms = start.elapsed_time(end) / args.steps
-    ms = max_over_ranks(ms)
+        ms, launches = h.timed(args.steps, None)
+        e2e_steps = max(3, min(args.steps, 6))
+        e2e_ms, h2d_bytes = h.e2e(e2e_steps)
     value = world * B / (ms / 1e3)
-
-    # ---- e2e: through the public API with host buffers, the way a training loop
-    # feeds it: every step's images/labels go host->device from pinned memory on a
-    # copy stream (prefetched one step ahead into a double buffer) and every step's
-    # loss comes back device->host (pinned, non-blocking; read one step later), so
-    # the copies overlap compute instead of draining the pipeline.  The timed region
-    # (wall clock and device events) covers all copies of all e2e steps.
-    e2e_steps = max(3, min(args.steps, 6))
-    h_images = [images.cpu().pin_memory() for _ in range(2)]
-    h_labels = [labels.cpu().pin_memory() for _ in range(2)]
-    d_images = [torch.empty_like(images) for _ in range(2)]
-    d_labels = [torch.empty_like(labels) for _ in range(2)]
-    h_loss = torch.empty(e2e_steps, dtype=torch.float32, pin_memory=True)
-    copy_stream = torch.cuda.Stream(dev)
-    ready = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
-    loss_evt = [torch.cuda.Event() for _ in range(e2e_steps)]
-
-    def h2d(i):
-        b = i % 2
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(done[b])  # the step that used this buffer has finished
-            d_images[b].copy_(h_images[b], non_blocking=True)
-            d_labels[b].copy_(h_labels[b], non_blocking=True)
-            ready[b].record(copy_stream)
-
-    barrier()
-    torch.cuda.synchronize()
-    for e in done:
-        e.record(stream)
-    t0 = time.perf_counter()
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_start.record(stream)
-    h2d(0)
-    losses = []
-    for i in range(e2e_steps):
-        b = i % 2
-        stream.wait_event(ready[b])
-        if i + 1 < e2e_steps:
-            h2d(i + 1)
-        loss = train_step(step, d_images[b], d_labels[b])
-        done[b].record(stream)
-        step += 1
-        h_loss[i].copy_(loss.detach().float(), non_blocking=True)  # D2H of the step's result
-        loss_evt[i].record(stream)
-        if i > 0:
-            loss_evt[i - 1].synchronize()
-            losses.append(float(h_loss[i - 1]))
-    loss_evt[-1].synchronize()
-    losses.append(float(h_loss[e2e_steps - 1]))
-    e_end.record(stream)
-    torch.cuda.synchronize()
-    assert all(v == v for v in losses), "non-finite loss"
-    e2e_ms = max_over_ranks(e_start.elapsed_time(e_end) / e2e_steps)
-    e2e_wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
-    e2e_value = world * B / (max(e2e_ms, e2e_wall_ms) / 1e3)
-    h2d_bytes = images.numel() * images.element_size() + labels.numel() * labels.element_size()
+    clock_summary = clocks.summary()
+    e2e_value = world * B / (e2e_ms / 1e3)
 
     peaks, peaks_kind = load_peaks()
     nact_of = {(m.out_features, m.in_features): m.k for m in model.diag_layers()}
@@ -404,22 +542,27 @@ def main():
         roof["entry_points"] = sorted(dominant_fns)
         roof["scope"] = ("dominant SURVEY §8 kernel family (all its C-ABI entry points), CUDA events on its "
                          "stream around each call, over --steps eager steps of this run (the timed steps "
-                         "replay the same kernels as one CUDA graph)" if graph else
-                         "dominant SURVEY §8 kernel family (all its C-ABI entry points) of the timed step, "
-                         "CUDA events on its stream")
+                         "replay the same kernels as one CUDA graph); n_act = K (post-anneal T = 1e-9)")
 
     extras = {}
     if not args.no_extras and rank == 0:
-        extras["infer"] = infer_images_per_s(model, images, args, dev)
-        extras["diagmm"] = diagmm_kernel_section(peaks, peaks_kind)
+        extras["infer"] = infer_images_per_s(model, h.inputs, args, dev)
         extras["routes"] = {"bench_route": args.route, "step_ms_by_fn": {k: round(v, 4) for k, v in per_fn.items()}}
+    inputs = h.inputs
+    h.release()
+    del model
+    if not args.no_extras and rank == 0 and world == 1:
+        extras["dense"] = dense_arms(cfg, inputs, h.labels, args, dev, value, extras.get("infer"))
+        extras["diagmm"] = diagmm_kernel_section(peaks, peaks_kind)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ips, sec, cores, tokens = cpu_reference_images_per_s(args.model, args.cpu_sample_images, 1, 1)
-        cpu = {"value": ips, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{args.cpu_sample_images} image(s) = {tokens} tokens through all 48 DiagLinear layers "
-                         f"(fwd+bwd+clip+AdamW, float64 oracle), {sec:.1f} s; attention/LN not timed"}
+        cpu = cpu_baseline_block(args.model, args.cpu_sample_images)
+        if "diagmm" in extras:
+            c1 = extras["diagmm"]["config1"]
+            c1["cpu_reference_ms"] = {"one_core": cpu_config1_ms(1),
+                                      "all_cores": cpu_config1_ms(len(os.sched_getaffinity(0))),
+                                      "what": "oracle layer_train_step (fwd + bwd + TopK + clip + AdamW), float64"}
 
     if rank == 0:
         line = {
@@ -433,18 +576,77 @@ def main():
                        "l2": "per-step working set (activations, candidate stores) >> 126 MB L2; no explicit flush",
                        "step": graph_note},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4,
-                    "ms_per_step": max(e2e_ms, e2e_wall_ms),
+                    "ms_per_step": e2e_ms,
                     "how": "pinned H2D of every step's images+labels on a copy stream (1-step prefetch) and a "
                            "non-blocking D2H of every step's loss, all inside the timed region"},
             "gpu_launches": int(launches),
             "roofline": roof,
             "cpu_baseline": cpu,
-            "clocks": clocks.summary(),
+            "clocks": clock_summary,
         }
         line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dense_arms(cfg, inputs, labels, args, dev, sparse_train_ips, sparse_infer):
+    """The paper's headline comparison (reference bench.py:72-150):
+    the same ViT with dense projections — nn.Linear (cuBLAS bf16 under autocast) and
+    TCLinear (the repo's tcgen05 GEMM on dense weights) — same step (graphed forward
+    + backward, clip, AdamW), same batch; plus the dense forward for inference."""
+    import dataclasses
+
+    import torch
+
+    from paper_2506_11449_b200.vit import ViT
+
+    out = {}
+    for kind in ("cublas", "tc"):
+        torch.manual_seed(1234)
+        model = ViT(dataclasses.replace(cfg, dense=kind), device=dev)
+        h = TrainHarness(model, (inputs, labels), dev, 1, args)
+        h.warm(3)
+        note = h.capture(args.graph if args.graph != "auto" else "on")
+        ms, _ = h.timed(args.steps)
+        inf = infer_dense(model, inputs, dev)
+        out[kind] = {"train_images_per_s": inputs.shape[0] / (ms / 1e3), "train_ms_per_step": ms, "step": note,
+                     "infer_images_per_s": inf["value"], "infer_ms_per_batch": inf["ms_per_batch"]}
+        h.release()
+        del model
+    ref = out["cublas"]
+    out["train_speedup_vs_dense"] = sparse_train_ips / ref["train_images_per_s"]
+    if sparse_infer:
+        out["infer_speedup_vs_dense"] = sparse_infer["value"] / ref["infer_images_per_s"]
+    out["note"] = ("speedups: this line's 90%-sparse value / the nn.Linear (cuBLAS bf16) dense ViT; 'tc' is the "
+                   "same dense model on our tcgen05 GEMM (dW on cuBLAS)")
+    return out
+
+
+def _graph_forward_ms(model, inputs, reps=5):
+    import torch
+
+    with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+        for _ in range(3):
+            model(inputs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            model(inputs)
+        g.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            g.replay()
+        e.record()
+        torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def infer_dense(model, inputs, dev):
+    ms = _graph_forward_ms(model, inputs)
+    return {"value": inputs.shape[0] / (ms / 1e3), "ms_per_batch": ms}
 
 
 def infer_images_per_s(model, images, args, dev):
@@ -475,24 +677,8 @@ def infer_images_per_s(model, images, args, dev):
             for parent, attr, mod in self.saved:
                 setattr(parent, attr, mod)
 
-    with _Swap(), torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
-        for _ in range(3):
-            model(images)
-        torch.cuda.synchronize()
-        # the forward replayed as one CUDA graph (frozen weights: every argument is static)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            model(images)
-        g.replay()
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 5
-        s.record()
-        for _ in range(reps):
-            g.replay()
-        e.record()
-        torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / reps
+    with _Swap():
+        ms = _graph_forward_ms(model, images)
     _ = FrozenDiagLinear
     return {"value": images.shape[0] / (ms / 1e3), "unit": "images/s", "ms_per_batch": ms,
             "route": "frozen (hard top-K, α̃ baked in), tensor-core route, GELU + residual fused in the epilogues, "

@@ -344,10 +344,52 @@ def diag_case(M, N, B, sparsity, act_dtype, peaks, fma_tflops, seed=0, reps=20, 
     return res
 
 
+def layer_step_case(n_in=768, n_out=3072, B=256, T=1e-3, reps=20, flush=None):
+    """BASELINE config 1 as the reference times it: one DiagLinear step — soft TopK
+    re-selection (K4), forward, backward (dX, dW, g_values / g_soft, K5 + l1) — through
+    the public module (eager autograd), float32, device time per step (CUDA events
+    around each step, L2 flushed before each; median)."""
+    import numpy as np
+
+    from .layer import DiagLinear
+    from .selection import TemperatureSchedule
+
+    lyr = DiagLinear(n_in, n_out, 0.9, seed=0, dtype=torch.float32,
+                     t_schedule=TemperatureSchedule("constant", T, T, 1))
+    rng = np.random.default_rng(0)
+    with torch.no_grad():
+        lyr.alpha.add_(torch.as_tensor(rng.standard_normal(lyr.candidates), device="cuda"))
+    x = torch.randn(B, n_in, device="cuda", requires_grad=True)
+    dy = torch.randn(B, n_out, device="cuda")
+    sink = torch.empty(1, device="cuda")
+
+    def step():
+        lyr.values.grad = lyr.alpha.grad = lyr.bias.grad = x.grad = None
+        lyr(x, step=0).backward(dy)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            torch.amax(flush, dim=0, keepdim=True, out=sink)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        step()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return {"us": ts[len(ts) // 2] * 1e3, "n_act": lyr.active_count(0), "k": lyr.k, "T": T,
+            "what": "K4 + fwd + dX + dW + K5 through DiagLinear (eager autograd), fp32, B=256"}
+
+
 def diagmm_config1(peaks, peaks_kind, fma_tflops):
     """BASELINE config 1 (DiagLinear 768->3072, 90%, B=256, fp32) + a few sweep points."""
     flush = torch.empty(64 * 1024 * 1024, device="cuda")  # 256 MB > 126 MB L2
     cfg1 = diag_case(3072, 768, 256, 0.9, torch.float32, peaks, fma_tflops, flush=flush)
+    cfg1["layer_step"] = layer_step_case(flush=flush)
     sweep = []
     for (dim, s, B) in [(4096, 0.9, 1), (4096, 0.9, 64), (4096, 0.9, 1024), (4096, 0.99, 1024),
                         (4096, 0.9, 8192)]:

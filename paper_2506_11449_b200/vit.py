@@ -166,6 +166,7 @@ class ViTConfig:
     classes: int = 1000
     sparsity: float = 0.9
     sparse_qkv: bool = True
+    dense: str = ""  # "" DiagLinear projections; "cublas": nn.Linear; "tc": TCLinear (the dense-model arms)
 
     @property
     def tokens(self) -> int:
@@ -176,8 +177,54 @@ VIT_B16 = ViTConfig()
 VIT_TINY16 = ViTConfig(dim=192, depth=12, heads=3)
 
 
+class _TCLinearFunction(torch.autograd.Function):
+    """Dense y = x W^T + b on our tcgen05 GEMM (W cast to bf16 per call, as autocast
+    does for nn.Linear); dX on the MN-major tcgen05 GEMM; dW / db on cuBLAS."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias):
+        W = weight.detach().to(torch.bfloat16)
+        x2 = x.reshape(-1, x.shape[-1]).to(torch.bfloat16).contiguous()
+        y = ops.tc_gemm(x2, W, None if bias is None else bias.detach())
+        ctx.save_for_backward(x2, W)
+        ctx.has_bias, ctx.shape = bias is not None, x.shape
+        return y.view(*x.shape[:-1], W.shape[0])
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, W = ctx.saved_tensors
+        g = dy.reshape(-1, W.shape[0]).to(torch.bfloat16).contiguous()
+        dx = ops.tc_gemm_nn(g, W).view(ctx.shape)
+        dW = torch.mm(g.t(), x2, out_dtype=torch.float32)
+        db = g.sum(0, dtype=torch.float32) if ctx.has_bias else None
+        return dx, dW, db
+
+
+class TCLinear(nn.Linear):
+    """nn.Linear whose bf16 products run on the repo's tcgen05 GEMM (dense-model arm)."""
+
+    def forward(self, x):
+        if x.is_cuda and self.in_features % 8 == 0 and self.out_features % 8 == 0:
+            return _TCLinearFunction.apply(x, self.weight, self.bias)
+        return super().forward(x)
+
+
+class DenseMLP(nn.Module):
+    """fc2(gelu_tanh(fc1(x))) (+ residual) with dense layers (the dense-model arms)."""
+
+    def __init__(self, fc1: nn.Module, fc2: nn.Module):
+        super().__init__()
+        self.fc1, self.fc2 = fc1, fc2
+
+    def forward(self, x, residual=None):
+        y = self.fc2(F.gelu(self.fc1(x), approximate="tanh"))
+        return y if residual is None else y + residual
+
+
 def _sparse(n_in, n_out, cfg: ViTConfig, seed: int, t_schedule, route, dense: bool = False):
-    if dense:
+    if cfg.dense == "tc":
+        return TCLinear(n_in, n_out)
+    if dense or cfg.dense:
         return nn.Linear(n_in, n_out)
     return DiagLinear(n_in, n_out, cfg.sparsity, seed=seed, t_schedule=t_schedule, route=route,
                       dtype=torch.float32)
@@ -194,7 +241,10 @@ class Block(nn.Module):
         self.norm2 = LayerNorm(d)
         self.fc1 = _sparse(d, cfg.mlp_ratio * d, cfg, 4 * idx + 2, t_schedule, route)
         self.fc2 = _sparse(cfg.mlp_ratio * d, d, cfg, 4 * idx + 3, t_schedule, route)
-        self.mlp = DiagMLP(self.fc1, self.fc2)  # GELU fused into the tensor-core epilogues
+        if isinstance(self.fc1, DiagLinear):
+            self.mlp = DiagMLP(self.fc1, self.fc2)  # GELU fused into the tensor-core epilogues
+        else:
+            self.mlp = DenseMLP(self.fc1, self.fc2)
 
     def forward(self, x):
         B, T, D = x.shape
