@@ -31,6 +31,54 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "ViT-B/16 90%-sparse images/s (train, infer); DiagMM GB/s vs roofline"
 UNIT = "images/s"
+
+
+class Workload:
+    """One BASELINE configuration: model, batch, unit.  vit_b16 (config 3, the metric's
+    model), vit_tiny16 (config 2, batch 128), gpt2_small (config 4, seq 1024)."""
+
+    def __init__(self, name):
+        from paper_2506_11449_b200.gpt2 import GPT2_SMALL
+        from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16
+
+        self.name = name
+        self.lm = name.startswith("gpt2")
+        self.cfg = {"vit_b16": VIT_B16, "vit_tiny16": VIT_TINY16, "gpt2_small": GPT2_SMALL}[name]
+        self.seq = self.cfg.ctx if self.lm else self.cfg.tokens
+        self.default_batch = {"vit_b16": 256, "vit_tiny16": 128, "gpt2_small": 32}[name]
+        self.unit = "tokens/s" if self.lm else UNIT
+        self.per_sample = self.seq if self.lm else 1  # units per batch element
+        self.metric = METRIC if name == "vit_b16" else (
+            "GPT-2 small 90%-sparse tokens/s (train, infer)" if self.lm
+            else "ViT-Tiny/16 90%-sparse images/s (train, infer)")
+        self.label_smoothing = 0.0 if self.lm else 0.1
+
+    def build(self, dev, route="auto", dense=""):
+        import dataclasses
+
+        from paper_2506_11449_b200.gpt2 import GPT2
+        from paper_2506_11449_b200.vit import ViT
+
+        cfg = dataclasses.replace(self.cfg, dense=dense) if dense else self.cfg
+        return GPT2(cfg, route=route, device=dev) if self.lm else ViT(cfg, route=route, device=dev)
+
+    def batch(self, B, dev, rank):
+        import torch
+
+        g = torch.Generator(device=dev).manual_seed(100 + rank)
+        if self.lm:
+            ids = torch.randint(0, self.cfg.vocab, (B, self.seq), device=dev, generator=g)
+            return ids, torch.randint(0, self.cfg.vocab, (B, self.seq), device=dev, generator=g)
+        images = torch.randn(B, 3, self.cfg.image, self.cfg.image, device=dev, generator=g).to(torch.bfloat16)
+        return images, torch.randint(0, self.cfg.classes, (B,), device=dev, generator=g)
+
+    def layer_shapes(self):
+        d = self.cfg.dim
+        per_block = [(d, 3 * d), (d, d), (d, self.cfg.mlp_ratio * d), (self.cfg.mlp_ratio * d, d)]
+        return per_block * self.cfg.depth
+
+    def cpu_sample_tokens(self, samples):
+        return samples * (256 if self.lm else self.seq)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 FMA_FP32_TFLOPS = 72.4  # measured FFMA peak, profiles/r01_microbench_fma_lds.txt
 
@@ -41,8 +89,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--batch", type=int, default=256, help="images per GPU")
-    p.add_argument("--model", choices=["vit_b16", "vit_tiny16"], default="vit_b16")
+    p.add_argument("--batch", type=int, default=None,
+                   help="images (ViT) / sequences (GPT-2) per GPU; default 256 / 128 (vit_tiny16) / 32 (gpt2_small)")
+    p.add_argument("--model", choices=["vit_b16", "vit_tiny16", "gpt2_small"], default="vit_b16")
     p.add_argument("--route", choices=["auto", "diag", "dense"], default="auto")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip infer / diagmm kernel sections")
@@ -115,15 +164,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU reference arm
-def vit_layer_shapes(model: str):
-    from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16
-
-    cfg = VIT_B16 if model == "vit_b16" else VIT_TINY16
-    d = cfg.dim
-    per_block = [(d, 3 * d), (d, d), (d, cfg.mlp_ratio * d), (cfg.mlp_ratio * d, d)]
-    return cfg, per_block * cfg.depth
-
-
 def cpu_model() -> str:
     try:
         for line in Path("/proc/cpuinfo").read_text().splitlines():
@@ -156,20 +196,21 @@ class _Threads:
             self.ctx.restore_original_limits()
 
 
-def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int, threads: int | None = None):
+def cpu_reference_rate(wl: "Workload", samples: int, steps: int, warmup: int, threads: int | None = None):
     """The reference's CPU DiagLinear path (oracle port, float64) on a bounded sample:
-    ``images`` images' tokens through every DiagLinear layer of the model, one
-    training step each (forward, backward + l1, clip, AdamW) in the post-anneal
-    regime (T = 1e-9, bench.py:188-194 of the reference).  Attention, LayerNorm
-    and the rest of the ViT are NOT timed, so this overstates the reference."""
+    ``samples`` images (ViT: 197 tokens each) or 256-token slices (GPT-2) through
+    every DiagLinear layer of the model, one training step each (forward, backward
+    + l1, clip, AdamW) in the post-anneal regime (T = 1e-9, bench.py:188-194 of the
+    reference).  Attention, LayerNorm and the rest of the model are NOT timed, so
+    this overstates the reference.  Returns (rate in the workload's unit, sec, cores, tokens)."""
     import numpy as np
 
     from oracle import layer as olayer  # checker / CPU baseline only
 
-    cfg, shapes = vit_layer_shapes(model)
-    tokens = images * cfg.tokens
+    shapes = wl.layer_shapes()
+    tokens = wl.cpu_sample_tokens(samples)
     rng = np.random.default_rng(0)
-    layers = [olayer.OracleDiagLayer(n_in, n_out, cfg.sparsity, t_kind="constant", t_init=1e-9,
+    layers = [olayer.OracleDiagLayer(n_in, n_out, wl.cfg.sparsity, t_kind="constant", t_init=1e-9,
                                      t_final=1e-9, t_total=1, l1_coeff=1e-4, seed=i)
               for i, (n_in, n_out) in enumerate(shapes)]
     xs = {s: rng.standard_normal((tokens, s[0])) for s in set(shapes)}
@@ -190,7 +231,8 @@ def cpu_reference_images_per_s(model: str, images: int, steps: int, warmup: int,
             one_step(warmup + s)
             times.append(time.perf_counter() - t0)
     sec = statistics.median(times)
-    return images / sec, sec, cores, tokens
+    units = tokens if wl.lm else samples
+    return units / sec, sec, cores, tokens
 
 
 def cpu_config1_ms(threads: int, reps: int = 3):
@@ -217,39 +259,39 @@ def cpu_config1_ms(threads: int, reps: int = 3):
     return statistics.median(ts) * 1e3
 
 
-def cpu_baseline_block(model: str, images: int):
+def cpu_baseline_block(wl: "Workload", samples: int):
     """cpu_baseline for the bench line: all host cores and 1 core."""
     allc = len(os.sched_getaffinity(0))
-    ips_all, sec_all, _, tokens = cpu_reference_images_per_s(model, images, 1, 1, threads=allc)
-    ips_one, sec_one, _, _ = cpu_reference_images_per_s(model, images, 1, 0, threads=1)
-    return {"value": ips_all, "unit": UNIT, "cores": allc, "kind": "port",
+    r_all, sec_all, _, tokens = cpu_reference_rate(wl, samples, 1, 1, threads=allc)
+    r_one, sec_one, _, _ = cpu_reference_rate(wl, samples, 1, 0, threads=1)
+    return {"value": r_all, "unit": wl.unit, "cores": allc, "kind": "port",
             "cpu_model": cpu_model(),
-            "sample": f"{images} image(s) = {tokens} tokens through all DiagLinear layers of {model} (fwd + bwd + "
-                      f"l1 + clip + AdamW, float64 oracle of the reference algorithm, post-anneal T = 1e-9); "
-                      f"attention, LayerNorm, patch embedding and head are NOT timed",
-            "all_cores": {"value": ips_all, "cores": allc, "sec_per_sample": sec_all},
-            "one_core": {"value": ips_one, "cores": 1, "sec_per_sample": sec_one}}
+            "sample": f"{tokens} tokens through all {len(wl.layer_shapes())} DiagLinear layers of {wl.name} (fwd + "
+                      f"bwd + l1 + clip + AdamW, float64 oracle of the reference algorithm, post-anneal T = 1e-9); "
+                      f"attention, LayerNorm, embeddings and head are NOT timed",
+            "all_cores": {"value": r_all, "cores": allc, "sec_per_sample": sec_all},
+            "one_core": {"value": r_one, "cores": 1, "sec_per_sample": sec_one}}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    wl = Workload(args.model)
     steps = max(1, min(args.steps, 3))
     warm = 1 if args.warmup > 0 else 0
-    ips, sec, cores, tokens = cpu_reference_images_per_s(args.model, args.cpu_sample_images, steps, warm)
+    rate, sec, cores, tokens = cpu_reference_rate(wl, args.cpu_sample_images, steps, warm)
     line = {
-        "impl": "reference", "metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": wl.metric, "value": rate, "unit": wl.unit, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers training step, CPU oracle port",
-                   "global_batch": args.cpu_sample_images, "seq_len": tokens // max(1, args.cpu_sample_images),
+                   "global_batch": args.cpu_sample_images, "seq_len": wl.seq,
                    "parallelism": "none (host threads via BLAS)"},
-        "cpu_baseline": {"value": ips, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{args.cpu_sample_images} image(s) = {tokens} tokens through all DiagLinear "
-                                   f"layers (fwd+bwd+clip+AdamW), float64, median of {steps}; attention / LayerNorm "
-                                   f"not timed"},
-        "e2e": {"value": ips, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": rate, "unit": wl.unit, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{tokens} tokens through all DiagLinear layers (fwd+bwd+clip+AdamW), float64, "
+                                   f"median of {steps}; attention / LayerNorm not timed"},
+        "e2e": {"value": rate, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -259,7 +301,7 @@ class TrainHarness:
     """One model's training step (forward, backward, DP all-reduce, clip, AdamW)
     on a fixed synthetic batch, with CUDA-graph capture of forward + backward."""
 
-    def __init__(self, model, batch, dev, world, args):
+    def __init__(self, model, batch, dev, world, args, label_smoothing=0.1):
         import torch
 
         from paper_2506_11449_b200 import AdamW, GlobalNormClipper, model_param_specs
@@ -275,6 +317,7 @@ class TrainHarness:
         self.graph = None
         self.graph_note = "off"
         self.step_no = 0
+        self.label_smoothing = label_smoothing
         self._torch = torch
 
     def fwd_bwd(self, step, inp, lbl):
@@ -287,7 +330,7 @@ class TrainHarness:
             self.model.set_step(step)
         with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
             logits = self.model(inp)
-        loss = F.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), lbl.reshape(-1), label_smoothing=0.1)
+        loss = F.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), lbl.reshape(-1), label_smoothing=self.label_smoothing)
         for pen in penalties(self.model, fused=True):  # l1 gradient folded into K5
             loss = loss + pen
         loss.backward()
@@ -453,15 +496,6 @@ def max_over_ranks(v: float, world: int, dev) -> float:
     return float(t.item())
 
 
-def make_batch(cfg, B, dev, rank):
-    import torch
-
-    g = torch.Generator(device=dev).manual_seed(100 + rank)
-    images = torch.randn(B, 3, cfg.image, cfg.image, device=dev, generator=g).to(torch.bfloat16)
-    labels = torch.randint(0, cfg.classes, (B,), device=dev, generator=g)
-    return images, labels
-
-
 def main():
     args = parse()
     if args.impl == "reference":
@@ -474,7 +508,6 @@ def main():
     import torch.distributed as dist
 
     from paper_2506_11449_b200 import profiling
-    from paper_2506_11449_b200.vit import VIT_B16, VIT_TINY16, ViT
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -492,11 +525,12 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
 
-    cfg = VIT_B16 if args.model == "vit_b16" else VIT_TINY16
+    wl = Workload(args.model)
+    cfg = wl.cfg
     torch.manual_seed(1234)  # dense params; DiagLinear init is seeded per layer (numpy stream)
-    model = ViT(cfg, route=args.route, device=dev)
-    B = args.batch
-    h = TrainHarness(model, make_batch(cfg, B, dev, rank), dev, world, args)
+    model = wl.build(dev, route=args.route)
+    B = args.batch or wl.default_batch
+    h = TrainHarness(model, wl.batch(B, dev, rank), dev, world, args, wl.label_smoothing)
 
     # warm-up (also profiles every C-ABI call once to find our dominant kernel)
     h.warm(max(args.warmup, 3))
@@ -529,9 +563,9 @@ def main():
         ms, launches = h.timed(args.steps, None)
         e2e_steps = max(3, min(args.steps, 6))
         e2e_ms, h2d_bytes = h.e2e(e2e_steps)
-    value = world * B / (ms / 1e3)
+    value = world * B * wl.per_sample / (ms / 1e3)
     clock_summary = clocks.summary()
-    e2e_value = world * B / (e2e_ms / 1e3)
+    e2e_value = world * B * wl.per_sample / (e2e_ms / 1e3)
 
     peaks, peaks_kind = load_peaks()
     nact_of = {(m.out_features, m.in_features): m.k for m in model.diag_layers()}
@@ -546,18 +580,19 @@ def main():
 
     extras = {}
     if not args.no_extras and rank == 0:
-        extras["infer"] = infer_images_per_s(model, h.inputs, args, dev)
+        extras["infer"] = infer_images_per_s(model, h.inputs, args, dev, wl.per_sample, wl.unit)
         extras["routes"] = {"bench_route": args.route, "step_ms_by_fn": {k: round(v, 4) for k, v in per_fn.items()}}
     inputs = h.inputs
     h.release()
     del model
     if not args.no_extras and rank == 0 and world == 1:
-        extras["dense"] = dense_arms(cfg, inputs, h.labels, args, dev, value, extras.get("infer"))
-        extras["diagmm"] = diagmm_kernel_section(peaks, peaks_kind)
+        extras["dense"] = dense_arms(wl, inputs, h.labels, args, dev, value, extras.get("infer"))
+        if wl.name == "vit_b16":
+            extras["diagmm"] = diagmm_kernel_section(peaks, peaks_kind)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_block(args.model, args.cpu_sample_images)
+        cpu = cpu_baseline_block(wl, args.cpu_sample_images)
         if "diagmm" in extras:
             c1 = extras["diagmm"]["config1"]
             c1["cpu_reference_ms"] = {"one_core": cpu_config1_ms(1),
@@ -566,16 +601,16 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.model} 90%-sparse DiagLinear (qkv/proj/fc1/fc2 x{cfg.depth}) training "
                                    f"step, DiagLinear route={args.route}",
-                       "model": args.model, "global_batch": world * B, "seq_len": cfg.tokens,
+                       "model": args.model, "global_batch": world * B, "seq_len": wl.seq,
                        "parallelism": f"dp{world}", "per_gpu_batch": B,
                        "l2": "per-step working set (activations, candidate stores) >> 126 MB L2; no explicit flush",
                        "step": graph_note},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4,
+            "e2e": {"value": e2e_value, "unit": wl.unit, "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4,
                     "ms_per_step": e2e_ms,
                     "how": "pinned H2D of every step's images+labels on a copy stream (1-step prefetch) and a "
                            "non-blocking D2H of every step's loss, all inside the timed region"},
@@ -590,34 +625,31 @@ def main():
         dist.destroy_process_group()
 
 
-def dense_arms(cfg, inputs, labels, args, dev, sparse_train_ips, sparse_infer):
+def dense_arms(wl, inputs, labels, args, dev, sparse_train_ips, sparse_infer):
     """The paper's headline comparison (reference bench.py:72-150):
     the same ViT with dense projections — nn.Linear (cuBLAS bf16 under autocast) and
     TCLinear (the repo's tcgen05 GEMM on dense weights) — same step (graphed forward
     + backward, clip, AdamW), same batch; plus the dense forward for inference."""
-    import dataclasses
-
     import torch
 
-    from paper_2506_11449_b200.vit import ViT
-
-    out = {}
+    out = {"unit": wl.unit}
+    units = inputs.shape[0] * wl.per_sample
     for kind in ("cublas", "tc"):
         torch.manual_seed(1234)
-        model = ViT(dataclasses.replace(cfg, dense=kind), device=dev)
-        h = TrainHarness(model, (inputs, labels), dev, 1, args)
+        model = wl.build(dev, dense=kind)
+        h = TrainHarness(model, (inputs, labels), dev, 1, args, wl.label_smoothing)
         h.warm(3)
         note = h.capture(args.graph if args.graph != "auto" else "on")
         ms, _ = h.timed(args.steps)
         inf = infer_dense(model, inputs, dev)
-        out[kind] = {"train_images_per_s": inputs.shape[0] / (ms / 1e3), "train_ms_per_step": ms, "step": note,
-                     "infer_images_per_s": inf["value"], "infer_ms_per_batch": inf["ms_per_batch"]}
+        out[kind] = {"train_per_s": units / (ms / 1e3), "train_ms_per_step": ms, "step": note,
+                     "infer_per_s": units / (inf["ms_per_batch"] / 1e3), "infer_ms_per_batch": inf["ms_per_batch"]}
         h.release()
         del model
     ref = out["cublas"]
-    out["train_speedup_vs_dense"] = sparse_train_ips / ref["train_images_per_s"]
+    out["train_speedup_vs_dense"] = sparse_train_ips / ref["train_per_s"]
     if sparse_infer:
-        out["infer_speedup_vs_dense"] = sparse_infer["value"] / ref["infer_images_per_s"]
+        out["infer_speedup_vs_dense"] = sparse_infer["value"] / ref["infer_per_s"]
     out["note"] = ("speedups: this line's 90%-sparse value / the nn.Linear (cuBLAS bf16) dense ViT; 'tc' is the "
                    "same dense model on our tcgen05 GEMM (dW on cuBLAS)")
     return out
@@ -645,11 +677,10 @@ def _graph_forward_ms(model, inputs, reps=5):
 
 
 def infer_dense(model, inputs, dev):
-    ms = _graph_forward_ms(model, inputs)
-    return {"value": inputs.shape[0] / (ms / 1e3), "ms_per_batch": ms}
+    return {"ms_per_batch": _graph_forward_ms(model, inputs)}
 
 
-def infer_images_per_s(model, images, args, dev):
+def infer_images_per_s(model, images, args, dev, per_sample=1, unit="images/s"):
     """Frozen-model inference (hard top-K, forward only) images/s at the same batch."""
     import torch
 
@@ -680,7 +711,7 @@ def infer_images_per_s(model, images, args, dev):
     with _Swap():
         ms = _graph_forward_ms(model, images)
     _ = FrozenDiagLinear
-    return {"value": images.shape[0] / (ms / 1e3), "unit": "images/s", "ms_per_batch": ms,
+    return {"value": images.shape[0] * per_sample / (ms / 1e3), "unit": unit, "ms_per_batch": ms,
             "route": "frozen (hard top-K, α̃ baked in), tensor-core route, GELU + residual fused in the epilogues, "
                      "forward replayed as one CUDA graph"}
 

@@ -34,12 +34,12 @@ class PackedQKVAttention(torch.autograd.Function):
     around the qkv DiagLinear, without autograd's unbind/stack copies."""
 
     @staticmethod
-    def forward(ctx, h):
+    def forward(ctx, h, causal=False):
         # q, k, v: strided views of h made autograd leaves of their own, so the
         # library op's registered backward gives dq, dk, dv and nothing else
         qkv = [t.detach().requires_grad_(True) for t in h.permute(2, 0, 3, 1, 4).unbind(0)]
         with torch.enable_grad():
-            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True)[0]
+            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True, 0.0, bool(causal))[0]
         ctx.graph = (out, qkv)
         ctx.h_shape = h.shape
         return out.detach()
@@ -61,7 +61,7 @@ class PackedQKVAttention(torch.autograd.Function):
             dhv = dh.permute(2, 0, 3, 1, 4)  # (3, B, H, T, hd) view of the packed gradient
             for i in range(3):
                 dhv[i].copy_(grads[i])
-        return dh
+        return dh, None
 
 
 class QKVAttentionFunction(torch.autograd.Function):
@@ -76,7 +76,7 @@ class QKVAttentionFunction(torch.autograd.Function):
     of DiagMMFunction (layers.py:143-167) for the qkv layer."""
 
     @staticmethod
-    def forward(ctx, x, values, alpha, bias, spec, B, T, H):
+    def forward(ctx, x, values, alpha, bias, spec, B, T, H, causal=False):
         M, N = spec.M, spec.N
         sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
         vals = values.detach()
@@ -85,7 +85,7 @@ class QKVAttentionFunction(torch.autograd.Function):
         hd = N // H
         qkv = [t_.detach().requires_grad_(True) for t_ in h.view(B, T, 3, H, hd).permute(2, 0, 3, 1, 4).unbind(0)]
         with torch.enable_grad():
-            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True)[0]
+            out = torch.ops.aten._scaled_dot_product_cudnn_attention(*qkv, None, True, 0.0, bool(causal))[0]
         ctx.graph = (out, qkv)
         ctx.save_for_backward(x, values, alpha)
         ctx.sel, ctx.spec, ctx.W, ctx.has_bias, ctx.bth = sel, spec, W, bias is not None, (B, T, H)
@@ -111,7 +111,7 @@ class QKVAttentionFunction(torch.autograd.Function):
         if need_soft:
             ga = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, gs, clamped=sel.clamped,
                                     l1_coeff=spec.l1)
-        return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None
+        return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None, None
 
 
 def _qkv_fusable(qkv, x2: torch.Tensor, H: int) -> bool:
@@ -231,10 +231,14 @@ def _sparse(n_in, n_out, cfg: ViTConfig, seed: int, t_schedule, route, dense: bo
 
 
 class Block(nn.Module):
-    def __init__(self, cfg: ViTConfig, idx: int, t_schedule, route):
+    """Pre-LN transformer block: x + proj(attn(qkv(LN(x)))), then x + fc2(gelu(fc1(LN(x)))).
+    ``causal`` masks the attention (GPT-2)."""
+
+    def __init__(self, cfg, idx: int, t_schedule, route, causal: bool = False):
         super().__init__()
         d = cfg.dim
         self.heads = cfg.heads
+        self.causal = bool(causal)
         self.norm1 = LayerNorm(d)
         self.qkv = _sparse(d, 3 * d, cfg, 4 * idx, t_schedule, route, dense=not cfg.sparse_qkv)
         self.proj = _sparse(d, d, cfg, 4 * idx + 1, t_schedule, route)
@@ -257,20 +261,21 @@ class Block(nn.Module):
             q = self.qkv
             step = q.step
             q.last_step = step
-            a = QKVAttentionFunction.apply(x2, q.values, q.alpha, q.bias, q._make_spec(step), B, T, self.heads)
+            a = QKVAttentionFunction.apply(x2, q.values, q.alpha, q.bias, q._make_spec(step), B, T, self.heads,
+                                           self.causal)
             a = a.transpose(1, 2).reshape(B, T, D)
             x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
             xn2, x = self.norm2.forward_skip(x)
             return self.mlp(xn2, residual=x)
         h = self.qkv(xn).view(B, T, 3, self.heads, D // self.heads)
         if backend == "cudnn" and h.is_cuda and h.dtype in (torch.bfloat16, torch.float16):
-            a = PackedQKVAttention.apply(h).transpose(1, 2).reshape(B, T, D)
+            a = PackedQKVAttention.apply(h, self.causal).transpose(1, 2).reshape(B, T, D)
         elif backend != "sdpa" and _flash_qkvpacked is not None and h.dtype in (torch.bfloat16, torch.float16):
             # packed q/k/v in, packed dq/dk/dv out: no unbind/stack copies
-            a = _flash_qkvpacked(h).reshape(B, T, D)
+            a = _flash_qkvpacked(h, causal=self.causal).reshape(B, T, D)
         else:
             q, k, v = h.permute(2, 0, 3, 1, 4).unbind(0)
-            a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B, T, D)
+            a = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal).transpose(1, 2).reshape(B, T, D)
         # skip connections fused into the proj / fc2 epilogues (DiagLinear residual=)
         x = self.proj(a, residual=x) if isinstance(self.proj, (DiagLinear, FrozenDiagLinear)) else x + self.proj(a)
         xn2, x = self.norm2.forward_skip(x)

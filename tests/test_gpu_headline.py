@@ -326,3 +326,75 @@ def test_vit_depth2_step_vs_fp32_reference_model():
     for n in ("patch.weight", "head.weight", "blocks.0.norm1.weight"):
         got = dict(model.named_parameters())[n].grad
         assert _err(got.float(), dense[n].grad.double()) <= MODEL_TOL, n
+
+
+def _diag_grads_ref(m, r, dW, T):
+    """g_values / g_alpha of a DiagLinear from the reference model's dense dW (layers.py:149-167)."""
+    gw = dW.double()[r.r, r.c].cpu().numpy()
+    g_values = np.zeros_like(r.values)
+    g_values[r.active] = r.soft[r.active, None] * gw
+    g_soft = np.zeros(r.values.shape[0])
+    g_soft[r.active] = (gw * r.values[r.active]).sum(axis=1)
+    g_alpha = oracle.soft_topk_grad(r.alpha, r.k, T, g_soft) + oracle.l1_term(r.alpha, m.l1_coeff)[1]
+    return g_values, g_alpha
+
+
+def test_gpt2_block_step_vs_fp32_reference_model():
+    """GPT-2 small geometry (768, 12 heads, seq 1024, causal), one block, all four
+    projections DiagLinear at 90 %: loss and every gradient of the
+    bf16 model (tensor-core route, qkv + causal cuDNN attention node, fused MLP /
+    residual epilogues) against a float32 PyTorch model carrying the oracle's W_K."""
+    import torch.nn.functional as F
+
+    from paper_2506_11449_b200 import penalties
+    from paper_2506_11449_b200.gpt2 import GPT2, GPT2Config
+
+    T = 0.05
+    cfg = GPT2Config(vocab=512, depth=1)
+    torch.manual_seed(0)
+    model = GPT2(cfg, t_schedule=TemperatureSchedule("constant", T, T, 1), device=DEV)
+    for i, m in enumerate(model.diag_layers()):
+        rng = np.random.default_rng(300 + i)
+        with torch.no_grad():
+            m.alpha.add_(torch.as_tensor(rng.standard_normal(m.candidates), device=DEV))
+            m.bias.copy_(torch.as_tensor(rng.standard_normal(m.out_features) * 0.05, device=DEV))
+    g = torch.Generator(device=DEV).manual_seed(2)
+    ids = torch.randint(0, cfg.vocab, (1, cfg.ctx), device=DEV, generator=g)
+    lbl = torch.randint(0, cfg.vocab, (1, cfg.ctx), device=DEV, generator=g)
+    model.set_step(0)
+    with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+        logits = model(ids)
+    loss = F.cross_entropy(logits.float().reshape(-1, cfg.vocab), lbl.reshape(-1))
+    for p in penalties(model, fused=True):
+        loss = loss + p
+    loss.backward()
+
+    refs = {id(m): _Ref(m, T) for m in model.diag_layers()}
+    W = {k: r.W.float().clone().requires_grad_(True) for k, r in refs.items()}
+    b = {id(m): m.bias.detach().float().clone().requires_grad_(True) for m in model.diag_layers()}
+    P = {n: p.detach().float().clone().requires_grad_(True) for n, p in model.named_parameters()
+         if "wte" in n or "wpe" in n or "ln" in n or "norm" in n}
+    lin = lambda m, x: x @ W[id(m)].t() + b[id(m)]  # noqa: E731
+    blk = model.blocks[0]
+    h = P["wte.weight"][ids] + P["wpe.weight"][None, : cfg.ctx]
+    hn = F.layer_norm(h, (cfg.dim,), P["blocks.0.norm1.weight"], P["blocks.0.norm1.bias"], 1e-5)
+    qkv = lin(blk.qkv, hn).view(1, cfg.ctx, 3, cfg.heads, cfg.dim // cfg.heads).permute(2, 0, 3, 1, 4)
+    a = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True).transpose(1, 2).reshape(1, -1, cfg.dim)
+    h = h + lin(blk.proj, a)
+    hn = F.layer_norm(h, (cfg.dim,), P["blocks.0.norm2.weight"], P["blocks.0.norm2.bias"], 1e-5)
+    h = h + lin(blk.fc2, F.gelu(lin(blk.fc1, hn), approximate="tanh"))
+    hn = F.layer_norm(h, (cfg.dim,), P["ln_f.weight"], P["ln_f.bias"], 1e-5)
+    ref_loss = F.cross_entropy((hn @ P["wte.weight"].t()).reshape(-1, cfg.vocab), lbl.reshape(-1))
+    pen = sum(m.l1_coeff * float(np.abs(refs[id(m)].alpha).sum()) for m in model.diag_layers())
+    ref_loss.backward()
+
+    assert abs(loss.item() - (ref_loss.item() + pen)) <= 1e-2 * abs(ref_loss.item() + pen)
+    MODEL_TOL = 5e-2
+    for m in model.diag_layers():
+        g_values, g_alpha = _diag_grads_ref(m, refs[id(m)], W[id(m)].grad, T)
+        assert _err(m.values.grad, g_values) <= MODEL_TOL
+        assert _err(m.alpha.grad, g_alpha) <= MODEL_TOL
+        assert _err(m.bias.grad, b[id(m)].grad) <= MODEL_TOL
+    got = dict(model.named_parameters())
+    for n in ("wte.weight", "wpe.weight", "blocks.0.norm1.weight"):
+        assert _err(got[n].grad.float(), P[n].grad.double()) <= MODEL_TOL, n
