@@ -105,7 +105,11 @@ DIAGMM_API int diagmm_backward_input(int dtype, int M, int N, int B, const void*
  * values[active[j],t], 0 elsewhere (layers.py:164-165).
  * g_bias (M,), may be NULL: column sums of dy (autodiff.py:77-79).
  * slot (C,) int32 from diagmm_topk_waterfill / diagmm_active_from_list.
- * workspace: at least diagmm_backward_weight_workspace(...) bytes. */
+ * workspace: at least diagmm_backward_weight_workspace(...) bytes.
+ * bucket (bucket_rows, L) in the values' type, may be NULL (bucket_rows 0):
+ * the data-parallel exchange buffer — active row j (j < bucket_rows) is ALSO
+ * written to bucket row j, so the all-reduce sends [g_values[active]] without
+ * a pack pass (inactive rows are exactly 0 on every rank). */
 DIAGMM_API size_t diagmm_backward_weight_workspace(int dtype, int M, int N, int B,
                                         int max_act);
 DIAGMM_API int diagmm_backward_weight(int dtype, int M, int N, int B, const void* dy,
@@ -114,7 +118,7 @@ DIAGMM_API int diagmm_backward_weight(int dtype, int M, int N, int B, const void
                            const int32_t* slot, const int32_t* n_act,
                            int max_act, void* g_values, double* g_soft,
                            void* g_bias, void* workspace, size_t ws_bytes,
-                           void* stream);
+                           void* bucket, int bucket_rows, void* stream);
 
 /* ---- K4: soft TopK (capped water-filling) + active set -------------------
  * alpha_soft = soft_topk(alpha, k, T) (selection.py:100-142); clamped[i] = 1
@@ -250,7 +254,7 @@ DIAGMM_API int diagmm_tc_gemm_bf16_nn(int Mdim, int Ndim, int K, const void* A, 
  * accumulated by extra warps from the same dy tiles the MMAs consume
  * (autodiff.py:77-79), so dy is read once.  Replaces the dense branch of
  * layers.py:150-153 + 159-165.  M, N multiples of 64; dy (B, M), x (B, N)
- * bf16, 16-byte aligned. */
+ * bf16, 16-byte aligned.  bucket / bucket_rows: as diagmm_backward_weight. */
 /* The same two products with the (B, M)/(B, K) left operand given as 2-3
  * separate row-major column blocks A0 | A1 | A2 of `ks` / `ms` columns each
  * (multiple of 64 / 128): the qkv layer's input and weight gradients read the
@@ -266,13 +270,15 @@ DIAGMM_API int diagmm_tc_backward_weight_split(int M, int N, int B, const void* 
                                                const double* alpha_soft, const int32_t* slot,
                                                const int32_t* n_act, int max_act, void* g_values,
                                                double* g_soft, void* g_bias, void* workspace,
-                                               size_t ws_bytes, void* stream);
+                                               size_t ws_bytes, void* bucket, int bucket_rows,
+                                               void* stream);
 DIAGMM_API size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act);
 DIAGMM_API int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x,
                                          const void* values, const double* alpha_soft,
                                          const int32_t* slot, const int32_t* n_act, int max_act,
                                          void* g_values, double* g_soft, void* g_bias,
-                                         void* workspace, size_t ws_bytes, void* stream);
+                                         void* workspace, size_t ws_bytes, void* bucket,
+                                         int bucket_rows, void* stream);
 
 /* ---- fused LayerNorm for the bf16 activations of the ViT caller ----------
  * Not a reference symbol: the caller's LayerNorm (vit.py) around DiagLinear.

@@ -31,7 +31,7 @@ SIGNATURES = {
     "diagmm_backward_input": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
     "diagmm_backward_weight_workspace": (_sz, [_i, _i, _i, _i, _i]),
     "diagmm_backward_weight": (
-        _i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
+        _i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
     "diagmm_topk_waterfill": (_i, [_i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "diagmm_topk_grad": (_i, [_i, _i, _d, _vp, _vp, _vp, _d, _vp, _i, _vp]),
     "diagmm_select_hard": (_i, [_i, _i, _vp, _vp, _vp]),
@@ -68,13 +68,13 @@ SIGNATURES["diagmm_sumsq_multi"] = (_i, [_i, C.POINTER(TensorDesc), _vp, _i, _vp
 SIGNATURES["diagmm_clip_scale_tree"] = (_i, [_i, _vp, _d, _vp, _vp, _vp])
 SIGNATURES["diagmm_tc_backward_weight_workspace"] = (_sz, [_i, _i, _i, _i])
 SIGNATURES["diagmm_tc_backward_weight"] = (
-    _i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp])
+    _i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16_ex"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16_nn"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_gemm_bf16_nn_split"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp])
 SIGNATURES["diagmm_tc_backward_weight_split"] = (
-    _i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp])
+    _i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _i, _vp])
 SIGNATURES["diagmm_pack_qkv_grad"] = (_i, [_i, _i, _i, _i, _vp, _vp, _vp, C.c_longlong, C.c_longlong, C.c_longlong,
                                            _vp, _vp])
 SIGNATURES["diagmm_layernorm_fwd"] = (_i, [_i, _i, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp])

@@ -12,7 +12,7 @@ template <typename T> size_t product_workspace(bool, int, int, int, int);
 template <typename T> size_t dw_workspace(int, int, int, int);
 template <typename T>
 int run_dw(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
-           const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t);
+           const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, void*, int);
 template <typename T>
 int run_materialize(int, int, const void*, const double*, const int32_t*, const int32_t*, int, void*,
                     cudaStream_t, bool);  // (slot, n_act, ..., transposed)
@@ -40,8 +40,8 @@ int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 size_t tc_dw_workspace(int, int, int, int);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
-                   const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, const void* dy1 = nullptr,
-                   const void* dy2 = nullptr, int a_ms = 0);
+                   const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, const void* dy1,
+                   const void* dy2, int a_ms, void* bucket, int bucket_rows);
 int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long long, long long, long long, void*,
                  cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
@@ -149,10 +149,11 @@ int diagmm_backward_weight(int dtype, int M, int N, int B, const void* dy, const
                            const void* values, const double* alpha_soft, const int32_t* active,
                            const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
                            double* g_soft, void* g_bias, void* workspace, size_t ws_bytes,
-                           void* stream) {
+                           void* bucket, int bucket_rows, void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
+  if (bucket_rows < 0 || (bucket_rows > 0 && !bucket)) return DIAGMM_ESHAPE;
   DIAGMM_DISPATCH(dtype, run_dw, M, N, B, dy, x, values, alpha_soft, active, slot, n_act, max_act,
-                  g_values, g_soft, g_bias, workspace, ws_bytes, S(stream))
+                  g_values, g_soft, g_bias, workspace, ws_bytes, S(stream), bucket, bucket_rows)
 }
 
 int diagmm_topk_waterfill(int C, int k, double temperature, const double* alpha, double* alpha_soft,
@@ -204,10 +205,11 @@ size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act) {
 int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x, const void* values,
                               const double* alpha_soft, const int32_t* slot, const int32_t* n_act, int max_act,
                               void* g_values, double* g_soft, void* g_bias, void* workspace, size_t ws_bytes,
-                              void* stream) {
+                              void* bucket, int bucket_rows, void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
+  if (bucket_rows < 0 || (bucket_rows > 0 && !bucket)) return DIAGMM_ESHAPE;
   return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
-                        workspace, ws_bytes, S(stream));
+                        workspace, ws_bytes, S(stream), nullptr, nullptr, 0, bucket, bucket_rows);
 }
 
 int diagmm_tc_gemm_bf16_nn_split(int Mdim, int Ndim, int K, const void* A0, const void* A1, const void* A2, int ks,
@@ -219,11 +221,12 @@ int diagmm_tc_gemm_bf16_nn_split(int Mdim, int Ndim, int K, const void* A0, cons
 int diagmm_tc_backward_weight_split(int M, int N, int B, const void* dy0, const void* dy1, const void* dy2, int ms,
                                     const void* x, const void* values, const double* alpha_soft,
                                     const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
-                                    double* g_soft, void* g_bias, void* workspace, size_t ws_bytes, void* stream) {
+                                    double* g_soft, void* g_bias, void* workspace, size_t ws_bytes, void* bucket,
+                                    int bucket_rows, void* stream) {
   if (int e = check_shape(M, N, B, max_act)) return e;
-  if (ms < 1) return DIAGMM_ESHAPE;
+  if (ms < 1 || bucket_rows < 0 || (bucket_rows > 0 && !bucket)) return DIAGMM_ESHAPE;
   return run_tc_dw_full(M, N, B, dy0, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
-                        workspace, ws_bytes, S(stream), dy1, dy2, ms);
+                        workspace, ws_bytes, S(stream), dy1, dy2, ms, bucket, bucket_rows);
 }
 
 // internal (not in the header): 2:4 sparse tensor-core throughput probe

@@ -861,7 +861,8 @@ __global__ void __launch_bounds__(256)
 k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
               const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
               const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
-              typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft) {
+              typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
+              typename Traits<T>::P* __restrict__ bucket, int bucket_rows) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
   static_assert(sizeof(A) == sizeof(P), "partials and values share the vector width");
@@ -887,6 +888,10 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   }
   const double sc = asoft ? asoft[i] : 1.0;
   const P* vrow = vals + (size_t)i * L;
+  // data-parallel exchange: the active row also lands in its compact bucket slot
+  // (bucket row s = the s-th active offset), which is what the all-reduce sends
+  P* brow = (bucket && s < bucket_rows) ? bucket + (size_t)s * L : nullptr;
+  const bool bvec = brow && (reinterpret_cast<uintptr_t>(bucket) & 15) == 0;
   double local = 0.0;
   if (vec) {
     // parts are summed in index order; up to 8 of their loads are in flight
@@ -919,12 +924,16 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
         local += (double)ge[e] * (double)ve[e];
       }
       reinterpret_cast<V*>(grow)[c] = o;
+      if (bvec) reinterpret_cast<V*>(brow)[c] = o;
+      else if (brow)
+        for (int e = 0; e < VW; ++e) brow[c * VW + e] = oe[e];
     }
   } else {
     for (int t = threadIdx.x; t < L; t += blockDim.x) {
       A gw = A(0);
       for (int p = 0; p < nparts; ++p) gw += partial[((size_t)p * max_act + s) * L + t];
       grow[t] = (P)(sc * (double)gw);
+      if (brow) brow[t] = grow[t];
       local += (double)gw * (double)vrow[t];
     }
   }
@@ -1469,7 +1478,7 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
 template <typename T>
 int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals, const double* asoft,
            const int32_t* active, const int32_t* slot, const int32_t* n_act, int max_act, void* g_values,
-           double* g_soft, void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st) {
+           double* g_soft, void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st, void* bucket, int bucket_rows) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
   constexpr int VEC = vec_rows<T>();
@@ -1502,7 +1511,8 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
     parts = 0;
   }
   k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
-                                       static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft);
+                                       static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
+                                       static_cast<P*>(bucket), bucket_rows);
   note_launch();
   if (g_bias) {
     A* cpart = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)));
@@ -1569,7 +1579,7 @@ size_t tc_dw_workspace(int M, int N, int B, int max_act) {
 int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const void* vals, const double* asoft,
                    const int32_t* slot, const int32_t* n_act, int max_act, void* g_values, double* g_soft,
                    void* g_bias, void* ws, size_t ws_bytes, cudaStream_t st, const void* dy1, const void* dy2,
-                   int a_ms) {
+                   int a_ms, void* bucket, int bucket_rows) {
   using T = __nv_bfloat16;
   using P = typename Traits<T>::P;
   const int C = M > N ? M : N, L = M < N ? M : N;
@@ -1594,7 +1604,8 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
     }
   }
   k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
-                                       static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft);
+                                       static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
+                                       static_cast<P*>(bucket), bucket_rows);
   note_launch();
   return status_from_cuda();
 }
@@ -1608,7 +1619,7 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
   template size_t dw_workspace<T>(int, int, int, int);                                                    \
   template int run_dw<T>(int, int, int, const void*, const void*, const void*, const double*,             \
                          const int32_t*, const int32_t*, const int32_t*, int, void*, double*, void*,      \
-                         void*, size_t, cudaStream_t);                                                    \
+                         void*, size_t, cudaStream_t, void*, int);                                        \
   template int run_materialize<T>(int, int, const void*, const double*, const int32_t*, const int32_t*,   \
                                   int, void*, cudaStream_t, bool);
 DIAGMM_INST(double)

@@ -276,8 +276,11 @@ def diag_backward_input(dy: torch.Tensor, values: torch.Tensor, sel: Selection, 
 
 def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection,
                          M: int, N: int, need_bias: bool = True, need_soft: bool = True,
-                         max_act: int | None = None, g_values: torch.Tensor | None = None):
-    """K3: (g_values (C, L), g_soft (C,) f64 | None, g_bias (M,) | None)."""
+                         max_act: int | None = None, g_values: torch.Tensor | None = None,
+                         bucket: torch.Tensor | None = None):
+    """K3: (g_values (C, L), g_soft (C,) f64 | None, g_bias (M,) | None).  ``bucket``
+    (rows, L) in the values' dtype: active row j (< rows) is also written there (the
+    data-parallel exchange buffer, dp.CompactGradExchange)."""
     _check_product(dy, M, values, M, N)
     _check_product(x, N, values, M, N)
     if dy.shape[0] != x.shape[0]:
@@ -298,8 +301,17 @@ def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor
     g_bias = torch.empty(M, dtype=values.dtype, device=dy.device) if need_bias else None
     _lib.call("diagmm_backward_weight", code, M, N, B, _p(dy), _p(x), _p(values.contiguous()),
               _p(sel.alpha_soft), _p(sel.active), _p(sel.slot), _p(sel.n_act), int(max_act),
-              _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(dy))
+              _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), *_bucket_args(bucket, values, L),
+              _stream(dy))
     return g_values, g_soft, g_bias
+
+
+def _bucket_args(bucket, values, L):
+    if bucket is None:
+        return None, 0
+    if bucket.dtype != values.dtype or bucket.dim() != 2 or bucket.shape[1] != L or not bucket.is_contiguous():
+        raise ShapeMismatch(f"bucket must be a contiguous (rows, {L}) {values.dtype} tensor")
+    return bucket.data_ptr(), bucket.shape[0]
 
 
 def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
@@ -495,7 +507,8 @@ def tc_gemm_nn(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = Non
 
 
 def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
-                       need_soft: bool = True, max_act: int | None = None, need_bias: bool = False):
+                       need_soft: bool = True, max_act: int | None = None, need_bias: bool = False,
+                       bucket: torch.Tensor | None = None):
     """K3 on the tensor cores (bf16): (g_values (C, L) f32, g_soft (C,) f64 | None[, g_bias (M,) f32])."""
     if dy.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
         raise TypeError("tc_backward_weight takes bfloat16 dy and x (the TMA maps are bf16)")
@@ -511,7 +524,8 @@ def tc_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor, 
     g_soft = torch.empty(C, dtype=torch.float64, device=dy.device) if need_soft else None
     g_bias = torch.empty(M, dtype=values.dtype, device=dy.device) if need_bias else None
     _lib.call("diagmm_tc_backward_weight", M, N, B, _p(dy), _p(x), _p(values.contiguous()), _p(sel.alpha_soft),
-              _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(dy))
+              _p(sel.slot), _p(sel.n_act), ma, _p(g_values), _p(g_soft), _p(g_bias), _p(ws), ws.numel(),
+              *_bucket_args(bucket, values, L), _stream(dy))
     return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)
 
 
@@ -536,7 +550,7 @@ def tc_gemm_nn_split(parts: list[torch.Tensor], b: torch.Tensor) -> torch.Tensor
 
 def tc_backward_weight_split(dy_parts: list[torch.Tensor], x: torch.Tensor, values: torch.Tensor, sel: Selection,
                              M: int, N: int, need_soft: bool = True, max_act: int | None = None,
-                             need_bias: bool = False):
+                             need_bias: bool = False, bucket: torch.Tensor | None = None):
     """tc_backward_weight with dy = cat(dy_parts, dim=1) read block by block (no concatenation)."""
     if not 2 <= len(dy_parts) <= 3:
         raise ValueError("tc_backward_weight_split takes 2 or 3 column blocks")
@@ -556,7 +570,7 @@ def tc_backward_weight_split(dy_parts: list[torch.Tensor], x: torch.Tensor, valu
     g_bias = torch.empty(M, dtype=values.dtype, device=x.device) if need_bias else None
     _lib.call("diagmm_tc_backward_weight_split", M, N, B, _p(ps[0]), _p(ps[1]), _p(ps[2]), ms, _p(x),
               _p(values.contiguous()), _p(sel.alpha_soft), _p(sel.slot), _p(sel.n_act), ma, _p(g_values),
-              _p(g_soft), _p(g_bias), _p(ws), ws.numel(), _stream(x))
+              _p(g_soft), _p(g_bias), _p(ws), ws.numel(), *_bucket_args(bucket, values, L), _stream(x))
     return (g_values, g_soft, g_bias) if need_bias else (g_values, g_soft)
 
 
