@@ -305,7 +305,7 @@ class TrainHarness:
         import torch
 
         from paper_2506_11449_b200 import AdamW, GlobalNormClipper, model_param_specs
-        from paper_2506_11449_b200.dp import GradientAllReducer, broadcast_parameters
+        from paper_2506_11449_b200.dp import CompactGradExchange, broadcast_parameters
 
         self.model, self.dev, self.world, self.args = model, dev, world, args
         broadcast_parameters(model)  # identical replicas
@@ -313,7 +313,9 @@ class TrainHarness:
         self.opt = AdamW(self.specs, lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
         self.clip = GlobalNormClipper(1.0)
         self.inputs, self.labels = batch
-        self.allreduce = GradientAllReducer([s.tensor for s in self.specs])
+        # data parallel: compact per-layer buckets written by K3, all-reduced from the
+        # gradient hooks as the backward produces them (overlapped), finished before the clip
+        self.exchange = CompactGradExchange(model) if world > 1 else None
         self.graph = None
         self.graph_note = "off"
         self.step_no = 0
@@ -337,8 +339,8 @@ class TrainHarness:
         return loss
 
     def update(self):
-        if self.world > 1:
-            self.allreduce()
+        if self.exchange is not None:
+            self.exchange.finish()
         _, scale = self.clip.compute(self.specs)
         self.opt.step(clip_scale=scale)
 
@@ -364,6 +366,9 @@ class TrainHarness:
         from paper_2506_11449_b200.graphed import GraphedStep, schedules_constant
 
         if not (mode == "on" or (mode == "auto" and schedules_constant(self.model))):
+            return self.graph_note
+        if self.exchange is not None:  # the exchange's per-layer launches read host-side counts: eager
+            self.graph_note = "eager steps (data parallel: per-layer all-reduces overlapped with the backward)"
             return self.graph_note
         step = self.step_no
         try:
@@ -462,6 +467,8 @@ class TrainHarness:
         return max(ms, wall), h2d_bytes
 
     def release(self):
+        if self.exchange is not None:
+            self.exchange.remove()
         self.graph = None
         self.opt = None
         self.specs = None
@@ -583,6 +590,7 @@ def main():
         extras["infer"] = infer_images_per_s(model, h.inputs, args, dev, wl.per_sample, wl.unit)
         extras["routes"] = {"bench_route": args.route, "step_ms_by_fn": {k: round(v, 4) for k, v in per_fn.items()}}
     inputs = h.inputs
+    h_exchange_bytes = h.exchange.bytes_last if h.exchange is not None else None
     h.release()
     del model
     if not args.no_extras and rank == 0 and world == 1:
@@ -615,6 +623,10 @@ def main():
                     "how": "pinned H2D of every step's images+labels on a copy stream (1-step prefetch) and a "
                            "non-blocking D2H of every step's loss, all inside the timed region"},
             "gpu_launches": int(launches),
+            "dp_exchange": (None if h_exchange_bytes is None else
+                            {"bytes_per_step": h_exchange_bytes,
+                             "what": "compact per-layer buckets [g_values[active] | g_alpha | g_bias] + dense params, "
+                                     "all-reduced from the gradient hooks (overlapped with the backward)"}),
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clock_summary,

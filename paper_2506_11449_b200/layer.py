@@ -96,6 +96,8 @@ class _OpSpec:
     fixed: ops.Selection | None = None
     presel: ops.Selection | None = None
     l1: float = 0.0  # set by penalties(fused=True): the l1 gradient is added inside K5
+    bucket: torch.Tensor | None = None  # dp.CompactGradExchange: K3 also writes the active rows here
+    sel: ops.Selection | None = None    # the selection the forward used (set by the forward)
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -142,6 +144,7 @@ class DiagMMFunction(torch.autograd.Function):
             sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
         else:
             sel = spec.fixed
+        spec.sel = sel
         dense = _use_dense(spec, sel, x.shape[0], x.dtype)
         vals = values.detach()
         W = None
@@ -191,10 +194,12 @@ class DiagMMFunction(torch.autograd.Function):
                 # tensor-core dW with the diagonal gather and the bias gradient fused (dy read once,
                 # no dense dW written)
                 g_values, g_soft, g_bias = ops.tc_backward_weight(dy, x.to(dy.dtype), vals, sel, M, N,
-                                                                  need_soft=need_soft, need_bias=True)
+                                                                  need_soft=need_soft, need_bias=True,
+                                                                  bucket=spec.bucket)
                 if not ctx.has_bias:
                     g_bias = None
             else:
+                spec.bucket = None  # this branch does not fill the exchange bucket (dp falls back to full)
                 dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
                     else (dy.t() @ x.to(dy.dtype)).to(out_dt)
                 g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
@@ -203,7 +208,7 @@ class DiagMMFunction(torch.autograd.Function):
             if ctx.needs_input_grad[0]:
                 dx = ops.diag_backward_input(dy, vals, sel, M, N)
             g_values, g_soft, g_bias = ops.diag_backward_weight(
-                dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft)
+                dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft, bucket=spec.bucket)
         if need_soft:
             g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
                                          clamped=sel.clamped, l1_coeff=spec.l1)
@@ -221,6 +226,7 @@ class DiagMLPFunction(torch.autograd.Function):
     def forward(ctx, x, v1, a1, b1, v2, a2, b2, s1: _OpSpec, s2: _OpSpec, fuse_fwd: bool = True, residual=None):
         sel1 = s1.presel or ops.soft_topk_select(a1.detach(), s1.k, s1.temperature)
         sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature)
+        s1.sel, s2.sel = sel1, sel2
         x = x.contiguous()
         W1 = ops.materialize(v1.detach(), sel1, s1.M, s1.N, dtype=x.dtype)
         if fuse_fwd:
@@ -252,11 +258,13 @@ class DiagMLPFunction(torch.autograd.Function):
         W1, W2 = ctx.W
         ctx.W = None
         d_pre = ops.tc_gemm_nn(dy, W2, None, epilogue=2, aux=pre)
-        gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True)
+        gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True,
+                                               bucket=s2.bucket)
         ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1)
         # fc1
         dx = ops.tc_gemm_nn(d_pre, W1)
-        gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True)
+        gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True,
+                                               bucket=s1.bucket)
         ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1)
         hb1, hb2 = ctx.has_bias
         d_res = dy0 if ctx.needs_input_grad[10] else None
@@ -375,7 +383,7 @@ class DiagLinear(nn.Module):
     def _make_spec(self, step: int) -> "_OpSpec":
         T = self.temperature(step)
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
-                       presel=self._take_preselection(step, T))
+                       presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None))
         self._last_spec = spec
         return spec
 

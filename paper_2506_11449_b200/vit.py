@@ -79,6 +79,7 @@ class QKVAttentionFunction(torch.autograd.Function):
     def forward(ctx, x, values, alpha, bias, spec, B, T, H, causal=False):
         M, N = spec.M, spec.N
         sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+        spec.sel = sel
         vals = values.detach()
         W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
         h = ops.tc_gemm(x.contiguous(), W, None if bias is None else bias.detach())
@@ -106,7 +107,7 @@ class QKVAttentionFunction(torch.autograd.Function):
         dx = ops.tc_gemm_nn_split(parts, W) if ctx.needs_input_grad[0] else None
         need_soft = alpha is not None and ctx.needs_input_grad[2]
         gv, gs, gb = ops.tc_backward_weight_split(parts, x, values.detach(), sel, M, N, need_soft=need_soft,
-                                                  need_bias=True)
+                                                  need_bias=True, bucket=spec.bucket)
         ga = None
         if need_soft:
             ga = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, gs, clamped=sel.clamped,
