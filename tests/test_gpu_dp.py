@@ -88,13 +88,13 @@ def _worker(rank, world, port, kind, q):
     h = x.shape[0] // world
     _loss(m, x[rank * h:(rank + 1) * h], y[rank * h:(rank + 1) * h], kind).backward()
     ex.finish()
+    n_act = [lyr._last_spec.sel.host_count() for lyr in m.layers[:2]]  # the selection this step used
     grads = {n: p.grad.detach().double().cpu().numpy().copy() for n, p in m.named_parameters()}
     specs = model_param_specs(m)
     _, sc = GlobalNormClipper(1.0).compute(specs)
     AdamW(specs, lr=1e-2).step(clip_scale=sc)
     torch.cuda.synchronize()
     params = {n: p.detach().double().cpu().numpy().copy() for n, p in m.named_parameters()}
-    n_act = [lyr.active_count(0) for lyr in m.layers[:2]]
     q.put((rank, grads, params, ex.bytes_last, n_act))
     dist.barrier()
     dist.destroy_process_group()
