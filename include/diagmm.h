@@ -144,6 +144,12 @@ typedef struct diagmm_topk_job {
   int32_t* active;
   int32_t* slot;
   int32_t* n_act;
+  /* NULL, or a DEVICE pair {T, (double)k} read by the kernel instead of
+   * temperature / k: one captured CUDA graph replays an annealing / sparsity
+   * schedule whose per-step values the host writes into that buffer
+   * (selection.py:189-214, training.py:608-619).  temperature / k still
+   * size and validate the launch. */
+  const double* params;
 } diagmm_topk_job;
 DIAGMM_API int diagmm_topk_waterfill_batched(int n, const diagmm_topk_job* jobs,
                                              void* stream);
@@ -153,11 +159,11 @@ DIAGMM_API int diagmm_topk_waterfill_batched(int n, const diagmm_topk_job* jobs,
  *     + l1_coeff * sign(alpha) (selection.py:217-222, layers.py:253-257).
  * clamped must come from diagmm_topk_waterfill on the same (alpha, k, T).
  * accumulate != 0 adds into g_alpha (Tape.backward accumulation,
- * autodiff.py:149-155). */
+ * autodiff.py:149-155).  params: NULL or the device {T, k} of diagmm_topk_job. */
 DIAGMM_API int diagmm_topk_grad(int C, int k, double temperature, const double* alpha,
                      const uint8_t* clamped, const double* g_soft,
                      double l1_coeff, double* g_alpha, int accumulate,
-                     void* stream);
+                     const double* params, void* stream);
 
 /* ---- hard TopK: select_hard (selection.py:176-186) -----------------------
  * idx (k,) = indices of the k largest alpha, ties to the smaller index,
@@ -199,7 +205,9 @@ DIAGMM_API int diagmm_clip_scale(int n, const double* partial, double max_norm,
  * reference's no-decay ParamSpecs, layers.py:259-266) and its 1-based step.
  * `tensors` is a HOST array of device pointers.
  *   diagmm_adamw_multi: adamw_step (training.py:346-358) on every tensor,
- *     gradients scaled by *clip_scale when non-NULL.
+ *     gradients scaled by *clip_scale when non-NULL; sched NULL, or a DEVICE
+ *     {lr, 1 - beta1^t, 1 - beta2^t} (host-computed, the reference's floats)
+ *     used instead of lr and the per-tensor steps (one CUDA graph per step).
  *   diagmm_sumsq_multi: per-chunk sum(grad^2) (float64, fixed order) into
  *     partial[0 .. diagmm_sumsq_multi_len(n, tensors)); fold them with
  *     diagmm_clip_scale_tree (clip_global_norm, training.py:406-417). */
@@ -215,7 +223,7 @@ typedef struct diagmm_tensor {
 } diagmm_tensor;
 DIAGMM_API int diagmm_adamw_multi(int n, const diagmm_tensor* tensors, double lr,
                                   double beta1, double beta2, double eps,
-                                  const double* clip_scale, void* stream);
+                                  const double* clip_scale, const double* sched, void* stream);
 DIAGMM_API int diagmm_sumsq_multi_len(int n, const diagmm_tensor* tensors);
 DIAGMM_API int diagmm_sumsq_multi(int n, const diagmm_tensor* tensors, double* partial,
                                   int partial_len, void* stream);

@@ -33,7 +33,7 @@ SIGNATURES = {
     "diagmm_backward_weight": (
         _i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
     "diagmm_topk_waterfill": (_i, [_i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "diagmm_topk_grad": (_i, [_i, _i, _d, _vp, _vp, _vp, _d, _vp, _i, _vp]),
+    "diagmm_topk_grad": (_i, [_i, _i, _d, _vp, _vp, _vp, _d, _vp, _i, _vp, _vp]),
     "diagmm_select_hard": (_i, [_i, _i, _vp, _vp, _vp]),
     "diagmm_active_from_list": (_i, [_i, _i, _vp, _vp, _vp, _vp]),
     "diagmm_adamw": (_i, [_i, _sz, _vp, _vp, _vp, _vp, _i, _d, _d, _d, _d, _d, _vp, _vp]),
@@ -51,7 +51,8 @@ class TopkJob(C.Structure):
     """diagmm_topk_job (include/diagmm.h)."""
 
     _fields_ = [("C", C.c_int), ("k", C.c_int), ("temperature", C.c_double), ("alpha", _vp),
-                ("alpha_soft", _vp), ("clamped", _vp), ("active", _vp), ("slot", _vp), ("n_act", _vp)]
+                ("alpha_soft", _vp), ("clamped", _vp), ("active", _vp), ("slot", _vp), ("n_act", _vp),
+                ("params", _vp)]
 
 
 class TensorDesc(C.Structure):
@@ -62,7 +63,7 @@ class TensorDesc(C.Structure):
 
 
 SIGNATURES["diagmm_topk_waterfill_batched"] = (_i, [_i, C.POINTER(TopkJob), _vp])
-SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp])
+SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp, _vp])
 SIGNATURES["diagmm_sumsq_multi_len"] = (_i, [_i, C.POINTER(TensorDesc)])
 SIGNATURES["diagmm_sumsq_multi"] = (_i, [_i, C.POINTER(TensorDesc), _vp, _i, _vp])
 SIGNATURES["diagmm_clip_scale_tree"] = (_i, [_i, _vp, _d, _vp, _vp, _vp])

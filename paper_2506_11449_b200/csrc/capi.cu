@@ -25,13 +25,14 @@ int run_waterfill_batched(int, const diagmm_topk_job*, cudaStream_t);
 int run_select_hard(int, int, const double*, int32_t*, cudaStream_t);
 int run_active_from_list(int, int, const int32_t*, int32_t*, int32_t*, cudaStream_t);
 int run_topk_grad(int, int, double, const double*, const uint8_t*, const double*, double, double*, int,
-                  cudaStream_t);
+                  const double*, cudaStream_t);
 template <typename P>
 int run_adamw(size_t, void*, const void*, void*, void*, int, double, double, double, double, double,
               const double*, cudaStream_t);
 template <typename P> int run_sumsq(size_t, const void*, double*, double*, cudaStream_t);
 int run_clip_scale(int, const double*, double, double*, double*, cudaStream_t);
-int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, const double*, cudaStream_t);
+int run_adamw_multi(int, const diagmm_tensor*, double, double, double, double, const double*, const double*,
+                    cudaStream_t);
 int mt_sumsq_parts(int, const diagmm_tensor*);
 int run_sumsq_multi(int, const diagmm_tensor*, double*, int, cudaStream_t);
 int run_clip_scale_tree(int, const double*, double, double*, double*, cudaStream_t);
@@ -167,8 +168,8 @@ int diagmm_topk_waterfill_batched(int n, const diagmm_topk_job* jobs, void* stre
 }
 
 int diagmm_adamw_multi(int n, const diagmm_tensor* tensors, double lr, double beta1, double beta2,
-                       double eps, const double* clip_scale, void* stream) {
-  return run_adamw_multi(n, tensors, lr, beta1, beta2, eps, clip_scale, S(stream));
+                       double eps, const double* clip_scale, const double* sched, void* stream) {
+  return run_adamw_multi(n, tensors, lr, beta1, beta2, eps, clip_scale, sched, S(stream));
 }
 int diagmm_sumsq_multi_len(int n, const diagmm_tensor* tensors) {
   return n > 0 && tensors ? mt_sumsq_parts(n, tensors) : 0;
@@ -260,8 +261,8 @@ int diagmm_layernorm_bwd_res(int M, int D, const void* x, const void* dy, const 
 
 int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, const uint8_t* clamped,
                      const double* g_soft, double l1_coeff, double* g_alpha, int accumulate,
-                     void* stream) {
-  return run_topk_grad(C, k, temperature, alpha, clamped, g_soft, l1_coeff, g_alpha, accumulate,
+                     const double* params, void* stream) {
+  return run_topk_grad(C, k, temperature, alpha, clamped, g_soft, l1_coeff, g_alpha, accumulate, params,
                        S(stream));
 }
 

@@ -180,16 +180,19 @@ __device__ __forceinline__ void adamw_range(const diagmm_tensor& d, size_t i0, s
 
 __global__ void __launch_bounds__(256)
 k_adamw_multi(const __grid_constant__ MtTable T, double lr, double b1, double b2, double eps,
-              const double* __restrict__ clip_scale) {
+              const double* __restrict__ clip_scale, const double* __restrict__ sched) {
   const int t = mt_find(T, blockIdx.x);
   const diagmm_tensor& d = T.t[t];
   const size_t i0 = (size_t)(blockIdx.x - T.first[t]) * kMtChunk;
   const size_t i1 = i0 + kMtChunk < d.n ? i0 + kMtChunk : d.n;
   const double s = clip_scale ? *clip_scale : 1.0;
+  // sched (device {lr, 1 - b1^t, 1 - b2^t}, host-computed): a CUDA-graph replay of the step
+  const double bc1 = sched ? sched[1] : T.bc1[t], bc2 = sched ? sched[2] : T.bc2[t];
+  if (sched) lr = sched[0];
   if (d.dtype == DIAGMM_F64)
-    adamw_range<double>(d, i0, i1, lr, b1, b2, eps, s, T.bc1[t], T.bc2[t]);
+    adamw_range<double>(d, i0, i1, lr, b1, b2, eps, s, bc1, bc2);
   else
-    adamw_range<float>(d, i0, i1, (float)lr, (float)b1, (float)b2, (float)eps, (float)s, T.bc1[t], T.bc2[t]);
+    adamw_range<float>(d, i0, i1, (float)lr, (float)b1, (float)b2, (float)eps, (float)s, bc1, bc2);
 }
 
 // per-chunk sum of squares of the gradients, written to part[first_out + block]
@@ -274,7 +277,7 @@ int mt_sumsq_parts(int n, const diagmm_tensor* ts) {
 }
 
 int run_adamw_multi(int n, const diagmm_tensor* ts, double lr, double b1, double b2, double eps,
-                    const double* clip_scale, cudaStream_t st) {
+                    const double* clip_scale, const double* sched, cudaStream_t st) {
   if (int e = mt_check(n, ts)) return e;
   for (int i = 0; i < n; ++i)
     if (ts[i].step < 1 || ts[i].param == nullptr || ts[i].m == nullptr || ts[i].v == nullptr)
@@ -284,7 +287,7 @@ int run_adamw_multi(int n, const diagmm_tensor* ts, double lr, double b1, double
       T.bc1[i] = 1.0 - pow(b1, (double)T.t[i].step);
       T.bc2[i] = 1.0 - pow(b2, (double)T.t[i].step);
     }
-    k_adamw_multi<<<chunks, 256, 0, st>>>(T, lr, b1, b2, eps, clip_scale);
+    k_adamw_multi<<<chunks, 256, 0, st>>>(T, lr, b1, b2, eps, clip_scale, sched);
     note_launch();
   });
   return status_from_cuda();

@@ -119,8 +119,9 @@ struct WaterfillJobs { diagmm_topk_job j[kMaxJobs]; };
 __global__ void __launch_bounds__(kSelThreads)
 k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
   const diagmm_topk_job& J = jobs.j[blockIdx.x];
-  const int C = J.C, k = J.k;
-  const double temperature = J.temperature;
+  // device {T, k} (a CUDA-graph replay of an annealing schedule) or the launch values
+  const int C = J.C, k = J.params ? (int)J.params[1] : J.k;
+  const double temperature = J.params ? J.params[0] : J.temperature;
   const double* __restrict__ alpha = J.alpha;
   double* __restrict__ asoft = J.alpha_soft;
   uint8_t* __restrict__ clamped = J.clamped;
@@ -274,9 +275,11 @@ __device__ double block_reduce_max(double v, double* buf) {
 }
 
 __global__ void __launch_bounds__(kSelThreads)
-k_topk_grad(int C, int k, double temperature, const double* __restrict__ alpha,
+k_topk_grad(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
             const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
-            double* __restrict__ g_alpha, int accumulate) {
+            double* __restrict__ g_alpha, int accumulate, const double* __restrict__ params) {
+  const int k = params ? (int)params[1] : k_arg;
+  const double temperature = params ? params[0] : t_arg;
   extern __shared__ __align__(16) unsigned char smem[];
   double* q = reinterpret_cast<double*>(smem);  // C
   double* buf = q + C;                          // blockDim
@@ -358,7 +361,7 @@ int run_waterfill_batched(int n, const diagmm_topk_job* jobs, cudaStream_t st) {
 
 int run_waterfill(int C, int k, double T, const double* alpha, double* asoft, uint8_t* clamped,
                   int32_t* active, int32_t* slot, int32_t* n_act, cudaStream_t st) {
-  diagmm_topk_job j{C, k, T, alpha, asoft, clamped, active, slot, n_act};
+  diagmm_topk_job j{C, k, T, alpha, asoft, clamped, active, slot, n_act, nullptr};
   return run_waterfill_batched(1, &j, st);
 }
 
@@ -384,14 +387,15 @@ int run_active_from_list(int C, int n, const int32_t* offs, int32_t* slot, int32
 }
 
 int run_topk_grad(int C, int k, double T, const double* alpha, const uint8_t* clamped,
-                  const double* up, double l1, double* g_alpha, int accumulate, cudaStream_t st) {
+                  const double* up, double l1, double* g_alpha, int accumulate, const double* params,
+                  cudaStream_t st) {
   if (C < 1) return DIAGMM_ESHAPE;
   if (!(T > 0.0)) return DIAGMM_ETEMPERATURE;
   if (k < 1 || k > C) return DIAGMM_EK;
   if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
   size_t sm = (size_t)C * 8 + kSelThreads * 8;
   cudaFuncSetAttribute(k_topk_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_topk_grad<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, clamped, up, l1, g_alpha, accumulate);
+  k_topk_grad<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, clamped, up, l1, g_alpha, accumulate, params);
   note_launch();
   return status_from_cuda();
 }

@@ -56,3 +56,51 @@ def schedules_constant(model: torch.nn.Module) -> bool:
 
     return all(m.t_schedule.kind == "constant" or m.t_schedule.t_init == m.t_schedule.t_final
                for m in model.modules() if isinstance(m, DiagLinear))
+
+
+class GraphedTrainStep:
+    """The WHOLE training step — soft TopK re-selection, forward, backward, global-norm
+    clip and AdamW — captured as ONE CUDA graph and replayed for every step of an
+    annealing / sparsity schedule: the per-step scalars (temperature, k, learning
+    rate, Adam bias corrections) come from ``schedule.DeviceSchedule``'s device buffer,
+    which ``step()`` refreshes (stream-ordered) before each replay.
+
+    ``fwd_bwd(*inputs)`` runs forward + backward and returns what the caller wants
+    back (loss, outputs); it must not read anything back to the host.  The warm-up
+    (allocator pools, library handles) runs forward + backward only, so the
+    parameters are untouched until the first ``step()``."""
+
+    def __init__(self, fwd_bwd, specs, optimizer, clipper, schedule, *static_inputs, warmup: int = 1,
+                 first_step: int = 0):
+        self.inputs, self.opt, self.sched = static_inputs, optimizer, schedule
+        dev = static_inputs[0].device
+        for s in specs:
+            s.tensor.grad = None
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                schedule.set_step(first_step)
+                fwd_bwd(*static_inputs)
+                for s in specs:
+                    s.tensor.grad = None
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = _lib.load().diagmm_launch_count()
+        with torch.cuda.graph(self.graph):
+            self.out = fwd_bwd(*static_inputs)
+            _, scale = clipper.compute(specs)
+            self.norm = _
+            optimizer.step(clip_scale=scale, sched=schedule.adam)
+        self.launches = _lib.load().diagmm_launch_count() - n0
+        torch.cuda.synchronize(dev)
+
+    def step(self, step: int, *inputs: torch.Tensor, lr: float | None = None):
+        self.sched.set_step(step, lr=lr)
+        for dst, src in zip(self.inputs, inputs):
+            if src is not dst:
+                dst.copy_(src, non_blocking=True)
+        self.graph.replay()
+        self.opt.advance_steps()
+        return self.out

@@ -97,6 +97,7 @@ class _OpSpec:
     presel: ops.Selection | None = None
     l1: float = 0.0  # set by penalties(fused=True): the l1 gradient is added inside K5
     bucket: torch.Tensor | None = None  # dp.CompactGradExchange: K3 also writes the active rows here
+    params: torch.Tensor | None = None  # schedule.DeviceSchedule: device {T, k} read by K4 / K5
     sel: ops.Selection | None = None    # the selection the forward used (set by the forward)
 
 
@@ -141,7 +142,8 @@ class DiagMMFunction(torch.autograd.Function):
     def forward(ctx, x, values, alpha, bias, spec: _OpSpec, residual=None):
         M, N = spec.M, spec.N
         if alpha is not None:
-            sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+            sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature,
+                                                      params=spec.params)
         else:
             sel = spec.fixed
         spec.sel = sel
@@ -211,7 +213,7 @@ class DiagMMFunction(torch.autograd.Function):
                 dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft, bucket=spec.bucket)
         if need_soft:
             g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
-                                         clamped=sel.clamped, l1_coeff=spec.l1)
+                                         clamped=sel.clamped, l1_coeff=spec.l1, params=spec.params)
         return dx, g_values, g_alpha, g_bias, None, d_res
 
 
@@ -224,8 +226,8 @@ class DiagMLPFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, v1, a1, b1, v2, a2, b2, s1: _OpSpec, s2: _OpSpec, fuse_fwd: bool = True, residual=None):
-        sel1 = s1.presel or ops.soft_topk_select(a1.detach(), s1.k, s1.temperature)
-        sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature)
+        sel1 = s1.presel or ops.soft_topk_select(a1.detach(), s1.k, s1.temperature, params=s1.params)
+        sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature, params=s2.params)
         s1.sel, s2.sel = sel1, sel2
         x = x.contiguous()
         W1 = ops.materialize(v1.detach(), sel1, s1.M, s1.N, dtype=x.dtype)
@@ -260,12 +262,14 @@ class DiagMLPFunction(torch.autograd.Function):
         d_pre = ops.tc_gemm_nn(dy, W2, None, epilogue=2, aux=pre)
         gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True,
                                                bucket=s2.bucket)
-        ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1)
+        ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1,
+                                 params=s2.params)
         # fc1
         dx = ops.tc_gemm_nn(d_pre, W1)
         gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True,
                                                bucket=s1.bucket)
-        ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1)
+        ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1,
+                                 params=s1.params)
         hb1, hb2 = ctx.has_bias
         d_res = dy0 if ctx.needs_input_grad[10] else None
         return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None, d_res)
@@ -383,7 +387,8 @@ class DiagLinear(nn.Module):
     def _make_spec(self, step: int) -> "_OpSpec":
         T = self.temperature(step)
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
-                       presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None))
+                       presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None),
+                       params=getattr(self, "_sched_params", None))
         self._last_spec = spec
         return spec
 
@@ -607,7 +612,8 @@ def preselect(layers, step: int) -> None:
     if not layers:
         return
     temps = [m.temperature(step) for m in layers]
-    sels = ops.soft_topk_select_many([m.alpha.detach() for m in layers], [m.k for m in layers], temps)
+    sels = ops.soft_topk_select_many([m.alpha.detach() for m in layers], [m.k for m in layers], temps,
+                                     params=[getattr(m, "_sched_params", None) for m in layers])
     for m, T, sel in zip(layers, temps, sels):
         m._presel = ((step, m.k, T), sel)
 

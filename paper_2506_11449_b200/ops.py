@@ -112,25 +112,30 @@ def new_selection(C: int, device, k: int = 1, temperature: float = 1.0) -> Selec
 
 
 def soft_topk_select(alpha: torch.Tensor, k: int, temperature: float,
-                     out: Selection | None = None, host_copy: bool = False) -> Selection:
+                     out: Selection | None = None, host_copy: bool = False,
+                     params: torch.Tensor | None = None) -> Selection:
     """K4: soft_topk + clamped set + active set (selection.py:100-142, layers.py:234).
 
     Nothing is read back to the host unless ``host_copy`` (or a later
-    ``host_count()``) asks for the active count."""
-    return soft_topk_select_many([alpha], [k], [temperature], [out], host_copy=host_copy)[0]
+    ``host_count()``) asks for the active count.  ``params``: a device float64
+    pair {T, k} the kernel reads instead of (temperature, k) — set per step by
+    schedule.DeviceSchedule, so a captured CUDA graph replays an annealing run."""
+    return soft_topk_select_many([alpha], [k], [temperature], [out], host_copy=host_copy,
+                                 params=[params])[0]
 
 
-def soft_topk_select_many(alphas, ks, temperatures, outs=None, host_copy: bool = False) -> list:
+def soft_topk_select_many(alphas, ks, temperatures, outs=None, host_copy: bool = False, params=None) -> list:
     """Batched K4: every selection in ONE launch (one CTA each) — the per-step
     re-selection of all DiagLinear layers of a model (layers.py:233 per layer)."""
     n = len(alphas)
     if not (len(ks) == len(temperatures) == n):
         raise ValueError("alphas, ks and temperatures must have the same length")
     outs = list(outs) if outs is not None else [None] * n
+    params = list(params) if params is not None else [None] * n
     jobs = (_lib.TopkJob * max(1, n))()
     sels = []
     stream = None
-    for i, (alpha, k, T, out) in enumerate(zip(alphas, ks, temperatures, outs)):
+    for i, (alpha, k, T, out, prm) in enumerate(zip(alphas, ks, temperatures, outs, params)):
         _need_cuda(alpha)
         if alpha.dtype != torch.float64 or alpha.dim() != 1:
             raise ShapeMismatch("alpha must be a float64 vector")
@@ -139,8 +144,10 @@ def soft_topk_select_many(alphas, ks, temperatures, outs=None, host_copy: bool =
         sel = out if out is not None else new_selection(C, a.device)
         sel.k, sel.temperature = int(k), float(T)
         sel._alpha_keepalive = a
+        if prm is not None and (prm.dtype != torch.float64 or prm.numel() != 2 or not prm.is_cuda):
+            raise ShapeMismatch("params must be a device float64 pair {T, k}")
         jobs[i] = _lib.TopkJob(C, int(k), float(T), _p(a), _p(sel.alpha_soft), _p(sel.clamped),
-                               _p(sel.active), _p(sel.slot), _p(sel.n_act))
+                               _p(sel.active), _p(sel.slot), _p(sel.n_act), _p(prm))
         stream = _stream(a) if stream is None else stream
         sels.append(sel)
     if n:
@@ -159,18 +166,20 @@ def soft_topk(alpha: torch.Tensor, k: int, temperature: float) -> torch.Tensor:
 
 def soft_topk_grad(alpha: torch.Tensor, k: int, temperature: float, upstream: torch.Tensor,
                    clamped: torch.Tensor | None = None, l1_coeff: float = 0.0,
-                   out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
-    """K5: soft_topk_grad (selection.py:145-173) [+ l1 * sign(alpha)]."""
+                   out: torch.Tensor | None = None, accumulate: bool = False,
+                   params: torch.Tensor | None = None) -> torch.Tensor:
+    """K5: soft_topk_grad (selection.py:145-173) [+ l1 * sign(alpha)]; ``params`` as for
+    soft_topk_select."""
     _need_cuda(alpha, upstream)
     a = alpha.contiguous()
     up = upstream.to(torch.float64).contiguous()
     if up.shape != a.shape:
         raise ValueError("upstream must match alpha's shape")
     if clamped is None:
-        clamped = soft_topk_select(a, k, temperature, host_copy=False).clamped
+        clamped = soft_topk_select(a, k, temperature, host_copy=False, params=params).clamped
     g = out if out is not None else torch.empty_like(a)
     _lib.call("diagmm_topk_grad", a.numel(), int(k), float(temperature), _p(a), _p(clamped), _p(up),
-              float(l1_coeff), _p(g), int(bool(accumulate)), _stream(a))
+              float(l1_coeff), _p(g), int(bool(accumulate)), _p(params), _stream(a))
     return g
 
 
@@ -286,8 +295,8 @@ def diag_backward_weight(dy: torch.Tensor, x: torch.Tensor, values: torch.Tensor
     if dy.shape[0] != x.shape[0]:
         raise ShapeMismatch("dy and x disagree on the batch size")
     C, L = geometry(M, N)
-    if max_act is None:
-        max_act = sel.host_count()
+    if max_act is None:  # grid sized by the candidate count, the device count bounds the work: no host sync
+        max_act = C
     B = x.shape[0]
     dy = dy.contiguous()
     x = x.contiguous().to(dy.dtype)

@@ -92,7 +92,12 @@ class AdamW:
         ]
 
     @torch.no_grad()
-    def step(self, lr: float | None = None, clip_scale: torch.Tensor | None = None) -> None:
+    def step(self, lr: float | None = None, clip_scale: torch.Tensor | None = None,
+             sched: torch.Tensor | None = None) -> None:
+        """One AdamW update of every tensor.  ``sched``: a device float64 triple
+        {lr, 1 - beta1^t, 1 - beta2^t} the kernel reads instead of ``lr`` and the
+        host step count (schedule.DeviceSchedule writes it before each replay of a
+        captured step)."""
         lr = self.lr if lr is None else lr
         b1, b2 = self.betas
         descs, keep = [], []
@@ -114,7 +119,17 @@ class AdamW:
             return
         arr = (_lib.TensorDesc * len(descs))(*descs)
         _lib.call("diagmm_adamw_multi", len(descs), arr, float(lr), float(b1), float(b2), float(self.eps),
-                  None if clip_scale is None else clip_scale.data_ptr(), stream)
+                  None if clip_scale is None else clip_scale.data_ptr(),
+                  None if sched is None else sched.data_ptr(), stream)
+
+    def next_step(self) -> int:
+        """The (1-based) step count of the next update (for host-computed bias corrections)."""
+        return max((st["t"] for st in self.state), default=0) + 1
+
+    def advance_steps(self) -> None:
+        """Host bookkeeping after an update that ran inside a replayed CUDA graph."""
+        for st in self.state:
+            st["t"] += 1
 
     def zero_grad(self) -> None:
         for s in self.specs:

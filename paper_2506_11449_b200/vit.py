@@ -78,7 +78,7 @@ class QKVAttentionFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, values, alpha, bias, spec, B, T, H, causal=False):
         M, N = spec.M, spec.N
-        sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature)
+        sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature, params=spec.params)
         spec.sel = sel
         vals = values.detach()
         W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
@@ -111,7 +111,7 @@ class QKVAttentionFunction(torch.autograd.Function):
         ga = None
         if need_soft:
             ga = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, gs, clamped=sel.clamped,
-                                    l1_coeff=spec.l1)
+                                    l1_coeff=spec.l1, params=spec.params)
         return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None, None
 
 

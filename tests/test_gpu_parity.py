@@ -920,3 +920,84 @@ def test_diagheur_forward_backward_vs_oracle(dtype, shape):
     assert scaled_err(xt.grad.cpu().numpy(), gx) <= tol
     assert scaled_err(lyr.values.grad.cpu().numpy(), gv) <= tol
     assert scaled_err(lyr.bias.grad.cpu().numpy(), up.sum(0)) <= tol
+
+
+def test_graphed_annealing_trajectory_vs_reference_golden():
+    """The golden 5-step trajectory (cosine T 2.0 -> 0.05, l1, clip 1.0, AdamW) replayed
+    from ONE captured CUDA graph of the whole step (K4 at the step's T read from the
+    device schedule buffer, forward, backward, K5, clip, AdamW with device bias
+    corrections): every step bit-exact masks and the reference's values."""
+    from paper_2506_11449_b200.graphed import GraphedTrainStep
+    from paper_2506_11449_b200.schedule import DeviceSchedule
+
+    g = load_golden("trajectory")
+    lyr = DiagLinear(32, 48, 0.8, seed=21, l1_coeff=1e-3, dtype=torch.float64,
+                     t_schedule=TemperatureSchedule("cosine", 2.0, 0.05, 5))
+    with torch.no_grad():
+        lyr.alpha.copy_(t(g["alpha_init"]))
+    specs = lyr.param_specs()
+    opt = AdamW(specs, lr=5e-2, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5)
+    sched = DeviceSchedule(lyr, opt)
+    x_buf, up_buf = t(g["xs"][0]).clone(), t(g["ups"][0]).clone()
+
+    def fwd_bwd(x, up):
+        y = lyr(x, step=0)  # T and k come from the device schedule, not the host step
+        ((y * up).sum() + lyr.penalty()).backward()
+        return y
+
+    gs = GraphedTrainStep(fwd_bwd, specs, opt, GlobalNormClipper(1.0), sched, x_buf, up_buf)
+    for s in range(5):
+        y = gs.step(s, t(g["xs"][s]), t(g["ups"][s]))
+        torch.cuda.synchronize()
+        assert scaled_err(y.detach().cpu().numpy(), g[f"s{s}_y"]) <= 1e-10, s
+        np.testing.assert_allclose(gs.norm.item(), float(g[f"s{s}_norm"]), rtol=1e-10)
+        assert scaled_err(lyr.values.detach().cpu().numpy(), g[f"s{s}_values"]) <= 1e-9, s
+        assert scaled_err(lyr.alpha.detach().cpu().numpy(), g[f"s{s}_alpha"]) <= 1e-9, s
+        assert scaled_err(lyr.bias.detach().cpu().numpy(), g[f"s{s}_bias"]) <= 1e-9, s
+        np.testing.assert_array_equal(lyr.active_set(s).cpu().numpy(), g[f"s{s}_active"])
+    assert gs.launches > 0
+    sched.detach()
+
+
+def test_graphed_step_with_set_k_schedule_matches_eager():
+    """A sparsity schedule that changes k between replays (set_k, training.py:608-619):
+    the graphed step (k from the device buffer) equals the eager step bit for bit."""
+    from paper_2506_11449_b200.graphed import GraphedTrainStep
+    from paper_2506_11449_b200.schedule import DeviceSchedule
+
+    rng = np.random.default_rng(12)
+    xs = [t(rng.standard_normal((16, 64)), torch.float32) for _ in range(4)]
+    ks = [40, 30, 22, 19]
+    finals = []
+    for graphed in (False, True):
+        lyr = DiagLinear(64, 96, 0.8, seed=2, l1_coeff=1e-3, dtype=torch.float32,
+                         t_schedule=TemperatureSchedule("linear", 1.0, 0.05, 4))
+        specs = lyr.param_specs()
+        opt, clip = AdamW(specs, lr=1e-2), GlobalNormClipper(1.0)
+        masks = []
+        if graphed:
+            sched = DeviceSchedule(lyr, opt)
+            xb = xs[0].clone()
+
+            def fwd_bwd(x):
+                y = lyr(x, step=0)
+                (y.square().mean() + lyr.penalty()).backward()
+                return y
+
+            gs = GraphedTrainStep(fwd_bwd, specs, opt, clip, sched, xb)
+        for s in range(4):
+            lyr.set_k(ks[s])
+            if graphed:
+                gs.step(s, xs[s])
+            else:
+                opt.zero_grad()
+                y = lyr(xs[s], step=s)
+                (y.square().mean() + lyr.penalty()).backward()
+                _, sc = clip.compute(specs)
+                opt.step(clip_scale=sc)
+            masks.append(lyr.active_set(s).cpu().numpy())
+        finals.append(([p.detach().clone() for p in lyr.parameters()], masks))
+    for a, b in zip(finals[0][0], finals[1][0]):
+        assert torch.equal(a, b)
+    for a, b in zip(finals[0][1], finals[1][1]):
+        np.testing.assert_array_equal(a, b)
