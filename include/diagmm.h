@@ -165,6 +165,19 @@ DIAGMM_API int diagmm_topk_grad(int C, int k, double temperature, const double* 
                      double l1_coeff, double* g_alpha, int accumulate,
                      const double* params, void* stream);
 
+/* ---- DiagHeur prune / regrow (layers.py:381-413) ------------------------
+ * In place on the device: prune the n_prune active diagonals of smallest L2
+ * value norm (ties -> smaller offset, np.lexsort((active, norms))), regrow the
+ * grow_idx[i]-th (0-based) offsets of the ascending list of offsets inactive
+ * before the swap with zero values, and rewrite active (first k entries,
+ * ascending) / slot / *n_act.  grow_idx (n_prune,) device int32 =
+ * rng.choice(C - k, n_prune, replace=False) on the reference's host RNG
+ * (numpy's rng.choice(pool, n) is pool[rng.choice(len(pool), n)]).
+ * values (C, L) DIAGMM_F64 or DIAGMM_F32. */
+DIAGMM_API int diagmm_diagheur_update(int dtype, int C, int L, int k, int32_t* active, int32_t* slot,
+                                      int32_t* n_act, void* values, int n_prune, const int32_t* grow_idx,
+                                      void* stream);
+
 /* ---- hard TopK: select_hard (selection.py:176-186) -----------------------
  * idx (k,) = indices of the k largest alpha, ties to the smaller index,
  * ascending. */

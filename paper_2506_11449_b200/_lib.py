@@ -35,6 +35,7 @@ SIGNATURES = {
     "diagmm_topk_waterfill": (_i, [_i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "diagmm_topk_grad": (_i, [_i, _i, _d, _vp, _vp, _vp, _d, _vp, _i, _vp, _vp]),
     "diagmm_select_hard": (_i, [_i, _i, _vp, _vp, _vp]),
+    "diagmm_diagheur_update": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
     "diagmm_active_from_list": (_i, [_i, _i, _vp, _vp, _vp, _vp]),
     "diagmm_adamw": (_i, [_i, _sz, _vp, _vp, _vp, _vp, _i, _d, _d, _d, _d, _d, _vp, _vp]),
     "diagmm_sumsq_scratch_len": (_i, []),

@@ -23,6 +23,8 @@ int run_waterfill(int, int, double, const double*, double*, uint8_t*, int32_t*, 
                   cudaStream_t);
 int run_waterfill_batched(int, const diagmm_topk_job*, cudaStream_t);
 int run_select_hard(int, int, const double*, int32_t*, cudaStream_t);
+template <typename P>
+int run_diagheur_update(int, int, int, int32_t*, int32_t*, int32_t*, void*, int, const int32_t*, cudaStream_t);
 int run_active_from_list(int, int, const int32_t*, int32_t*, int32_t*, cudaStream_t);
 int run_topk_grad(int, int, double, const double*, const uint8_t*, const double*, double, double*, int,
                   const double*, cudaStream_t);
@@ -264,6 +266,15 @@ int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, cons
                      const double* params, void* stream) {
   return run_topk_grad(C, k, temperature, alpha, clamped, g_soft, l1_coeff, g_alpha, accumulate, params,
                        S(stream));
+}
+
+int diagmm_diagheur_update(int dtype, int C, int L, int k, int32_t* active, int32_t* slot, int32_t* n_act,
+                           void* values, int n_prune, const int32_t* grow_idx, void* stream) {
+  if (dtype == DIAGMM_F64)
+    return run_diagheur_update<double>(C, L, k, active, slot, n_act, values, n_prune, grow_idx, S(stream));
+  if (dtype == DIAGMM_F32)
+    return run_diagheur_update<float>(C, L, k, active, slot, n_act, values, n_prune, grow_idx, S(stream));
+  return DIAGMM_ESHAPE;
 }
 
 int diagmm_select_hard(int C, int k, const double* alpha, int32_t* idx, void* stream) {

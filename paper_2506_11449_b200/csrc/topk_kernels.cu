@@ -400,4 +400,94 @@ int run_topk_grad(int C, int k, double T, const double* alpha, const uint8_t* cl
   return status_from_cuda();
 }
 
+// DiagHeur prune / regrow (layers.py:381-413) on the device, one CTA:
+// L2 norms of the k active rows (float64), a stable ascending sort by
+// (norm, offset) (np.lexsort((active, norms)), ties -> smaller offset), the
+// first n_prune are pruned; the regrown offsets are grow_idx[i]-th entries of
+// the ascending list of the offsets inactive BEFORE the swap (numpy's
+// rng.choice(pool, n) is pool[rng.choice(len(pool), n)], so the host draws only
+// the indices from the reference's RNG stream); their value rows are zeroed,
+// and the new active set (sorted survivors + grown) is compacted in place.
+template <typename P>
+__global__ void __launch_bounds__(kSelThreads)
+k_diagheur_update(int C, int L, int k, int32_t* __restrict__ active, int32_t* __restrict__ slot,
+                  int32_t* __restrict__ n_act, P* __restrict__ values, int n_prune,
+                  const int32_t* __restrict__ grow_idx) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NP = next_pow2(k);
+  double* key = reinterpret_cast<double*>(smem);                          // NP
+  int* idx = reinterpret_cast<int*>(key + NP);                            // NP
+  int* inact = idx + NP;                                                  // C
+  int* ibuf = inact + C;                                                  // blockDim
+  unsigned char* flag = reinterpret_cast<unsigned char*>(ibuf + blockDim.x);  // C
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int i = tid; i < C; i += blockDim.x) flag[i] = 0;
+  for (int i = tid; i < NP; i += blockDim.x) {
+    key[i] = -CUDART_INF;
+    idx[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int j = tid; j < k; j += blockDim.x) flag[active[j]] = 1;
+  // ---- norms of the active rows: one warp per row, fixed lane order + shuffle tree
+  for (int j = warp; j < k; j += nw) {
+    const int o = active[j];
+    const P* row = values + (size_t)o * L;
+    double acc = 0.0;
+    for (int t = lane; t < L; t += 32) {
+      const double v = (double)row[t];
+      acc = fma(v, v, acc);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) {
+      key[j] = -sqrt(acc);  // descending sort of -norm = ascending norm; ties -> smaller offset
+      idx[j] = o;
+    }
+  }
+  __syncthreads();
+  bitonic_sort_desc(key, idx, NP);
+  // ---- the pool: offsets inactive before the swap, ascending
+  {
+    const int per = (C + blockDim.x - 1) / blockDim.x;
+    const int lo = min(C, tid * per), hi = min(C, lo + per);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += flag[i] ? 0 : 1;
+    int total = 0;
+    int pos = block_exclusive_scan(cnt, ibuf, &total);
+    for (int i = lo; i < hi; ++i)
+      if (!flag[i]) inact[pos++] = i;
+  }
+  __syncthreads();
+  for (int i = tid; i < n_prune; i += blockDim.x) flag[idx[i]] = 0;
+  __syncthreads();
+  for (int i = tid; i < n_prune; i += blockDim.x) flag[inact[grow_idx[i]]] = 1;
+  // regrown rows start from zero (the reference's values[grown] = 0)
+  for (int i = warp; i < n_prune; i += nw) {
+    P* row = values + (size_t)inact[grow_idx[i]] * L;
+    for (int t = lane; t < L; t += 32) row[t] = P(0);
+  }
+  __syncthreads();
+  compact_flags(flag, C, active, slot, n_act, ibuf);
+}
+
+template <typename P>
+int run_diagheur_update(int C, int L, int k, int32_t* active, int32_t* slot, int32_t* n_act, void* values,
+                        int n_prune, const int32_t* grow_idx, cudaStream_t st) {
+  if (C < 1 || L < 1 || k < 1 || k > C || n_prune < 0 || n_prune > k || n_prune > C - k) return DIAGMM_ESHAPE;
+  if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  if (n_prune == 0) return DIAGMM_OK;
+  int NP = 1;
+  while (NP < k) NP <<= 1;
+  const size_t sm = (size_t)NP * 12 + (size_t)C * 4 + kSelThreads * 4 + C + 16;
+  cudaFuncSetAttribute(k_diagheur_update<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_diagheur_update<P><<<1, kSelThreads, sm, st>>>(C, L, k, active, slot, n_act, static_cast<P*>(values), n_prune,
+                                                   grow_idx);
+  note_launch();
+  return status_from_cuda();
+}
+template int run_diagheur_update<double>(int, int, int, int32_t*, int32_t*, int32_t*, void*, int, const int32_t*,
+                                         cudaStream_t);
+template int run_diagheur_update<float>(int, int, int, int32_t*, int32_t*, int32_t*, void*, int, const int32_t*,
+                                        cudaStream_t);
+
 }  // namespace diagmm

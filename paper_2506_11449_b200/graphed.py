@@ -88,11 +88,13 @@ class GraphedTrainStep:
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
         n0 = _lib.load().diagmm_launch_count()
+        steps0 = [st["t"] for st in optimizer.state]
         with torch.cuda.graph(self.graph):
             self.out = fwd_bwd(*static_inputs)
-            _, scale = clipper.compute(specs)
-            self.norm = _
+            self.norm, scale = clipper.compute(specs)
             optimizer.step(clip_scale=scale, sched=schedule.adam)
+        for st, t0 in zip(optimizer.state, steps0):  # capture ran no update: undo its host bookkeeping
+            st["t"] = t0
         self.launches = _lib.load().diagmm_launch_count() - n0
         torch.cuda.synchronize(dev)
 

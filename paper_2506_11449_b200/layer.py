@@ -528,7 +528,11 @@ class FrozenDiagLinear(nn.Module):
 
 
 class DiagHeurLinear(nn.Module):
-    """Magnitude-prune / random-regrow baseline over whole diagonals (layers.py:313-378)."""
+    """Magnitude-prune / random-regrow baseline over whole diagonals (layers.py:313-378).
+
+    The active set lives on the device (a Selection: active / slot / n_act) and
+    ``diagheur_update`` swaps it in place with one kernel; ``active`` reads it
+    back as a sorted numpy array (the reference's attribute)."""
 
     def __init__(self, in_features: int, out_features: int, sparsity: float = 0.9, *,
                  update_every: int = 100, prune_fraction: float = 0.3, bias: bool = True,
@@ -549,13 +553,23 @@ class DiagHeurLinear(nn.Module):
         device = torch.device(device) if device is not None else torch.device("cuda")
         self.values = nn.Parameter(torch.from_numpy(vals).to(device=device, dtype=pdt))
         self.bias = nn.Parameter(torch.zeros(M, device=device, dtype=pdt)) if bias else None
-        self.active = np.sort(rng.choice(self.candidates, self.k, replace=False))
-        self._sel = None
+        self._sel = ops.selection_from_offsets(
+            self.candidates, torch.as_tensor(np.sort(rng.choice(self.candidates, self.k, replace=False)),
+                                             device=device))
+
+    @property
+    def active(self) -> np.ndarray:
+        """Sorted active offsets (host copy of the device set)."""
+        return self._sel.active[: self.k].cpu().numpy().astype(np.int64)
+
+    @active.setter
+    def active(self, offsets) -> None:
+        offs = np.sort(np.asarray(offsets, dtype=np.int64))
+        if offs.size != self.k:
+            raise ValueError(f"DiagHeur keeps exactly k={self.k} diagonals")
+        self._sel = ops.selection_from_offsets(self.candidates, torch.as_tensor(offs, device=self.values.device))
 
     def _selection(self) -> ops.Selection:
-        if self._sel is None:
-            offs = torch.as_tensor(self.active, device=self.values.device)
-            self._sel = ops.selection_from_offsets(self.candidates, offs)
         return self._sel
 
     def forward(self, x: torch.Tensor, step: int = 0) -> torch.Tensor:
@@ -574,31 +588,38 @@ class DiagHeurLinear(nn.Module):
         return specs
 
     def effective_matrix(self, step: int = 0) -> DiagMatrix:
-        act = torch.as_tensor(self.active, device=self.values.device)
+        act = self._sel.active[: self.k].long()
         return DiagMatrix(self.out_features, self.in_features, act, self.values.detach()[act])
 
 
 def diagheur_update(layer: DiagHeurLinear, rng: np.random.Generator, step: int | None = None,
                     total_steps: int | None = None) -> DiagHeurLinear:
-    """layers.py:381-413: prune the weakest ceil(frac*k) diagonals, regrow at random."""
+    """layers.py:381-413: prune the ceil(frac*k) weakest diagonals (L2 norm, ties ->
+    smaller offset), regrow as many uniformly random inactive ones with zero values.
+    Everything runs on the device (diagmm_diagheur_update); the host only draws the
+    regrowth indices from the reference's RNG stream (rng.choice(pool, n) ==
+    pool[rng.choice(len(pool), n)]) — no device-to-host copy."""
     frac = layer.prune_fraction
     if step is not None and total_steps:
         frac = frac * 0.5 * (1.0 + np.cos(np.pi * min(step, total_steps) / total_steps))
     n = min(ceil(frac * layer.k), layer.candidates - layer.k)
     if n <= 0:
         return layer
-    act = torch.as_tensor(layer.active, device=layer.values.device)
-    norms = torch.linalg.vector_norm(layer.values.detach()[act].double(), dim=1).cpu().numpy()
-    order = np.lexsort((layer.active, norms))
-    pruned = layer.active[order[:n]]
-    survivors = np.setdiff1d(layer.active, pruned)
-    pool_mask = np.ones(layer.candidates, dtype=bool)
-    pool_mask[layer.active] = False
-    grown = rng.choice(np.flatnonzero(pool_mask), n, replace=False)
+    idx = rng.choice(layer.candidates - layer.k, n, replace=False)
+    sel = layer._sel
+    dev = layer.values.device
+    grow = torch.as_tensor(idx.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+    code = 0 if layer.values.dtype == torch.float64 else 1
+    from . import _lib
+
     with torch.no_grad():
-        layer.values[torch.as_tensor(grown, device=layer.values.device)] = 0.0
-    layer.active = np.sort(np.concatenate([survivors, grown]))
-    layer._sel = None
+        _lib.call("diagmm_diagheur_update", code, layer.candidates, layer.diag_len, layer.k, sel.active.data_ptr(),
+                  sel.slot.data_ptr(), sel.n_act.data_ptr(), layer.values.data_ptr(), int(n), grow.data_ptr(),
+                  torch.cuda.current_stream(dev).cuda_stream)
+    sel.n_act_host = torch.full((1,), layer.k, dtype=torch.int32)
+    sel.event = torch.cuda.Event()
+    sel.event.record(torch.cuda.current_stream(dev))
+    layer._keep = grow  # the copy is stream-ordered; keep its source alive until it ran
     return layer
 
 

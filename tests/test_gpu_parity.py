@@ -1001,3 +1001,84 @@ def test_graphed_step_with_set_k_schedule_matches_eager():
         assert torch.equal(a, b)
     for a, b in zip(finals[0][1], finals[1][1]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_diagheur_update_on_device_vs_reference_golden():
+    """diagheur_update (layers.py:381-413) as one device kernel: prune by L2 norm, regrow
+    from the reference's RNG stream, zero the regrown rows — bit-exact active set and
+    values against the reference's own update."""
+    from paper_2506_11449_b200 import DiagHeurLinear, diagheur_update
+
+    g = load_golden("misc")
+    h = DiagHeurLinear(24, 40, 0.8, seed=41, prune_fraction=0.3, dtype=torch.float64)
+    np.testing.assert_array_equal(h.active, g["heur_active0"])
+    np.testing.assert_array_equal(h.values.detach().cpu().numpy(), g["heur_values0"])
+    n0 = ops._lib.load().diagmm_launch_count()
+    diagheur_update(h, np.random.default_rng(42), step=10, total_steps=100)
+    assert ops._lib.load().diagmm_launch_count() == n0 + 1  # one kernel
+    np.testing.assert_array_equal(h.active, g["heur_active1"])
+    np.testing.assert_array_equal(h.values.detach().cpu().numpy(), g["heur_values1"])
+    sel = h._selection()
+    slot = sel.slot.cpu().numpy()
+    assert sel.n_act.item() == h.k and np.all(slot[g["heur_active1"]] == np.arange(h.k)) and (slot >= 0).sum() == h.k
+
+
+@pytest.mark.parametrize("C_shape", [(768, 3072), (96, 64)])
+def test_diagheur_update_on_device_vs_oracle(C_shape):
+    """Larger layers and repeated updates against the oracle's diagheur_swap."""
+    from paper_2506_11449_b200 import DiagHeurLinear, diagheur_update
+
+    n_in, n_out = C_shape
+    h = DiagHeurLinear(n_in, n_out, 0.9, seed=3, prune_fraction=0.3, dtype=torch.float32)
+    rng_dev, rng_ref = np.random.default_rng(7), np.random.default_rng(7)
+    vals = h.values.detach().double().cpu().numpy()
+    act = h.active
+    for s in range(3):
+        with torch.no_grad():  # some zero rows / ties among the norms too
+            h.values[torch.as_tensor(act[:2], device=DEV)] = 0.0
+        vals[act[:2]] = 0.0
+        diagheur_update(h, rng_dev, step=s, total_steps=5)
+        vals, act = olayer.diagheur_swap(vals, act, h.k, h.candidates, 0.3, rng_ref, step=s, total_steps=5)
+        np.testing.assert_array_equal(h.active, act)
+        np.testing.assert_array_equal(h.values.detach().double().cpu().numpy(), vals.astype(np.float32))
+
+
+def test_checkpoint_load_reference_file_and_round_trip(tmp_path):
+    """load_checkpoint reads the checkpoint the REFERENCE wrote (training.py:721-766)
+    and predicts its logits; save_checkpoint writes the same schema back (atomic)
+    and reloads to the same predictions."""
+    import json
+
+    from diagtest_util import GOLDEN
+    from paper_2506_11449_b200.checkpoint import load_checkpoint, save_checkpoint
+    from paper_2506_11449_b200.errors import MalformedFile
+
+    io = load_golden("ref_checkpoint_io")
+    inf, cfg = load_checkpoint(str(GOLDEN / "ref_checkpoint.json"))
+    assert cfg["sparsity"] == 0.8
+    got = inf.predict_logits(io["x"]).cpu().numpy()
+    assert scaled_err(got, io["logits"]) <= 1e-12
+    # our writer, our reader: same predictions, the reference's schema
+    from paper_2506_11449_b200.vit import MLPModel
+
+    m = MLPModel(sizes=(48, 64, 40, 6), kinds=("dynadiag", "dynadiag", "dense"), dtype=torch.float64,
+                 t_schedule=TemperatureSchedule("cosine", 2.0, 0.05, 10))
+    path = tmp_path / "ck.json"
+    save_checkpoint(m, str(path), {"note": "test"})
+    doc = json.loads(path.read_text())
+    assert [e["kind"] for e in doc["layers"]] == ["frozen_diag", "frozen_diag", "dense"]
+    assert set(doc["layers"][0]["weight"]) == {"rows", "cols", "offsets", "values"}
+    assert np.asarray(doc["layers"][2]["weight"]).shape == (40, 6)  # (in, out) as the reference stores it
+    inf2, _ = load_checkpoint(str(path))
+    x = t(io["x"])
+    frozen = [lyr.freeze() if isinstance(lyr, DiagLinear) else lyr for lyr in m.layers]
+    h = x
+    for i, lyr in enumerate(frozen):
+        h = lyr(h)
+        if i < len(frozen) - 1:
+            h = torch.relu(h)
+    torch.testing.assert_close(inf2.predict_logits(io["x"]), h.detach(), rtol=1e-12, atol=1e-12)
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"layers": [{"kind": "nope", "bias": null}]}')
+    with pytest.raises(MalformedFile):
+        load_checkpoint(str(bad))
