@@ -917,10 +917,29 @@ int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32
   return status_from_cuda();
 }
 
+int run_tc_gemm2_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
+                      void* aux, int epi, cudaStream_t st, bool b_kn, const void* A1, const void* A2, int a_ks);
+
+// CTA-pair (cta_group::2) kernel when the problem fills every pair with 256 x 256
+// tiles; DIAGMM_TC_PAIR=0 forces the single-CTA kernel (A/B comparisons)
+static bool use_pair(int Mdim, int Ndim) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("DIAGMM_TC_PAIR");
+    mode = e ? atoi(e) : 1;
+  }
+  if (mode == 0) return false;
+  if (mode == 2) return true;
+  const long long tiles = (long long)ceil_div(Mdim, 256) * ceil_div(Ndim, 256);
+  return tiles >= num_sms() / 2;
+}
+
 int run_tc_gemm_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, const float* bias, void* out, int ldo,
                      void* aux, int epi, cudaStream_t st, bool b_kn, const void* A1, const void* A2, int a_ks) {
   using namespace tc;
   constexpr int BN = 256;
+  if (use_pair(Mdim, Ndim))
+    return run_tc_gemm2_bf16(Mdim, Ndim, K, A, B, bias, out, ldo, aux, epi, st, b_kn, A1, A2, a_ks);
   if (Mdim < 1 || Ndim < 1 || K < 1 || K % 8 || ldo < Ndim) return DIAGMM_ESHAPE;
   if (b_kn && Ndim % 8) return DIAGMM_ESHAPE;  // B (K, N) rows must be 16-byte multiples
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return DIAGMM_ESHAPE;
