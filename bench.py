@@ -96,8 +96,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip infer / diagmm kernel sections")
     p.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
-                   help="replay forward+backward as one CUDA graph (auto: when the temperature schedule is "
-                        "constant, so the captured TopK arguments stay valid)")
+                   help="replay the whole training step as one CUDA graph (auto/on: yes at N=1; the "
+                        "per-step schedule scalars come from a device buffer; off: eager)")
     p.add_argument("--cpu-sample-images", type=int, default=1)
     return p.parse_args()
 
@@ -317,6 +317,7 @@ class TrainHarness:
         # gradient hooks as the backward produces them (overlapped), finished before the clip
         self.exchange = CompactGradExchange(model) if world > 1 else None
         self.graph = None
+        self.sched = None
         self.graph_note = "off"
         self.step_no = 0
         self.label_smoothing = label_smoothing
@@ -348,8 +349,7 @@ class TrainHarness:
         inp = self.inputs if inp is None else inp
         lbl = self.labels if lbl is None else lbl
         if self.graph is not None:
-            loss = self.graph.step(inp, lbl)  # inputs copied into the captured buffers, replay
-            self.update()  # clip + AdamW eager: the Adam step count / bias corrections change every step
+            loss = self.graph.step(self.step_no, inp, lbl)  # schedule scalars + inputs in, one replay
         else:
             loss = self.fwd_bwd(self.step_no, inp, lbl)
             self.update()
@@ -363,25 +363,31 @@ class TrainHarness:
         self._torch.cuda.synchronize()
 
     def capture(self, mode="auto"):
-        from paper_2506_11449_b200.graphed import GraphedStep, schedules_constant
+        """Capture the WHOLE step (TopK at the step's T / k from the device schedule,
+        forward, backward, clip, AdamW) as one CUDA graph (graphed.GraphedTrainStep);
+        any temperature / sparsity schedule replays the same graph."""
+        from paper_2506_11449_b200.graphed import GraphedTrainStep
+        from paper_2506_11449_b200.schedule import DeviceSchedule
 
-        if not (mode == "on" or (mode == "auto" and schedules_constant(self.model))):
+        if mode == "off":
             return self.graph_note
         if self.exchange is not None:  # the exchange's per-layer launches read host-side counts: eager
             self.graph_note = "eager steps (data parallel: per-layer all-reduces overlapped with the backward)"
             return self.graph_note
         step = self.step_no
         try:
-            self.graph = GraphedStep(lambda i, l: self.fwd_bwd(step, i, l), [s_.tensor for s_ in self.specs],
-                                     self.inputs, self.labels)
-            self.graph_note = "forward+backward replayed as one CUDA graph; clip + AdamW eager"
+            self.sched = DeviceSchedule(self.model, self.opt)
+            self.graph = GraphedTrainStep(lambda i, l: self.fwd_bwd(step, i, l), self.specs, self.opt, self.clip,
+                                          self.sched, self.inputs, self.labels, first_step=step)
+            self.graph_note = ("whole step (TopK, forward, backward, clip, AdamW) replayed as one CUDA graph; "
+                               "per-step T / k / lr / Adam bias corrections from the device schedule buffer")
         except Exception as exc:  # noqa: BLE001 - a capture failure must not cost the measurement
             if mode == "on":
                 raise
             self.graph = None
             self.opt.zero_grad()
             self._torch.cuda.synchronize()
-            self.graph_note = f"capture failed ({type(exc).__name__}), eager steps"
+            self.graph_note = f"capture failed ({type(exc).__name__}: {exc}), eager steps"
         for _ in range(2):
             self.train_step()
         return self.graph_note
@@ -469,6 +475,8 @@ class TrainHarness:
     def release(self):
         if self.exchange is not None:
             self.exchange.remove()
+        if self.sched is not None:
+            self.sched.detach()
         self.graph = None
         self.opt = None
         self.specs = None
