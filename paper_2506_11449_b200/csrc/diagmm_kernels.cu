@@ -647,6 +647,166 @@ k_product_narrow(int B, int C, int L, const T* __restrict__ in, const typename T
   }
 }
 
+// --------------------------------------------------------------------------- few rows, one launch
+// B <= kRowsMax (weights dominate the traffic): ONE kernel, no pre-scale pass, no
+// partial buffer, no reduce launch.  A CTA owns 32 output positions (one per
+// lane) x BT rows; its 16 warps take interleaved slices of the active list and
+// are folded in a fixed order in shared memory; with NS > 1 the diagonal list is
+// also split over the NS CTAs of a thread-block cluster, folded through
+// distributed shared memory in rank order (deterministic).  Weights are formed
+// at use time (alpha_soft x the stored fp32 / fp64 value, the reference's
+// `weights`, layers.py:235); a lane loads its weight and its input elements
+// with coalesced warp-wide loads (32 consecutive positions), U diagonals ahead.
+constexpr int kRowsMax = 8;
+constexpr int kRowsWarps = 16;
+template <typename T, int BT, bool GATHER, int NS>
+__global__ void __launch_bounds__(kRowsWarps * 32)
+k_product_rows(int B, int C, int L, const T* __restrict__ in, const typename Traits<T>::P* __restrict__ vals,
+               const double* __restrict__ asoft, const int32_t* __restrict__ active,
+               const int32_t* __restrict__ n_act_p, int max_act, const typename Traits<T>::P* __restrict__ bias,
+               T* __restrict__ out) {
+  using A = typename Vec<T>::A;
+  using P = typename Traits<T>::P;
+  __shared__ A red[kRowsWarps][BT][32];
+  const int n_act = min(*n_act_p, max_act);
+  const int in_w = GATHER ? C : L, out_w = GATHER ? L : C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + lane;
+  const int b0 = blockIdx.y * BT;
+  const int nb = min(BT, B - b0);
+  const int rank = NS > 1 ? (int)blockIdx.z : 0;
+  in += (size_t)b0 * in_w;
+  A acc[BT];
+#pragma unroll
+  for (int b = 0; b < BT; ++b) acc[b] = A(0);
+  // diagonals of this warp: j = rank * kRowsWarps + warp + (NS * kRowsWarps) * q
+  constexpr int STRIDE = NS * kRowsWarps;
+  const int jfirst = rank * kRowsWarps + warp;
+  const int nq = n_act > jfirst ? (n_act - jfirst + STRIDE - 1) / STRIDE : 0;
+  constexpr int U = BT <= 2 ? 8 : 4;
+  for (int q0 = 0; q0 < nq; q0 += 32) {
+    // 32 diagonals' offsets and scales fetched lane-parallel, then shuffled out
+    int o_l = 0;
+    double s_l = 0.0;
+    if (q0 + lane < nq) {
+      o_l = __ldg(active + jfirst + STRIDE * (q0 + lane));
+      s_l = asoft ? __ldg(asoft + o_l) : 1.0;
+    }
+    const int cnt = min(32, nq - q0);
+    for (int qq = 0; qq < cnt; qq += U) {
+      P wr[U];
+      int xi[U];
+      double sc[U];
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int o = __shfl_sync(0xffffffffu, o_l, (qq + r) & 31);
+        sc[r] = __shfl_sync(0xffffffffu, s_l, (qq + r) & 31);
+        int c, xx;
+        bool ok;
+        if (GATHER) {
+          c = p;
+          ok = p < L;
+          xx = p + o;
+          xx = xx >= C ? xx - C : xx;
+        } else {
+          c = p - o;
+          c = c < 0 ? c + C : c;
+          ok = p < C && c < L;
+          xx = c;
+        }
+        ok = ok && (qq + r < cnt);
+        wr[r] = ok ? __ldg(vals + (size_t)o * L + c) : P(0);
+        xi[r] = ok ? xx : 0;
+      }
+      A xv[U][BT];
+#pragma unroll
+      for (int r = 0; r < U; ++r)
+#pragma unroll
+        for (int b = 0; b < BT; ++b) xv[r][b] = b < nb ? to_acc<A>(__ldg(in + (size_t)b * in_w + xi[r])) : A(0);
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const A w = (A)(sc[r] * (double)wr[r]);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) acc[b] = fma(w, xv[r][b], acc[b]);
+      }
+    }
+  }
+  // fixed-order fold: the 16 warps, then (NS > 1) the cluster ranks
+#pragma unroll
+  for (int b = 0; b < BT; ++b) red[warp][b][lane] = acc[b];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      A sum = A(0);
+#pragma unroll
+      for (int w = 0; w < kRowsWarps; ++w) sum += red[w][b][lane];
+      red[0][b][lane] = sum;
+    }
+  }
+  if constexpr (NS > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (rank == 0 && warp == 0) {
+      for (int r = 1; r < NS; ++r) {
+        const A* peer = cluster.map_shared_rank(&red[0][0][0], r);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) red[0][b][lane] += peer[b * 32 + lane];
+      }
+    }
+    cluster.sync();  // peers keep their shared memory alive until rank 0 has read it
+    if (rank != 0) return;
+  }
+  if (warp == 0 && p < out_w) {
+    const A bz = bias ? (A)bias[p] : A(0);
+    for (int b = 0; b < nb; ++b) out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(red[0][b][lane] + bz);
+  }
+}
+
+template <typename T>
+static int run_product_rows(bool gather, int B, int C, int L, const void* in, const void* vals, const double* asoft,
+                            const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
+                            cudaStream_t st) {
+  using P = typename Traits<T>::P;
+  const int out_w = gather ? L : C;
+  const int tiles = ceil_div(out_w, 32) * ceil_div(B, kRowsMax);
+  // split the diagonal list over a cluster when the tiles leave SMs idle
+  int ns = 1;
+  while (ns < 8 && (long long)tiles * ns * 2 <= num_sms() && max_act >= ns * 2 * kRowsWarps * 4) ns *= 2;
+  const int bt = B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : 8));
+  auto tin = static_cast<const T*>(in);
+  auto tv = static_cast<const P*>(vals);
+  auto tb = static_cast<const P*>(bias);
+  auto to = static_cast<T*>(out);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ceil_div(out_w, 32), ceil_div(B, bt), ns);
+  cfg.blockDim = dim3(kRowsWarps * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = ns;
+  cfg.attrs = attr;
+  cfg.numAttrs = ns > 1 ? 1 : 0;
+#define DIAGMM_ROWS(BT, NS)                                                                                    \
+  if (bt == BT && ns == NS) {                                                                                  \
+    if (gather)                                                                                                \
+      cudaLaunchKernelEx(&cfg, k_product_rows<T, BT, true, NS>, B, C, L, tin, tv, asoft, active, n_act,        \
+                         max_act, tb, to);                                                                     \
+    else                                                                                                       \
+      cudaLaunchKernelEx(&cfg, k_product_rows<T, BT, false, NS>, B, C, L, tin, tv, asoft, active, n_act,       \
+                         max_act, tb, to);                                                                     \
+  }
+#define DIAGMM_ROWS_NS(BT) DIAGMM_ROWS(BT, 1) DIAGMM_ROWS(BT, 2) DIAGMM_ROWS(BT, 4) DIAGMM_ROWS(BT, 8)
+  DIAGMM_ROWS_NS(1) DIAGMM_ROWS_NS(2) DIAGMM_ROWS_NS(4) DIAGMM_ROWS_NS(8)
+#undef DIAGMM_ROWS_NS
+#undef DIAGMM_ROWS
+  note_launch();
+  return status_from_cuda();
+}
+
 // dW for narrow batches: one warp per diagonal, lanes over 128 positions, the
 // B-row contraction in registers; unscaled gw -> partial (finalized by
 // k_dw_finalize exactly like the wide path).
@@ -870,8 +1030,10 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   using V = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
   using VA = typename std::conditional<sizeof(A) == 8, double2, float4>::type;
   __shared__ double red[kWarps];
-  const int i = blockIdx.x;
   const int n_act = min(*n_act_p, max_act);
+  // persistent over candidate rows (grid-stride): ~90 % of the rows are a zero fill,
+  // far too little work per CTA to pay a CTA launch each
+  for (int i = blockIdx.x; i < C; i += gridDim.x) {
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
   const bool vec = L % VW == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0 &&
@@ -884,7 +1046,7 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
       for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
     }
     if (g_soft && threadIdx.x == 0) g_soft[i] = 0.0;
-    return;
+    continue;
   }
   const double sc = asoft ? asoft[i] : 1.0;
   const P* vrow = vals + (size_t)i * L;
@@ -947,8 +1109,14 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
       g_soft[i] = tot;
     }
+    __syncthreads();  // red is reused by the next row
+  }
   }
 }
+
+// one CTA per candidate row: measured faster than a persistent grid-stride loop
+// (4096^2, B = 1: 22.3 vs 26.6 us for the whole dW)
+static int finalize_grid(int C) { return C; }
 
 // Column sums of dy (bias gradient): 32-row partials, then a fixed-order fold.
 constexpr int kColRows = 32;
@@ -1306,6 +1474,18 @@ static void launch_product(const ProductPlan& p, cudaStream_t st, int B, int C, 
   note_launch();
 }
 
+// largest batch the one-launch few-rows kernel (k_product_rows) takes
+static int rows_max_b() {
+  static int v = -1;
+  if (v < 0) {
+    // measured (4096^2, 90 %, bf16): B = 1 fwd 6.0 vs 12.9 us (narrow kernel + reduce),
+    // B = 8 15.7 vs 13.4 us (the cluster-split staged kernel keeps B > 4)
+    const char* e = getenv("DIAGMM_ROWS_MAX_B");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
 // largest batch the narrow (staging-free) product kernels take (row blocks of 8)
 static int narrow_max_b() {
   static int v = -1;
@@ -1378,6 +1558,8 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
   if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
+  if (B <= rows_max_b())
+    return run_product_rows<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, st);
   if (B <= narrow_max_b())
     return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
                                  static_cast<A*>(ws), st);
@@ -1484,12 +1666,12 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   constexpr int VEC = vec_rows<T>();
   const int C = M > N ? M : N, L = M < N ? M : N;
   if (ws_bytes < dw_workspace<T>(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
-  int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * VEC, &parts, &rpp);
-  A* partial = static_cast<A*>(ws);
   const bool tall = M >= N;
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
+  int parts, rpp;
+  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * VEC, &parts, &rpp);
+  A* partial = static_cast<A*>(ws);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   if (B > 0 && B <= narrow_dw_max_b() && max_act > 0) {
     parts = 1;
@@ -1510,7 +1692,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<finalize_grid(C), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
                                        static_cast<P*>(bucket), bucket_rows);
   note_launch();
@@ -1603,7 +1785,7 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
       cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), st);
     }
   }
-  k_dw_finalize<T><<<C, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<finalize_grid(C), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
                                        static_cast<P*>(bucket), bucket_rows);
   note_launch();
