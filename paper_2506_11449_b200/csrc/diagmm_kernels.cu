@@ -1022,7 +1022,8 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
               const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
               const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
               typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
-              typename Traits<T>::P* __restrict__ bucket, int bucket_rows) {
+              typename Traits<T>::P* __restrict__ bucket, int bucket_rows,
+              const int32_t* __restrict__ active_rows) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
   static_assert(sizeof(A) == sizeof(P), "partials and values share the vector width");
@@ -1033,7 +1034,10 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   const int n_act = min(*n_act_p, max_act);
   // persistent over candidate rows (grid-stride): ~90 % of the rows are a zero fill,
   // far too little work per CTA to pay a CTA launch each
-  for (int i = blockIdx.x; i < C; i += gridDim.x) {
+  for (int ii = blockIdx.x; ii < (active_rows ? n_act : C); ii += gridDim.x) {
+  // active_rows: the CTAs walk the active list only (the zero rows are filled
+  // concurrently by k_zero_inactive on a side stream)
+  const int i = active_rows ? active_rows[ii] : ii;
   const int s = slot[i];
   P* grow = g_values + (size_t)i * L;
   const bool vec = L % VW == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0 &&
@@ -1117,6 +1121,48 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
 // one CTA per candidate row: measured faster than a persistent grid-stride loop
 // (4096^2, B = 1: 22.3 vs 26.6 us for the whole dW)
 static int finalize_grid(int C) { return C; }
+
+// The reference's zero rows of g_values (inactive candidates, layers.py:159-163)
+// and their g_soft, one CTA per candidate row; active rows are left to the finalize.
+template <typename P>
+__global__ void __launch_bounds__(256)
+k_zero_inactive(int C, int L, const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
+                P* __restrict__ g_values, double* __restrict__ g_soft) {
+  constexpr int VW = 16 / sizeof(P);
+  using V = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
+  const int i = blockIdx.x;
+  const int n_act = min(*n_act_p, max_act);
+  const int s = slot[i];
+  if (s >= 0 && s < n_act) return;
+  P* grow = g_values + (size_t)i * L;
+  if (L % VW == 0 && (reinterpret_cast<uintptr_t>(g_values) & 15) == 0) {
+    V* g4 = reinterpret_cast<V*>(grow);
+    for (int t = threadIdx.x; t < L / VW; t += blockDim.x) g4[t] = V{};
+  } else {
+    for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+  }
+  if (g_soft && threadIdx.x == 0) g_soft[i] = 0.0;
+}
+
+// A side stream per device for work that overlaps the main stream's kernels
+// inside one C-ABI call (fork / join through events: legal under CUDA-graph
+// capture, where it becomes two parallel branches).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream& side_stream() {
+  static SideStream ss[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& r = ss[dev & 15];
+  if (!r.s) {
+    cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+  }
+  return r;
+}
 
 // Column sums of dy (bias gradient): 32-row partials, then a fixed-order fold.
 constexpr int kColRows = 32;
@@ -1673,8 +1719,29 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * VEC, &parts, &rpp);
   A* partial = static_cast<A*>(ws);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
-  if (B > 0 && B <= narrow_dw_max_b() && max_act > 0) {
-    parts = 1;
+  const bool narrow = B > 0 && B <= narrow_dw_max_b() && max_act > 0;
+  if (narrow) parts = 1;
+  // side stream, concurrently with the dW kernels and the active-row finalize on
+  // `st` (disjoint outputs): the zero rows of g_values (+ g_soft) and the bias
+  // gradient; joined back into `st` at the end
+  SideStream& ss = side_stream();
+  cudaEventRecord(ss.fork, st);
+  cudaStreamWaitEvent(ss.s, ss.fork, 0);
+  k_zero_inactive<P><<<C, 256, 0, ss.s>>>(C, L, slot, n_act, max_act, static_cast<P*>(g_values), g_soft);
+  note_launch();
+  if (g_bias) {
+    A* cpart = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)));
+    if (B > 0) {
+      k_colsum_partial<T><<<dim3(ceil_div(M, 256), cparts), 256, 0, ss.s>>>(B, M, static_cast<const T*>(dy), cpart);
+      note_launch();
+      k_colsum_final<T><<<ceil_div(M, 32), 256, 0, ss.s>>>(M, cparts, cpart, static_cast<P*>(g_bias));
+      note_launch();
+    } else {
+      cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), ss.s);
+    }
+  }
+  cudaEventRecord(ss.join, ss.s);
+  if (narrow) {
     dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
     if (B <= 4) k_dw_narrow<T, 4><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
     else k_dw_narrow<T, 8><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
@@ -1692,21 +1759,11 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<finalize_grid(C), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<max_act > 0 ? max_act : 1, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
-                                       static_cast<P*>(bucket), bucket_rows);
+                                       static_cast<P*>(bucket), bucket_rows, active);
   note_launch();
-  if (g_bias) {
-    A* cpart = reinterpret_cast<A*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)));
-    if (B > 0) {
-      k_colsum_partial<T><<<dim3(ceil_div(M, 256), cparts), 256, 0, st>>>(B, M, static_cast<const T*>(dy), cpart);
-      note_launch();
-      k_colsum_final<T><<<ceil_div(M, 32), 256, 0, st>>>(M, cparts, cpart, static_cast<P*>(g_bias));
-      note_launch();
-    } else {
-      cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), st);
-    }
-  }
+  cudaStreamWaitEvent(st, ss.join, 0);
   return status_from_cuda();
 }
 
@@ -1787,7 +1844,7 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
   }
   k_dw_finalize<T><<<finalize_grid(C), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
-                                       static_cast<P*>(bucket), bucket_rows);
+                                       static_cast<P*>(bucket), bucket_rows, nullptr);
   note_launch();
   return status_from_cuda();
 }
