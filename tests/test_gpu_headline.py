@@ -44,10 +44,31 @@ TOKENS = 256 * 197  # ViT-B/16, 256 images per GPU
 SAMPLE_ROWS = 64
 
 
+MEASURED: dict = {}  # test -> the largest scaled error each check saw (written to gpurun_out/)
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    yield
+    import json
+    import os
+    from pathlib import Path
+
+    out = Path(os.environ.get("GRAFT_REPO_ROOT", Path(__file__).resolve().parents[1])) / "gpurun_out"
+    if out.is_dir() and MEASURED:
+        (out / "headline_parity_errors.json").write_text(json.dumps(MEASURED, indent=1, sort_keys=True))
+
+
+@pytest.fixture(autouse=True)
+def _name(request):
+    global _CUR
+    _CUR = request.node.name
+    yield
+
+
+_CUR = "?"
 
 
 def _layer(n_in, n_out, seed, T):
@@ -113,8 +134,10 @@ def _bf16(shape, seed, scale=1.0):
 
 
 def _err(got, want):
-    return scaled_err(got.double().cpu().numpy() if torch.is_tensor(got) else got,
-                      want.cpu().numpy() if torch.is_tensor(want) else want)
+    e = scaled_err(got.double().cpu().numpy() if torch.is_tensor(got) else got,
+                   want.cpu().numpy() if torch.is_tensor(want) else want)
+    MEASURED.setdefault(_CUR, []).append(e)
+    return e
 
 
 def _check_layer_grads(lyr, ref, dy64, x64, tol_w=DW_TOL):
@@ -310,7 +333,7 @@ def test_vit_depth2_step_vs_fp32_reference_model():
     ref_loss.backward()
 
     assert abs(loss.item() - (ref_loss.item() + pen)) <= 1e-2 * abs(ref_loss.item() + pen)
-    MODEL_TOL = 5e-2  # whole bf16 model (activations rounded at every layer) vs float32
+    MODEL_TOL = 1e-2  # whole bf16 model vs float32 (measured <= 2.6e-3 on B200, profiles/r02_headline_parity_errors.json)
     for m in model.diag_layers():
         r = refs[id(m)]
         dW = Wleaf[id(m)].grad.double()
@@ -389,7 +412,7 @@ def test_gpt2_block_step_vs_fp32_reference_model():
     ref_loss.backward()
 
     assert abs(loss.item() - (ref_loss.item() + pen)) <= 1e-2 * abs(ref_loss.item() + pen)
-    MODEL_TOL = 5e-2
+    MODEL_TOL = 2e-3  # measured <= 1.5e-4 on B200 (profiles/r02_headline_parity_errors.json)
     for m in model.diag_layers():
         g_values, g_alpha = _diag_grads_ref(m, refs[id(m)], W[id(m)].grad, T)
         assert _err(m.values.grad, g_values) <= MODEL_TOL
