@@ -40,6 +40,7 @@
 //    overlap one CTA's staging with another's FMAs.
 #include "common.cuh"
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1427,6 +1428,344 @@ k_gather_finish(int C, int L, const P* __restrict__ vals, const double* __restri
   }
 }
 
+// --------------------------------------------------------------------------- K1/K2 v6
+// Row-tiled products, v6 (bf16 / fp32, B above the few-rows kernels).  ncu of
+// the v4 kernel (profiles/r02_ncu_fma_*.txt) showed every diagonal waiting a
+// full memory latency on its weights: the register ring's loads sit behind
+// per-diagonal branches, so ptxas cannot count them on a scoreboard and waits
+// for all of them.  v6 moves the ring into shared memory:
+//  * weights are pre-scaled into a LANE-INTERLEAVED store — per 128-position
+//    tile, lane l's four positions (l + 32u) are adjacent — so one diagonal of
+//    one warp is 256 B (bf16) / 512 B (fp32) of contiguous memory, fetched by
+//    cp.async into a per-warp D-deep ring (explicit wait_group counts: the
+//    fetch of diagonal q + D - 1 overlaps the FMAs of diagonal q), and read back
+//    with ONE LDS.64 / LDS.128 per lane;
+//  * the staged input row is laid out so that every diagonal of a warp is a
+//    single warp-uniform base column: circular rows (C + 128-column halo) for
+//    the gather form and near-square scatter form, zero guard bands around the
+//    L real columns for tall scatter forms (C >= L + 128) — no per-position
+//    wrap or clamp in the inner loop;
+//  * per diagonal a lane issues G*4 LDS.128 and G*4*VEC FMAs plus ~10 other
+//    instructions: the shared-memory crossbar (one 16-byte unit per VEC FMAs)
+//    stays the only bound.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// acc[r] += x[r] * w  with the bf16 weight in the low (HI = 0) or high half of w2
+template <int HI>
+__device__ __forceinline__ void fma_vec_h(float (&a)[8], uint4 x, uint32_t w2) {
+  const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (HI == 0)
+      asm("{\n.reg .b16 x0, x1, w0, w1;\n"
+          "mov.b32 {x0, x1}, %2;\n"
+          "mov.b32 {w0, w1}, %3;\n"
+          "fma.rn.f32.bf16 %0, x0, w0, %0;\n"
+          "fma.rn.f32.bf16 %1, x1, w0, %1;\n}"
+          : "+f"(a[2 * i]), "+f"(a[2 * i + 1])
+          : "r"(xs[i]), "r"(w2));
+    else
+      asm("{\n.reg .b16 x0, x1, w0, w1;\n"
+          "mov.b32 {x0, x1}, %2;\n"
+          "mov.b32 {w0, w1}, %3;\n"
+          "fma.rn.f32.bf16 %0, x0, w1, %0;\n"
+          "fma.rn.f32.bf16 %1, x1, w1, %1;\n}"
+          : "+f"(a[2 * i]), "+f"(a[2 * i + 1])
+          : "r"(xs[i]), "r"(w2));
+  }
+}
+
+// Lane-interleaved pre-scaled weights: wil[(j * ntile + tile) * 128 + lane * 4 + u]
+// = s_j * values[o_j, c(p)] at position p = tile * 128 + lane + 32u (0 where the
+// reference has no entry or p >= out_w).  One thread = one lane's four weights
+// (reads coalesced per u, one vector store).
+constexpr int kIlJ = 4;  // diagonals per thread per pass (all their loads in flight together)
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_prescale_il(int C, int L, int out_w, int ntile, int gather, const typename Traits<T>::P* __restrict__ vals,
+              const double* __restrict__ asoft, const int32_t* __restrict__ active,
+              const int32_t* __restrict__ n_act_p, int max_act, typename WType<T>::type* __restrict__ wil) {
+  using P = typename Traits<T>::P;
+  using WT = typename WType<T>::type;
+  const int n_act = min(*n_act_p, max_act);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (tile, lane)
+  if (e >= ntile * kWarp) return;
+  const int tile = e >> 5, lane = e & 31;
+  for (int j0 = blockIdx.y * kIlJ; j0 < n_act; j0 += gridDim.y * kIlJ) {
+    int o[kIlJ];
+    double sc[kIlJ];
+    P v[kIlJ][4];
+#pragma unroll
+    for (int i = 0; i < kIlJ; ++i) o[i] = j0 + i < n_act ? __ldg(active + j0 + i) : -1;
+#pragma unroll
+    for (int i = 0; i < kIlJ; ++i) {
+      sc[i] = (o[i] >= 0 && asoft) ? __ldg(asoft + o[i]) : 1.0;
+      const P* vr = vals + (size_t)(o[i] >= 0 ? o[i] : 0) * L;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = tile * kWarpPos + lane + kWarp * u;
+        int c = p;
+        if (!gather) { c = p - o[i]; c = c < 0 ? c + C : c; }
+        v[i][u] = (o[i] >= 0 && p < out_w && c < L) ? __ldg(vr + c) : P(0);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kIlJ; ++i) {
+      if (o[i] < 0) break;
+      WT w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double x = sc[i] * (double)v[i][u];
+        if constexpr (sizeof(WT) == 2) w[u] = __double2bfloat16(x);
+        else w[u] = (WT)x;
+      }
+      WT* dst = wil + ((size_t)(j0 + i) * ntile + tile) * kWarpPos + lane * 4;
+      if constexpr (sizeof(WT) == 2) {
+        uint2 pk;
+        pk.x = (uint32_t)__bfloat16_as_ushort(w[0]) | ((uint32_t)__bfloat16_as_ushort(w[1]) << 16);
+        pk.y = (uint32_t)__bfloat16_as_ushort(w[2]) | ((uint32_t)__bfloat16_as_ushort(w[3]) << 16);
+        *reinterpret_cast<uint2*>(dst) = pk;
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
+
+template <typename T> struct V6Ring { static constexpr int D = 8; };   // bf16: 8 x 256 B per warp
+template <> struct V6Ring<float> { static constexpr int D = 8; };      // fp32: 8 x 512 B per warp
+template <typename T>
+__host__ __device__ constexpr int v6_wbytes() { return kWarpPos * (int)sizeof(typename WType<T>::type); }
+
+// staged tile | fold buffer (max) ; then the per-warp weight rings ; then the active list
+template <typename T>
+__host__ __device__ inline size_t v6_tile_bytes(int g, int stage_w, int pw, int nw, bool cluster) {
+  const size_t tile = (size_t)g * stage_w * 16;
+  const size_t row = (size_t)g * vec_rows<T>() * pw * kWarpPos * sizeof(typename Vec<T>::A);
+  const int dw = nw / pw;
+  const size_t red = (dw > 1 || cluster) ? (size_t)dw * row + (cluster ? row : 0) : 0;
+  return align16(tile > red ? tile : red);
+}
+template <typename T>
+__host__ __device__ inline size_t v6_smem(int g, int stage_w, int pw, int nw, bool cluster, int max_act) {
+  return v6_tile_bytes<T>(g, stage_w, pw, nw, cluster) + (size_t)nw * V6Ring<T>::D * v6_wbytes<T>() +
+         align16((size_t)(max_act > 0 ? max_act : 1) * sizeof(int32_t));
+}
+
+// MODE: 0 gather (circular row), 1 scatter circular (zeros beyond L), 2 scatter
+// with zero guard bands (C >= L + 128).  256 or 512 threads (blockDim.x);
+// PW position warps x DW = warps / PW diagonal warps.
+template <typename T, int G, int MODE>
+__global__ void __launch_bounds__(512, 1)
+k_product6(int B, int C, int L, const T* __restrict__ in, const typename WType<T>::type* __restrict__ wil,
+           int ntile, const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+           const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out, int PW, int nsplit, int stage_w,
+           int vec_ok) {
+  using U = typename Vec<T>::U;
+  using A = typename Vec<T>::A;
+  constexpr int VEC = vec_rows<T>();
+  constexpr int RT = G * VEC;
+  constexpr int D = V6Ring<T>::D;
+  constexpr int WB = v6_wbytes<T>();
+  constexpr bool kBf16 = sizeof(typename WType<T>::type) == 2;
+  using WV = typename std::conditional<kBf16, uint2, float4>::type;  // one lane's four weights
+  extern __shared__ __align__(128) unsigned char smem[];
+  U* xs = reinterpret_cast<U*>(smem);
+  A* red = reinterpret_cast<A*>(smem);  // reused after the main loop
+  const bool cluster_fold = nsplit > 1;
+  const int nthr = blockDim.x, nw = nthr >> 5;
+  unsigned char* rings = smem + v6_tile_bytes<T>(G, stage_w, PW, nw, cluster_fold);
+  int32_t* s_act = reinterpret_cast<int32_t*>(rings + nw * D * WB);
+  const int n_act = min(*n_act_p, max_act);
+  const int in_w = MODE == 0 ? C : L;
+  const int out_w = MODE == 0 ? L : C;
+  const int DW = nw / PW;
+  const int t0 = blockIdx.x * PW * kWarpPos;
+  const int b0 = blockIdx.y * RT;
+  const int lane = threadIdx.x & (kWarp - 1), warp = threadIdx.x >> 5;
+  const int pw = warp % PW, dw = warp / PW;
+  const int p0 = t0 + pw * kWarpPos;
+  const int tl = p0 / kWarpPos;
+
+  for (int i = threadIdx.x; i < n_act; i += nthr) s_act[i] = __ldg(active + i);
+  __syncthreads();
+  int lo1, hi1, lo2, hi2;
+  if (MODE == 0) { lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0; }
+  else scatter_ranges(s_act, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
+  const int len1 = hi1 - lo1;
+  const int total = p0 < out_w ? len1 + (hi2 - lo2) : 0;
+  const int per = (total + nsplit - 1) / nsplit;
+  const int cb = min(total, (int)blockIdx.z * per), ce = min(total, cb + per);
+  const int vb = cb + dw;
+  const int nq = ce - vb > 0 ? (ce - vb + DW - 1) / DW : 0;
+  unsigned char* ring = rings + warp * D * WB;
+  const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(wil) + (size_t)tl * WB + lane * 16;
+  const size_t jstride = (size_t)ntile * WB;
+  auto jof = [&](int q) {
+    const int v = vb + DW * q;
+    return v < len1 ? lo1 + v : lo2 + (v - len1);
+  };
+  auto issue = [&](int q) {
+    if (q < nq && lane * 16 < WB) cp_async16(ring + (q % D) * WB + lane * 16, wsrc + (size_t)jof(q) * jstride);
+    cp_async_commit();
+  };
+  // warp-uniform base column of diagonal q (see the staged-row modes above)
+  auto base_of = [&](int q) {
+    const int o = s_act[jof(q)];
+    int base;
+    if (MODE == 0) {
+      base = p0 + o;
+      base = base >= C ? base - C : base;
+    } else if (MODE == 1) {
+      base = p0 + C - o;
+      base = base >= C ? base - C : base;
+    } else {
+      int d = p0 - o;
+      d = d < -(kWarpPos - 1) ? d + C : (d > L - 1 ? d - C : d);
+      base = d + kWarpPos;
+    }
+    return base;
+  };
+  // the first D - 2 diagonals' weights are in flight while the rows are staged
+#pragma unroll
+  for (int q = 0; q < D - 2; ++q) issue(q);
+  const int c0 = MODE == 2 ? C - kWarpPos : 0;
+  stage_t<T, 16 / vec_rows<T>()>(xs, stage_w, stage_w, in, B, in_w, b0, G, c0, C, MODE == 0 ? C : L, vec_ok != 0);
+  __syncthreads();
+
+  A acc[G][kU][VEC];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int r = 0; r < VEC; ++r) acc[g][u][r] = A(0);
+
+  auto fmas = [&](const U (&xv)[G][kU], const WV& w) {
+    if constexpr (kBf16) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        fma_vec_h<0>(acc[g][0], xv[g][0], w.x);
+        fma_vec_h<1>(acc[g][1], xv[g][1], w.x);
+        fma_vec_h<0>(acc[g][2], xv[g][2], w.y);
+        fma_vec_h<1>(acc[g][3], xv[g][3], w.y);
+      }
+    } else {
+      const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) fma_vec(acc[g][u], xv[g][u], wv[u]);
+    }
+  };
+  auto load_x = [&](U (&xv)[G][kU], int base) {
+    const U* xr = xs + base + lane;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) xv[g][u] = xr[(size_t)g * stage_w + kWarp * u];
+  };
+  // Two diagonals per step: both weights and all 2*G*4 input units are requested
+  // before the first FMA.  The base columns of 32 diagonals are computed
+  // lane-parallel once and shuffled out.
+  int base_l = 0;
+  int q = 0;
+  for (; q + 1 < nq; q += 2) {
+    if ((q & 31) == 0) base_l = q + lane < nq ? base_of(q + lane) : 0;
+    __syncwarp();      // slots (q - 2) % D and (q - 1) % D were read by every lane ...
+    issue(q + D - 2);  // ... before they are refilled
+    issue(q + D - 1);
+    cp_async_wait<D - 2>();
+    __syncwarp();      // the other lanes' copies of slots q % D, (q + 1) % D are visible
+    const WV w0 = *reinterpret_cast<const WV*>(ring + (q % D) * WB + lane * sizeof(WV));
+    const WV w1 = *reinterpret_cast<const WV*>(ring + ((q + 1) % D) * WB + lane * sizeof(WV));
+    U x0[G][kU], x1[G][kU];
+    load_x(x0, __shfl_sync(0xffffffffu, base_l, q & 31));
+    load_x(x1, __shfl_sync(0xffffffffu, base_l, (q + 1) & 31));
+    fmas(x0, w0);
+    fmas(x1, w1);
+  }
+  if (q < nq) {  // odd tail
+    if ((q & 31) == 0) base_l = q + lane < nq ? base_of(q + lane) : 0;
+    __syncwarp();
+    issue(q + D - 2);
+    cp_async_wait<D - 2>();
+    __syncwarp();
+    const WV w0 = *reinterpret_cast<const WV*>(ring + (q % D) * WB + lane * sizeof(WV));
+    U x0[G][kU];
+    load_x(x0, __shfl_sync(0xffffffffu, base_l, q & 31));
+    fmas(x0, w0);
+  }
+  cp_async_wait<0>();
+
+  if (DW == 1 && !cluster_fold) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = p0 + lane + kWarp * u;
+      if (p >= out_w) continue;
+      const A bb = bias ? (A)bias[p] : A(0);
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int r = 0; r < VEC; ++r) {
+          const int b = b0 + g * VEC + r;
+          if (b < B) out[(size_t)b * out_w + p] = from_acc<T>(acc[g][u][r] + bb);
+        }
+    }
+    return;
+  }
+  // fixed-order fold of the DW diagonal slices (then the cluster ranks)
+  const int TT = PW * kWarpPos;
+  const int tt_shift = 31 - __clz(TT);
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int r = 0; r < VEC; ++r)
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        red[((size_t)dw * RT + g * VEC + r) * TT + pw * kWarpPos + lane + kWarp * u] = acc[g][u][r];
+  __syncthreads();
+  A* fin = red + (size_t)DW * RT * TT;
+  for (int i = threadIdx.x; i < RT * TT; i += nthr) {
+    const int b = i >> tt_shift, tt = i & (TT - 1);
+    const int p = t0 + tt;
+    A s = A(0);
+    for (int w = 0; w < DW; ++w) s += red[((size_t)w * RT + b) * TT + tt];
+    if (cluster_fold) {
+      fin[i] = s;
+    } else if (b0 + b < B && p < out_w) {
+      if (bias) s += (A)bias[p];
+      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+    }
+  }
+  if (cluster_fold) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int rank = (int)cl.block_rank(), nr = (int)cl.num_blocks();
+    const int per_r = (RT * TT + nr - 1) / nr;
+    const int i0 = rank * per_r, i1 = min(RT * TT, i0 + per_r);
+    for (int i = i0 + threadIdx.x; i < i1; i += nthr) {
+      const int b = i >> tt_shift, tt = i & (TT - 1);
+      const int p = t0 + tt;
+      if (b0 + b >= B || p >= out_w) continue;
+      A s = A(0);
+      for (int r = 0; r < nr; ++r) s += cl.map_shared_rank(fin, r)[i];
+      if (bias) s += (A)bias[p];
+      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+    }
+    cl.sync();
+  }
+}
+
 // ================================================================ host side
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -1581,6 +1920,160 @@ static int run_product_narrow(bool gather, int B, int C, int L, const void* in, 
   return status_from_cuda();
 }
 
+// ---- v6 planner: staged-row mode and (G, warps, PW, nsplit) by a per-SM cost model
+struct Plan6 {
+  int g = 0, nw = 0, pw = 0, ns = 1, gx = 0, gy = 0, stage_w = 0, mode = 0;
+  size_t smem = 0;
+};
+// smallest batch routed to v6 (0 = never): below it the cluster-split FW kernel,
+// which needs no pre-scale pass, is faster (4096^2 90 % bf16, B = 8: 16 vs 19.5 us)
+static int product_v6_min_b() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIAGMM_PRODUCT_V6");
+    const char* m = getenv("DIAGMM_V6_MIN_B");
+    v = (e && atoi(e) == 0) ? 0 : (m ? atoi(m) : 32);
+  }
+  return v;
+}
+template <typename T>
+static Plan6 plan_product6(bool gather, int B, int C, int L, int max_act) {
+  constexpr int VEC = vec_rows<T>();
+  const int out_w = gather ? L : C;
+  Plan6 best;
+  const int mode = gather ? 0 : (C >= L + kWarpPos ? 2 : 1);
+  const int stage_w = mode == 2 ? (L + 2 * kWarpPos + VEC - 1) / VEC * VEC : C + kWarpPos;
+  const double n = max_act > 0 ? max_act : 1;
+  // diagonals touching one 128-position tile
+  const double ndiag = gather ? n : n * std::min(1.0, (L + kWarpPos - 1.0) / C);
+  const double fma_rate = sizeof(T) == 2 ? 64.0 : 32.0;  // FMA / clk / SM at the shared-memory bound
+  const int sms = num_sms();
+  const size_t smem_sm = 228 * 1024;
+  double best_t = 1e30;
+  const int gs[2] = {2, 1};  // fp32 G = 4 spills with two diagonals' units in flight
+  const int ngs = 2;
+  for (int gi = 0; gi < ngs; ++gi) {
+    const int g = gs[gi];
+    const int rt = g * VEC;
+    for (int nw : {8, 16}) {
+      for (int pw : {16, 8, 4, 2, 1}) {
+        if (pw > nw || (pw > 1 && (pw / 2) * kWarpPos >= out_w)) continue;
+        const int dw = nw / pw;
+        for (int ns : {1, 2, 4, 8}) {
+          if (ns > 1 && ndiag / ns < 4.0 * dw) break;
+          const size_t sm = v6_smem<T>(g, stage_w, pw, nw, ns > 1, max_act);
+          if (sm > 227 * 1024) continue;
+          int res = (int)(smem_sm / (sm + 1024));
+          res = std::min(res, 2048 / (nw * 32));
+          res = std::min(res, 65536 / (nw * 32 * 128));  // 128 registers per thread
+          if (res < 1) continue;
+          const long long gx = ceil_div(out_w, pw * kWarpPos), gy = ceil_div(B, rt);
+          const long long ctas = gx * gy * ns;
+          // resident warps per SM hide the LDS -> FMA latency: below 16 the rate drops
+          const double per_sm = std::min<double>(res, std::ceil((double)ctas / sms));
+          const double warps = per_sm * nw;
+          const double rate = fma_rate * std::min(1.0, warps / 16.0);
+          const double work = pw * kWarpPos * (double)rt * ndiag / ns;  // FMAs per CTA
+          const double stage = (double)g * stage_w * 16 / 64.0;
+          const double fold = (dw > 1 || ns > 1) ? dw * (double)rt * pw * kWarpPos * 4 * 2 / 128.0 +
+                                                       (ns > 1 ? (double)rt * pw * kWarpPos * 4 * ns / 64.0 : 0)
+                                                 : 0.0;
+          const double waves = std::ceil((double)ctas / (res * (double)sms));
+          const double t = waves * (per_sm * work / rate + stage + fold + 1500.0);
+          if (t < best_t * 0.999) {
+            best_t = t;
+            best.g = g; best.nw = nw; best.pw = pw; best.ns = ns; best.gx = (int)gx; best.gy = (int)gy;
+            best.stage_w = stage_w; best.mode = mode; best.smem = sm;
+          }
+        }
+      }
+    }
+  }
+  return best;
+}
+template <typename T>
+static size_t v6_wil_bytes(bool gather, int C, int L, int max_act) {
+  const int out_w = gather ? L : C;
+  return align16((size_t)(max_act > 0 ? max_act : 1) * ceil_div(out_w, kWarpPos) * kWarpPos *
+                 sizeof(typename WType<T>::type));
+}
+
+template <typename T, int G, int MODE>
+static void launch_product6(const Plan6& p, cudaStream_t st, int B, int C, int L, const T* in,
+                            const typename WType<T>::type* wil, int ntile, const int32_t* active,
+                            const int32_t* n_act, int max_act, const typename Traits<T>::P* bias, T* out,
+                            int vec_ok) {
+  auto k = k_product6<T, G, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.gx, p.gy, p.ns);
+  cfg.blockDim = dim3(p.nw * kWarp);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (p.ns > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = p.ns;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, k, B, C, L, in, wil, ntile, active, n_act, max_act, bias, out, p.pw, p.ns, p.stage_w,
+                     vec_ok);
+  note_launch();
+}
+
+template <typename T, int G>
+static void launch_product6_m(const Plan6& p, cudaStream_t st, int B, int C, int L, const T* in,
+                              const typename WType<T>::type* wil, int ntile, const int32_t* active,
+                              const int32_t* n_act, int max_act, const typename Traits<T>::P* bias, T* out,
+                              int vec_ok) {
+  if (p.mode == 0) launch_product6<T, G, 0>(p, st, B, C, L, in, wil, ntile, active, n_act, max_act, bias, out, vec_ok);
+  else if (p.mode == 1) launch_product6<T, G, 1>(p, st, B, C, L, in, wil, ntile, active, n_act, max_act, bias, out, vec_ok);
+  else launch_product6<T, G, 2>(p, st, B, C, L, in, wil, ntile, active, n_act, max_act, bias, out, vec_ok);
+}
+
+template <typename T>
+static int run_product6(bool gather, int B, int C, int L, const void* in, const void* vals, const double* asoft,
+                        const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
+                        void* ws, cudaStream_t st) {
+  using P = typename Traits<T>::P;
+  using WT = typename WType<T>::type;
+  constexpr int VEC = vec_rows<T>();
+  const int out_w = gather ? L : C, in_w = gather ? C : L;
+  Plan6 p = plan_product6<T>(gather, B, C, L, max_act);
+  if (const char* f = getenv("DIAGMM_V6_FORCE")) {  // "G,warps,PW,nsplit" (tuning experiments)
+    int g, nw, pw, ns;
+    if (sscanf(f, "%d,%d,%d,%d", &g, &nw, &pw, &ns) == 4) {
+      p.g = g; p.nw = nw; p.pw = pw; p.ns = ns;
+      p.gx = ceil_div(out_w, pw * kWarpPos);
+      p.gy = ceil_div(B, g * VEC);
+      p.smem = v6_smem<T>(g, p.stage_w, pw, nw, ns > 1, max_act);
+    }
+  }
+  if (p.g == 0) return DIAGMM_ETOOLARGE;
+  if (getenv("DIAGMM_V6_DEBUG"))
+    fprintf(stderr, "[v6] %s B=%d C=%d L=%d k=%d: G=%d warps=%d PW=%d ns=%d grid=%dx%dx%d mode=%d smem=%zu\n",
+            gather ? "gather" : "scatter", B, C, L, max_act, p.g, p.nw, p.pw, p.ns, p.gx, p.gy, p.ns, p.mode, p.smem);
+  const int ntile = ceil_div(out_w, kWarpPos);
+  WT* wil = static_cast<WT*>(ws);
+  if (max_act > 0) {
+    const int jb = ceil_div(max_act, kIlJ);
+    dim3 grid(ceil_div(ntile * kWarp, 256), jb < 65535 ? jb : 65535);
+    k_prescale_il<T><<<grid, 256, 0, st>>>(C, L, out_w, ntile, gather ? 1 : 0, static_cast<const P*>(vals), asoft,
+                                           active, n_act, max_act, wil);
+    note_launch();
+  }
+  const int vec_ok = in_w % VEC == 0 && C % VEC == 0 && aligned16(in);
+  auto tin = static_cast<const T*>(in);
+  auto tb = static_cast<const P*>(bias);
+  auto to = static_cast<T*>(out);
+  if (p.g == 1) launch_product6_m<T, 1>(p, st, B, C, L, tin, wil, ntile, active, n_act, max_act, tb, to, vec_ok);
+  else launch_product6_m<T, 2>(p, st, B, C, L, tin, wil, ntile, active, n_act, max_act, tb, to, vec_ok);
+  return status_from_cuda();
+}
+
 // workspace = [compact weights (max_act x ldw) | split partials]
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
@@ -1590,7 +2083,11 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   const size_t wbytes = align16((size_t)(max_act > 0 ? max_act : 1) * w_ld<T>(out_w) * sizeof(typename WType<T>::type));
   const size_t narrow = B <= narrow_max_b()
                             ? (size_t)narrow_chunks(out_w, max_act, B) * B * out_w * sizeof(A) : 0;
-  const size_t wide = wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
+  size_t wide = wbytes + (p.nsplit > 1 ? (size_t)p.nsplit * B * out_w * sizeof(A) : 0);
+  if constexpr (sizeof(T) <= 4) {
+    const size_t v6 = v6_wil_bytes<T>(gather, C, L, max_act);
+    wide = wide > v6 ? wide : v6;
+  }
   return wide > narrow ? wide : narrow;
 }
 
@@ -1609,6 +2106,10 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   if (B <= narrow_max_b())
     return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
                                  static_cast<A*>(ws), st);
+  if constexpr (sizeof(T) <= 4) {
+    if (product_v6_min_b() > 0 && B >= product_v6_min_b())
+      return run_product6<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, ws, st);
+  }
   const int out_w = gather ? L : C, in_w = gather ? C : L;
   const int cols = gather ? C + kHalo : scatter_cols<T>(L);
   ProductPlan p = plan_product<T>(B, out_w, cols, max_act);
@@ -1668,15 +2169,20 @@ static int dw_win_cap(int C, int max_act, int dwj) {
 }
 
 // diagonals per dW CTA: 64, or 32 when 64-diagonal tiles would not cover the SMs
-static int dw_diags(int L, int max_act) {
-  const long long t64 = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, kDwGroups * 16);
-  return t64 < num_sms() ? kDwGroups * 8 : kDwGroups * 16;
+static int dw_diags(int C, int L, int max_act) {
+  const int n = max_act > 0 ? max_act : 1;
+  const long long t64 = (long long)ceil_div(L, kDwTile) * ceil_div(n, kDwGroups * 16);
+  int jw = t64 < num_sms() ? 8 : 16;
+  // a CTA stages the circular window spanned by its diagonals: spread offsets
+  // (high sparsity) take fewer diagonals per CTA so the window stays in shared
+  // memory (2 CTAs / SM) instead of falling back to the direct global gather
+  while (jw > 2 && kDwTile + 1.5 * kDwGroups * jw * (double)C / n > 3200.0) jw /= 2;
+  return kDwGroups * jw;
 }
-
-static void dw_parts(int B, int L, int max_act, int rb, int* parts, int* rows_per_part) {
+static void dw_parts(int B, int C, int L, int max_act, int rb, int* parts, int* rows_per_part) {
   // as many row parts as keep the grid within ONE wave at two resident CTAs
   // per SM (a second, partial wave would double the kernel time)
-  const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, dw_diags(L, max_act));
+  const long long tiles = (long long)ceil_div(L, kDwTile) * ceil_div(max_act > 0 ? max_act : 1, dw_diags(C, L, max_act));
   long long p = 2LL * num_sms() / tiles;
   if (p < 1) p = 1;
   const long long max_p = ceil_div(B, rb);
@@ -1694,7 +2200,7 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
   const int L = M < N ? M : N;
   const int C = M > N ? M : N;
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * vec_rows<T>(), &parts, &rpp);
+  dw_parts(B > 0 ? B : 1, C, L, max_act, kDwNG * vec_rows<T>(), &parts, &rpp);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
   const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
@@ -1716,7 +2222,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const T* aop = static_cast<const T*>(tall ? dy : x);
   const T* bop = static_cast<const T*>(tall ? x : dy);
   int parts, rpp;
-  dw_parts(B > 0 ? B : 1, L, max_act, kDwNG * VEC, &parts, &rpp);
+  dw_parts(B > 0 ? B : 1, C, L, max_act, kDwNG * VEC, &parts, &rpp);
   A* partial = static_cast<A*>(ws);
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const bool narrow = B > 0 && B <= narrow_dw_max_b() && max_act > 0;
@@ -1747,11 +2253,13 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
     else k_dw_narrow<T, 8><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
     note_launch();
   } else if (B > 0 && max_act > 0) {
-    const int dwj = dw_diags(L, max_act);
+    const int dwj = dw_diags(C, L, max_act);
     const int cap = dw_win_cap<T>(C, max_act, dwj);
     const size_t sm = dw_smem<T>(cap);
     const int vec_ok = C % VEC == 0 && L % VEC == 0 && aligned16(aop) && aligned16(bop);
-    auto k = dwj == kDwGroups * 16 ? k_dw<T, 16> : k_dw<T, 8>;
+    auto k = dwj == kDwGroups * 16 ? k_dw<T, 16>
+             : dwj == kDwGroups * 8 ? k_dw<T, 8>
+             : dwj == kDwGroups * 4 ? k_dw<T, 4> : k_dw<T, 2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid(ceil_div(L, kDwTile), ceil_div(max_act, dwj), parts);
     k<<<grid, kThreads, sm, st>>>(B, C, L, aop, bop, active, n_act, max_act, cap, rpp, partial, vec_ok);

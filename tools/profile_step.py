@@ -65,3 +65,12 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     step(4)
     torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=a.rows, max_name_column_width=70))
+# kernels only, by self device time
+ev = [e for e in prof.key_averages() if e.device_type.name == "CUDA" or getattr(e, "self_device_time_total", 0) > 0]
+tot = sum(getattr(e, "self_device_time_total", 0) for e in ev)
+print(f"\n# kernels by self device time (total {tot / 1e3:.2f} ms)")
+for e in sorted(ev, key=lambda e: -getattr(e, "self_device_time_total", 0))[:a.rows]:
+    t = getattr(e, "self_device_time_total", 0)
+    if t <= 0:
+        continue
+    print(f"{t / 1e3:8.3f} ms {100 * t / tot:5.1f}% x{e.count:4d}  {e.key[:110]}")
