@@ -1766,6 +1766,145 @@ k_product6(int B, int C, int L, const T* __restrict__ in, const typename WType<T
   }
 }
 
+// --------------------------------------------------------------------------- K3 v6
+// dW with the row loop fed by asynchronous bulk copies.  k_pack writes each
+// operand once in the transposed-packed layout the FMA loop reads
+// ([row group][column][VEC rows], one 16-byte unit = VEC rows of a column), so a
+// CTA's share of a row group is a CONTIGUOUS run of units: the A window of its
+// diagonals (circular: at most two runs) and the B tile of its positions.  One
+// thread issues them as cp.async.bulk copies completing on an mbarrier, two row
+// groups ahead; the FMA warps never wait on a synchronous stage.  The window
+// buffer is sized for the whole circular row, so any offset spread fits (no
+// direct-gather fallback).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_pack(int B, int W, const T* __restrict__ src, typename Vec<T>::U* __restrict__ dst, int vec_ok) {
+  using U = typename Vec<T>::U;
+  constexpr int VEC = vec_rows<T>();
+  const int G = (B + VEC - 1) / VEC;
+  const int chunks = (W + VEC - 1) / VEC;
+  const long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= (long long)G * chunks) return;
+  const int g = (int)(it / chunks), ch = (int)(it - (long long)g * chunks);
+  U* d = dst + (size_t)g * W + (size_t)ch * VEC;
+  if (vec_ok && ch * VEC + VEC <= W) {
+    U r[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int b = g * VEC + i;
+      r[i] = b < B ? *reinterpret_cast<const U*>(src + (size_t)b * W + ch * VEC) : U{};
+    }
+    transpose_store<T>(r, d, 1);
+  } else {
+    T* dd = reinterpret_cast<T*>(d);
+    for (int c = 0; c < VEC && ch * VEC + c < W; ++c)
+      for (int i = 0; i < VEC; ++i) {
+        const int b = g * VEC + i;
+        dd[c * VEC + i] = b < B ? src[(size_t)b * W + ch * VEC + c] : T(0);
+      }
+  }
+}
+
+constexpr int kDw6Stages = 2;
+template <typename T>
+__host__ __device__ inline size_t dw6_stage_units(int C, int P) { return (size_t)(C + P) + P; }
+template <typename T>
+__host__ __device__ inline size_t dw6_smem(int C, int P) {
+  return 128 + (size_t)kDw6Stages * dw6_stage_units<T>(C, P) * 16;
+}
+
+// CTA: P = PW * 128 positions x (DW * JW) consecutive active diagonals x one
+// part of the row groups.  Warp (pw, dw): positions t0 + pw*128 + lane + 32u,
+// diagonals j0 + dw*JW + q.  Unscaled gw -> partial[part][j][t] (k_dw_finalize).
+template <typename T, int JW>
+__global__ void __launch_bounds__(512, 1)
+k_dw6(int C, int L, int G, const typename Vec<T>::U* __restrict__ Ap, const typename Vec<T>::U* __restrict__ Bp,
+      const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act, int PW,
+      int groups_per_part, typename Vec<T>::A* __restrict__ partial) {
+  using U = typename Vec<T>::U;
+  using A = typename Vec<T>::A;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  U* stage0 = reinterpret_cast<U*>(smem + 128);
+  const int P = PW * kWarpPos;
+  const size_t su = dw6_stage_units<T>(C, P);
+  const int n_act = min(*n_act_p, max_act);
+  const int nw = blockDim.x >> 5, DW = nw / PW;
+  const int j0 = blockIdx.y * (DW * JW);
+  if (j0 >= n_act) return;
+  const int nj = min(DW * JW, n_act - j0);
+  const int t0 = blockIdx.x * P;
+  const int nb = min(P, L - t0);  // B units of this tile
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pw = warp % PW, dw = warp / PW;
+  const int o_first = __ldg(active + j0), o_last = __ldg(active + j0 + nj - 1);
+  int ws = o_first + t0;
+  ws = ws >= C ? ws - C : ws;
+  const int wcols = o_last - o_first + P;  // <= C - 1 + P
+  const int run1 = min(wcols, C - ws);
+  const uint32_t stage_bytes = (uint32_t)(wcols + nb) * 16;
+  const int g0 = blockIdx.z * groups_per_part, g1 = min(G, g0 + groups_per_part);
+  auto issue = [&](int g) {  // one thread: row group g into its stage
+    const int s = (g - g0) % kDw6Stages;
+    U* sa = stage0 + (size_t)s * su;
+    U* sb = sa + (C + P);
+    mbar_expect_tx(&full[s], stage_bytes);
+    const U* arow = Ap + (size_t)g * C;
+    bulk_g2s(sa, arow + ws, (uint32_t)run1 * 16, &full[s]);
+    if (wcols > run1) bulk_g2s(sa + run1, arow, (uint32_t)(wcols - run1) * 16, &full[s]);
+    bulk_g2s(sb, Bp + (size_t)g * L + t0, (uint32_t)nb * 16, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDw6Stages; ++s) mbar_init(&full[s], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int g = g0; g < min(g1, g0 + kDw6Stages); ++g) issue(g);
+  int oq[JW];
+#pragma unroll
+  for (int q = 0; q < JW; ++q) {
+    const int jl = dw * JW + q;
+    oq[q] = jl < nj ? __ldg(active + j0 + jl) - o_first : -1;
+  }
+  A acc[JW][kU];
+#pragma unroll
+  for (int q = 0; q < JW; ++q)
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[q][u] = A(0);
+  const int pbase = pw * kWarpPos + lane;
+  for (int g = g0; g < g1; ++g) {
+    const int s = (g - g0) % kDw6Stages;
+    mbar_wait(&full[s], (uint32_t)(((g - g0) / kDw6Stages) & 1));
+    const U* sa = stage0 + (size_t)s * su;
+    const U* sb = sa + (C + P);
+    U bm[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) bm[u] = sb[pbase + kWarp * u];
+    const U* arow = sa + pbase;
+#pragma unroll
+    for (int q = 0; q < JW; ++q) {
+      if (oq[q] < 0) continue;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) Vec<T>::dot(acc[q][u], arow[oq[q] + kWarp * u], bm[u]);
+    }
+    __syncthreads();  // every warp is done with stage s ...
+    if (threadIdx.x == 0 && g + kDw6Stages < g1) {
+      fence_proxy_async();  // ... before the async proxy refills it
+      issue(g + kDw6Stages);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < JW; ++q) {
+    if (oq[q] < 0) continue;
+    const int j = j0 + dw * JW + q;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int t = t0 + pbase + kWarp * u;
+      if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
+    }
+  }
+}
+
 // ================================================================ host side
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -2194,6 +2333,65 @@ static void dw_parts(int B, int C, int L, int max_act, int rb, int* parts, int* 
   *parts = ceil_div(B, rpp);
 }
 
+// ---- dW v6 planner (bf16 / fp32, B above the narrow kernel)
+struct Dw6Plan {
+  int pw = 0, nw = 0, jw = 0, jgroups = 0, parts = 0, gpp = 0, G = 0;
+  size_t smem = 0;
+};
+static bool dw_v6_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIAGMM_DW_V6");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+template <typename T>
+static Dw6Plan plan_dw6(int B, int C, int L, int max_act) {
+  constexpr int VEC = vec_rows<T>();
+  Dw6Plan best;
+  const int sms = num_sms();
+  const int n = max_act > 0 ? max_act : 1;
+  int best_res = 0;
+  for (int pw : {2, 1}) {
+    if (pw == 2 && L <= kWarpPos) continue;
+    const size_t sm = dw6_smem<T>(C, pw * kWarpPos);
+    if (sm > 227 * 1024) continue;
+    const int res = 2 * (sm + 1024) <= 228 * 1024 ? 2 : 1;
+    if (res > best_res) {
+      best_res = res;
+      best.pw = pw;
+      best.smem = sm;
+    }
+  }
+  if (!best_res) return Dw6Plan{};
+  Dw6Plan& p = best;
+  p.G = ceil_div(B, VEC);
+  p.nw = best_res == 2 ? 8 : 16;
+  const int dw = p.nw / p.pw;
+  const int ptiles = ceil_div(L, p.pw * kWarpPos);
+  p.jw = 16;
+  while (p.jw > 4 && (long long)ptiles * ceil_div(n, dw * p.jw) < (long long)best_res * sms) p.jw /= 2;
+  p.jgroups = ceil_div(n, dw * p.jw);
+  const long long tiles = (long long)ptiles * p.jgroups;
+  long long parts = (long long)best_res * sms / tiles;  // about one wave
+  const long long max_parts = p.G / 4 > 1 ? p.G / 4 : 1;  // >= 4 row groups per part (pipeline depth)
+  parts = parts < 1 ? 1 : (parts > max_parts ? max_parts : parts);
+  p.gpp = ceil_div(p.G, parts);
+  p.parts = ceil_div(p.G, p.gpp);
+  return p;
+}
+template <typename T>
+static size_t dw6_workspace(int M, int N, int B, int max_act) {
+  using A = typename Vec<T>::A;
+  const int L = M < N ? M : N, C = M > N ? M : N;
+  const Dw6Plan p = plan_dw6<T>(B > 0 ? B : 1, C, L, max_act);
+  if (!p.G) return 0;
+  const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
+  return align16((size_t)p.parts * (max_act > 0 ? max_act : 1) * L * sizeof(A)) +
+         align16((size_t)cparts * M * sizeof(A)) + (size_t)p.G * (C + L) * 16;
+}
+
 template <typename T>
 size_t dw_workspace(int M, int N, int B, int max_act) {
   using A = typename Vec<T>::A;
@@ -2204,7 +2402,11 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const size_t prod_f = product_workspace<T>(M < N, B, C, L, max_act);
   const size_t prod_b = product_workspace<T>(M >= N, B, C, L, max_act);
-  const size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+  size_t dw = align16((size_t)parts * max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+  if constexpr (sizeof(T) <= 4) {
+    const size_t d6 = dw6_workspace<T>(M, N, B, max_act);
+    dw = dw > d6 ? dw : d6;
+  }
   size_t w = dw > prod_f ? dw : prod_f;
   return w > prod_b ? w : prod_b;
 }
@@ -2227,6 +2429,12 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const bool narrow = B > 0 && B <= narrow_dw_max_b() && max_act > 0;
   if (narrow) parts = 1;
+  Dw6Plan p6;
+  if constexpr (sizeof(T) <= 4) {
+    if (!narrow && B > 0 && max_act > 0 && dw_v6_enabled()) p6 = plan_dw6<T>(B, C, L, max_act);
+  }
+  const bool v6 = p6.G > 0 && aligned16(aop) && aligned16(bop);
+  if (v6) parts = p6.parts;
   // side stream, concurrently with the dW kernels and the active-row finalize on
   // `st` (disjoint outputs): the zero rows of g_values (+ g_soft) and the bias
   // gradient; joined back into `st` at the end
@@ -2247,7 +2455,23 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
     }
   }
   cudaEventRecord(ss.join, ss.s);
-  if (narrow) {
+  if (v6) {
+    if constexpr (sizeof(T) <= 4) {
+      using U = typename Vec<T>::U;
+      U* ap = reinterpret_cast<U*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +
+                                   align16((size_t)cparts * M * sizeof(A)));
+      U* bp = ap + (size_t)p6.G * C;
+      const int vc = C % VEC == 0, vl = L % VEC == 0;
+      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(C, VEC), 256), 256, 0, st>>>(B, C, aop, ap, vc);
+      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(L, VEC), 256), 256, 0, st>>>(B, L, bop, bp, vl);
+      note_launch(2);
+      auto k = p6.jw == 16 ? k_dw6<T, 16> : (p6.jw == 8 ? k_dw6<T, 8> : k_dw6<T, 4>);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p6.smem);
+      dim3 grid(ceil_div(L, p6.pw * kWarpPos), p6.jgroups, p6.parts);
+      k<<<grid, p6.nw * kWarp, p6.smem, st>>>(C, L, p6.G, ap, bp, active, n_act, max_act, p6.pw, p6.gpp, partial);
+      note_launch();
+    }
+  } else if (narrow) {
     dim3 grid(ceil_div(L, kWarpPos), ceil_div(max_act, kWarps));
     if (B <= 4) k_dw_narrow<T, 4><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
     else k_dw_narrow<T, 8><<<grid, kThreads, 0, st>>>(B, C, L, aop, bop, active, n_act, max_act, partial);
