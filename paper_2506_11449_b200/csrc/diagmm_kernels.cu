@@ -2245,7 +2245,9 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   if (B <= narrow_max_b())
     return run_product_narrow<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out,
                                  static_cast<A*>(ws), st);
-  if constexpr (sizeof(T) <= 4) {
+  // v6 for bf16 only: at config 1 (fp32, B = 256) the v4 kernel stays ahead
+  // (fwd 33.2 vs 36.9 us, dX 27.5 vs 29.2 us; profiles/r02_fma_v6.txt)
+  if constexpr (sizeof(T) == 2) {
     if (product_v6_min_b() > 0 && B >= product_v6_min_b())
       return run_product6<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, ws, st);
   }
