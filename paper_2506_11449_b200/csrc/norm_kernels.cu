@@ -113,12 +113,15 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
     const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * D);
     const uint4* gr = reinterpret_cast<const uint4*>(dy + (size_t)row * D);
     const float mu = mean[row], rs = rstd[row];
-    uint4 cx[NV], cg[NV];
+    uint4 cx[NV], cg[NV], cr[NV];
+    // the skip-connection gradient is requested with x and dy (one memory latency per row, not two)
+    const uint4* rr_row = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * D) : nullptr;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 8;
       cx[i] = c < D ? xr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
       cg[i] = c < D ? gr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
+      cr[i] = (rr_row && c < D) ? rr_row[i * 32 + lane] : make_uint4(0, 0, 0, 0);
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -152,7 +155,7 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
       for (int e = 0; e < 8; ++e) o[e] = rs * (g[e] * wr[e] - s1 - (xh[e] - mu) * rs * s2);
       if (dres) {  // the skip connection's gradient, summed here instead of by a separate add
         float rr[8];
-        unpack8(reinterpret_cast<const uint4*>(dres + (size_t)row * D)[i * 32 + lane], rr);
+        unpack8(cr[i], rr);
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] += rr[e];
       }
