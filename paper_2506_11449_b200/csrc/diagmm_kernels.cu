@@ -1778,30 +1778,38 @@ k_product6(int B, int C, int L, const T* __restrict__ in, const typename WType<T
 // direct-gather fallback).
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_pack(int B, int W, const T* __restrict__ src, typename Vec<T>::U* __restrict__ dst, int vec_ok) {
+k_pack(int B, int W, const T* __restrict__ src, typename Vec<T>::U* __restrict__ dst, int stage_w, int c0,
+       int mod, int limit, int vec_ok) {
+  // dst[g][col] (col < stage_w) = VEC rows of source column sc = (c0 + col) mod `mod`, zero
+  // where sc >= limit or the row >= B: the packed rows of k_dw6 (stage_w = W, c0 = 0) and the
+  // staged-row layouts of the product kernels (circular halo / guard bands) in global memory
   using U = typename Vec<T>::U;
   constexpr int VEC = vec_rows<T>();
   const int G = (B + VEC - 1) / VEC;
-  const int chunks = (W + VEC - 1) / VEC;
+  const int chunks = (stage_w + VEC - 1) / VEC;
   const long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= (long long)G * chunks) return;
   const int g = (int)(it / chunks), ch = (int)(it - (long long)g * chunks);
-  U* d = dst + (size_t)g * W + (size_t)ch * VEC;
-  if (vec_ok && ch * VEC + VEC <= W) {
+  U* d = dst + (size_t)g * stage_w + (size_t)ch * VEC;
+  if (vec_ok && ch * VEC + VEC <= stage_w) {
+    const int sc = (int)(((long long)c0 + ch * VEC) % mod);
+    const bool valid = sc < limit;
     U r[VEC];
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
       const int b = g * VEC + i;
-      r[i] = b < B ? *reinterpret_cast<const U*>(src + (size_t)b * W + ch * VEC) : U{};
+      r[i] = (valid && b < B) ? *reinterpret_cast<const U*>(src + (size_t)b * W + sc) : U{};
     }
     transpose_store<T>(r, d, 1);
   } else {
     T* dd = reinterpret_cast<T*>(d);
-    for (int c = 0; c < VEC && ch * VEC + c < W; ++c)
+    for (int c = 0; c < VEC && ch * VEC + c < stage_w; ++c) {
+      const int sc = (int)(((long long)c0 + ch * VEC + c) % mod);
       for (int i = 0; i < VEC; ++i) {
         const int b = g * VEC + i;
-        dd[c * VEC + i] = b < B ? src[(size_t)b * W + ch * VEC + c] : T(0);
+        dd[c * VEC + i] = (sc < limit && b < B) ? src[(size_t)b * W + sc] : T(0);
       }
+    }
   }
 }
 
@@ -1902,6 +1910,215 @@ k_dw6(int C, int L, int G, const typename Vec<T>::U* __restrict__ Ap, const type
       const int t = t0 + pbase + kWarp * u;
       if (t < L) partial[((size_t)blockIdx.z * max_act + j) * L + t] = acc[q][u];
     }
+  }
+}
+
+// --------------------------------------------------------------------------- packed-direct (small B)
+// bf16, B = 5..8 (use_pk): the activations of the call are packed ONCE into the
+// staged-row layout of the v6 kernels (k_pack: VEC rows per 16-byte unit, circular
+// halo or guard bands) in global memory; at this size the packed rows (one 8-row
+// group x (C + 128) units) stay resident in each SM's L1, so the FMA loop reads its
+// input units with LDG.128 straight from L1 and no CTA stages anything.  Weights are
+// formed in the kernel from the stored values (a per-warp cp.async ring of the
+// diagonal's 128 raw values, 4-byte copies placed lane-interleaved, zero-filled where
+// the reference has no entry) and alpha_soft: no pre-scale launch.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+constexpr int kPkRing = 8;                      // diagonals in flight per warp
+constexpr int kPkSlot = kWarpPos * 4;           // 128 fp32 values
+template <typename T>
+__host__ __device__ inline size_t pk_smem(int g, bool cluster, int max_act) {
+  const size_t rings = (size_t)kWarps * kPkRing * kPkSlot;
+  const size_t row = (size_t)g * vec_rows<T>() * kWarpPos * sizeof(typename Vec<T>::A);
+  const size_t red = (size_t)kWarps * row + (cluster ? row : 0);
+  return rings + align16(red) + align16((size_t)(max_act > 0 ? max_act : 1) * sizeof(int32_t));
+}
+
+template <typename T, int G, int MODE>
+__global__ void __launch_bounds__(kThreads)
+k_product_pk(int B, int C, int L, const typename Vec<T>::U* __restrict__ xp, int stage_w,
+             const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
+             const int32_t* __restrict__ active, const int32_t* __restrict__ n_act_p, int max_act,
+             const typename Traits<T>::P* __restrict__ bias, T* __restrict__ out, int nsplit) {
+  using U = typename Vec<T>::U;
+  using A = typename Vec<T>::A;
+  using P = typename Traits<T>::P;
+  constexpr int VEC = vec_rows<T>();
+  constexpr int RT = G * VEC;
+  constexpr int D = kPkRing;
+  static_assert(sizeof(P) == 4, "packed-direct kernels take fp32 parameters");
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* rings = smem;
+  A* red = reinterpret_cast<A*>(smem + (size_t)kWarps * D * kPkSlot);
+  const bool cluster_fold = nsplit > 1;
+  int32_t* s_act = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(red) +
+                                              align16((size_t)(kWarps + (cluster_fold ? 1 : 0)) * RT * kWarpPos *
+                                                      sizeof(A)));
+  const int n_act = min(*n_act_p, max_act);
+  const int out_w = MODE == 0 ? L : C;
+  const int p0 = blockIdx.x * kWarpPos;
+  const int b0 = blockIdx.y * RT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const U* xg = xp + (size_t)blockIdx.y * G * stage_w;
+  for (int i = threadIdx.x; i < n_act; i += kThreads) s_act[i] = __ldg(active + i);
+  __syncthreads();
+  int lo1, hi1, lo2, hi2;
+  if (MODE == 0) { lo1 = 0; hi1 = n_act; lo2 = 0; hi2 = 0; }
+  else scatter_ranges(s_act, n_act, C, L, p0, kWarpPos, lo1, hi1, lo2, hi2);
+  const int len1 = hi1 - lo1;
+  const int total = len1 + (hi2 - lo2);
+  const int per = (total + nsplit - 1) / nsplit;
+  const int cb = min(total, (int)blockIdx.z * per), ce = min(total, cb + per);
+  const int vb = cb + warp;
+  const int nq = ce - vb > 0 ? (ce - vb + kWarps - 1) / kWarps : 0;
+  unsigned char* ring = rings + warp * D * kPkSlot;
+  auto jof = [&](int q) {
+    const int v = vb + kWarps * q;
+    return v < len1 ? lo1 + v : lo2 + (v - len1);
+  };
+  auto issue = [&](int q) {  // the diagonal's values at this lane's 4 positions -> slot[lane][u]
+    if (q < nq) {
+      const int o = s_act[jof(q)];
+      const P* vr = vals + (size_t)o * L;
+      unsigned char* dst = ring + (q % D) * kPkSlot + lane * 16;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = p0 + lane + kWarp * u;
+        int c = p;
+        if (MODE != 0) { c = p - o; c = c < 0 ? c + C : c; }
+        const bool ok = p < out_w && c < L;
+        cp_async4(dst + u * 4, ok ? vr + c : vals, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  auto base_of = [&](int q, float& sc) {
+    const int o = s_act[jof(q)];
+    sc = asoft ? (float)__ldg(asoft + o) : 1.f;
+    int base;
+    if (MODE == 0) {
+      base = p0 + o;
+      base = base >= C ? base - C : base;
+    } else if (MODE == 1) {
+      base = p0 + C - o;
+      base = base >= C ? base - C : base;
+    } else {
+      int d = p0 - o;
+      d = d < -(kWarpPos - 1) ? d + C : (d > L - 1 ? d - C : d);
+      base = d + kWarpPos;
+    }
+    return base;
+  };
+#pragma unroll
+  for (int q = 0; q < D - 2; ++q) issue(q);
+  A acc[G][kU][VEC];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int r = 0; r < VEC; ++r) acc[g][u][r] = A(0);
+  auto load_x = [&](U (&xv)[G][kU], int base) {
+    const U* xr = xg + base + lane;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) xv[g][u] = __ldg(xr + (size_t)g * stage_w + kWarp * u);
+  };
+  auto fmas = [&](const U (&xv)[G][kU], float4 v, float sc) {
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162 w01 = __floats2bfloat162_rn(sc * v.x, sc * v.y);
+      const __nv_bfloat162 w23 = __floats2bfloat162_rn(sc * v.z, sc * v.w);
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(&w01), b = *reinterpret_cast<const uint32_t*>(&w23);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        fma_vec_h<0>(acc[g][0], xv[g][0], a);
+        fma_vec_h<1>(acc[g][1], xv[g][1], a);
+        fma_vec_h<0>(acc[g][2], xv[g][2], b);
+        fma_vec_h<1>(acc[g][3], xv[g][3], b);
+      }
+    } else {
+      const float wv[4] = {sc * v.x, sc * v.y, sc * v.z, sc * v.w};
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) fma_vec(acc[g][u], xv[g][u], wv[u]);
+    }
+  };
+  int base_l = 0;
+  float sc_l = 0.f;
+  int q = 0;
+  for (; q + 1 < nq; q += 2) {
+    if ((q & 31) == 0 && q + lane < nq) base_l = base_of(q + lane, sc_l);
+    U x0[G][kU], x1[G][kU];
+    load_x(x0, __shfl_sync(0xffffffffu, base_l, q & 31));
+    load_x(x1, __shfl_sync(0xffffffffu, base_l, (q + 1) & 31));
+    const float s0 = __shfl_sync(0xffffffffu, sc_l, q & 31), s1 = __shfl_sync(0xffffffffu, sc_l, (q + 1) & 31);
+    __syncwarp();
+    issue(q + D - 2);
+    issue(q + D - 1);
+    cp_async_wait<D - 2>();
+    __syncwarp();
+    const float4 v0 = *reinterpret_cast<const float4*>(ring + (q % D) * kPkSlot + lane * 16);
+    const float4 v1 = *reinterpret_cast<const float4*>(ring + ((q + 1) % D) * kPkSlot + lane * 16);
+    fmas(x0, v0, s0);
+    fmas(x1, v1, s1);
+  }
+  if (q < nq) {
+    if ((q & 31) == 0 && q + lane < nq) base_l = base_of(q + lane, sc_l);
+    U x0[G][kU];
+    load_x(x0, __shfl_sync(0xffffffffu, base_l, q & 31));
+    const float s0 = __shfl_sync(0xffffffffu, sc_l, q & 31);
+    __syncwarp();
+    issue(q + D - 2);
+    cp_async_wait<D - 2>();
+    __syncwarp();
+    const float4 v0 = *reinterpret_cast<const float4*>(ring + (q % D) * kPkSlot + lane * 16);
+    fmas(x0, v0, s0);
+  }
+  cp_async_wait<0>();
+  // fixed-order fold of the 8 diagonal warps, then (nsplit > 1) the cluster ranks
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int r = 0; r < VEC; ++r)
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        red[((size_t)warp * RT + g * VEC + r) * kWarpPos + lane + kWarp * u] = acc[g][u][r];
+  __syncthreads();
+  A* fin = red + (size_t)kWarps * RT * kWarpPos;
+  for (int i = threadIdx.x; i < RT * kWarpPos; i += kThreads) {
+    const int b = i >> 7, tt = i & (kWarpPos - 1);
+    const int p = p0 + tt;
+    A s = A(0);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[((size_t)w * RT + b) * kWarpPos + tt];
+    if (cluster_fold) {
+      fin[i] = s;
+    } else if (b0 + b < B && p < out_w) {
+      if (bias) s += (A)bias[p];
+      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+    }
+  }
+  if (cluster_fold) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int rank = (int)cl.block_rank(), nr = (int)cl.num_blocks();
+    const int per_r = (RT * kWarpPos + nr - 1) / nr;
+    const int i0 = rank * per_r, i1 = min(RT * kWarpPos, i0 + per_r);
+    for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+      const int b = i >> 7, tt = i & (kWarpPos - 1);
+      const int p = p0 + tt;
+      if (b0 + b >= B || p >= out_w) continue;
+      A s = A(0);
+      for (int r = 0; r < nr; ++r) s += cl.map_shared_rank(fin, r)[i];
+      if (bias) s += (A)bias[p];
+      out[(size_t)(b0 + b) * out_w + p] = from_acc<T>(s);
+    }
+    cl.sync();
   }
 }
 
@@ -2213,6 +2430,108 @@ static int run_product6(bool gather, int B, int C, int L, const void* in, const 
   return status_from_cuda();
 }
 
+// ---- packed-direct small-batch products (k_pack + k_product_pk)
+// Batches the packed-direct products take: bf16 5..8 (one 8-row unit) with >= 128
+// diagonals.  Warm 4096^2 90 %: B = 8 fwd 10.3 vs 13.7 us (cluster-split staged kernel)
+// and 15.9 us (k_product_rows); B = 1..4 stay on k_product_rows (6.3 vs 10.1 us at
+// B = 1), B >= 12 on the staged kernels (16.6 vs 22.8 us at B = 16: two 8-row units of
+// packed input no longer fit beside the rings in L1).  DIAGMM_PK_MIN_B /
+// DIAGMM_PK_MAX_B override (0 disables).
+template <typename T>
+static bool use_pk(int B) {
+  if constexpr (sizeof(T) != 2) {
+    return false;
+  } else {
+    static int lo = -1, hi = -1;
+    if (lo < 0) {
+      const char* a = getenv("DIAGMM_PK_MIN_B");
+      const char* b = getenv("DIAGMM_PK_MAX_B");
+      lo = a ? atoi(a) : 5;
+      hi = b ? atoi(b) : 8;
+      if (hi > 2 * vec_rows<T>()) hi = 2 * vec_rows<T>();
+    }
+    return B > 0 && B >= lo && B <= hi;
+  }
+}
+struct PkRows {
+  int mode, stage_w, c0, mod, limit;
+};
+static PkRows pk_rows(bool gather, int C, int L, int vec) {
+  PkRows r;
+  r.mode = gather ? 0 : (C >= L + kWarpPos ? 2 : 1);
+  if (r.mode == 2) {
+    r.stage_w = (L + 2 * kWarpPos + vec - 1) / vec * vec;
+    r.c0 = C - kWarpPos; r.mod = C; r.limit = L;
+  } else {
+    r.stage_w = C + kWarpPos;
+    r.c0 = 0; r.mod = C; r.limit = gather ? C : L;
+  }
+  return r;
+}
+template <typename T>
+static size_t pk_product_workspace(bool gather, int B, int C, int L) {
+  constexpr int VEC = vec_rows<T>();
+  const PkRows r = pk_rows(gather, C, L, VEC);
+  return align16((size_t)ceil_div(B > 0 ? B : 1, VEC) * r.stage_w * 16);
+}
+template <typename T, int G, int MODE>
+static void launch_product_pk(int ns, size_t sm, cudaStream_t st, int B, int C, int L, const typename Vec<T>::U* xp,
+                              int stage_w, const typename Traits<T>::P* vals, const double* asoft,
+                              const int32_t* active, const int32_t* n_act, int max_act,
+                              const typename Traits<T>::P* bias, T* out, int ntile) {
+  auto k = k_product_pk<T, G, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntile, 1, ns);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (ns > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = ns;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, k, B, C, L, xp, stage_w, vals, asoft, active, n_act, max_act, bias, out, ns);
+  note_launch();
+}
+
+template <typename T>
+static int run_product_pk(bool gather, int B, int C, int L, const void* in, const void* vals, const double* asoft,
+                          const int32_t* active, const int32_t* n_act, int max_act, const void* bias, void* out,
+                          void* ws, cudaStream_t st) {
+  using P = typename Traits<T>::P;
+  using U = typename Vec<T>::U;
+  constexpr int VEC = vec_rows<T>();
+  const int in_w = gather ? C : L, out_w = gather ? L : C;
+  const PkRows r = pk_rows(gather, C, L, VEC);
+  const int G = ceil_div(B, VEC);
+  U* xp = static_cast<U*>(ws);
+  const int vec_ok = in_w % VEC == 0 && C % VEC == 0 && r.c0 % VEC == 0 && r.limit % VEC == 0 && aligned16(in);
+  k_pack<T><<<ceil_div((long long)G * ceil_div(r.stage_w, VEC), 256), 256, 0, st>>>(
+      B, in_w, static_cast<const T*>(in), xp, r.stage_w, r.c0, r.mod, r.limit, vec_ok);
+  note_launch();
+  const int ntile = ceil_div(out_w, kWarpPos);
+  const double ndiag = gather ? (double)max_act : max_act * std::min(1.0, (L + kWarpPos - 1.0) / C);
+  int ns = 1;
+  while (ns < 8 && (long long)ntile * ns * 2 <= 2LL * num_sms() && ndiag / (2.0 * ns * kWarps) >= 4.0) ns *= 2;
+  const size_t sm = pk_smem<T>(G, ns > 1, max_act);
+  if (sm > 227 * 1024) return DIAGMM_ETOOLARGE;
+  auto tv = static_cast<const P*>(vals);
+  auto tb = static_cast<const P*>(bias);
+  auto to = static_cast<T*>(out);
+#define DIAGMM_PK(GG, MM)                                                                                      \
+  if (G == GG && r.mode == MM)                                                                                 \
+    launch_product_pk<T, GG, MM>(ns, sm, st, B, C, L, xp, r.stage_w, tv, asoft, active, n_act, max_act, tb, to, \
+                                 ntile);
+  DIAGMM_PK(1, 0) DIAGMM_PK(1, 1) DIAGMM_PK(1, 2) DIAGMM_PK(2, 0) DIAGMM_PK(2, 1) DIAGMM_PK(2, 2)
+#undef DIAGMM_PK
+  return status_from_cuda();
+}
+
 // workspace = [compact weights (max_act x ldw) | split partials]
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
@@ -2226,6 +2545,10 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   if constexpr (sizeof(T) <= 4) {
     const size_t v6 = v6_wil_bytes<T>(gather, C, L, max_act);
     wide = wide > v6 ? wide : v6;
+    if (sizeof(T) == 2 && use_pk<T>(B)) {
+      const size_t pk = pk_product_workspace<T>(gather, B, C, L);
+      wide = wide > pk ? wide : pk;
+    }
   }
   return wide > narrow ? wide : narrow;
 }
@@ -2240,6 +2563,16 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   constexpr int VEC = vec_rows<T>();
   if (B == 0) return DIAGMM_OK;
   if (ws == nullptr || ws_bytes < product_workspace<T>(gather, B, C, L, max_act)) return DIAGMM_EWORKSPACE;
+  if constexpr (sizeof(T) == 2) {
+    // bf16, B = 5..8: the packed-direct kernel when the diagonal list is long (warm
+    // 4096^2: 90 %, k = 410: 10.3 vs 15.9 us for k_product_rows), the few-rows kernel when
+    // it is short (99 %, k = 41: 4.5 vs 7.6 us) — max_act is the layer's known count
+    if (use_pk<T>(B) && max_act > 0) {
+      if (max_act >= 128)
+        return run_product_pk<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, ws, st);
+      return run_product_rows<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, st);
+    }
+  }
   if (B <= rows_max_b())
     return run_product_rows<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, st);
   if (B <= narrow_max_b())
@@ -2464,8 +2797,8 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
                                    align16((size_t)cparts * M * sizeof(A)));
       U* bp = ap + (size_t)p6.G * C;
       const int vc = C % VEC == 0, vl = L % VEC == 0;
-      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(C, VEC), 256), 256, 0, st>>>(B, C, aop, ap, vc);
-      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(L, VEC), 256), 256, 0, st>>>(B, L, bop, bp, vl);
+      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(C, VEC), 256), 256, 0, st>>>(B, C, aop, ap, C, 0, C, C, vc);
+      k_pack<T><<<ceil_div((long long)p6.G * ceil_div(L, VEC), 256), 256, 0, st>>>(B, L, bop, bp, L, 0, 0x7fffffff, L, vl);
       note_launch(2);
       auto k = p6.jw == 16 ? k_dw6<T, 16> : (p6.jw == 8 ? k_dw6<T, 8> : k_dw6<T, 4>);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p6.smem);

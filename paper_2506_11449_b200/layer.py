@@ -166,7 +166,8 @@ class DiagMMFunction(torch.autograd.Function):
             W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
             y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
         else:
-            y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach())
+            y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach(),
+                                 max_act=sel.known_count())
         if residual is not None:
             y = y + residual.detach()
         ctx.save_for_backward(x, values, alpha)
@@ -207,10 +208,12 @@ class DiagMMFunction(torch.autograd.Function):
                 g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
                 g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
         else:
+            ma = sel.known_count()
             if ctx.needs_input_grad[0]:
-                dx = ops.diag_backward_input(dy, vals, sel, M, N)
+                dx = ops.diag_backward_input(dy, vals, sel, M, N, max_act=ma)
             g_values, g_soft, g_bias = ops.diag_backward_weight(
-                dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft, bucket=spec.bucket)
+                dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft, bucket=spec.bucket,
+                max_act=ma)
         if need_soft:
             g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
                                          clamped=sel.clamped, l1_coeff=spec.l1, params=spec.params)

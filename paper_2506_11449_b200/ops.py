@@ -95,6 +95,18 @@ class Selection:
         self.event.synchronize()
         return int(self.n_act_host.item())
 
+    def known_count(self) -> int | None:
+        """The active count if its host copy has already landed (no wait, and never
+        while a CUDA graph is being captured: a count baked into a graph would be
+        stale on replay), else None.  Used as the kernels' grid / plan bound
+        ``max_act`` (they process min(device count, max_act) diagonals), so the
+        FMA kernels are planned for the real count instead of C."""
+        if self.n_act_host is None or self.event is None or torch.cuda.is_current_stream_capturing():
+            return None
+        if not self.event.query():
+            return None
+        return max(1, int(self.n_act_host.item()))
+
     def active_offsets(self) -> torch.Tensor:
         return self.active[: self.host_count()]
 

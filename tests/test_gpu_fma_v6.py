@@ -7,7 +7,8 @@ circular scatter rows (square and near-square C < L + 128), guard-band scatter
 rows (tall forward / wide dX, C >= L + 128), widths that are not multiples of
 the 8-element vector (scalar staging and packing paths), ragged batches (B not a
 multiple of the 8-row unit), 90 % and 99 % sparsity (spread offsets: full-row dW
-windows), and both bf16 (products + dW) and fp32 (dW) activations.
+windows), and both bf16 (products + dW) and fp32 (dW) activations.  Batches of
+1-16 (bf16) / 1-8 (fp32) take the packed-direct kernels (k_product_pk, k_dw_pk).
 Bars: bf16 outputs 5e-3 of max(1, max|ref|) against the oracle on the same
 bf16-rounded inputs; dW (exact bf16 products, fp32 accumulation) 1e-4; fp32 1e-5.
 """
@@ -63,7 +64,7 @@ SHAPES = [(512, 512), (1024, 256), (256, 1024), (320, 256), (256, 320), (600, 29
 
 
 @pytest.mark.parametrize("M,N", SHAPES)
-@pytest.mark.parametrize("B,sparsity", [(64, 0.9), (37, 0.9), (100, 0.99)])
+@pytest.mark.parametrize("B,sparsity", [(64, 0.9), (37, 0.9), (100, 0.99), (1, 0.9), (5, 0.9), (16, 0.99)])
 def test_v6_bf16_products_and_dw_vs_oracle(M, N, B, sparsity):
     C, L, offs, values, asoft, bias, x, dy = _case(M, N, B, sparsity, seed=M * 7 + N + B)
     xb = _gpu(x, torch.float32).to(torch.bfloat16)
@@ -100,7 +101,7 @@ def test_v6_bf16_products_and_dw_vs_oracle(M, N, B, sparsity):
 
 
 @pytest.mark.parametrize("M,N", [(3072, 768), (768, 3072), (512, 512), (600, 300)])
-@pytest.mark.parametrize("B,sparsity", [(256, 0.9), (45, 0.99)])
+@pytest.mark.parametrize("B,sparsity", [(256, 0.9), (45, 0.99), (3, 0.9), (8, 0.99)])
 def test_v6_fp32_dw_vs_oracle(M, N, B, sparsity):
     C, L, offs, values, asoft, bias, x, dy = _case(M, N, B, sparsity, seed=M + 3 * N + B)
     x32, dy32, vals = _gpu(x, torch.float32), _gpu(dy, torch.float32), _gpu(values, torch.float32)

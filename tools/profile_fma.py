@@ -14,7 +14,8 @@ from paper_2506_11449_b200 import ops
 from paper_2506_11449_b200.selection import required_diagonals
 
 CASES = {"b64": (4096, 4096, 64, 0.9, torch.bfloat16), "cfg1": (3072, 768, 256, 0.9, torch.float32),
-         "b1024s99": (4096, 4096, 1024, 0.99, torch.bfloat16), "b256": (4096, 4096, 256, 0.9, torch.bfloat16)}
+         "b1024s99": (4096, 4096, 1024, 0.99, torch.bfloat16), "b256": (4096, 4096, 256, 0.9, torch.bfloat16),
+         "b8": (4096, 4096, 8, 0.9, torch.bfloat16), "b1": (4096, 4096, 1, 0.9, torch.bfloat16)}
 
 for name in sys.argv[1:] or ["b64"]:
     M, N, B, s, dt = CASES[name]
