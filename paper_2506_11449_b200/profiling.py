@@ -391,8 +391,8 @@ def diagmm_config1(peaks, peaks_kind, fma_tflops):
     cfg1 = diag_case(3072, 768, 256, 0.9, torch.float32, peaks, fma_tflops, flush=flush)
     cfg1["layer_step"] = layer_step_case(flush=flush)
     sweep = []
-    for (dim, s, B) in [(4096, 0.9, 1), (4096, 0.9, 64), (4096, 0.9, 1024), (4096, 0.99, 1024),
-                        (4096, 0.9, 8192)]:
+    for (dim, s, B) in [(4096, 0.9, 1), (4096, 0.9, 8), (4096, 0.9, 64), (4096, 0.9, 1024), (4096, 0.99, 1),
+                        (4096, 0.99, 8), (4096, 0.99, 64), (4096, 0.99, 1024), (4096, 0.9, 8192)]:
         sweep.append(diag_case(dim, dim, B, s, torch.bfloat16, peaks, fma_tflops, reps=10, flush=flush))
     # the ViT-B/16 MLP shape at its per-step token count (256 images x 197 tokens)
     vit = diag_case(3072, 768, 50432, 0.9, torch.bfloat16, peaks, fma_tflops, reps=5, flush=flush)
