@@ -185,20 +185,22 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
   }
 }
 
-// 32 columns per CTA; the 8 warps take parts w, w+8, ... and are folded in
-// warp order (fixed, deterministic).
-__global__ void __launch_bounds__(256)
+// 32 columns per CTA; the 32 warps take parts w, w+32, ... (4 loads in flight each) and
+// are folded in warp order (fixed, deterministic): with ~300 partial rows every warp
+// walks ~10 of them, so the fold costs ~3 memory latencies instead of ~10.
+constexpr int kFoldWarps = 32;
+__global__ void __launch_bounds__(kFoldWarps * 32)
 k_ln_fold(int D, int nparts, const float* __restrict__ part, float* __restrict__ dw, float* __restrict__ dbias) {
-  __shared__ float red[2][8][33];
+  __shared__ float red[2][kFoldWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
   if (c < D)
-    for (int p0 = w; p0 < nparts; p0 += 32) {  // 4 parts' loads in flight, summed in part order
+    for (int p0 = w; p0 < nparts; p0 += 4 * kFoldWarps) {  // 4 parts' loads in flight, summed in part order
       float va[4], vb[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int p = p0 + 8 * k;
+        const int p = p0 + kFoldWarps * k;
         va[k] = p < nparts ? part[((size_t)p * 2 + 0) * D + c] : 0.f;
         vb[k] = p < nparts ? part[((size_t)p * 2 + 1) * D + c] : 0.f;
       }
@@ -211,7 +213,7 @@ k_ln_fold(int D, int nparts, const float* __restrict__ part, float* __restrict__
   if (w == 0 && c < D) {
     float sa = 0.f, sb = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { sa += red[0][k][lane]; sb += red[1][k][lane]; }
+    for (int k = 0; k < kFoldWarps; ++k) { sa += red[0][k][lane]; sb += red[1][k][lane]; }
     dw[c] = sa;
     dbias[c] = sb;
   }
@@ -299,7 +301,7 @@ int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, cons
     default: k_ln_bwd<4><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
   }
   note_launch();
-  k_ln_fold<<<ceil_div(D, 32), 256, 0, st>>>(D, ctas, part, dw, db);
+  k_ln_fold<<<ceil_div(D, 32), kFoldWarps * 32, 0, st>>>(D, ctas, part, dw, db);
   note_launch();
   return status_from_cuda();
 }
