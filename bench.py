@@ -235,6 +235,76 @@ def cpu_reference_rate(wl: "Workload", samples: int, steps: int, warmup: int, th
     return units / sec, sec, cores, tokens
 
 
+def _reference_pkg():
+    """The UNMODIFIED reference package (diagsparse) installed offline into
+    baseline/_ref (git-ignored, travels to the GPU box), or None."""
+    ref = Path(__file__).resolve().parent / "baseline" / "_ref"
+    if not (ref / "diagsparse").is_dir():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import diagsparse  # noqa: F401
+        from diagsparse import autodiff, layers, selection, training
+    except Exception:  # noqa: BLE001 - absent or broken install: the caller falls back to the port
+        return None
+    return autodiff, layers, selection, training
+
+
+def cpu_reference_pkg_rate(wl: "Workload", samples: int, steps: int, warmup: int, threads: int | None = None):
+    """The reference's OWN CPU implementation of the path, through its public API:
+    one diagsparse.layers.DynaDiagLayer per DiagLinear of the model, each step
+    ``forward`` on a Tape (its _record_diag_matmul op, BCSR / dense switch and all),
+    a surrogate loss <y, up> + the layer's l1 penalty, ``Tape.backward``,
+    ``training.clip_global_norm`` and ``training.AdamW`` — post-anneal (T = 1e-9),
+    float64, on ``samples`` images.  Returns (rate, sec, cores, tokens) or None when
+    the reference package is not installed."""
+    import numpy as np
+
+    pkg = _reference_pkg()
+    if pkg is None:
+        return None
+    autodiff, rlayers, rsel, rtrain = pkg
+    shapes = wl.layer_shapes()
+    tokens = wl.cpu_sample_tokens(samples)
+    rng = np.random.default_rng(0)
+    sched = rsel.TemperatureSchedule("constant", 1e-9, 1e-9, 1)
+    layers = [rlayers.DynaDiagLayer(n_in, n_out, wl.cfg.sparsity, t_schedule=sched, l1_coeff=1e-4, seed=i)
+              for i, (n_in, n_out) in enumerate(shapes)]
+    params = [p for lyr in layers for p in lyr.parameters()]
+    opt = rtrain.AdamW(params, rtrain.OptimizerConfig(lr=1e-3, betas=(0.9, 0.99), eps=1e-8, weight_decay=5e-5))
+    xs = {s: rng.standard_normal((tokens, s[0])) for s in set(shapes)}
+    ups = {s: rng.standard_normal((tokens, s[1])) * 1e-3 for s in set(shapes)}
+
+    def one_step(step):
+        tape = autodiff.Tape()
+        total = None
+        for lyr, shp in zip(layers, shapes):
+            y = lyr.forward(autodiff.Tensor(xs[shp]), tape, step)
+            up = ups[shp]
+            loss = tape.record(autodiff.Tensor(np.asarray(float((y.value * up).sum()))), (y,),
+                               lambda g, up=up: (float(g) * up,))
+            term = tape.add(loss, lyr.penalty(tape))
+            total = term if total is None else tape.add(total, term)
+        opt.zero_grad()
+        tape.backward(total)
+        rtrain.clip_global_norm(params, 1.0)
+        opt.step(1e-3)
+
+    cores = threads or len(os.sched_getaffinity(0))
+    with _Threads(cores):
+        for s in range(warmup):
+            one_step(s)
+        times = []
+        for s in range(steps):
+            t0 = time.perf_counter()
+            one_step(warmup + s)
+            times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    units = tokens if wl.lm else samples
+    return units / sec, sec, cores, tokens
+
+
 def cpu_config1_ms(threads: int, reps: int = 3):
     """BASELINE config 1 on the reference's CPU algorithm (oracle port, float64):
     DiagLinear 768 -> 3072 at 90 %, batch 256, forward + backward + TopK update +
@@ -262,12 +332,20 @@ def cpu_config1_ms(threads: int, reps: int = 3):
 def cpu_baseline_block(wl: "Workload", samples: int):
     """cpu_baseline for the bench line: all host cores and 1 core."""
     allc = len(os.sched_getaffinity(0))
-    r_all, sec_all, _, tokens = cpu_reference_rate(wl, samples, 1, 1, threads=allc)
-    r_one, sec_one, _, _ = cpu_reference_rate(wl, samples, 1, 0, threads=1)
-    return {"value": r_all, "unit": wl.unit, "cores": allc, "kind": "port",
+    kind, what = "reference", "the unmodified reference package (baseline/_ref diagsparse)"
+    got_all = cpu_reference_pkg_rate(wl, samples, 1, 1, threads=allc)
+    if got_all is None:
+        kind, what = "port", "float64 oracle port of the reference algorithm"
+        got_all = cpu_reference_rate(wl, samples, 1, 1, threads=allc)
+        got_one = cpu_reference_rate(wl, samples, 1, 0, threads=1)
+    else:
+        got_one = cpu_reference_pkg_rate(wl, samples, 1, 0, threads=1)
+    r_all, sec_all, _, tokens = got_all
+    r_one, sec_one, _, _ = got_one
+    return {"value": r_all, "unit": wl.unit, "cores": allc, "kind": kind,
             "cpu_model": cpu_model(),
             "sample": f"{tokens} tokens through all {len(wl.layer_shapes())} DiagLinear layers of {wl.name} (fwd + "
-                      f"bwd + l1 + clip + AdamW, float64 oracle of the reference algorithm, post-anneal T = 1e-9); "
+                      f"bwd + l1 + clip + AdamW, float64, {what}, post-anneal T = 1e-9); "
                       f"attention, LayerNorm, embeddings and head are NOT timed",
             "all_cores": {"value": r_all, "cores": allc, "sec_per_sample": sec_all},
             "one_core": {"value": r_one, "cores": 1, "sec_per_sample": sec_one}}
@@ -280,17 +358,24 @@ def run_reference(args):
     wl = Workload(args.model)
     steps = max(1, min(args.steps, 3))
     warm = 1 if args.warmup > 0 else 0
-    rate, sec, cores, tokens = cpu_reference_rate(wl, args.cpu_sample_images, steps, warm)
+    got = cpu_reference_pkg_rate(wl, args.cpu_sample_images, steps, warm)
+    kind = "reference"
+    what = ("the unmodified reference package (baseline/_ref diagsparse: DynaDiagLayer.forward on its Tape, "
+            "Tape.backward, clip_global_norm, AdamW)")
+    if got is None:  # reference package not installed: the oracle port of its algorithm
+        got = cpu_reference_rate(wl, args.cpu_sample_images, steps, warm)
+        kind, what = "port", "float64 oracle port of the reference algorithm"
+    rate, sec, cores, tokens = got
     line = {
         "impl": "reference", "metric": wl.metric, "value": rate, "unit": wl.unit, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers training step, CPU oracle port",
+        "config": {"workload": f"{args.model} 90%-sparse DiagLinear layers training step, CPU, {what}",
                    "global_batch": args.cpu_sample_images, "seq_len": wl.seq,
                    "parallelism": "none (host threads via BLAS)"},
-        "cpu_baseline": {"value": rate, "unit": wl.unit, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{tokens} tokens through all DiagLinear layers (fwd+bwd+clip+AdamW), float64, "
-                                   f"median of {steps}; attention / LayerNorm not timed"},
+        "cpu_baseline": {"value": rate, "unit": wl.unit, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{tokens} tokens through all DiagLinear layers (fwd+bwd+l1+clip+AdamW), float64, "
+                                   f"median of {steps}, {what}; attention / LayerNorm not timed"},
         "e2e": {"value": rate, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
