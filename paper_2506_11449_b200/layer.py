@@ -115,6 +115,11 @@ def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype
     if act_dtype == torch.bfloat16 and B >= dense_route_min_tokens():
         return True
     L = min(spec.M, spec.N)
+    if torch.cuda.is_current_stream_capturing():
+        # inside a CUDA-graph capture the device count cannot be read (and a host value
+        # would be baked into the graph): the switch uses the TopK budget k instead; both
+        # routes give the reference's results, and the kernels bound their grids by C
+        return 4 * spec.k * L >= spec.M * spec.N
     return 4 * sel.host_count() * L >= spec.M * spec.N
 
 

@@ -135,3 +135,35 @@ def test_v6_deterministic():
         outs.append((y.clone(), dx.clone(), gv.clone(), gs.clone()))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_fp32_fma_route_step_graph_capturable():
+    """A float32 DiagLinear model on the FMA kernels captured as one CUDA graph
+    (forward + backward: no host read of the active count inside the capture, grids
+    bounded by C) gives the eager step's gradients."""
+    from paper_2506_11449_b200 import DiagLinear, TemperatureSchedule
+    from paper_2506_11449_b200.graphed import GraphedStep
+
+    torch.manual_seed(0)
+    sched = TemperatureSchedule("constant", 0.05, 0.05, 1)
+    layers = [DiagLinear(256, 512, 0.9, seed=1, dtype=torch.float32, t_schedule=sched),
+              DiagLinear(512, 256, 0.9, seed=2, dtype=torch.float32, t_schedule=sched)]
+    x = torch.randn(48, 256, device="cuda")
+    up = torch.randn(48, 256, device="cuda")
+    params = [p for m in layers for p in m.parameters()]
+
+    def fwd_bwd(inp, u):
+        h = layers[1](layers[0](inp, step=0), step=0)
+        loss = (h * u).sum()
+        loss.backward()
+        return loss
+
+    fwd_bwd(x, up)
+    eager = [p.grad.detach().clone() for p in params]
+    for p in params:
+        p.grad = None
+    gs = GraphedStep(fwd_bwd, params, x.clone(), up.clone())
+    gs.step(x, up)
+    torch.cuda.synchronize()
+    for p, g in zip(params, eager):
+        assert torch.allclose(p.grad, g, rtol=1e-5, atol=1e-6 * float(g.abs().max())), p.shape
