@@ -381,8 +381,31 @@ def layer_step_case(n_in=768, n_out=3072, B=256, T=1e-3, reps=20, flush=None):
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     ts.sort()
-    return {"us": ts[len(ts) // 2] * 1e3, "n_act": lyr.active_count(0), "k": lyr.k, "T": T,
-            "what": "K4 + fwd + dX + dW + K5 through DiagLinear (eager autograd), fp32, B=256"}
+    eager_us = ts[len(ts) // 2] * 1e3
+    # the same step captured as one CUDA graph (the FMA route needs no host read inside a
+    # capture): device time without the eager autograd / Python launch overhead
+    from .graphed import GraphedStep
+
+    def fwd_bwd(inp, up):
+        lyr(inp, step=0).backward(up)
+        return up
+
+    params = [lyr.values, lyr.alpha, lyr.bias, x]
+    gs = GraphedStep(fwd_bwd, params, x, dy)
+    gts = []
+    for _ in range(reps):
+        if flush is not None:
+            torch.amax(flush, dim=0, keepdim=True, out=sink)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        gs.step(x, dy)
+        e.record()
+        torch.cuda.synchronize()
+        gts.append(s.elapsed_time(e))
+    gts.sort()
+    return {"us": eager_us, "graphed_us": gts[len(gts) // 2] * 1e3, "n_act": lyr.active_count(0), "k": lyr.k,
+            "T": T, "what": "K4 + fwd + dX + dW + K5 through DiagLinear, fp32, B=256: eager autograd (us) and "
+                            "the same step replayed as one CUDA graph (graphed_us); L2 flushed before each"}
 
 
 def diagmm_config1(peaks, peaks_kind, fma_tflops):
