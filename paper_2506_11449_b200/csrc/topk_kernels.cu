@@ -20,6 +20,7 @@
 // 3), and the tests check the masks bit-for-bit.
 #include "common.cuh"
 #include <math_constants.h>
+#include <type_traits>
 
 namespace diagmm {
 
@@ -60,6 +61,91 @@ __device__ void bitonic_sort_desc(double* key, int* idx, int NP) {
       __syncthreads();
     }
   }
+}
+
+// Same ordering, fewer instructions and barriers: every thread holds E = NP / blockDim
+// consecutive positions in registers; a compare-exchange stage whose partner distance j
+// is below E stays inside the thread, below 32E it is a warp shuffle, and only the
+// j >= 32E stages (15 of the 78 at NP = 4096) go through shared memory with barriers.
+// The result is the unique (key desc, index asc) order, identical to bitonic_sort_desc.
+template <int E>
+__device__ void sort_desc_regs(double* key, int* idx, int NP) {
+  const int t = threadIdx.x;
+  double kr[E];
+  int ir[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    kr[e] = key[t * E + e];
+    ir[e] = idx[t * E + e];
+  }
+  for (int k = 2; k <= NP; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+        // in-thread pairs (e, e ^ j); j is a power of two below E, dispatched to a
+        // compile-time distance so the arrays stay in registers
+        auto local = [&](auto J) {
+          constexpr int JJ = decltype(J)::value;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int f = e ^ JJ;
+            if (f > e) {
+              const bool up = ((t * E + e) & k) == 0;
+              const bool swap = up ? before(kr[f], ir[f], kr[e], ir[e]) : before(kr[e], ir[e], kr[f], ir[f]);
+              if (swap) {
+                const double tk = kr[e]; kr[e] = kr[f]; kr[f] = tk;
+                const int ti = ir[e]; ir[e] = ir[f]; ir[f] = ti;
+              }
+            }
+          }
+        };
+        if (j == 1) local(std::integral_constant<int, 1>{});
+        else if (j == 2) local(std::integral_constant<int, (E > 2 ? 2 : 1)>{});
+        else local(std::integral_constant<int, (E > 4 ? 4 : 1)>{});
+      } else if (j < 32 * E) {
+        const int lm = j / E;
+        const bool lower = (t & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double pk = __shfl_xor_sync(0xffffffffu, kr[e], lm);
+          const int pi = __shfl_xor_sync(0xffffffffu, ir[e], lm);
+          const bool up = ((t * E + e) & k) == 0;
+          const bool mine_first = before(kr[e], ir[e], pk, pi);
+          // the lower position of an ascending ("up") pair keeps the element that comes first
+          const bool keep_mine = (lower == up) ? mine_first : !mine_first;
+          if (!keep_mine) { kr[e] = pk; ir[e] = pi; }
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) { key[t * E + e] = kr[e]; idx[t * E + e] = ir[e]; }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = t * E + e, q = p ^ j;
+          const double pk = key[q];
+          const int pi = idx[q];
+          const bool up = (p & k) == 0, lower = p < q;
+          const bool mine_first = before(kr[e], ir[e], pk, pi);
+          const bool keep_mine = (lower == up) ? mine_first : !mine_first;
+          if (!keep_mine) { kr[e] = pk; ir[e] = pi; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) { key[t * E + e] = kr[e]; idx[t * E + e] = ir[e]; }
+  __syncthreads();
+}
+
+// key / idx: NP (power of two) entries in shared memory, sorted in place
+__device__ void sort_desc(double* key, int* idx, int NP) {
+  const int nt = blockDim.x;
+  if (nt == 1024 && NP == 1024) sort_desc_regs<1>(key, idx, NP);
+  else if (nt == 1024 && NP == 2048) sort_desc_regs<2>(key, idx, NP);
+  else if (nt == 1024 && NP == 4096) sort_desc_regs<4>(key, idx, NP);
+  else if (nt == 1024 && NP == 8192) sort_desc_regs<8>(key, idx, NP);
+  else bitonic_sort_desc(key, idx, NP);
 }
 
 __device__ __forceinline__ int next_pow2(int n) {
@@ -144,7 +230,7 @@ k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
     idx[i] = i < C ? i : 0x7fffffff;
   }
   __syncthreads();
-  bitonic_sort_desc(key, idx, NP);
+  sort_desc(key, idx, NP);
 
   // ---- suffix scan of R (positions 0..C-1, chunked per thread)
   const int per = (C + nt - 1) / nt;
@@ -218,7 +304,7 @@ k_select_hard(int C, int k, const double* __restrict__ alpha, int32_t* __restric
     idx[i] = i < C ? i : 0x7fffffff;
   }
   __syncthreads();
-  bitonic_sort_desc(key, idx, NP);
+  sort_desc(key, idx, NP);
   for (int i = threadIdx.x; i < C; i += blockDim.x) flag[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < k; i += blockDim.x) flag[idx[i]] = 1;
@@ -445,7 +531,7 @@ k_diagheur_update(int C, int L, int k, int32_t* __restrict__ active, int32_t* __
     }
   }
   __syncthreads();
-  bitonic_sort_desc(key, idx, NP);
+  sort_desc(key, idx, NP);
   // ---- the pool: offsets inactive before the swap, ascending
   {
     const int per = (C + blockDim.x - 1) / blockDim.x;
