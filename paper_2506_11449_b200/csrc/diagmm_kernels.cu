@@ -13,6 +13,11 @@
 //   dW: gw[j,t] = sum_b Aop[b,(o_j+t) mod C] * Bop[b,t]   (layers.py:149-158)
 //        tall: Aop = dy, Bop = x;   wide: Aop = x, Bop = dy.
 //
+// Which kernel runs (run_product / run_dw):
+//   products  B <= 4: k_product_rows; bf16 B 5..8: k_product_pk (>= 128 diagonals) or
+//             k_product_rows; bf16 B >= 32: k_product6 (v6); otherwise k_product (v4)
+//   dW        B <= 8: k_dw_narrow; bf16 / fp32 B > 8: k_dw6 (v6); fp64: k_dw (v4)
+//
 // B200 design (v4):
 //  * Every multiply needs a gathered operand at a data-dependent shift, so
 //    there is no register reuse of it: each FMA consumes one value read from
@@ -1429,7 +1434,7 @@ k_gather_finish(int C, int L, const P* __restrict__ vals, const double* __restri
 }
 
 // --------------------------------------------------------------------------- K1/K2 v6
-// Row-tiled products, v6 (bf16 / fp32, B above the few-rows kernels).  ncu of
+// Row-tiled products, v6 (bf16, B >= 32; fp32 stays on v4).  ncu of
 // the v4 kernel (profiles/r02_ncu_fma_*.txt) showed every diagonal waiting a
 // full memory latency on its weights: the register ring's loads sit behind
 // per-diagonal branches, so ptxas cannot count them on a scoreboard and waits
