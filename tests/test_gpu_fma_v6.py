@@ -167,3 +167,27 @@ def test_fp32_fma_route_step_graph_capturable():
     torch.cuda.synchronize()
     for p, g in zip(params, eager):
         assert torch.allclose(p.grad, g, rtol=1e-5, atol=1e-6 * float(g.abs().max())), p.shape
+
+
+@pytest.mark.parametrize("B", [1, 5, 16, 64])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_empty_active_set_every_plan(B, dtype):
+    """No active diagonal (the reference's empty pattern is rejected, but a soft TopK can
+    leave n_act = 0 on the device): every product plan returns the bias, dX is zero, and
+    dW writes exact zero rows with the bias gradient intact."""
+    M, N = 512, 256
+    C, L = max(M, N), min(M, N)
+    sel = ops.selection_from_offsets(C, torch.tensor([3], device="cuda"))
+    sel.n_act.zero_()  # the device count the kernels read
+    sel.n_act_host = None
+    vals = torch.randn(C, L, device="cuda")
+    bias = torch.randn(M, device="cuda")
+    x = torch.randn(B, N, device="cuda").to(dtype)
+    dy = torch.randn(B, M, device="cuda").to(dtype)
+    y = ops.diag_forward(x, vals, sel, M, N, bias, max_act=1)
+    assert torch.equal(y.float(), bias.expand(B, M).to(dtype).float())
+    dx = ops.diag_backward_input(dy, vals, sel, M, N, max_act=1)
+    assert not dx.any()
+    gv, gs, gb = ops.diag_backward_weight(dy, x, vals, sel, M, N, max_act=1)
+    assert not gv.any() and not gs.any()
+    assert torch.allclose(gb, dy.float().sum(0), rtol=1e-4, atol=1e-3)
