@@ -421,7 +421,14 @@ class TrainHarness:
         loss = F.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), lbl.reshape(-1), label_smoothing=self.label_smoothing)
         for pen in penalties(self.model, fused=True):  # l1 gradient folded into K5
             loss = loss + pen
-        loss.backward()
+        if self.world == 1 and os.environ.get("DIAGMM_DEFER_K5", "1") != "0":
+            # every layer's K5 as ONE batched launch after the backward (bit-identical)
+            from paper_2506_11449_b200 import deferred_topk_grads
+
+            with deferred_topk_grads():
+                loss.backward()
+        else:
+            loss.backward()
         return loss
 
     def update(self):

@@ -165,6 +165,22 @@ DIAGMM_API int diagmm_topk_grad(int C, int k, double temperature, const double* 
                      double l1_coeff, double* g_alpha, int accumulate,
                      const double* params, void* stream);
 
+/* ---- K5 batched: every layer's soft TopK gradient in ONE launch (one CTA each)
+ * after the backward (replaces one diagmm_topk_grad launch per layer; same math,
+ * bit-identical results).  g_soft must be complete when this is enqueued. */
+typedef struct diagmm_topk_grad_job {
+  int C, k;
+  double temperature;
+  const double* alpha;
+  const uint8_t* clamped;
+  const double* g_soft;
+  double l1_coeff;
+  double* g_alpha;
+  int accumulate;
+  const double* params; /* NULL or the device {T, k} of diagmm_topk_job */
+} diagmm_topk_grad_job;
+DIAGMM_API int diagmm_topk_grad_batched(int n, const diagmm_topk_grad_job* jobs, void* stream);
+
 /* ---- DiagHeur prune / regrow (layers.py:381-413) ------------------------
  * In place on the device: prune the n_prune active diagonals of smallest L2
  * value norm (ties -> smaller offset, np.lexsort((active, norms))), regrow the

@@ -40,6 +40,7 @@ from .layer import (  # noqa: F401
     DiagMLP,
     FrozenDiagLinear,
     ParamSpec,
+    deferred_topk_grads,
     diagheur_update,
     penalties,
     preselect,

@@ -63,7 +63,16 @@ class TensorDesc(C.Structure):
                 ("m", _vp), ("v", _vp), ("weight_decay", C.c_double)]
 
 
+class TopkGradJob(C.Structure):
+    """diagmm_topk_grad_job (include/diagmm.h)."""
+
+    _fields_ = [("C", C.c_int), ("k", C.c_int), ("temperature", C.c_double), ("alpha", _vp), ("clamped", _vp),
+                ("g_soft", _vp), ("l1_coeff", C.c_double), ("g_alpha", _vp), ("accumulate", C.c_int),
+                ("params", _vp)]
+
+
 SIGNATURES["diagmm_topk_waterfill_batched"] = (_i, [_i, C.POINTER(TopkJob), _vp])
+SIGNATURES["diagmm_topk_grad_batched"] = (_i, [_i, C.POINTER(TopkGradJob), _vp])
 SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp, _vp])
 SIGNATURES["diagmm_sumsq_multi_len"] = (_i, [_i, C.POINTER(TensorDesc)])
 SIGNATURES["diagmm_sumsq_multi"] = (_i, [_i, C.POINTER(TensorDesc), _vp, _i, _vp])

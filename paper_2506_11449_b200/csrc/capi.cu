@@ -28,6 +28,7 @@ int run_diagheur_update(int, int, int, int32_t*, int32_t*, int32_t*, void*, int,
 int run_active_from_list(int, int, const int32_t*, int32_t*, int32_t*, cudaStream_t);
 int run_topk_grad(int, int, double, const double*, const uint8_t*, const double*, double, double*, int,
                   const double*, cudaStream_t);
+int run_topk_grad_batched(int, const diagmm_topk_grad_job*, cudaStream_t);
 template <typename P>
 int run_adamw(size_t, void*, const void*, void*, void*, int, double, double, double, double, double,
               const double*, cudaStream_t);
@@ -266,6 +267,10 @@ int diagmm_topk_grad(int C, int k, double temperature, const double* alpha, cons
                      const double* params, void* stream) {
   return run_topk_grad(C, k, temperature, alpha, clamped, g_soft, l1_coeff, g_alpha, accumulate, params,
                        S(stream));
+}
+
+int diagmm_topk_grad_batched(int n, const diagmm_topk_grad_job* jobs, void* stream) {
+  return run_topk_grad_batched(n, jobs, S(stream));
 }
 
 int diagmm_diagheur_update(int dtype, int C, int L, int k, int32_t* active, int32_t* slot, int32_t* n_act,

@@ -360,15 +360,15 @@ __device__ double block_reduce_max(double v, double* buf) {
   return r;
 }
 
-__global__ void __launch_bounds__(kSelThreads)
-k_topk_grad(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
-            const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
-            double* __restrict__ g_alpha, int accumulate, const double* __restrict__ params) {
+// K5 body for one layer (one CTA); shared by the per-layer and the batched kernels
+__device__ void topk_grad_block(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
+                                const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
+                                double* __restrict__ g_alpha, int accumulate, const double* __restrict__ params,
+                                double* smem) {
   const int k = params ? (int)params[1] : k_arg;
   const double temperature = params ? params[0] : t_arg;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* q = reinterpret_cast<double*>(smem);  // C
-  double* buf = q + C;                          // blockDim
+  double* q = smem;       // C
+  double* buf = q + C;    // blockDim
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (C + nt - 1) / nt;
   const int lo = min(C, tid * per), hi = min(C, lo + per);
@@ -408,6 +408,24 @@ k_topk_grad(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
     }
     g_alpha[i] = accumulate ? g_alpha[i] + g : g;
   }
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_topk_grad(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
+            const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
+            double* __restrict__ g_alpha, int accumulate, const double* __restrict__ params) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  topk_grad_block(C, k_arg, t_arg, alpha, clamped, up, l1, g_alpha, accumulate, params,
+                  reinterpret_cast<double*>(smem));
+}
+
+struct TopkGradJobs { diagmm_topk_grad_job j[kMaxJobs]; };
+__global__ void __launch_bounds__(kSelThreads)
+k_topk_grad_batched(const __grid_constant__ TopkGradJobs jobs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const diagmm_topk_grad_job& J = jobs.j[blockIdx.x];
+  topk_grad_block(J.C, J.k, J.temperature, J.alpha, J.clamped, J.g_soft, J.l1_coeff, J.g_alpha, J.accumulate,
+                  J.params, reinterpret_cast<double*>(smem));
 }
 
 // ---------------------------------------------------------------- launchers
@@ -469,6 +487,31 @@ int run_active_from_list(int C, int n, const int32_t* offs, int32_t* slot, int32
   if (C < 1 || n < 0 || n > C) return DIAGMM_ESHAPE;
   k_active_from_list<<<1, kSelThreads, 0, st>>>(C, n, offs, slot, n_act);
   note_launch();
+  return status_from_cuda();
+}
+
+int run_topk_grad_batched(int n, const diagmm_topk_grad_job* jobs, cudaStream_t st) {
+  if (n < 0) return DIAGMM_ESHAPE;
+  for (int i = 0; i < n; ++i) {
+    const diagmm_topk_grad_job& j = jobs[i];
+    if (j.C < 1) return DIAGMM_ESHAPE;
+    if (!(j.temperature > 0.0)) return DIAGMM_ETEMPERATURE;
+    if (j.k < 1 || j.k > j.C) return DIAGMM_EK;
+    if (j.C > kSelMaxC) return DIAGMM_ETOOLARGE;
+  }
+  for (int b = 0; b < n; b += kMaxJobs) {
+    const int cnt = n - b < kMaxJobs ? n - b : kMaxJobs;
+    TopkGradJobs P{};
+    int cmax = 1;
+    for (int i = 0; i < cnt; ++i) {
+      P.j[i] = jobs[b + i];
+      cmax = P.j[i].C > cmax ? P.j[i].C : cmax;
+    }
+    const size_t sm = (size_t)cmax * 8 + kSelThreads * 8;
+    cudaFuncSetAttribute(k_topk_grad_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_topk_grad_batched<<<cnt, kSelThreads, sm, st>>>(P);
+    note_launch();
+  }
   return status_from_cuda();
 }
 

@@ -19,6 +19,8 @@ the transpose), K3 (per-diagonal dW, g_values, g_soft, g_bias) and K5
 
 from __future__ import annotations
 
+import contextlib
+
 from dataclasses import dataclass
 from math import ceil, sqrt
 
@@ -99,6 +101,7 @@ class _OpSpec:
     bucket: torch.Tensor | None = None  # dp.CompactGradExchange: K3 also writes the active rows here
     params: torch.Tensor | None = None  # schedule.DeviceSchedule: device {T, k} read by K4 / K5
     sel: ops.Selection | None = None    # the selection the forward used (set by the forward)
+    alpha_param: torch.Tensor | None = None  # the layer's alpha Parameter (deferred K5 writes its .grad)
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -138,6 +141,63 @@ def dense_route_min_tokens() -> int:
     import os
 
     return int(os.environ.get("DIAGMM_DENSE_MIN_TOKENS", "512"))
+
+
+class _K5Queue:
+    """K5 jobs queued by the backwards inside ``deferred_topk_grads()``."""
+
+    def __init__(self):
+        self.jobs = []
+
+    def flush(self) -> None:
+        """ONE batched launch for every queued layer (layers whose alpha appears more than
+        once go in later launches, so each accumulation sees the previous one)."""
+        pending = self.jobs
+        self.jobs = []
+        while pending:
+            batch, rest, seen = [], [], set()
+            for job in pending:
+                (rest if id(job[0]) in seen else batch).append(job)
+                seen.add(id(job[0]))
+            calls = []
+            for alpha, k, T, g_soft, clamped, l1, params in batch:
+                acc = alpha.grad is not None
+                calls.append((alpha.detach(), k, T, g_soft, clamped, l1, alpha.grad if acc else None, acc, params))
+            outs = ops.soft_topk_grad_many(calls)
+            for (alpha, *_), g in zip(batch, outs):
+                if alpha.grad is None:
+                    alpha.grad = g
+            pending = rest
+
+
+_K5_QUEUE: "_K5Queue | None" = None  # module-wide: autograd runs CUDA backwards on its own device thread
+
+
+@contextlib.contextmanager
+def deferred_topk_grads():
+    """Inside this context the DiagLinear backwards queue their soft-TopK gradients (K5)
+    instead of launching one kernel per layer, and return no alpha gradient to autograd;
+    on exit ONE batched launch writes every layer's g_alpha into ``alpha.grad``
+    (accumulating, as autograd would).  Results are bit-identical to the per-layer path.
+    Single-process use (the data-parallel exchange hooks alpha's autograd accumulation)."""
+    global _K5_QUEUE
+    prev, q = _K5_QUEUE, _K5Queue()
+    _K5_QUEUE = q
+    try:
+        yield q
+    finally:
+        _K5_QUEUE = prev
+    q.flush()
+
+
+def _k5(spec: "_OpSpec", alpha: torch.Tensor, g_soft: torch.Tensor, sel: ops.Selection):
+    """g_alpha of one layer now, or queued for the batched launch (returns None then)."""
+    q = _K5_QUEUE
+    if q is not None and spec.alpha_param is not None:
+        q.jobs.append((spec.alpha_param, spec.k, spec.temperature, g_soft, sel.clamped, spec.l1, spec.params))
+        return None
+    return ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft, clamped=sel.clamped,
+                              l1_coeff=spec.l1, params=spec.params)
 
 
 class DiagMMFunction(torch.autograd.Function):
@@ -220,8 +280,7 @@ class DiagMMFunction(torch.autograd.Function):
                 dy, x, vals, sel, M, N, need_bias=ctx.has_bias, need_soft=need_soft, bucket=spec.bucket,
                 max_act=ma)
         if need_soft:
-            g_alpha = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft,
-                                         clamped=sel.clamped, l1_coeff=spec.l1, params=spec.params)
+            g_alpha = _k5(spec, alpha, g_soft, sel)
         return dx, g_values, g_alpha, g_bias, None, d_res
 
 
@@ -270,14 +329,12 @@ class DiagMLPFunction(torch.autograd.Function):
         d_pre = ops.tc_gemm_nn(dy, W2, None, epilogue=2, aux=pre)
         gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True,
                                                bucket=s2.bucket)
-        ga2 = ops.soft_topk_grad(a2.detach(), s2.k, s2.temperature, gs2, clamped=sel2.clamped, l1_coeff=s2.l1,
-                                 params=s2.params)
+        ga2 = _k5(s2, a2, gs2, sel2)
         # fc1
         dx = ops.tc_gemm_nn(d_pre, W1)
         gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True,
                                                bucket=s1.bucket)
-        ga1 = ops.soft_topk_grad(a1.detach(), s1.k, s1.temperature, gs1, clamped=sel1.clamped, l1_coeff=s1.l1,
-                                 params=s1.params)
+        ga1 = _k5(s1, a1, gs1, sel1)
         hb1, hb2 = ctx.has_bias
         d_res = dy0 if ctx.needs_input_grad[10] else None
         return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None, d_res)
@@ -396,7 +453,7 @@ class DiagLinear(nn.Module):
         T = self.temperature(step)
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
                        presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None),
-                       params=getattr(self, "_sched_params", None))
+                       params=getattr(self, "_sched_params", None), alpha_param=self.alpha)
         self._last_spec = spec
         return spec
 
@@ -675,5 +732,5 @@ def penalties(model: nn.Module, fused: bool = False) -> list[torch.Tensor]:
 
 __all__ = [
     "DiagLinear", "DiagMMFunction", "DiagMLP", "DiagMLPFunction", "FrozenDiagLinear", "DiagHeurLinear", "DiagMatrix",
-    "ParamSpec", "diagheur_update", "penalties", "preselect", "EPS_ACTIVE",
+    "ParamSpec", "diagheur_update", "penalties", "preselect", "EPS_ACTIVE", "deferred_topk_grads",
 ]

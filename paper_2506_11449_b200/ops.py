@@ -195,6 +195,32 @@ def soft_topk_grad(alpha: torch.Tensor, k: int, temperature: float, upstream: to
     return g
 
 
+def soft_topk_grad_many(jobs) -> list:
+    """Batched K5: ``jobs`` = [(alpha, k, T, upstream, clamped, l1, out, accumulate, params)];
+    every layer's soft TopK gradient in ONE launch (one CTA each) — bit-identical to
+    calling ``soft_topk_grad`` per layer.  Returns the ``out`` tensors (allocated when None)."""
+    n = len(jobs)
+    if n == 0:
+        return []
+    arr = (_lib.TopkGradJob * n)()
+    outs, keep = [], []
+    stream = None
+    for i, (alpha, k, T, up, clamped, l1, out, acc, prm) in enumerate(jobs):
+        _need_cuda(alpha, up)
+        a = alpha.contiguous()
+        u = up.to(torch.float64).contiguous()
+        if u.shape != a.shape or clamped is None:
+            raise ValueError("batched K5 needs the upstream at alpha's shape and the clamped set")
+        g = out if out is not None else torch.empty_like(a)
+        keep += [a, u, clamped, g]
+        arr[i] = _lib.TopkGradJob(a.numel(), int(k), float(T), _p(a), _p(clamped), _p(u), float(l1), _p(g),
+                                  int(bool(acc)), _p(prm))
+        outs.append(g)
+        stream = _stream(a) if stream is None else stream
+    _lib.call("diagmm_topk_grad_batched", n, arr, stream)
+    return outs
+
+
 def select_hard(alpha: torch.Tensor, k: int) -> torch.Tensor:
     """select_hard (selection.py:176-186): int64 indices, ascending."""
     _need_cuda(alpha)

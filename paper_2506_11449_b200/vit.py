@@ -17,7 +17,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from . import _lib, ops
-from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, preselect
+from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, _k5, preselect
 from .selection import TemperatureSchedule
 
 
@@ -110,8 +110,7 @@ class QKVAttentionFunction(torch.autograd.Function):
                                                   need_bias=True, bucket=spec.bucket)
         ga = None
         if need_soft:
-            ga = ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, gs, clamped=sel.clamped,
-                                    l1_coeff=spec.l1, params=spec.params)
+            ga = _k5(spec, alpha, gs, sel)
         return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None, None
 
 
