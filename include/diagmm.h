@@ -362,6 +362,20 @@ DIAGMM_API int diagmm_materialize_transposed(int dtype, int M, int N, const void
                        const double* alpha_soft, const int32_t* active,
                        const int32_t* slot, const int32_t* n_act, int max_act,
                        void* w_dense_t, void* stream);
+
+/* Every layer's W_K in ONE launch (bf16 or fp32 W, one dtype per call): the
+ * model-level pre-pass right after the batched soft TopK, so the tensor-core route
+ * does not pay one small launch per layer.  Same values as diagmm_materialize. */
+typedef struct diagmm_materialize_job {
+  int M, N;
+  const void* values;       /* (C, L) float32 candidate store */
+  const double* alpha_soft; /* NULL: scale 1 */
+  const int32_t* slot;
+  const int32_t* n_act;
+  int max_act;
+  void* w;                  /* (M, N) output */
+} diagmm_materialize_job;
+DIAGMM_API int diagmm_materialize_batched(int dtype, int n, const diagmm_materialize_job* jobs, void* stream);
 DIAGMM_API int diagmm_gather_dense_grad(int dtype, int M, int N, const void* dW,
                              const void* values, const double* alpha_soft,
                              const int32_t* active, const int32_t* slot,

@@ -71,6 +71,14 @@ class TopkGradJob(C.Structure):
                 ("params", _vp)]
 
 
+class MaterializeJob(C.Structure):
+    """diagmm_materialize_job (include/diagmm.h)."""
+
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("values", _vp), ("alpha_soft", _vp), ("slot", _vp),
+                ("n_act", _vp), ("max_act", C.c_int), ("w", _vp)]
+
+
+SIGNATURES["diagmm_materialize_batched"] = (_i, [_i, _i, C.POINTER(MaterializeJob), _vp])
 SIGNATURES["diagmm_topk_waterfill_batched"] = (_i, [_i, C.POINTER(TopkJob), _vp])
 SIGNATURES["diagmm_topk_grad_batched"] = (_i, [_i, C.POINTER(TopkGradJob), _vp])
 SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp, _vp])

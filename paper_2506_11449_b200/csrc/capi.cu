@@ -13,6 +13,7 @@ template <typename T> size_t dw_workspace(int, int, int, int);
 template <typename T>
 int run_dw(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
            const int32_t*, const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, void*, int);
+template <typename T> int run_materialize_batched(int, const diagmm_materialize_job*, cudaStream_t);
 template <typename T>
 int run_materialize(int, int, const void*, const double*, const int32_t*, const int32_t*, int, void*,
                     cudaStream_t, bool);  // (slot, n_act, ..., transposed)
@@ -330,6 +331,13 @@ int diagmm_materialize(int dtype, int M, int N, const void* values, const double
   (void)active;
   DIAGMM_DISPATCH(dtype, run_materialize, M, N, values, alpha_soft, slot, n_act, max_act, w_dense,
                   S(stream), false)
+}
+
+int diagmm_materialize_batched(int dtype, int n, const diagmm_materialize_job* jobs, void* stream) {
+  if (n < 0) return DIAGMM_ESHAPE;
+  if (dtype == DIAGMM_BF16) return run_materialize_batched<__nv_bfloat16>(n, jobs, S(stream));
+  if (dtype == DIAGMM_F32) return run_materialize_batched<float>(n, jobs, S(stream));
+  return DIAGMM_ESHAPE;
 }
 
 int diagmm_materialize_transposed(int dtype, int M, int N, const void* values, const double* alpha_soft,

@@ -1280,10 +1280,9 @@ k_materialize(int M, int N, const typename Traits<T>::P* __restrict__ vals, cons
 // and a scattered value load for every output element.
 constexpr int kMTR = 32, kMTC = 256;
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_materialize_tiles(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
+__device__ void materialize_tile(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
                     const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
-                    T* __restrict__ w, int vec) {
+                    T* __restrict__ w, int vec, int tx, int ty) {
   static_assert(sizeof(T) <= 4, "tile kernel for bf16 / fp32");
   __shared__ __align__(16) T tile[kMTR][kMTC];
   __shared__ int s_list[kMTR + kMTC];
@@ -1292,7 +1291,7 @@ k_materialize_tiles(int M, int N, const typename Traits<T>::P* __restrict__ vals
   const int n_act = min(*n_act_p, max_act);
   const bool tall = M >= N;
   const int mod = tall ? M : N, L = tall ? N : M;
-  const int r0 = blockIdx.y * kMTR, c0 = blockIdx.x * kMTC;
+  const int r0 = ty * kMTR, c0 = tx * kMTC;
   constexpr int VW = 16 / sizeof(T);
   for (int i = threadIdx.x; i < kMTR * kMTC / VW; i += blockDim.x)
     reinterpret_cast<uint4*>(&tile[0][0])[i] = make_uint4(0, 0, 0, 0);
@@ -1339,6 +1338,40 @@ k_materialize_tiles(int M, int N, const typename Traits<T>::P* __restrict__ vals
       for (int e = 0; e < VW && cb + e < N; ++e) dst[e] = tile[i][ch * VW + e];
     }
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_materialize_tiles(int M, int N, const typename Traits<T>::P* __restrict__ vals, const double* __restrict__ asoft,
+                    const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p, int max_act,
+                    T* __restrict__ w, int vec) {
+  materialize_tile<T>(M, N, vals, asoft, slot, n_act_p, max_act, w, vec, blockIdx.x, blockIdx.y);
+}
+
+// every layer's W_K in ONE launch (the model-level pre-pass after the batched K4):
+// the flat grid walks the layers' tiles; a CTA finds its layer in the tile prefix
+constexpr int kMatJobs = 64;
+struct MatJobs {
+  diagmm_materialize_job j[kMatJobs];
+  int start[kMatJobs + 1];  // first flat tile of each job
+  int tiles_x[kMatJobs];
+  int vec[kMatJobs];
+  int n;
+};
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_materialize_batched(const __grid_constant__ MatJobs P) {
+  int lo = 0, hi = P.n - 1;  // the job whose [start, next start) holds this tile
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const diagmm_materialize_job& J = P.j[lo];
+  const int local = t - P.start[lo];
+  materialize_tile<T>(J.M, J.N, static_cast<const typename Traits<T>::P*>(J.values), J.alpha_soft, J.slot,
+                      J.n_act, J.max_act, static_cast<T*>(J.w), P.vec[lo], local % P.tiles_x[lo],
+                      local / P.tiles_x[lo]);
 }
 
 // Dense dW -> per-diagonal rows, pass 1: a CTA stages a tile of dW (coalesced)
@@ -2860,6 +2893,34 @@ int run_materialize(int M, int N, const void* vals, const double* asoft, const i
   note_launch();
   return status_from_cuda();
 }
+
+template <typename T>
+int run_materialize_batched(int n, const diagmm_materialize_job* jobs, cudaStream_t st) {
+  if constexpr (sizeof(T) > 4) {
+    return DIAGMM_ESHAPE;
+  } else {
+    for (int b = 0; b < n; b += kMatJobs) {
+      MatJobs P{};
+      P.n = n - b < kMatJobs ? n - b : kMatJobs;
+      int total = 0;
+      for (int i = 0; i < P.n; ++i) {
+        const diagmm_materialize_job& j = jobs[b + i];
+        if (j.M < 1 || j.N < 1) return DIAGMM_ESHAPE;
+        P.j[i] = j;
+        P.start[i] = total;
+        P.tiles_x[i] = ceil_div(j.N, kMTC);
+        P.vec[i] = (j.N % (16 / (int)sizeof(T)) == 0) && aligned16(j.w);
+        total += P.tiles_x[i] * ceil_div(j.M, kMTR);
+      }
+      P.start[P.n] = total;
+      k_materialize_batched<T><<<total, 256, 0, st>>>(P);
+      note_launch();
+    }
+    return status_from_cuda();
+  }
+}
+template int run_materialize_batched<float>(int, const diagmm_materialize_job*, cudaStream_t);
+template int run_materialize_batched<__nv_bfloat16>(int, const diagmm_materialize_job*, cudaStream_t);
 
 template <typename P>
 int run_gather_dense(int M, int N, const void* dW, const void* vals, const double* asoft, const int32_t* slot,

@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import torch
 from torch import nn
 
-from .layer import DiagLinear, preselect
+from .layer import DiagLinear, dense_route_min_tokens, preselect
+from .vit import _premat_enabled
 from .selection import TemperatureSchedule
 from .vit import Block, LayerNorm
 
@@ -66,7 +67,12 @@ class GPT2(nn.Module):
         """ids (B, S) int64 -> logits (B, S, vocab)."""
         diag = self.diag_layers()
         if diag:
-            preselect(diag, diag[0].step)  # one batched soft-TopK launch for all layers
+            # one batched soft-TopK launch for all layers (+ one batched W_K build on the
+            # tensor-core route)
+            mat = (torch.bfloat16 if torch.is_autocast_enabled("cuda") and ids.is_cuda
+                   and torch.get_autocast_dtype("cuda") == torch.bfloat16
+                   and ids.numel() >= dense_route_min_tokens() and _premat_enabled() else None)
+            preselect(diag, diag[0].step, materialize=mat)
         S = ids.shape[1]
         pos = torch.arange(S, device=ids.device)
         x = self.wte(ids) + self.wpe(pos)[None]

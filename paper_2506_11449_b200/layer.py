@@ -102,6 +102,7 @@ class _OpSpec:
     params: torch.Tensor | None = None  # schedule.DeviceSchedule: device {T, k} read by K4 / K5
     sel: ops.Selection | None = None    # the selection the forward used (set by the forward)
     alpha_param: torch.Tensor | None = None  # the layer's alpha Parameter (deferred K5 writes its .grad)
+    prew: torch.Tensor | None = None    # W_K materialized by preselect's batched pre-pass (same selection)
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -200,6 +201,15 @@ def _k5(spec: "_OpSpec", alpha: torch.Tensor, g_soft: torch.Tensor, sel: ops.Sel
                               l1_coeff=spec.l1, params=spec.params)
 
 
+def _w_k(spec: "_OpSpec", dtype: torch.dtype, values, sel, M: int, N: int) -> torch.Tensor:
+    """W_K for this forward: the pre-pass's (preselect(materialize=...)) when it was built
+    for this selection and dtype, else materialized now."""
+    W, spec.prew = spec.prew, None
+    if W is not None and W.dtype == dtype and tuple(W.shape) == (M, N):
+        return W
+    return ops.materialize(values, sel, M, N, dtype=dtype)
+
+
 class DiagMMFunction(torch.autograd.Function):
     """y = x @ W_K^T + bias for the soft-selected diagonals (layers.py:108-170, 230-251)."""
 
@@ -219,7 +229,7 @@ class DiagMMFunction(torch.autograd.Function):
         if tc:
             # tensor-core route: our tcgen05 GEMM on the dense-equivalent W_K (bias fused);
             # W_K is kept for the input gradient (read MN-major there: no W_K^T is built)
-            W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+            W = _w_k(spec, x.dtype, vals, sel, M, N)
             bz = None if bias is None else bias.detach()
             if residual is not None and residual.dtype == x.dtype:
                 # the caller's residual add fused into the epilogue (one rounding)
@@ -228,7 +238,7 @@ class DiagMMFunction(torch.autograd.Function):
             else:
                 y = ops.tc_gemm(x.contiguous(), W, bz)
         elif dense:
-            W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+            W = _w_k(spec, x.dtype, vals, sel, M, N)
             y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
         else:
             y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach(),
@@ -297,13 +307,13 @@ class DiagMLPFunction(torch.autograd.Function):
         sel2 = s2.presel or ops.soft_topk_select(a2.detach(), s2.k, s2.temperature, params=s2.params)
         s1.sel, s2.sel = sel1, sel2
         x = x.contiguous()
-        W1 = ops.materialize(v1.detach(), sel1, s1.M, s1.N, dtype=x.dtype)
+        W1 = _w_k(s1, x.dtype, v1.detach(), sel1, s1.M, s1.N)
         if fuse_fwd:
             act, pre = ops.tc_gemm_ex(x, W1, None if b1 is None else b1.detach(), epilogue=1)
         else:
             pre = ops.tc_gemm(x, W1, None if b1 is None else b1.detach())
             act = F.gelu(pre, approximate="tanh")
-        W2 = ops.materialize(v2.detach(), sel2, s2.M, s2.N, dtype=x.dtype)
+        W2 = _w_k(s2, x.dtype, v2.detach(), sel2, s2.M, s2.N)
         bz2 = None if b2 is None else b2.detach()
         if residual is not None and residual.dtype == x.dtype:  # residual add fused into fc2's epilogue
             y, _ = ops.tc_gemm_ex(act, W2, bz2, epilogue=3, aux=residual.detach())
@@ -454,6 +464,7 @@ class DiagLinear(nn.Module):
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
                        presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None),
                        params=getattr(self, "_sched_params", None), alpha_param=self.alpha)
+        spec.prew = self._take_premat(step, T) if spec.presel is not None else None
         self._last_spec = spec
         return spec
 
@@ -461,6 +472,12 @@ class DiagLinear(nn.Module):
         ps, self._presel = self._presel, None
         if ps is not None and ps[0] == (step, self.k, T):
             return ps[1]
+        return None
+
+    def _take_premat(self, step: int, T: float):
+        pm, self._premat = getattr(self, "_premat", None), None
+        if pm is not None and pm[0] == (step, self.k, T):
+            return pm[1]
         return None
 
     def extra_repr(self) -> str:
@@ -688,12 +705,14 @@ def diagheur_update(layer: DiagHeurLinear, rng: np.random.Generator, step: int |
     return layer
 
 
-def preselect(layers, step: int) -> None:
+def preselect(layers, step: int, materialize: torch.dtype | None = None) -> None:
     """Run the soft TopK of every layer for ``step`` in ONE launch (batched K4)
     and hand each layer its selection for its next forward at that step.
-    Call it right before the model's forward (alpha must not change between
-    the two); a layer whose forward does not match (step, k, T) re-selects
-    on its own, so the result never differs from the per-layer path."""
+    Call it right before the model's forward (alpha and values must not change
+    between the two); a layer whose forward does not match (step, k, T) re-selects
+    on its own, so the result never differs from the per-layer path.
+    ``materialize``: also build every auto-route layer's dense W_K of that dtype in
+    ONE launch (the tensor-core route's operand; identical to the per-layer build)."""
     layers = [m for m in layers if isinstance(m, DiagLinear)]
     if not layers:
         return
@@ -702,6 +721,13 @@ def preselect(layers, step: int) -> None:
                                      params=[getattr(m, "_sched_params", None) for m in layers])
     for m, T, sel in zip(layers, temps, sels):
         m._presel = ((step, m.k, T), sel)
+    if materialize is not None:
+        todo = [(m, T, sel) for m, T, sel in zip(layers, temps, sels)
+                if m.route == "auto" and m.values.dtype == torch.float32]
+        Ws = ops.materialize_many([(m.values.detach(), sel, m.out_features, m.in_features) for m, _, sel in todo],
+                                  materialize)
+        for (m, T, _), W in zip(todo, Ws):
+            m._premat = ((step, m.k, T), W)
 
 
 def penalties(model: nn.Module, fused: bool = False) -> list[torch.Tensor]:

@@ -379,6 +379,31 @@ def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
     return W
 
 
+def materialize_many(items, dtype: torch.dtype) -> list:
+    """Every layer's dense W_K in ONE launch: ``items`` = [(values, sel, M, N)] (float32
+    stores), W of ``dtype`` (bf16 / fp32) — identical to ``materialize`` per layer."""
+    n = len(items)
+    if n == 0:
+        return []
+    code = _code(dtype)
+    arr = (_lib.MaterializeJob * n)()
+    outs, keep = [], []
+    stream = None
+    for i, (values, sel, M, N) in enumerate(items):
+        _need_cuda(values)
+        C, L = geometry(M, N)
+        if tuple(values.shape) != (C, L) or values.dtype != torch.float32:
+            raise ShapeMismatch(f"values {tuple(values.shape)} {values.dtype} for a batched ({M}, {N}) W")
+        v = values.contiguous()
+        W = torch.empty((M, N), dtype=dtype, device=values.device)
+        keep.append(v)
+        arr[i] = _lib.MaterializeJob(M, N, _p(v), _p(sel.alpha_soft), _p(sel.slot), _p(sel.n_act), C, _p(W))
+        outs.append(W)
+        stream = _stream(values) if stream is None else stream
+    _lib.call("diagmm_materialize_batched", code, n, arr, stream)
+    return outs
+
+
 def gather_dense_grad(dW: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
                       need_soft: bool = True):
     """g_values / g_soft from a dense dW (M, N) (the dense branch of layers.py:150-153)."""

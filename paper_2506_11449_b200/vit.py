@@ -17,7 +17,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from . import _lib, ops
-from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, _k5, preselect
+from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, _k5, _w_k, dense_route_min_tokens, preselect
 from .selection import TemperatureSchedule
 
 
@@ -81,7 +81,7 @@ class QKVAttentionFunction(torch.autograd.Function):
         sel = spec.presel or ops.soft_topk_select(alpha.detach(), spec.k, spec.temperature, params=spec.params)
         spec.sel = sel
         vals = values.detach()
-        W = ops.materialize(vals, sel, M, N, dtype=x.dtype)
+        W = _w_k(spec, x.dtype, vals, sel, M, N)
         h = ops.tc_gemm(x.contiguous(), W, None if bias is None else bias.detach())
         hd = N // H
         qkv = [t_.detach().requires_grad_(True) for t_ in h.view(B, T, 3, H, hd).permute(2, 0, 3, 1, 4).unbind(0)]
@@ -320,12 +320,24 @@ class ViT(nn.Module):
     def forward(self, images):
         diag = self.diag_layers()
         if diag:
-            preselect(diag, diag[0].step)  # one batched soft-TopK launch for all layers
+            # one batched soft-TopK launch for all layers (+ one batched W_K build when the
+            # bf16 token count puts them on the tensor-core route)
+            tokens = images.shape[0] * ((images.shape[-1] // self.cfg.patch) ** 2 + 1)
+            mat = (torch.bfloat16 if torch.is_autocast_enabled("cuda") and images.is_cuda
+                   and torch.get_autocast_dtype("cuda") == torch.bfloat16 and tokens >= dense_route_min_tokens()
+                   and _premat_enabled() else None)
+            preselect(diag, diag[0].step, materialize=mat)
         x = self._patchify(images)
         x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
         for blk in self.blocks:
             x = blk(x)
         return self.head(self.norm(x)[:, 0])
+
+
+def _premat_enabled() -> bool:
+    import os
+
+    return os.environ.get("DIAGMM_PREMAT", "1") != "0"
 
 
 class MLPModel(nn.Module):

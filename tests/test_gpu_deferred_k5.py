@@ -93,3 +93,25 @@ def test_deferred_k5_fma_route_and_graph():
     torch.cuda.synchronize()
     for m, r in zip(graph_layers, ref):
         assert torch.equal(m.alpha.grad, r)
+
+
+def test_batched_w_k_prepass_bitwise_equal(monkeypatch):
+    """preselect(materialize=bf16): every layer's W_K built in one launch before the forward
+    gives the same logits and gradients, bit for bit, as the per-layer builds."""
+    def run(premat: str):
+        monkeypatch.setenv("DIAGMM_PREMAT", premat)
+        torch.manual_seed(0)
+        model = ViT(ViTConfig(dim=256, depth=2, heads=4, classes=10), device="cuda")
+        g = torch.Generator(device="cuda").manual_seed(7)
+        img = torch.randn(4, 3, 224, 224, device="cuda", generator=g).to(torch.bfloat16)
+        model.set_step(0)
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+            logits = model(img)
+        logits.float().square().sum().backward()
+        torch.cuda.synchronize()
+        return [logits.detach().clone()] + [p.grad.detach().clone() for p in model.parameters() if p.grad is not None]
+
+    ref, got = run("0"), run("1")
+    assert len(ref) == len(got)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
