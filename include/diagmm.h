@@ -309,6 +309,35 @@ DIAGMM_API int diagmm_tc_backward_weight_split(int M, int N, int B, const void* 
                                                double* g_soft, void* g_bias, void* workspace,
                                                size_t ws_bytes, void* bucket, int bucket_rows,
                                                void* stream);
+
+/* Deferred finalize of the tensor-core dW (single process): _partials runs only the
+ * dW GEMM with its fused diagonal gather (split-K partials + bias column partials into
+ * `workspace`, the layout of diagmm_tc_backward_weight; dy given whole (ms = 0) or as
+ * column blocks), and _finalize_batched later folds every layer's partials into
+ * g_values / g_soft / g_bias (+ the bucket rows) in ONE launch — the same fixed-order
+ * reductions as diagmm_tc_backward_weight, bit-identical results.  `parts` of a job is
+ * diagmm_tc_dw_splits(M, N, B). */
+DIAGMM_API int diagmm_tc_dw_splits(int M, int N, int B);
+DIAGMM_API int diagmm_tc_backward_weight_partials(int M, int N, int B, const void* dy0, const void* dy1,
+                                                  const void* dy2, int ms, const void* x, const int32_t* slot,
+                                                  const int32_t* n_act, int max_act, int need_bias,
+                                                  void* workspace, size_t ws_bytes, void* stream);
+typedef struct diagmm_dw_finalize_job {
+  int M, N, parts;
+  const float* partial;   /* workspace of the _partials call */
+  const float* colsum;    /* its bias column partials (NULL: no bias gradient) */
+  int max_act;
+  const int32_t* slot;
+  const int32_t* n_act;
+  const double* alpha_soft;
+  const float* values;
+  float* g_values;        /* (C, L) */
+  double* g_soft;         /* (C,) or NULL */
+  float* g_bias;          /* (M,) or NULL */
+  float* bucket;          /* or NULL */
+  int bucket_rows;
+} diagmm_dw_finalize_job;
+DIAGMM_API int diagmm_tc_dw_finalize_batched(int n, const diagmm_dw_finalize_job* jobs, void* stream);
 DIAGMM_API size_t diagmm_tc_backward_weight_workspace(int M, int N, int B, int max_act);
 DIAGMM_API int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x,
                                          const void* values, const double* alpha_soft,

@@ -78,7 +78,19 @@ class MaterializeJob(C.Structure):
                 ("n_act", _vp), ("max_act", C.c_int), ("w", _vp)]
 
 
+class DwFinalizeJob(C.Structure):
+    """diagmm_dw_finalize_job (include/diagmm.h)."""
+
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("parts", C.c_int), ("partial", _vp), ("colsum", _vp),
+                ("max_act", C.c_int), ("slot", _vp), ("n_act", _vp), ("alpha_soft", _vp), ("values", _vp),
+                ("g_values", _vp), ("g_soft", _vp), ("g_bias", _vp), ("bucket", _vp), ("bucket_rows", C.c_int)]
+
+
 SIGNATURES["diagmm_materialize_batched"] = (_i, [_i, _i, C.POINTER(MaterializeJob), _vp])
+SIGNATURES["diagmm_tc_dw_splits"] = (_i, [_i, _i, _i])
+SIGNATURES["diagmm_tc_backward_weight_partials"] = (
+    _i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp, _sz, _vp])
+SIGNATURES["diagmm_tc_dw_finalize_batched"] = (_i, [_i, C.POINTER(DwFinalizeJob), _vp])
 SIGNATURES["diagmm_topk_waterfill_batched"] = (_i, [_i, C.POINTER(TopkJob), _vp])
 SIGNATURES["diagmm_topk_grad_batched"] = (_i, [_i, C.POINTER(TopkGradJob), _vp])
 SIGNATURES["diagmm_adamw_multi"] = (_i, [_i, C.POINTER(TensorDesc), _d, _d, _d, _d, _vp, _vp, _vp])

@@ -44,6 +44,11 @@ int run_tc_gemm_bf16(int, int, int, const void*, const void*, const float*, void
                      bool b_kn = false, const void* A1 = nullptr, const void* A2 = nullptr, int a_ks = 0);
 int run_tc_sparse_probe(int, int, int, const void*, const void*, void*, cudaStream_t);
 size_t tc_dw_workspace(int, int, int, int);
+int tc_dw_splits(int M, int N, int ntok);
+int run_tc_dw(int M, int N, int ntok, const void* dy, const void* x, const int32_t* slot, const int32_t* n_act,
+              int max_act, float* partial, size_t partial_bytes, float* colsum, cudaStream_t st, const void* dy1,
+              const void* dy2, int a_ms);
+int run_dw_finalize_batched(int n, const diagmm_dw_finalize_job* jobs, cudaStream_t st);
 int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const double*, const int32_t*,
                    const int32_t*, int, void*, double*, void*, void*, size_t, cudaStream_t, const void* dy1,
                    const void* dy2, int a_ms, void* bucket, int bucket_rows);
@@ -215,6 +220,28 @@ int diagmm_tc_backward_weight(int M, int N, int B, const void* dy, const void* x
   if (bucket_rows < 0 || (bucket_rows > 0 && !bucket)) return DIAGMM_ESHAPE;
   return run_tc_dw_full(M, N, B, dy, x, values, alpha_soft, slot, n_act, max_act, g_values, g_soft, g_bias,
                         workspace, ws_bytes, S(stream), nullptr, nullptr, 0, bucket, bucket_rows);
+}
+
+int diagmm_tc_dw_splits(int M, int N, int B) { return tc_dw_splits(M, N, B > 0 ? B : 1); }
+
+int diagmm_tc_backward_weight_partials(int M, int N, int B, const void* dy0, const void* dy1, const void* dy2, int ms,
+                                       const void* x, const int32_t* slot, const int32_t* n_act, int max_act,
+                                       int need_bias, void* workspace, size_t ws_bytes, void* stream) {
+  if (int e = check_shape(M, N, B, max_act)) return e;
+  if (ms < 0 || B < 1) return DIAGMM_ESHAPE;
+  if (ws_bytes < tc_dw_workspace(M, N, B, max_act)) return DIAGMM_EWORKSPACE;
+  const int L = M < N ? M : N;
+  const int ks = tc_dw_splits(M, N, B);
+  const size_t pbytes = ((size_t)ks * (max_act > 0 ? max_act : 1) * L * sizeof(float) + 15) / 16 * 16;
+  float* partial = static_cast<float*>(workspace);
+  float* colsum = reinterpret_cast<float*>(static_cast<char*>(workspace) + pbytes);
+  return run_tc_dw(M, N, B, dy0, x, slot, n_act, max_act > 0 ? max_act : 1, partial, pbytes,
+                   need_bias ? colsum : nullptr, S(stream), dy1, dy2, ms);
+}
+
+int diagmm_tc_dw_finalize_batched(int n, const diagmm_dw_finalize_job* jobs, void* stream) {
+  if (n < 0) return DIAGMM_ESHAPE;
+  return run_dw_finalize_batched(n, jobs, S(stream));
 }
 
 int diagmm_tc_gemm_bf16_nn_split(int Mdim, int Ndim, int K, const void* A0, const void* A1, const void* A2, int ks,

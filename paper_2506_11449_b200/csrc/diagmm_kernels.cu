@@ -1022,25 +1022,24 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // issued before its first use, so an active row costs ~one memory latency and
 // the ~90 % inactive rows are a vectorised zero fill.  g_soft: per-thread sums
 // in a fixed order, then a fixed shuffle/warp tree (deterministic).
+// One candidate row of the finalize (shared by the per-layer and the batched kernels):
+// reduce the dW partials over parts (fixed order), scale into g_values, zero inactive
+// rows, g_soft, the data-parallel bucket row.
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
-              const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
-              const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
-              typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
-              typename Traits<T>::P* __restrict__ bucket, int bucket_rows,
-              const int32_t* __restrict__ active_rows) {
+__device__ void finalize_row(int ii, int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial,
+                             int max_act, const int32_t* __restrict__ slot, int n_act,
+                             const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
+                             typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
+                             typename Traits<T>::P* __restrict__ bucket, int bucket_rows,
+                             const int32_t* __restrict__ active_rows) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
-  static_assert(sizeof(A) == sizeof(P), "partials and values share the vector width");
   constexpr int VW = 16 / sizeof(P);
   using V = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
   using VA = typename std::conditional<sizeof(A) == 8, double2, float4>::type;
-  __shared__ double red[kWarps];
-  const int n_act = min(*n_act_p, max_act);
-  // persistent over candidate rows (grid-stride): ~90 % of the rows are a zero fill,
-  // far too little work per CTA to pay a CTA launch each
-  for (int ii = blockIdx.x; ii < (active_rows ? n_act : C); ii += gridDim.x) {
+  const int lane = threadIdx.x & 31;  // one WARP per row: no barrier, rows of a CTA run concurrently
+  do {
+
   // active_rows: the CTAs walk the active list only (the zero rows are filled
   // concurrently by k_zero_inactive on a side stream)
   const int i = active_rows ? active_rows[ii] : ii;
@@ -1051,12 +1050,12 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   if (s < 0 || s >= n_act) {
     if (vec) {
       V* g4 = reinterpret_cast<V*>(grow);
-      for (int t = threadIdx.x; t < L / VW; t += blockDim.x) g4[t] = V{};
+      for (int t = lane; t < L / VW; t += 32) g4[t] = V{};
     } else {
-      for (int t = threadIdx.x; t < L; t += blockDim.x) grow[t] = P(0);
+      for (int t = lane; t < L; t += 32) grow[t] = P(0);
     }
-    if (g_soft && threadIdx.x == 0) g_soft[i] = 0.0;
-    continue;
+    if (g_soft && lane == 0) g_soft[i] = 0.0;
+    break;
   }
   const double sc = asoft ? asoft[i] : 1.0;
   const P* vrow = vals + (size_t)i * L;
@@ -1070,7 +1069,7 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
     const int nv = L / VW;
     const size_t zs = (size_t)max_act * L / VW;
     const VA* pbase = reinterpret_cast<const VA*>(partial + (size_t)s * L);
-    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    for (int c = lane; c < nv; c += 32) {
       const V v = reinterpret_cast<const V*>(vrow)[c];
       VA gw = nparts > 0 ? pbase[c] : VA{};
       A* ge = reinterpret_cast<A*>(&gw);
@@ -1101,7 +1100,7 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
         for (int e = 0; e < VW; ++e) brow[c * VW + e] = oe[e];
     }
   } else {
-    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+    for (int t = lane; t < L; t += 32) {
       A gw = A(0);
       for (int p = 0; p < nparts; ++p) gw += partial[((size_t)p * max_act + s) * L + t];
       grow[t] = (P)(sc * (double)gw);
@@ -1109,19 +1108,29 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
       local += (double)gw * (double)vrow[t];
     }
   }
-  if (g_soft) {
+  if (g_soft) {  // per-lane sums in a fixed order, then a fixed shuffle tree (deterministic)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-      g_soft[i] = tot;
-    }
-    __syncthreads();  // red is reused by the next row
+    if (lane == 0) g_soft[i] = local;
   }
-  }
+    } while (false);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
+              const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
+              const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
+              typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
+              typename Traits<T>::P* __restrict__ bucket, int bucket_rows,
+              const int32_t* __restrict__ active_rows) {
+  static_assert(sizeof(typename Vec<T>::A) == sizeof(typename Traits<T>::P), "partials and values share the vector width");
+  const int n_act = min(*n_act_p, max_act);
+  // one warp per row, grid-stride over rows: ~90 % of the rows are a zero fill
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
+  for (int ii = w; ii < (active_rows ? n_act : C); ii += nw)
+    finalize_row<T>(ii, C, L, nparts, partial, max_act, slot, n_act, asoft, vals, g_values, g_soft, bucket,
+                    bucket_rows, active_rows);
 }
 
 // one CTA per candidate row: measured faster than a persistent grid-stride loop
@@ -1184,14 +1193,13 @@ k_colsum_partial(int B, int M, const T* __restrict__ dy, typename Vec<T>::A* __r
   part[(size_t)blockIdx.y * M + r] = acc;
 }
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
-               typename Traits<T>::P* __restrict__ g_bias) {
+__device__ void colsum_final_block(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
+                                   typename Traits<T>::P* __restrict__ g_bias, int blk) {
   using A = typename Vec<T>::A;
   __shared__ A red[8][33];
   // 32 columns per CTA, the 8 warps split the parts, fixed-order fold
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.x * 32 + lane;
+  const int r = blk * 32 + lane;
   A acc = A(0);
   if (r < M)
     for (int p = w; p < nparts; p += 8) acc += part[(size_t)p * M + r];
@@ -1203,6 +1211,65 @@ k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
     for (int i = 0; i < 8; ++i) s += red[i][lane];
     g_bias[r] = (typename Traits<T>::P)s;
   }
+}
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_colsum_final(int M, int nparts, const typename Vec<T>::A* __restrict__ part,
+               typename Traits<T>::P* __restrict__ g_bias) {
+  colsum_final_block<T>(M, nparts, part, g_bias, blockIdx.x);
+}
+
+// Every layer's finalize (+ bias column fold) in ONE launch: per job C / kFinRows row CTAs, then
+// ceil(M / 32) bias CTAs; a CTA finds its job by binary search on the prefix.
+constexpr int kFinJobs = 64;
+constexpr int kFinRows = 8;  // a CTA per row made the batched launch CTA-launch bound (0.31 ms for ViT-B)
+struct FinJobs {
+  diagmm_dw_finalize_job j[kFinJobs];
+  int start[kFinJobs + 1];
+  int rows[kFinJobs];
+  int n;
+};
+__global__ void __launch_bounds__(256)
+k_dw_finalize_batched(const __grid_constant__ FinJobs P) {
+  using T = __nv_bfloat16;
+  int lo = 0, hi = P.n - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const diagmm_dw_finalize_job& J = P.j[lo];
+  const int local = t - P.start[lo];
+  const int C = J.M > J.N ? J.M : J.N, L = J.M < J.N ? J.M : J.N;
+  if (local < P.rows[lo]) {  // kFinRows = 8 candidate rows per CTA, one per warp (most are zero fills)
+    const int n_act = min(*J.n_act, J.max_act);
+    const int r = local * kFinRows + (threadIdx.x >> 5);
+    if (r < C)
+      finalize_row<T>(r, C, L, J.parts, J.partial, J.max_act, J.slot, n_act, J.alpha_soft, J.values, J.g_values,
+                      J.g_soft, J.bucket, J.bucket_rows, nullptr);
+  } else {
+    colsum_final_block<T>(J.M, J.parts, J.colsum, J.g_bias, local - P.rows[lo]);
+  }
+}
+
+int run_dw_finalize_batched(int n, const diagmm_dw_finalize_job* jobs, cudaStream_t st) {
+  for (int b = 0; b < n; b += kFinJobs) {
+    FinJobs P{};
+    P.n = n - b < kFinJobs ? n - b : kFinJobs;
+    int total = 0;
+    for (int i = 0; i < P.n; ++i) {
+      const diagmm_dw_finalize_job& j = jobs[b + i];
+      if (j.M < 1 || j.N < 1 || j.parts < 0 || j.max_act < 0) return DIAGMM_ESHAPE;
+      P.j[i] = j;
+      P.start[i] = total;
+      P.rows[i] = ceil_div(j.M > j.N ? j.M : j.N, kFinRows);
+      total += P.rows[i] + (j.g_bias && j.colsum ? ceil_div(j.M, 32) : 0);
+    }
+    P.start[P.n] = total;
+    k_dw_finalize_batched<<<total, 256, 0, st>>>(P);
+    note_launch();
+  }
+  return status_from_cuda();
 }
 
 // --------------------------------------------------------------------------- dense route
@@ -2864,7 +2931,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<max_act > 0 ? max_act : 1, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<ceil_div(max_act > 0 ? max_act : 1, kWarps), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
                                        static_cast<P*>(bucket), bucket_rows, active);
   note_launch();
@@ -2975,7 +3042,7 @@ int run_tc_dw_full(int M, int N, int B, const void* dy, const void* x, const voi
       cudaMemsetAsync(g_bias, 0, (size_t)M * sizeof(P), st);
     }
   }
-  k_dw_finalize<T><<<finalize_grid(C), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  k_dw_finalize<T><<<ceil_div(C, kWarps), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
                                        static_cast<P*>(bucket), bucket_rows, nullptr);
   note_launch();

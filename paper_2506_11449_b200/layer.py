@@ -103,6 +103,8 @@ class _OpSpec:
     sel: ops.Selection | None = None    # the selection the forward used (set by the forward)
     alpha_param: torch.Tensor | None = None  # the layer's alpha Parameter (deferred K5 writes its .grad)
     prew: torch.Tensor | None = None    # W_K materialized by preselect's batched pre-pass (same selection)
+    values_param: torch.Tensor | None = None  # the layer's values / bias Parameters (deferred finalize)
+    bias_param: torch.Tensor | None = None
 
 
 def _use_dense(spec: _OpSpec, sel: ops.Selection, B: int, act_dtype: torch.dtype) -> bool:
@@ -144,15 +146,38 @@ def dense_route_min_tokens() -> int:
     return int(os.environ.get("DIAGMM_DENSE_MIN_TOKENS", "512"))
 
 
+def _accumulate(param: torch.Tensor, g: torch.Tensor) -> None:
+    """What autograd's AccumulateGrad does for a dense gradient."""
+    if param.grad is None:
+        param.grad = g
+    else:
+        param.grad.add_(g)
+
+
 class _K5Queue:
-    """K5 jobs queued by the backwards inside ``deferred_topk_grads()``."""
+    """Work queued by the backwards inside ``deferred_topk_grads()``: tensor-core dW
+    finalizes (``fin``) and K5 jobs (``jobs``)."""
 
     def __init__(self):
         self.jobs = []
+        self.fin = []
 
     def flush(self) -> None:
-        """ONE batched launch for every queued layer (layers whose alpha appears more than
-        once go in later launches, so each accumulation sees the previous one)."""
+        """ONE batched finalize launch for every deferred tensor-core dW (g_values, g_soft,
+        g_bias), then ONE batched K5 launch for every queued layer (layers whose alpha
+        appears more than once go in later launches, so each accumulation sees the
+        previous one)."""
+        if self.fin:
+            fin, self.fin = self.fin, []
+            outs = ops.dw_finalize_many([f[0] for f in fin])
+            for (_, vp, bp, k5), (gv, gs, gb) in zip(fin, outs):
+                if vp.requires_grad:
+                    _accumulate(vp, gv)
+                if bp is not None and gb is not None and bp.requires_grad:
+                    _accumulate(bp, gb)
+                if k5 is not None:
+                    alpha_param, k, T, clamped, l1, params = k5
+                    self.jobs.append((alpha_param, k, T, gs, clamped, l1, params))
         pending = self.jobs
         self.jobs = []
         while pending:
@@ -199,6 +224,28 @@ def _k5(spec: "_OpSpec", alpha: torch.Tensor, g_soft: torch.Tensor, sel: ops.Sel
         return None
     return ops.soft_topk_grad(alpha.detach(), spec.k, spec.temperature, g_soft, clamped=sel.clamped,
                               l1_coeff=spec.l1, params=spec.params)
+
+
+def _tc_weight_grads(spec: "_OpSpec", dy_parts, x: torch.Tensor, vals: torch.Tensor, sel: ops.Selection,
+                     has_bias: bool, need_soft: bool, alpha):
+    """(g_values, g_bias, g_alpha) of a tensor-core layer (fused-gather dW + bias gradient +
+    K5) — or (None, None, None) inside ``deferred_topk_grads()``, where only the dW GEMM runs
+    now and the finalize / K5 join the batched launches after the backward."""
+    M, N = spec.M, spec.N
+    q = _K5_QUEUE
+    if q is not None and spec.bucket is None and spec.values_param is not None and spec.alpha_param is not None:
+        rec = ops.tc_backward_weight_begin(dy_parts, x, vals, sel, M, N, need_bias=has_bias, need_soft=need_soft)
+        k5 = (spec.alpha_param, spec.k, spec.temperature, sel.clamped, spec.l1, spec.params) if need_soft else None
+        q.fin.append((rec, spec.values_param, spec.bias_param if has_bias else None, k5))
+        return None, None, None
+    if isinstance(dy_parts, (list, tuple)):
+        gv, gs, gb = ops.tc_backward_weight_split(list(dy_parts), x, vals, sel, M, N, need_soft=need_soft,
+                                                  need_bias=True, bucket=spec.bucket)
+    else:
+        gv, gs, gb = ops.tc_backward_weight(dy_parts, x, vals, sel, M, N, need_soft=need_soft, need_bias=True,
+                                            bucket=spec.bucket)
+    ga = _k5(spec, alpha, gs, sel) if need_soft else None
+    return gv, (gb if has_bias else None), ga
 
 
 def _w_k(spec: "_OpSpec", dtype: torch.dtype, values, sel, M: int, N: int) -> torch.Tensor:
@@ -270,12 +317,10 @@ class DiagMMFunction(torch.autograd.Function):
             out_dt = vals.dtype
             if ctx.tc and M % 64 == 0 and N % 64 == 0:
                 # tensor-core dW with the diagonal gather and the bias gradient fused (dy read once,
-                # no dense dW written)
-                g_values, g_soft, g_bias = ops.tc_backward_weight(dy, x.to(dy.dtype), vals, sel, M, N,
-                                                                  need_soft=need_soft, need_bias=True,
-                                                                  bucket=spec.bucket)
-                if not ctx.has_bias:
-                    g_bias = None
+                # no dense dW written); K5 included
+                g_values, g_bias, g_alpha = _tc_weight_grads(spec, dy, x.to(dy.dtype), vals, sel, ctx.has_bias,
+                                                             need_soft, alpha)
+                return dx, g_values, g_alpha, g_bias, None, d_res
             else:
                 spec.bucket = None  # this branch does not fill the exchange bucket (dp falls back to full)
                 dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
@@ -337,14 +382,10 @@ class DiagMLPFunction(torch.autograd.Function):
         W1, W2 = ctx.W
         ctx.W = None
         d_pre = ops.tc_gemm_nn(dy, W2, None, epilogue=2, aux=pre)
-        gv2, gs2, gb2 = ops.tc_backward_weight(dy, act, v2d, sel2, s2.M, s2.N, need_soft=True, need_bias=True,
-                                               bucket=s2.bucket)
-        ga2 = _k5(s2, a2, gs2, sel2)
+        gv2, gb2, ga2 = _tc_weight_grads(s2, dy, act, v2d, sel2, True, True, a2)
         # fc1
         dx = ops.tc_gemm_nn(d_pre, W1)
-        gv1, gs1, gb1 = ops.tc_backward_weight(d_pre, x, v1d, sel1, s1.M, s1.N, need_soft=True, need_bias=True,
-                                               bucket=s1.bucket)
-        ga1 = _k5(s1, a1, gs1, sel1)
+        gv1, gb1, ga1 = _tc_weight_grads(s1, d_pre, x, v1d, sel1, True, True, a1)
         hb1, hb2 = ctx.has_bias
         d_res = dy0 if ctx.needs_input_grad[10] else None
         return (dx, gv1, ga1, gb1 if hb1 else None, gv2, ga2, gb2 if hb2 else None, None, None, None, d_res)
@@ -463,7 +504,8 @@ class DiagLinear(nn.Module):
         T = self.temperature(step)
         spec = _OpSpec(self.out_features, self.in_features, self.k, T, self.route,
                        presel=self._take_preselection(step, T), bucket=getattr(self, "_dp_bucket", None),
-                       params=getattr(self, "_sched_params", None), alpha_param=self.alpha)
+                       params=getattr(self, "_sched_params", None), alpha_param=self.alpha,
+                       values_param=self.values, bias_param=self.bias)
         spec.prew = self._take_premat(step, T) if spec.presel is not None else None
         self._last_spec = spec
         return spec

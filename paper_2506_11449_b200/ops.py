@@ -379,6 +379,64 @@ def materialize(values: torch.Tensor, sel: Selection, M: int, N: int,
     return W
 
 
+def tc_backward_weight_begin(dy_parts, x: torch.Tensor, values: torch.Tensor, sel: Selection, M: int, N: int,
+                             need_bias: bool = True, need_soft: bool = True, max_act: int | None = None) -> dict:
+    """First half of ``tc_backward_weight`` / ``tc_backward_weight_split`` for a deferred
+    finalize: only the dW GEMM (split-K partials + bias column partials, into a workspace
+    owned by the returned record).  ``dw_finalize_many`` completes it later; together they
+    are bit-identical to the one-call path.  ``dy_parts``: dy, or its 1-3 column blocks."""
+    parts = list(dy_parts) if isinstance(dy_parts, (list, tuple)) else [dy_parts]
+    if any(p.dtype != torch.bfloat16 for p in parts) or x.dtype != torch.bfloat16:
+        raise TypeError("tc_backward_weight_begin takes bfloat16 dy and x (the TMA maps are bf16)")
+    C, L = geometry(M, N)
+    if tuple(values.shape) != (C, L) or values.dtype != torch.float32:
+        raise ShapeMismatch(f"values {tuple(values.shape)} {values.dtype} for a ({M}, {N}) layer")
+    B = x.shape[0]
+    ms = parts[0].shape[1] if len(parts) > 1 else 0
+    if ms == 0 and parts[0].shape != (B, M):
+        raise ShapeMismatch(f"dy {tuple(parts[0].shape)} vs ({B}, {M})")
+    ma = C if max_act is None else int(max_act)
+    lib = _lib.load()
+    ws = torch.empty(max(16, lib.diagmm_tc_backward_weight_workspace(M, N, B, ma)), dtype=torch.uint8,
+                     device=x.device)
+    ps = [p.contiguous() for p in parts]
+    x = x.contiguous()
+    _lib.call("diagmm_tc_backward_weight_partials", M, N, B, _p(ps[0]), _p(ps[1] if len(ps) > 1 else None),
+              _p(ps[2] if len(ps) > 2 else None), ms, _p(x), _p(sel.slot), _p(sel.n_act), ma, int(bool(need_bias)),
+              _p(ws), ws.numel(), _stream(x))
+    ks = lib.diagmm_tc_dw_splits(M, N, B)
+    pbytes = (ks * max(ma, 1) * L * 4 + 15) // 16 * 16
+    return {"M": M, "N": N, "parts": ks, "ws": ws, "colsum_off": pbytes if need_bias else None, "max_act": ma,
+            "sel": sel, "values": values.contiguous(), "need_soft": need_soft, "keep": ps + [x]}
+
+
+def dw_finalize_many(records) -> list:
+    """Complete ``tc_backward_weight_begin`` records in ONE launch; returns
+    [(g_values (C, L), g_soft (C,) | None, g_bias (M,) | None)]."""
+    n = len(records)
+    if n == 0:
+        return []
+    arr = (_lib.DwFinalizeJob * n)()
+    outs = []
+    stream = None
+    for i, r in enumerate(records):
+        M, N = r["M"], r["N"]
+        C, L = geometry(M, N)
+        v = r["values"]
+        gv = torch.empty(C, L, dtype=v.dtype, device=v.device)
+        gs = torch.empty(C, dtype=torch.float64, device=v.device) if r["need_soft"] else None
+        gb = torch.empty(M, dtype=v.dtype, device=v.device) if r["colsum_off"] is not None else None
+        ws = r["ws"]
+        colsum = ws.data_ptr() + r["colsum_off"] if r["colsum_off"] is not None else None
+        sel = r["sel"]
+        arr[i] = _lib.DwFinalizeJob(M, N, r["parts"], _p(ws), colsum, r["max_act"], _p(sel.slot), _p(sel.n_act),
+                                    _p(sel.alpha_soft), _p(v), _p(gv), _p(gs), _p(gb), None, 0)
+        outs.append((gv, gs, gb))
+        stream = _stream(v) if stream is None else stream
+    _lib.call("diagmm_tc_dw_finalize_batched", n, arr, stream)
+    return outs
+
+
 def materialize_many(items, dtype: torch.dtype) -> list:
     """Every layer's dense W_K in ONE launch: ``items`` = [(values, sel, M, N)] (float32
     stores), W of ``dtype`` (bf16 / fp32) — identical to ``materialize`` per layer."""

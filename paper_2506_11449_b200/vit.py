@@ -17,7 +17,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from . import _lib, ops
-from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, _k5, _w_k, dense_route_min_tokens, preselect
+from .layer import DiagLinear, DiagMLP, FrozenDiagLinear, _tc_weight_grads, _w_k, dense_route_min_tokens, preselect
 from .selection import TemperatureSchedule
 
 
@@ -106,12 +106,8 @@ class QKVAttentionFunction(torch.autograd.Function):
         parts = [d.permute(0, 2, 1, 3).reshape(B * T, N) for d in grads]
         dx = ops.tc_gemm_nn_split(parts, W) if ctx.needs_input_grad[0] else None
         need_soft = alpha is not None and ctx.needs_input_grad[2]
-        gv, gs, gb = ops.tc_backward_weight_split(parts, x, values.detach(), sel, M, N, need_soft=need_soft,
-                                                  need_bias=True, bucket=spec.bucket)
-        ga = None
-        if need_soft:
-            ga = _k5(spec, alpha, gs, sel)
-        return dx, gv, ga, gb if ctx.has_bias else None, None, None, None, None, None
+        gv, gb, ga = _tc_weight_grads(spec, parts, x, values.detach(), sel, ctx.has_bias, need_soft, alpha)
+        return dx, gv, ga, gb, None, None, None, None, None
 
 
 def _qkv_fusable(qkv, x2: torch.Tensor, H: int) -> bool:
