@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libdiagmm.so"
-SOURCES = ["diagmm_kernels.cu", "topk_kernels.cu", "optim_kernels.cu", "norm_kernels.cu", "tc_kernels.cu", "tc2_kernels.cu", "capi.cu"]
+SOURCES = ["diagmm_kernels.cu", "topk_kernels.cu", "optim_kernels.cu", "norm_kernels.cu", "tc_kernels.cu", "tc2_kernels.cu", "tf32_kernels.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -2638,6 +2638,27 @@ static int run_product_pk(bool gather, int B, int C, int L, const void* in, cons
 }
 
 // workspace = [compact weights (max_act x ldw) | split partials]
+// the fp32 tensor-core route (3xTF32, tf32_kernels.cu)
+int tf32x3_min_b();
+size_t tf32_product_workspace(bool gather, int B, int C, int L);
+int run_product_tf32(bool gather, int B, int C, int L, const float* in, const float* vals, const double* asoft,
+                     const int32_t* active, const int32_t* n_act, int max_act, const float* bias, float* out,
+                     void* ws, cudaStream_t st);
+size_t tf32_dw_workspace(int M, int N, int B);
+int run_dw_tf32(int M, int N, int B, const float* dy, const float* x, const int32_t* active, const int32_t* n_act,
+                int max_act, float* partial, void* ws, cudaStream_t st);
+// fp32 on the tensor cores (3xTF32) when it beats the FMA kernels (warm B200,
+// tools/tf32_time.py, profiles/r02_tf32x3.txt): from B = 512 on every shape
+// (3072 x 768: 114 vs 165 us fwd + bwd), from B = 256 on layers of >= 8 M
+// candidates (4096^2: 358 vs 408 us); at config 1 (B = 256) the two tie.
+template <typename T>
+static bool use_tf32(int B, int C, int L) {
+  if (!std::is_same<T, float>::value || B < 1) return false;
+  const int m = tf32x3_min_b();
+  if (m >= 0) return m > 0 && B >= m;
+  return B >= 512 || (B >= 256 && (long long)C * L >= (8LL << 20));
+}
+
 template <typename T>
 size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
   using A = typename Vec<T>::A;
@@ -2654,6 +2675,10 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
       const size_t pk = pk_product_workspace<T>(gather, B, C, L);
       wide = wide > pk ? wide : pk;
     }
+  }
+  if (use_tf32<T>(B, C, L)) {
+    const size_t tf = tf32_product_workspace(gather, B, C, L);
+    wide = wide > tf ? wide : tf;
   }
   return wide > narrow ? wide : narrow;
 }
@@ -2677,6 +2702,13 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
         return run_product_pk<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, ws, st);
       return run_product_rows<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, st);
     }
+  }
+  if constexpr (std::is_same<T, float>::value) {
+    // fp32 with a batch the FMA pipe cannot keep up with: 3xTF32 on the tensor cores
+    if (use_tf32<T>(B, C, L))
+      return run_product_tf32(gather, B, C, L, static_cast<const float*>(in), static_cast<const float*>(vals), asoft,
+                              active, n_act, max_act, static_cast<const float*>(bias), static_cast<float*>(out), ws,
+                              st);
   }
   if (B <= rows_max_b())
     return run_product_rows<T>(gather, B, C, L, in, vals, asoft, active, n_act, max_act, bias, out, st);
@@ -2847,6 +2879,11 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
     const size_t d6 = dw6_workspace<T>(M, N, B, max_act);
     dw = dw > d6 ? dw : d6;
   }
+  if (use_tf32<T>(B, C, L)) {
+    const size_t tf = align16((size_t)max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A)) +
+                      tf32_dw_workspace(M, N, B);
+    dw = dw > tf ? dw : tf;
+  }
   size_t w = dw > prod_f ? dw : prod_f;
   return w > prod_b ? w : prod_b;
 }
@@ -2869,9 +2906,11 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const bool narrow = B > 0 && B <= narrow_dw_max_b() && max_act > 0;
   if (narrow) parts = 1;
+  const bool tf = use_tf32<T>(B, C, L) && max_act > 0;  // 3xTF32 dense gw, gathered: one part
+  if (tf) parts = 1;
   Dw6Plan p6;
   if constexpr (sizeof(T) <= 4) {
-    if (!narrow && B > 0 && max_act > 0 && dw_v6_enabled()) p6 = plan_dw6<T>(B, C, L, max_act);
+    if (!tf && !narrow && B > 0 && max_act > 0 && dw_v6_enabled()) p6 = plan_dw6<T>(B, C, L, max_act);
   }
   const bool v6 = p6.G > 0 && aligned16(aop) && aligned16(bop);
   if (v6) parts = p6.parts;
@@ -2895,7 +2934,16 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
     }
   }
   cudaEventRecord(ss.join, ss.s);
-  if (v6) {
+  if (tf) {
+    if constexpr (std::is_same<T, float>::value) {
+      void* tws = static_cast<char*>(ws) + align16((size_t)max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A));
+      if (int e = run_dw_tf32(M, N, B, static_cast<const float*>(dy), static_cast<const float*>(x), active, n_act,
+                              max_act, partial, tws, st)) {
+        cudaStreamWaitEvent(st, ss.join, 0);
+        return e;
+      }
+    }
+  } else if (v6) {
     if constexpr (sizeof(T) <= 4) {
       using U = typename Vec<T>::U;
       U* ap = reinterpret_cast<U*>(static_cast<char*>(ws) + align16((size_t)parts * max_act * L * sizeof(A)) +

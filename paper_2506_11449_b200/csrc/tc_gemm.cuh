@@ -86,6 +86,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // ld elements, box (box_rows, 64), 128-byte swizzle.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                     uint64_t ld);
+// Host: 2-D fp32 tensor map (K-major, box (box_rows, 32), 128-byte swizzle) for the 3xTF32 route.
+bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, uint64_t ld);
 // Host: MN-major staging map of a (rows, cols) row-major bf16 matrix (cols contiguous):
 // box (64 cols, BK rows), 128-byte swizzle.
 bool make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols);

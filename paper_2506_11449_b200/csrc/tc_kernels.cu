@@ -776,7 +776,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // cuTensorMapEncodeTiled with the failure recorded for diagmm_last_error()
 static bool encode_2d(CUtensorMap* map, const void* base, const cuuint64_t (&dims)[2], const cuuint64_t (&strides)[1],
-                      const cuuint32_t (&box)[2], CUtensorMapSwizzle swz) {
+                      const cuuint32_t (&box)[2], CUtensorMapSwizzle swz,
+                      CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   auto fn = encode_fn();
   if (!fn) {
     last_cuda_error() = "cuTensorMapEncodeTiled entry point unavailable";
@@ -790,7 +791,7 @@ static bool encode_2d(CUtensorMap* map, const void* base, const cuuint64_t (&dim
     bound = true;
   }
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  const CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -812,6 +813,14 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   const cuuint64_t strides[1] = {ld * 2};
   const cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
   return encode_2d(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// fp32 (read as tf32 by kind::tf32 MMAs), K-major: box (32 fp32 = 128 bytes, box_rows), 128-byte swizzle
+bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, uint64_t ld) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  return encode_2d(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
 // MN-major staging of a (rows = K, cols = N) row-major matrix: boxes of 64
