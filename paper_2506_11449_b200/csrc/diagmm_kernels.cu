@@ -2648,14 +2648,16 @@ size_t tf32_dw_workspace(int M, int N, int B);
 int run_dw_tf32(int M, int N, int B, const float* dy, const float* x, const int32_t* active, const int32_t* n_act,
                 int max_act, float* partial, void* ws, cudaStream_t st);
 // fp32 on the tensor cores (3xTF32) when it beats the FMA kernels (warm B200,
-// tools/tf32_time.py, profiles/r02_tf32x3.txt): from B = 512 on every shape
-// (3072 x 768: 114 vs 165 us fwd + bwd), from B = 256 on layers of >= 8 M
-// candidates (4096^2: 358 vs 408 us); at config 1 (B = 256) the two tie.
+// tools/tf32_time.py, profiles/r02_tf32x3.txt): products from B = 256 (config 1
+// fwd 22.3 vs 30.2 us, dX 23.6 vs 23.6; 4096^2: 81 vs 131 us), dW from B = 512, or
+// from B = 256 on layers of >= 8 M candidates (config 1 dW: 32.5 vs 31.5 us).
+// DIAGMM_TF32X3_MIN_B=n replaces both rules by B >= n (0: never).
 template <typename T>
-static bool use_tf32(int B, int C, int L) {
+static bool use_tf32(int B, int C, int L, bool dw) {
   if (!std::is_same<T, float>::value || B < 1) return false;
   const int m = tf32x3_min_b();
   if (m >= 0) return m > 0 && B >= m;
+  if (!dw) return B >= 256;
   return B >= 512 || (B >= 256 && (long long)C * L >= (8LL << 20));
 }
 
@@ -2676,7 +2678,7 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
       wide = wide > pk ? wide : pk;
     }
   }
-  if (use_tf32<T>(B, C, L)) {
+  if (use_tf32<T>(B, C, L, false)) {
     const size_t tf = tf32_product_workspace(gather, B, C, L);
     wide = wide > tf ? wide : tf;
   }
@@ -2705,7 +2707,7 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   }
   if constexpr (std::is_same<T, float>::value) {
     // fp32 with a batch the FMA pipe cannot keep up with: 3xTF32 on the tensor cores
-    if (use_tf32<T>(B, C, L))
+    if (use_tf32<T>(B, C, L, false))
       return run_product_tf32(gather, B, C, L, static_cast<const float*>(in), static_cast<const float*>(vals), asoft,
                               active, n_act, max_act, static_cast<const float*>(bias), static_cast<float*>(out), ws,
                               st);
@@ -2879,7 +2881,7 @@ size_t dw_workspace(int M, int N, int B, int max_act) {
     const size_t d6 = dw6_workspace<T>(M, N, B, max_act);
     dw = dw > d6 ? dw : d6;
   }
-  if (use_tf32<T>(B, C, L)) {
+  if (use_tf32<T>(B, C, L, true)) {
     const size_t tf = align16((size_t)max_act * L * sizeof(A)) + align16((size_t)cparts * M * sizeof(A)) +
                       tf32_dw_workspace(M, N, B);
     dw = dw > tf ? dw : tf;
@@ -2906,7 +2908,7 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   const int cparts = ceil_div(B > 0 ? B : 1, kColRows);
   const bool narrow = B > 0 && B <= narrow_dw_max_b() && max_act > 0;
   if (narrow) parts = 1;
-  const bool tf = use_tf32<T>(B, C, L) && max_act > 0;  // 3xTF32 dense gw, gathered: one part
+  const bool tf = use_tf32<T>(B, C, L, true) && max_act > 0;  // 3xTF32 dense gw, gathered: one part
   if (tf) parts = 1;
   Dw6Plan p6;
   if constexpr (sizeof(T) <= 4) {

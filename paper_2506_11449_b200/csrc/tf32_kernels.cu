@@ -152,15 +152,19 @@ k_tf32x3(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtenso
     for (int it = 0; it < nkb; ++it) {
       const int s = it % NST, round = it / NST;
       mbar_wait_parity(&full[s], round & 1);
-      unsigned char* st = smem + (size_t)s * S::stage;
+      // explicit shared-space accesses (a generic pointer here compiles to LD / ST.E)
+      const uint32_t sb = smem_u32(smem + (size_t)s * S::stage);
 #pragma unroll 4
       for (int q = tt; q < S::half / 16; q += 128) {
-        float4* ph = reinterpret_cast<float4*>(st) + q;
-        const float4 v = *ph;
-        float4 h, l;
+        const uint32_t a = sb + (uint32_t)q * 16;
+        float4 v, h, l;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
         split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y); split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
-        *ph = h;
-        *reinterpret_cast<float4*>(st + S::half + q * 16) = l;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(h.x), "f"(h.y), "f"(h.z), "f"(h.w)
+                     : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + (uint32_t)S::half), "f"(l.x), "f"(l.y),
+                     "f"(l.z), "f"(l.w)
+                     : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
       __syncwarp();
