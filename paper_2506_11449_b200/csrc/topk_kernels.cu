@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include <math_constants.h>
 #include <type_traits>
+#include <cstdlib>
 
 namespace diagmm {
 
@@ -197,10 +198,234 @@ __device__ __forceinline__ Affine compose(Affine f, Affine g) {  // f o g
   return {f.a * g.a, f.a * g.b + f.b};
 }
 
+// Deterministic block reductions over per-thread partials: a fixed shuffle
+// tree inside each warp, then warp 0 folds the 32 warp results (2 barriers).
+__device__ double block_reduce_sum(double v, double* buf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) buf[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) buf[32] = r;
+  }
+  __syncthreads();
+  r = buf[32];
+  __syncthreads();
+  return r;
+}
+__device__ double block_reduce_max(double v, double* buf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) buf[w] = v;
+  __syncthreads();
+  double r = -CUDART_INF;
+  if (w == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : -CUDART_INF;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) buf[32] = r;
+  }
+  __syncthreads();
+  r = buf[32];
+  __syncthreads();
+  return r;
+}
+
+// ---- K4 through a radix select (k < C, k <= 1024): only the top-k need an order.
+// The reference's tail log-sum-exp over sorted positions i < k splits into the
+// top-k part (a suffix scan over the k sorted keys) and the rest, which enters
+// only through R_k = sum_{l > k} exp(z_l - z_k) at the (k+1)-th largest key z_k
+// (a fixed-order block reduction).  Soft scores of every candidate are
+// (k - m) exp(z_i - S_m) or 1 (the top m), so the rest never needs sorting.
+// The k-th largest key comes from 8 MSB-first 8-bit histogram passes over
+// order-preserving 64-bit keys; ties at it are taken in index order (numpy's
+// stable argsort).  Same decisions as the full sort (tests: masks bit-exact vs
+// the golden vectors and the oracle); S differs from the full-sort path's in the
+// last ulps only (different summation tree for the tail).
+
+// larger double -> larger unsigned key (z canon'd: no -0.0)
+__device__ __forceinline__ unsigned long long okey(double z) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(z);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ int block_reduce_min_int(int v, double* buf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  int* ib = reinterpret_cast<int*>(buf);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) ib[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int r = lane < (int)(blockDim.x >> 5) ? ib[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = min(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) ib[32] = r;
+  }
+  __syncthreads();
+  const int r = ib[32];
+  __syncthreads();
+  return r;
+}
+
+// key: z in index order (C); skey / sidx: >= next_pow2(k) scratch entries;
+// buf: >= 66 doubles; ibuf: blockDim ints.  Writes asoft / clamped / key (= scores).
+__device__ void waterfill_radix(int C, int k, double* key, double* skey, int* sidx, Affine* maps, double* buf,
+                                int* ibuf, double* __restrict__ asoft, uint8_t* __restrict__ clamped) {
+  __shared__ int s_b, s_need, s_m;
+  __shared__ double s_Sm;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (C + nt - 1) / nt;
+  const int lo = min(C, tid * per), hi = min(C, lo + per);
+  // ---- radix select of the k-th largest key
+  unsigned long long prefix = 0;
+  int need = k;
+  int* hist = ibuf;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    for (int i = lo; i < hi; ++i) {
+      const unsigned long long u = okey(key[i]);
+      if (pass == 0 || (u >> (shift + 8)) == prefix) atomicAdd(&hist[(u >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {  // lane l: bins 255 - 8l .. 248 - 8l, the highest first
+      int c[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c[q] = hist[255 - 8 * tid - q]; sum += c[q]; }
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= o) inc += v;
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, inc >= need);
+      if (tid == __ffs(ball) - 1) {
+        int cum = inc - sum, b = 255 - 8 * tid;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (cum + c[q] >= need) { b = 255 - 8 * tid - q; break; }
+          cum += c[q];
+        }
+        s_b = b;
+        s_need = need - cum;
+      }
+    }
+    __syncthreads();
+    prefix = (prefix << 8) | (unsigned long long)s_b;
+    need = s_need;
+    __syncthreads();
+  }
+  const unsigned long long ustar = prefix;  // the k-th largest; `need` of its ties are taken, in index order
+  // ---- compact the top-k (index order), pad, sort by (key desc, index asc)
+  int nties = 0;
+  for (int i = lo; i < hi; ++i) nties += okey(key[i]) == ustar ? 1 : 0;
+  int tot = 0;
+  int tie_rank = block_exclusive_scan(nties, ibuf, &tot);
+  int nsel = 0;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long u = okey(key[i]);
+    if (u > ustar) ++nsel;
+    else if (u == ustar) { if (tie_rank < need) ++nsel; ++tie_rank; }
+  }
+  tie_rank -= nties;
+  int pos = block_exclusive_scan(nsel, ibuf, &tot);
+  int NPk = 1;
+  while (NPk < k) NPk <<= 1;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long u = okey(key[i]);
+    bool take = u > ustar;
+    if (u == ustar) { take = tie_rank < need; ++tie_rank; }
+    if (take) { skey[pos] = key[i]; sidx[pos] = i; ++pos; }
+  }
+  tie_rank -= nties;
+  for (int p = k + tid; p < NPk; p += nt) { skey[p] = -CUDART_INF; sidx[p] = 0x7fffffff; }
+  __syncthreads();
+  sort_desc(skey, sidx, NPk);
+  // ---- the rest: z_k = its largest key, R_k = sum over the rest but that element
+  double zr = -CUDART_INF;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long u = okey(key[i]);
+    if (u < ustar || (u == ustar && tie_rank >= need)) zr = fmax(zr, key[i]);
+    if (u == ustar) ++tie_rank;
+  }
+  tie_rank -= nties;
+  const double zk = block_reduce_max(zr, buf);
+  int first = 0x7fffffff;  // the rest's element at sorted position k: smallest index with key zk
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long u = okey(key[i]);
+    const bool rest = u < ustar || (u == ustar && tie_rank >= need);
+    if (u == ustar) ++tie_rank;
+    if (rest && key[i] == zk && first == 0x7fffffff) first = i;
+  }
+  tie_rank -= nties;
+  const int ik = block_reduce_min_int(first, buf);
+  double sr = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long u = okey(key[i]);
+    const bool rest = u < ustar || (u == ustar && tie_rank >= need);
+    if (u == ustar) ++tie_rank;
+    if (rest && i != ik) sr += exp(key[i] - zk);
+  }
+  const double Rk = block_reduce_sum(sr, buf);
+  // ---- suffix scan over the k sorted positions (one per thread): R_i = a_i (1 + R_{i+1})
+  const double zi = tid < k ? skey[tid] : 0.0;
+  const double znext = tid + 1 < k ? skey[tid + 1] : zk;
+  const double a = tid < k ? exp(znext - zi) : 0.0;
+  maps[tid] = tid < k ? Affine{a, a} : Affine{1.0, 0.0};
+  if (tid == 0) s_m = k;
+  __syncthreads();
+  for (int d = 1; d < nt; d <<= 1) {
+    const Affine mine = maps[tid];
+    const Affine nxt = tid + d < nt ? maps[tid + d] : Affine{1.0, 0.0};
+    __syncthreads();
+    maps[tid] = compose(mine, nxt);
+    __syncthreads();
+  }
+  const double Ri = maps[tid].a * Rk + maps[tid].b;
+  // ---- clamp count m = first i < k with (k - i) exp(z_i - S_i) < 1
+  double Si = 0.0;
+  if (tid < k) {
+    Si = zi + log1p(Ri);
+    if (!((double)(k - tid) * exp(zi - Si) >= 1.0)) atomicMin(&s_m, tid);
+  }
+  __syncthreads();
+  const int m = s_m;
+  if (m < k && tid == m) s_Sm = Si;
+  if (m == k && tid == 0) s_Sm = zk + log1p(Rk);
+  __syncthreads();
+  const double Sm = s_Sm;
+  // ---- scores in index order, then the top m clamped to 1
+  for (int i = lo; i < hi; ++i) {
+    const double v = (double)(k - m) * exp(key[i] - Sm);
+    key[i] = v;
+    asoft[i] = v;
+    if (clamped) clamped[i] = 0;
+  }
+  __syncthreads();
+  if (tid < m) {
+    const int o = sidx[tid];
+    key[o] = 1.0;
+    asoft[o] = 1.0;
+    if (clamped) clamped[o] = 1;
+  }
+  __syncthreads();
+}
+
 // Up to kMaxJobs independent selections per launch, one CTA each (all the
 // DiagLinear layers of a model re-select in one launch, SURVEY §7 hard part 2).
 constexpr int kMaxJobs = 64;
-struct WaterfillJobs { diagmm_topk_job j[kMaxJobs]; };
+struct WaterfillJobs {
+  diagmm_topk_job j[kMaxJobs];
+  int radix;  // top-k radix-select path (DIAGMM_K4_RADIX, default on)
+};
 
 __global__ void __launch_bounds__(kSelThreads)
 k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
@@ -230,6 +455,14 @@ k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
     idx[i] = i < C ? i : 0x7fffffff;
   }
   __syncthreads();
+  if (jobs.radix && k < C && k <= nt && nt == kSelThreads) {  // sort the top-k only
+    waterfill_radix(C, k, key, R, idx, maps, reinterpret_cast<double*>(maps + 64), ibuf, asoft, clamped);
+    unsigned char* flag = reinterpret_cast<unsigned char*>(R);
+    for (int i = tid; i < C; i += nt) flag[i] = key[i] >= 1e-3 ? 1 : 0;
+    __syncthreads();
+    compact_flags(flag, C, active, slot, n_act, ibuf);
+    return;
+  }
   sort_desc(key, idx, NP);
 
   // ---- suffix scan of R (positions 0..C-1, chunked per thread)
@@ -319,45 +552,6 @@ k_active_from_list(int C, int n, const int32_t* __restrict__ offs, int32_t* __re
   __syncthreads();
   for (int j = threadIdx.x; j < n; j += blockDim.x) slot[offs[j]] = j;
   if (threadIdx.x == 0 && n_act) *n_act = n;
-}
-
-// Deterministic block reductions over per-thread partials: a fixed shuffle
-// tree inside each warp, then warp 0 folds the 32 warp results (2 barriers).
-__device__ double block_reduce_sum(double v, double* buf) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) buf[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (w == 0) {
-    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (lane == 0) buf[32] = r;
-  }
-  __syncthreads();
-  r = buf[32];
-  __syncthreads();
-  return r;
-}
-__device__ double block_reduce_max(double v, double* buf) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) buf[w] = v;
-  __syncthreads();
-  double r = -CUDART_INF;
-  if (w == 0) {
-    r = lane < (int)(blockDim.x >> 5) ? buf[lane] : -CUDART_INF;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
-    if (lane == 0) buf[32] = r;
-  }
-  __syncthreads();
-  r = buf[32];
-  __syncthreads();
-  return r;
 }
 
 // K5 body for one layer (one CTA); shared by the per-layer and the batched kernels
@@ -450,6 +644,8 @@ int run_waterfill_batched(int n, const diagmm_topk_job* jobs, cudaStream_t st) {
   for (int b = 0; b < n; b += kMaxJobs) {
     const int cnt = n - b < kMaxJobs ? n - b : kMaxJobs;
     WaterfillJobs P{};
+    const char* re = getenv("DIAGMM_K4_RADIX");  // read per call (A/B tests flip it)
+    P.radix = re ? atoi(re) : 1;
     int cmax = 1;
     for (int i = 0; i < cnt; ++i) {
       P.j[i] = jobs[b + i];
