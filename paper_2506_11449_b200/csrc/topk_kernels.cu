@@ -155,21 +155,34 @@ __device__ __forceinline__ int next_pow2(int n) {
   return p;
 }
 
-// Exclusive prefix sum of one int per thread over the block (deterministic).
+// Exclusive prefix sum of one int per thread over the block: warp shuffles, the
+// warp totals scanned by warp 0, 3 barriers (integer: exact in any order).
 __device__ int block_exclusive_scan(int v, int* buf, int* total) {
-  const int tid = threadIdx.x;
-  buf[tid] = v;
-  __syncthreads();
-  for (int d = 1; d < blockDim.x; d <<= 1) {
-    int add = tid >= d ? buf[tid - d] : 0;
-    __syncthreads();
-    buf[tid] += add;
-    __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = (blockDim.x + 31) >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
-  const int incl = buf[tid];
-  *total = buf[blockDim.x - 1];
+  if (lane == 31) buf[w] = inc;
   __syncthreads();
-  return incl - v;
+  if (w == 0) {
+    const int t = lane < nw ? buf[lane] : 0;
+    int ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    if (lane < nw) buf[32 + lane] = ti - t;  // exclusive warp bases
+    if (lane == 31) buf[64] = ti;
+  }
+  __syncthreads();
+  const int r = buf[32 + w] + inc - v;
+  *total = buf[64];
+  __syncthreads();
+  return r;
 }
 
 // Compact the flagged indices (flag[i] != 0, i < C) into `out` ascending.
@@ -286,14 +299,24 @@ __device__ void waterfill_radix(int C, int k, double* key, double* skey, int* si
   // ---- radix select of the k-th largest key
   unsigned long long prefix = 0;
   int need = k;
-  int* hist = ibuf;
+  // two histograms used alternately: a pass zeroes the next pass's while it counts (2 barriers a pass)
+  if (tid < 256) ibuf[tid] = 0;
+  __syncthreads();
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
-    if (tid < 256) hist[tid] = 0;
-    __syncthreads();
-    for (int i = lo; i < hi; ++i) {
-      const unsigned long long u = okey(key[i]);
-      if (pass == 0 || (u >> (shift + 8)) == prefix) atomicAdd(&hist[(u >> shift) & 255], 1);
+    int* hist = ibuf + (pass & 1) * 256;
+    if (tid < 256) ibuf[((pass + 1) & 1) * 256 + tid] = 0;
+    // warp-aggregated: keys of similar magnitude share their top bytes, so most of
+    // a warp hits one bin (one atomic per distinct digit per warp instead)
+    for (int e = 0; e < per; ++e) {
+      const int i = lo + e;
+      int digit = -1;
+      if (i < hi) {
+        const unsigned long long u = okey(key[i]);
+        if (pass == 0 || (u >> (shift + 8)) == prefix) digit = (int)((u >> shift) & 255);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit >= 0 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[digit], __popc(peers));
     }
     __syncthreads();
     if (tid < 32) {  // lane l: bins 255 - 8l .. 248 - 8l, the highest first
@@ -321,8 +344,8 @@ __device__ void waterfill_radix(int C, int k, double* key, double* skey, int* si
     __syncthreads();
     prefix = (prefix << 8) | (unsigned long long)s_b;
     need = s_need;
-    __syncthreads();
   }
+  __syncthreads();  // s_b / s_need / the histograms are reused below
   const unsigned long long ustar = prefix;  // the k-th largest; `need` of its ties are taken, in index order
   // ---- compact the top-k (index order), pad, sort by (key desc, index asc)
   int nties = 0;
@@ -337,8 +360,7 @@ __device__ void waterfill_radix(int C, int k, double* key, double* skey, int* si
   }
   tie_rank -= nties;
   int pos = block_exclusive_scan(nsel, ibuf, &tot);
-  int NPk = 1;
-  while (NPk < k) NPk <<= 1;
+  const int NPk = nt;  // k <= nt: pad to the block width for the register / shuffle sort
   for (int i = lo; i < hi; ++i) {
     const unsigned long long u = okey(key[i]);
     bool take = u > ustar;
@@ -379,17 +401,30 @@ __device__ void waterfill_radix(int C, int k, double* key, double* skey, int* si
   const double zi = tid < k ? skey[tid] : 0.0;
   const double znext = tid + 1 < k ? skey[tid + 1] : zk;
   const double a = tid < k ? exp(znext - zi) : 0.0;
-  maps[tid] = tid < k ? Affine{a, a} : Affine{1.0, 0.0};
+  // inclusive suffix composition F_t o F_{t+1} o ... : shuffles inside each warp, then
+  // the warps' totals composed by warp 0 (2 barriers)
+  Affine F = tid < k ? Affine{a, a} : Affine{1.0, 0.0};
+  const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double na = __shfl_down_sync(0xffffffffu, F.a, o), nb = __shfl_down_sync(0xffffffffu, F.b, o);
+    if (lane + o < 32) F = compose(F, Affine{na, nb});
+  }
+  if (lane == 0) maps[w] = F;  // the whole warp's map
   if (tid == 0) s_m = k;
   __syncthreads();
-  for (int d = 1; d < nt; d <<= 1) {
-    const Affine mine = maps[tid];
-    const Affine nxt = tid + d < nt ? maps[tid + d] : Affine{1.0, 0.0};
-    __syncthreads();
-    maps[tid] = compose(mine, nxt);
-    __syncthreads();
+  if (w == 0) {
+    Affine G = lane < nw ? maps[lane] : Affine{1.0, 0.0};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double na = __shfl_down_sync(0xffffffffu, G.a, o), nb = __shfl_down_sync(0xffffffffu, G.b, o);
+      if (lane + o < 32) G = compose(G, Affine{na, nb});
+    }
+    maps[32 + lane] = G;  // composition of warps lane .. nw-1
   }
-  const double Ri = maps[tid].a * Rk + maps[tid].b;
+  __syncthreads();
+  if (w + 1 < nw) F = compose(F, maps[32 + w + 1]);
+  const double Ri = F.a * Rk + F.b;
   // ---- clamp count m = first i < k with (k - i) exp(z_i - S_i) < 1
   double Si = 0.0;
   if (tid < k) {
@@ -441,10 +476,11 @@ k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
   int32_t* __restrict__ n_act = J.n_act;
   extern __shared__ __align__(16) unsigned char smem[];
   const int NP = next_pow2(C);
-  double* key = reinterpret_cast<double*>(smem);                              // NP
-  double* R = key + NP;                                                       // NP
-  int* idx = reinterpret_cast<int*>(R + NP);                                  // NP
-  Affine* maps = reinterpret_cast<Affine*>(smem + ((size_t)NP * 20 + 15) / 16 * 16);  // blockDim
+  const int NPs = NP > kSelThreads ? NP : kSelThreads;  // regions hold the radix path's padded top-k too
+  double* key = reinterpret_cast<double*>(smem);                              // NPs
+  double* R = key + NPs;                                                      // NPs
+  int* idx = reinterpret_cast<int*>(R + NPs);                                 // NPs
+  Affine* maps = reinterpret_cast<Affine*>(smem + ((size_t)NPs * 20 + 15) / 16 * 16);  // blockDim
   int* ibuf = reinterpret_cast<int*>(maps + blockDim.x);                      // blockDim
   __shared__ int s_m;
   __shared__ double s_Sm;
@@ -624,7 +660,7 @@ k_topk_grad_batched(const __grid_constant__ TopkGradJobs jobs) {
 
 // ---------------------------------------------------------------- launchers
 static size_t waterfill_smem(int C) {
-  int NP = 1;
+  int NP = kSelThreads;  // at least the radix path's padded top-k (k_waterfill: NPs)
   while (NP < C) NP <<= 1;
   return ((size_t)NP * 20 + 15) / 16 * 16 + kSelThreads * (sizeof(Affine) + sizeof(int)) + 64;
 }
