@@ -2647,17 +2647,19 @@ int run_product_tf32(bool gather, int B, int C, int L, const float* in, const fl
 size_t tf32_dw_workspace(int M, int N, int B);
 int run_dw_tf32(int M, int N, int B, const float* dy, const float* x, const int32_t* active, const int32_t* n_act,
                 int max_act, float* partial, void* ws, cudaStream_t st);
-// fp32 on the tensor cores (3xTF32) when it beats the FMA kernels (warm B200,
-// tools/tf32_time.py, profiles/r02_tf32x3.txt): products from B = 256 (config 1
-// fwd 22.3 vs 30.2 us, dX 23.6 vs 23.6; 4096^2: 81 vs 131 us), dW from B = 512, or
-// from B = 256 on layers of >= 8 M candidates (config 1 dW: 32.5 vs 31.5 us).
-// DIAGMM_TF32X3_MIN_B=n replaces both rules by B >= n (0: never).
+// fp32 on the tensor cores (3xTF32) when it beats the FMA kernels (B200,
+// tools/tf32_time.py warm and bench.py's cold-L2 per-op timing, profiles/r02_tf32x3.txt):
+// products from B = 512, and from B = 256 when the output is at least as wide as the
+// input (scatter orientation or square: config 1 fwd 30.2 -> 23.0 us warm, 34.7 -> 32.0
+// cold; the narrow-output gather product needs a 12-way split-K there and loses cold,
+// 27.8 vs 32.6 us); dW from B = 512, or from B = 256 on layers of >= 8 M candidates.
+// DIAGMM_TF32X3_MIN_B=n replaces the rules by B >= n (0: never).
 template <typename T>
-static bool use_tf32(int B, int C, int L, bool dw) {
+static bool use_tf32(int B, int C, int L, bool dw, bool gather = false) {
   if (!std::is_same<T, float>::value || B < 1) return false;
   const int m = tf32x3_min_b();
   if (m >= 0) return m > 0 && B >= m;
-  if (!dw) return B >= 256;
+  if (!dw) return B >= 512 || (B >= 256 && (!gather || C == L));
   return B >= 512 || (B >= 256 && (long long)C * L >= (8LL << 20));
 }
 
@@ -2678,7 +2680,7 @@ size_t product_workspace(bool gather, int B, int C, int L, int max_act) {
       wide = wide > pk ? wide : pk;
     }
   }
-  if (use_tf32<T>(B, C, L, false)) {
+  if (use_tf32<T>(B, C, L, false, gather)) {
     const size_t tf = tf32_product_workspace(gather, B, C, L);
     wide = wide > tf ? wide : tf;
   }
@@ -2707,7 +2709,7 @@ int run_product(bool gather, int B, int C, int L, const void* in, const void* va
   }
   if constexpr (std::is_same<T, float>::value) {
     // fp32 with a batch the FMA pipe cannot keep up with: 3xTF32 on the tensor cores
-    if (use_tf32<T>(B, C, L, false))
+    if (use_tf32<T>(B, C, L, false, gather))
       return run_product_tf32(gather, B, C, L, static_cast<const float*>(in), static_cast<const float*>(vals), asoft,
                               active, n_act, max_act, static_cast<const float*>(bias), static_cast<float*>(out), ws,
                               st);
