@@ -9,6 +9,7 @@
 // registers over its rows, written as per-CTA partials and folded in a fixed
 // order by a second kernel (deterministic, no atomics).
 #include "common.cuh"
+#include <type_traits>
 
 namespace diagmm {
 
@@ -105,31 +106,52 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
   for (int c = threadIdx.x; c < NV * 256; c += blockDim.x) s_w[c] = c < D ? w[c] : 0.f;
   __syncthreads();
   const int r0 = blockIdx.x * rows_per_cta, r1 = min(M, r0 + rows_per_cta);
-  // Two passes per row: statistics (s1, s2) and the dgamma/dbeta update, then
-  // dx — the second pass re-reads the row from L1 instead of holding it in
-  // registers, which keeps two CTAs (16 warps) resident per SM.
-#pragma unroll 1
-  for (int row = r0 + warp; row < r1; row += kLnWarps) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)row * D);
-    const uint4* gr = reinterpret_cast<const uint4*>(dy + (size_t)row * D);
-    const float mu = mean[row], rs = rstd[row];
-    uint4 cx[NV], cg[NV], cr[NV];
-    // the skip-connection gradient is requested with x and dy (one memory latency per row, not two)
-    const uint4* rr_row = dres ? reinterpret_cast<const uint4*>(dres + (size_t)row * D) : nullptr;
+  // Rows stream through a per-warp double buffer in shared memory (cp.async, 16 B per
+  // lane per chunk): the next row's x / dy / dres are in flight while this row is
+  // computed, two rows per warp instead of one (the dgamma / dbeta accumulators leave
+  // no registers for a register prefetch).  Each lane reads back only the chunks it
+  // copied itself, so cp.async.wait_group is the only synchronisation needed.
+  extern __shared__ __align__(16) uint4 s_rows[];  // [warp][2 slots][3 tensors][NV * 32]
+  uint4* wb = s_rows + (size_t)warp * 2 * 3 * NV * 32;
+  auto issue = [&](int row, int slot) {
+    if (row < r1) {
+      uint4* d = wb + (size_t)slot * 3 * NV * 32;
+      const __nv_bfloat16* src[3] = {x + (size_t)row * D, dy + (size_t)row * D,
+                                     dres ? dres + (size_t)row * D : nullptr};
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = (i * 32 + lane) * 8;
-      cx[i] = c < D ? xr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
-      cg[i] = c < D ? gr[i * 32 + lane] : make_uint4(0, 0, 0, 0);
-      cr[i] = (rr_row && c < D) ? rr_row[i * 32 + lane] : make_uint4(0, 0, 0, 0);
+      for (int t = 0; t < 3; ++t) {
+        if (!src[t]) continue;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int c = (i * 32 + lane) * 8;
+          if (c < D)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d + t * NV * 32 + i * 32 + lane)),
+                         "l"(reinterpret_cast<const uint4*>(src[t]) + i * 32 + lane)
+                         : "memory");
+        }
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int slot = 0;
+  issue(r0 + warp, 0);
+#pragma unroll 1
+  for (int row = r0 + warp; row < r1; row += kLnWarps, slot ^= 1) {
+    issue(row + kLnWarps, slot ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    const uint4* bx = wb + (size_t)slot * 3 * NV * 32;
+    const uint4* bg = bx + NV * 32;
+    const uint4* br = bg + NV * 32;
+    const float mu = mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c >= D) continue;
       float xh[8], g[8];
-      unpack8(cx[i], xh);
-      unpack8(cg[i], g);
-      const float* wr = s_w + (i * 32 + lane) * 8;
+      unpack8(bx[i * 32 + lane], xh);
+      unpack8(bg[i * 32 + lane], g);
+      const float* wr = s_w + c;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         xh[e] = (xh[e] - mu) * rs;
@@ -148,20 +170,21 @@ k_ln_bwd(int M, int D, int rows_per_cta, const __nv_bfloat16* __restrict__ x, co
       const int c = (i * 32 + lane) * 8;
       if (c >= D) continue;
       float xh[8], g[8], o[8];
-      unpack8(xr[i * 32 + lane], xh);  // L1 hit
-      unpack8(gr[i * 32 + lane], g);
+      unpack8(bx[i * 32 + lane], xh);
+      unpack8(bg[i * 32 + lane], g);
       const float* wr = s_w + c;
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = rs * (g[e] * wr[e] - s1 - (xh[e] - mu) * rs * s2);
       if (dres) {  // the skip connection's gradient, summed here instead of by a separate add
         float rr[8];
-        unpack8(cr[i], rr);
+        unpack8(br[i * 32 + lane], rr);
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] += rr[e];
       }
       dr[i * 32 + lane] = pack8(o);
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // fold the warps of this CTA in a fixed order (warp 0, 1, ...), then one
   // partial row per CTA
   for (int k = 0; k < kLnWarps; ++k) {
@@ -294,11 +317,17 @@ int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, cons
   auto G = static_cast<const __nv_bfloat16*>(dy);
   auto DX = static_cast<__nv_bfloat16*>(dx);
   auto R = static_cast<const __nv_bfloat16*>(dres);
+  auto go = [&](auto NVc) {
+    constexpr int NV = decltype(NVc)::value;
+    const size_t sm = (size_t)kLnWarps * 2 * 3 * NV * 32 * sizeof(uint4);
+    cudaFuncSetAttribute(k_ln_bwd<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_ln_bwd<NV><<<ctas, kLnWarps * 32, sm, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R);
+  };
   switch (ln_nv(D)) {
-    case 1: k_ln_bwd<1><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
-    case 2: k_ln_bwd<2><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
-    case 3: k_ln_bwd<3><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
-    default: k_ln_bwd<4><<<ctas, kLnWarps * 32, 0, st>>>(M, D, rpc, X, G, w, mean, rstd, DX, part, R); break;
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    default: go(std::integral_constant<int, 4>{}); break;
   }
   note_launch();
   k_ln_fold<<<ceil_div(D, 32), kFoldWarps * 32, 0, st>>>(D, ctas, part, dw, db);
