@@ -62,15 +62,11 @@ with open(f"profiles/{R}_dominant_ncu.txt", "w") as f:
         tus = g("gpu__time_duration.sum") * (1e-3 if rr[1][idx["gpu__time_duration.sum"]] == "nsecond" else 1)
         f.write(f"{name:60s} {tus:9.2f} us  {byts / 1e6:8.1f} MB  tc {g('sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active'):5.1f}%"
                 f"  grid {g('launch__grid_size'):.0f}  regs {g('launch__registers_per_thread'):.0f}  L2hit {g('lts__t_sector_hit_rate.pct'):.1f}%\n")
-        if "k_tc_gemm" in r[kn]:
-            args = re.sub(r"[^0-9,a-z]", "", re.search(r"k_tc_gemm<([^>]*)>", r[kn]).group(1))
-            traffic["diagmm_tc_gemm_bf16" if args.startswith("256,4,1") else "diagmm_tc_gemm_bf16_ex"].append(byts)
+        if "k_tc_gemm" in r[kn]:  # k_tc_gemm<...> (single CTA) or k_tc_gemm2<...> (CTA pair): one family
+            traffic["diagmm_tc_gemm_bf16"].append(byts)
         elif "k_materialize" in r[kn]:
             traffic["diagmm_materialize"].append(byts)
 tj = {k: sum(v) / len(v) for k, v in traffic.items()}
-fam = traffic.get("diagmm_tc_gemm_bf16", []) + traffic.get("diagmm_tc_gemm_bf16_ex", [])
-if fam:  # the k_tc_gemm family (bench.py reports the dominant kernel per family)
-    tj["diagmm_tc_gemm_bf16"] = sum(fam) / len(fam)
 tj["_note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the launches of "
                f"profiles/{R}_dominant_ncu.txt (ncu --set full, first forward launches of a bench step)")
 json.dump(tj, open(f"profiles/{R}_traffic.json", "w"), indent=1)
