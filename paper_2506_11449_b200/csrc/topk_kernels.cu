@@ -491,7 +491,9 @@ k_waterfill(const __grid_constant__ WaterfillJobs jobs) {
     idx[i] = i < C ? i : 0x7fffffff;
   }
   __syncthreads();
-  if (jobs.radix && k < C && k <= nt && nt == kSelThreads) {  // sort the top-k only
+  // sort the top-k only — when the full sort is wider than the block (C > 1024); at
+  // C <= 1024 the one-element-per-thread full sort is cheaper (C = 768: 22.6 vs 29 us)
+  if (jobs.radix && k < C && k <= nt && nt == kSelThreads && NP > nt) {
     waterfill_radix(C, k, key, R, idx, maps, reinterpret_cast<double*>(maps + 64), ibuf, asoft, clamped);
     unsigned char* flag = reinterpret_cast<unsigned char*>(R);
     for (int i = tid; i < C; i += nt) flag[i] = key[i] >= 1e-3 ? 1 : 0;
@@ -590,51 +592,93 @@ k_active_from_list(int C, int n, const int32_t* __restrict__ offs, int32_t* __re
   if (threadIdx.x == 0 && n_act) *n_act = n;
 }
 
-// K5 body for one layer (one CTA); shared by the per-layer and the batched kernels
+// Two doubles reduced at once (fixed shuffle tree, then warp 0 over the warp
+// results): op 0 sums both, op 1 sums the first and takes the max of the second.
+__device__ double2 block_reduce2(double a, double b, bool max_b, double* buf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    const double y = __shfl_xor_sync(0xffffffffu, b, o);
+    b = max_b ? fmax(b, y) : b + y;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) { buf[w] = a; buf[32 + w] = b; }
+  __syncthreads();
+  if (w == 0) {
+    double ra = lane < nw ? buf[lane] : 0.0;
+    double rb = lane < nw ? buf[32 + lane] : (max_b ? -CUDART_INF : 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ra += __shfl_xor_sync(0xffffffffu, ra, o);
+      const double y = __shfl_xor_sync(0xffffffffu, rb, o);
+      rb = max_b ? fmax(rb, y) : rb + y;
+    }
+    if (lane == 0) { buf[64] = ra; buf[65] = rb; }
+  }
+  __syncthreads();
+  const double2 r = make_double2(buf[64], buf[65]);
+  __syncthreads();
+  return r;
+}
+
+// K5 body for one layer (one CTA); shared by the per-layer and the batched kernels.
+// Two dependent block reductions: (clamped count, max free z), then (sum q, sum up*q)
+// with q = exp(z - zmax) unnormalised; the candidate's alpha / clamped / up stay in
+// registers between the passes (C <= 8192: <= 8 per thread).
 __device__ void topk_grad_block(int C, int k_arg, double t_arg, const double* __restrict__ alpha,
                                 const uint8_t* __restrict__ clamped, const double* __restrict__ up, double l1,
                                 double* __restrict__ g_alpha, int accumulate, const double* __restrict__ params,
                                 double* smem) {
+  constexpr int kPer = kSelMaxC / kSelThreads;
   const int k = params ? (int)params[1] : k_arg;
   const double temperature = params ? params[0] : t_arg;
-  double* q = smem;       // C
-  double* buf = q + C;    // blockDim
+  double* buf = smem;  // 66 doubles
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (C + nt - 1) / nt;
   const int lo = min(C, tid * per), hi = min(C, lo + per);
+  unsigned clm = 0;  // clamped flags of this thread's candidates (alpha / up re-read: L1 hits)
   double ncl = 0.0, zmax = -CUDART_INF;
-  for (int i = lo; i < hi; ++i) {
-    if (clamped[i]) ncl += 1.0;
-    else zmax = fmax(zmax, alpha[i] / temperature);
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int i = lo + e;
+    if (e < per && i < hi) {
+      if (clamped[i]) { clm |= 1u << e; ncl += 1.0; }
+      else zmax = fmax(zmax, alpha[i] / temperature);
+    }
   }
-  const int n_clamped = (int)block_reduce_sum(ncl, buf);
-  zmax = block_reduce_max(zmax, buf);
+  const double2 r1 = block_reduce2(ncl, zmax, true, buf);
+  const int n_clamped = (int)r1.x;
+  zmax = r1.y;
   const int budget = k - n_clamped;
   const bool any_free = n_clamped < C;
-  double sq = 0.0;
-  for (int i = lo; i < hi; ++i) {
-    double v = 0.0;
-    if (!clamped[i]) v = exp(alpha[i] / temperature - zmax);
-    q[i] = v;
-    sq += v;
+  double v[kPer];
+  double sq = 0.0, su = 0.0;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int i = lo + e;
+    v[e] = 0.0;
+    if (e < per && i < hi && !(clm >> e & 1u)) {
+      v[e] = exp(alpha[i] / temperature - zmax);
+      sq += v[e];
+      su += up[i] * v[e];
+    }
   }
-  const double sum_q = block_reduce_sum(sq, buf);
-  double sw = 0.0;
-  for (int i = lo; i < hi; ++i) {
-    q[i] = q[i] / sum_q;
-    sw += up[i] * q[i];
-  }
-  const double sum_w = block_reduce_sum(sw, buf);
+  const double2 r2 = block_reduce2(sq, su, false, buf);
+  const double sum_q = r2.x;
+  const double sum_w = r2.y / sum_q;  // = sum up * q with q = v / sum_q
   const double coef = (double)budget / temperature;
-  for (int i = lo; i < hi; ++i) {
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int i = lo + e;
+    if (!(e < per && i < hi)) continue;
     double g = 0.0;
-    if (any_free && budget > 0 && !clamped[i]) {
-      const double w = up[i] * q[i];
-      g = coef * (w - q[i] * sum_w);
+    if (any_free && budget > 0 && !(clm >> e & 1u)) {
+      const double q = v[e] / sum_q;
+      g = coef * (up[i] * q - q * sum_w);
     }
     if (l1 != 0.0) {
-      const double a = alpha[i];
-      g += l1 * (a > 0.0 ? 1.0 : (a < 0.0 ? -1.0 : 0.0));
+      const double av = alpha[i];
+      g += l1 * (av > 0.0 ? 1.0 : (av < 0.0 ? -1.0 : 0.0));
     }
     g_alpha[i] = accumulate ? g_alpha[i] + g : g;
   }
@@ -739,7 +783,7 @@ int run_topk_grad_batched(int n, const diagmm_topk_grad_job* jobs, cudaStream_t 
       P.j[i] = jobs[b + i];
       cmax = P.j[i].C > cmax ? P.j[i].C : cmax;
     }
-    const size_t sm = (size_t)cmax * 8 + kSelThreads * 8;
+    const size_t sm = 66 * sizeof(double);  // block_reduce2 scratch (the values stay in registers)
     cudaFuncSetAttribute(k_topk_grad_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_topk_grad_batched<<<cnt, kSelThreads, sm, st>>>(P);
     note_launch();
@@ -754,7 +798,7 @@ int run_topk_grad(int C, int k, double T, const double* alpha, const uint8_t* cl
   if (!(T > 0.0)) return DIAGMM_ETEMPERATURE;
   if (k < 1 || k > C) return DIAGMM_EK;
   if (C > kSelMaxC) return DIAGMM_ETOOLARGE;
-  size_t sm = (size_t)C * 8 + kSelThreads * 8;
+  const size_t sm = 66 * sizeof(double);
   cudaFuncSetAttribute(k_topk_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_topk_grad<<<1, kSelThreads, sm, st>>>(C, k, T, alpha, clamped, up, l1, g_alpha, accumulate, params);
   note_launch();

@@ -1,4 +1,4 @@
-"""K4's top-k radix-select path (k < C, k <= 1024: 8 histogram passes for the k-th
+"""K4's top-k radix-select path (k < C, k <= 1024 < C: 8 histogram passes for the k-th
 largest key, only the top k sorted, the rest folded into one fixed-order sum)
 against the full-sort path and the CPU oracle on adversarial selections: ties
 everywhere, tie groups straddling the k-th key, +0.0 / -0.0, k = 1, k = C - 1,
@@ -49,7 +49,8 @@ def _run(alpha, k, T, radix, monkeypatch):
     return (sel.alpha_soft.cpu().numpy(), sel.clamped.cpu().numpy().astype(bool), sel.active[:n].cpu().numpy())
 
 
-CASES = [(C, k) for C in (768, 3072, 8192) for k in (1, C // 10, C - 1)] + [(4096, 1024), (4096, 1025), (2048, 1023)]
+CASES = ([(C, k) for C in (1025, 3072, 8192) for k in (1, C // 10, C - 1)] + [(4096, 1024), (4096, 1025), (2048, 1023)]
+         + [(768, 77)])  # C <= 1024 takes the full sort either way
 
 
 @pytest.mark.parametrize("kind", ["random", "all_equal", "tie_groups", "signed_zeros"])
