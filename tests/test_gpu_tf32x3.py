@@ -115,3 +115,46 @@ def test_tf32x3_graph_capture_and_default_rule(monkeypatch):
     assert torch.equal(out, eager)
     monkeypatch.delenv("DIAGMM_TF32X3_MIN_B")
     assert torch.equal(ops.diag_forward(x, vals, sel, M, N, max_act=len(offs)), eager)
+
+
+def test_diaglinear_fp32_training_step_on_tf32_route(monkeypatch):
+    """A float32 DiagLinear step at B = 512 (the route's default range) through the public
+    module: y, dx, d values, d alpha, d bias equal the FMA-route step's to the fp32 bar
+    (both against the same fp64-accurate arithmetic), and the step replays from a graph."""
+    from paper_2506_11449_b200 import DiagLinear, TemperatureSchedule
+    from paper_2506_11449_b200.graphed import GraphedStep
+
+    sched = TemperatureSchedule("constant", 0.05, 0.05, 1)
+    x = torch.randn(512, 768, device="cuda")
+    up = torch.randn(512, 3072, device="cuda")
+
+    def step(route_min_b):
+        monkeypatch.setenv("DIAGMM_TF32X3_MIN_B", route_min_b)
+        torch.manual_seed(0)
+        lyr = DiagLinear(768, 3072, 0.9, seed=3, dtype=torch.float32, t_schedule=sched, l1_coeff=1e-4)
+        xi = x.clone().requires_grad_(True)
+        y = lyr(xi, step=0)
+        (y * up).sum().backward()
+        torch.cuda.synchronize()
+        return lyr, [y.detach(), xi.grad, lyr.values.grad, lyr.alpha.grad, lyr.bias.grad]
+
+    _, fma = step("0")
+    lyr, tf = step("1")
+    for a, b in zip(tf, fma):
+        scale = max(1.0, float(b.abs().max()))
+        assert float((a.double() - b.double()).abs().max()) <= F32_TOL * scale
+    params = list(lyr.parameters())
+    for p in params:
+        p.grad = None
+
+    def fwd_bwd(inp, u):
+        loss = (lyr(inp, step=0) * u).sum()
+        loss.backward()
+        return loss
+
+    gs = GraphedStep(fwd_bwd, params, x.clone(), up.clone())
+    gs.step(x, up)
+    torch.cuda.synchronize()
+    for p, ref in zip([lyr.values, lyr.alpha, lyr.bias], tf[2:]):
+        scale = max(1.0, float(ref.abs().max()))
+        assert float((p.grad.double() - ref.double()).abs().max()) <= F32_TOL * scale
