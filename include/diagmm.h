@@ -374,6 +374,20 @@ DIAGMM_API int diagmm_pack_qkv_grad(int B, int T, int H, int hd, const void* dq,
                                     const void* dv, long long stride_b, long long stride_h,
                                     long long stride_t, void* dqkv, void* stream);
 
+/* ViT patch embedding for the caller (no reference counterpart on the path):
+ * patchify: images (B, Cin, H, W) bf16 -> (B * (H/p) * (W/p), Cin*p*p) bf16 in conv2d
+ * weight order (p % 8 == 0); embed_fwd: x (B, T, D) bf16 = [bf16(cls); y] + bf16(pos)
+ * with y the (B * (T-1), D) patch projections, cls (D,) and pos (T, D) fp32;
+ * embed_bwd: from gx (B, T, D) the contiguous patch gradient dy (B * (T-1), D) and the
+ * fp32 gradients of pos (T, D), cls (D,) and the patch bias (D,) (any may be NULL). */
+DIAGMM_API int diagmm_vit_patchify(int B, int Cin, int H, int W, int p, const void* images, void* patches,
+                                   void* stream);
+DIAGMM_API int diagmm_vit_embed_fwd(int B, int T, int D, const void* y, const float* cls, const float* pos,
+                                    void* x, void* stream);
+DIAGMM_API size_t diagmm_vit_embed_bwd_workspace(int T, int D);
+DIAGMM_API int diagmm_vit_embed_bwd(int B, int T, int D, const void* gx, void* dy, float* dpos, float* dcls,
+                                    float* dbias, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- dense-equivalent route (reference's own BLAS switch) ---------------
  * The reference multiplies the materialized matrix with BLAS when the
  * structural density reaches 1/4 (diagcore.py:226-228) and computes dW

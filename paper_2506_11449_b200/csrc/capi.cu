@@ -55,6 +55,10 @@ int run_tc_dw_full(int, int, int, const void*, const void*, const void*, const d
 int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long long, long long, long long, void*,
                  cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
+int run_vit_patchify(int, int, int, int, int, const void*, void*, cudaStream_t);
+int run_vit_embed_fwd(int, int, int, const void*, const float*, const float*, void*, cudaStream_t);
+size_t vit_embed_bwd_workspace(int, int);
+int run_vit_embed_bwd(int, int, int, const void*, void*, float*, float*, float*, void*, size_t, cudaStream_t);
 size_t ln_bwd_workspace(int, int);
 int run_ln_bwd(int, int, const void*, const void*, const float*, const float*, const float*, void*, float*, float*,
                void*, size_t, cudaStream_t, const void* dres = nullptr);
@@ -265,6 +269,19 @@ int diagmm_tc_backward_weight_split(int M, int N, int B, const void* dy0, const 
 DIAGMM_API int diagmm_internal_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void* B, void* out,
                                                void* stream) {
   return run_tc_sparse_probe(Mdim, Ndim, K, Acomp, B, out, S(stream));
+}
+
+int diagmm_vit_patchify(int B, int Cin, int H, int W, int p, const void* images, void* patches, void* stream) {
+  return run_vit_patchify(B, Cin, H, W, p, images, patches, S(stream));
+}
+int diagmm_vit_embed_fwd(int B, int T, int D, const void* y, const float* cls, const float* pos, void* x,
+                         void* stream) {
+  return run_vit_embed_fwd(B, T, D, y, cls, pos, x, S(stream));
+}
+size_t diagmm_vit_embed_bwd_workspace(int T, int D) { return vit_embed_bwd_workspace(T, D); }
+int diagmm_vit_embed_bwd(int B, int T, int D, const void* gx, void* dy, float* dpos, float* dcls, float* dbias,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  return run_vit_embed_bwd(B, T, D, gx, dy, dpos, dcls, dbias, workspace, ws_bytes, S(stream));
 }
 
 int diagmm_pack_qkv_grad(int B, int T, int H, int hd, const void* dq, const void* dk, const void* dv,

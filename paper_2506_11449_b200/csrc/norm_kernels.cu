@@ -9,6 +9,7 @@
 // registers over its rows, written as per-CTA partials and folded in a fixed
 // order by a second kernel (deterministic, no atomics).
 #include "common.cuh"
+#include <algorithm>
 #include <type_traits>
 
 namespace diagmm {
@@ -332,6 +333,162 @@ int run_ln_bwd(int M, int D, const void* x, const void* dy, const float* w, cons
   note_launch();
   k_ln_fold<<<ceil_div(D, 32), kFoldWarps * 32, 0, st>>>(D, ctas, part, dw, db);
   note_launch();
+  return status_from_cuda();
+}
+
+
+// ---------------------------------------------------------------- ViT patch embedding
+// (caller-side, around the DiagLinear blocks): the patchify copy, the cls / position
+// assembly and their backward as three streaming kernels instead of framework
+// permute-copy, cat, broadcast-add, slice-copy and two reductions.
+
+// images (B, Cin, H, W) bf16 -> patches (B * (H/p) * (W/p), Cin * p * p) bf16, column
+// order (c, i, j) = conv2d's weight layout; one 16-byte chunk (8 pixels of a patch row)
+// per thread: 16-byte loads and stores (p % 8 == 0).
+__global__ void __launch_bounds__(256)
+k_vit_patchify(int B, int Cin, int H, int W, int p, const uint4* __restrict__ img, uint4* __restrict__ out) {
+  const int gh = H / p, gw = W / p, cpr = p / 8;  // 16-byte chunks per patch row
+  const long long per_patch = (long long)Cin * p * cpr;
+  const long long n = (long long)B * gh * gw * per_patch;
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+    const long long pi = e / per_patch;
+    const int r = (int)(e - pi * per_patch);
+    const int c = r / (p * cpr), rem = r - c * p * cpr, i = rem / cpr, j8 = rem - i * cpr;
+    const int b = (int)(pi / (gh * gw)), pp = (int)(pi - (long long)b * gh * gw), ph = pp / gw, pw = pp - ph * gw;
+    const long long src = ((((long long)b * Cin + c) * H + ph * p + i) * W + pw * p) / 8 + j8;
+    out[e] = __ldcs(img + src);
+  }
+}
+
+__device__ __forceinline__ float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// x (B, T, D) bf16: x[b, 0] = bf16(cls) + bf16(pos[0]), x[b, t] = y[b, t-1] + bf16(pos[t]) —
+// one bf16 rounding of each sum, as the framework's cat + broadcast add of bf16 operands.
+__global__ void __launch_bounds__(256)
+k_vit_embed_fwd(int B, int T, int D, const __nv_bfloat16* __restrict__ y, const float* __restrict__ cls,
+                const float* __restrict__ pos, __nv_bfloat16* __restrict__ x) {
+  const int d8 = D / 8;
+  const long long n = (long long)B * T * d8;
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+    const long long row = e / d8;
+    const int c = (int)(e - row * d8) * 8;
+    const int b = (int)(row / T), t = (int)(row - (long long)b * T);
+    float a[8];
+    if (t == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = bf16r(__ldg(cls + c + k));
+    } else {
+      unpack8(__ldg(reinterpret_cast<const uint4*>(y + ((size_t)b * (T - 1) + t - 1) * D + c)), a);
+    }
+    const float4 p0 = __ldg(reinterpret_cast<const float4*>(pos + (size_t)t * D + c));
+    const float4 p1 = __ldg(reinterpret_cast<const float4*>(pos + (size_t)t * D + c + 4));
+    const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += bf16r(pv[k]);
+    reinterpret_cast<uint4*>(x)[e] = pack8(a);
+  }
+}
+
+// Backward, pass 1: dy[b, t-1] = gx[b, t] (t >= 1, contiguous for the patch GEMM's
+// weight gradient) and per-group column sums part[g][t][d] = sum_{b in group g} gx[b, t, d]
+// (fp32, batches in index order).  grid (T, groups), D/8 threads.
+constexpr int kEmbGroups = 16;
+__global__ void __launch_bounds__(128)
+k_vit_embed_bwd(int B, int T, int D, const __nv_bfloat16* __restrict__ gx, __nv_bfloat16* __restrict__ dy,
+                float* __restrict__ part) {
+  const int t = blockIdx.x, g = blockIdx.y, d8 = D / 8;
+  const int bpg = (B + gridDim.y - 1) / gridDim.y, b0 = g * bpg, b1 = min(B, b0 + bpg);
+  for (int c8 = threadIdx.x; c8 < d8; c8 += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int b = b0; b < b1; ++b) {
+      const uint4 u = __ldcs(reinterpret_cast<const uint4*>(gx + ((size_t)b * T + t) * D) + c8);
+      if (t > 0) reinterpret_cast<uint4*>(dy + ((size_t)b * (T - 1) + t - 1) * D)[c8] = u;
+      float f[8];
+      unpack8(u, f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += f[k];
+    }
+    float* pr = part + ((size_t)g * T + t) * D + c8 * 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pr[k] = acc[k];
+  }
+}
+
+// pass 2: fold the groups in order, one thread per (t, d).  dpos[t] = bf16-rounded sum
+// (the framework reduces the bf16 broadcast gradient to bf16), dcls = the fp32 sum at
+// t = 0; the fp32 per-t sums go to tsum for the bias gradient.
+__global__ void __launch_bounds__(256)
+k_vit_embed_fold(int T, int D, int groups, const float* __restrict__ part, float* __restrict__ tsum,
+                 float* __restrict__ dpos, float* __restrict__ dcls) {
+  const int t = blockIdx.y, d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  float s = 0.f;
+  for (int g = 0; g < groups; ++g) s += __ldcg(part + ((size_t)g * T + t) * D + d);
+  tsum[(size_t)t * D + d] = s;
+  if (dpos) dpos[(size_t)t * D + d] = bf16r(s);
+  if (t == 0 && dcls) dcls[d] = s;
+}
+
+// pass 3: dbias = bf16-rounded sum over t >= 1 (the patch GEMM's bias gradient in bf16):
+// 32 columns per CTA, warp w takes t = 1 + w, 1 + w + 8, ..., folded in warp order.
+__global__ void __launch_bounds__(256)
+k_vit_embed_bias(int T, int D, const float* __restrict__ tsum, float* __restrict__ dbias) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, d = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (d < D)
+    for (int t = 1 + w; t < T; t += 8) s += __ldcg(tsum + (size_t)t * D + d);
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && d < D) {
+    float r = 0.f;
+    for (int k = 0; k < 8; ++k) r += red[k][lane];
+    dbias[d] = bf16r(r);
+  }
+}
+
+int run_vit_patchify(int B, int Cin, int H, int W, int p, const void* img, void* out, cudaStream_t st) {
+  if (B < 1 || Cin < 1 || p < 8 || p % 8 || H % p || W % p || (reinterpret_cast<uintptr_t>(img) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return DIAGMM_ESHAPE;
+  const long long n = (long long)B * Cin * H * W / 8;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 16);
+  k_vit_patchify<<<blocks, 256, 0, st>>>(B, Cin, H, W, p, static_cast<const uint4*>(img), static_cast<uint4*>(out));
+  note_launch();
+  return status_from_cuda();
+}
+
+int run_vit_embed_fwd(int B, int T, int D, const void* y, const float* cls, const float* pos, void* x,
+                      cudaStream_t st) {
+  if (B < 1 || T < 2 || D % 8 || (reinterpret_cast<uintptr_t>(y) & 15) || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(pos) & 15))
+    return DIAGMM_ESHAPE;
+  const long long n = (long long)B * T * (D / 8);
+  const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 16);
+  k_vit_embed_fwd<<<blocks, 256, 0, st>>>(B, T, D, static_cast<const __nv_bfloat16*>(y), cls, pos,
+                                          static_cast<__nv_bfloat16*>(x));
+  note_launch();
+  return status_from_cuda();
+}
+
+size_t vit_embed_bwd_workspace(int T, int D) { return (size_t)(kEmbGroups + 1) * T * D * sizeof(float); }
+
+int run_vit_embed_bwd(int B, int T, int D, const void* gx, void* dy, float* dpos, float* dcls, float* dbias,
+                      void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (B < 1 || T < 2 || D % 8 || (reinterpret_cast<uintptr_t>(gx) & 15) || (reinterpret_cast<uintptr_t>(dy) & 15))
+    return DIAGMM_ESHAPE;
+  if (ws_bytes < vit_embed_bwd_workspace(T, D)) return DIAGMM_EWORKSPACE;
+  float* part = static_cast<float*>(ws);
+  k_vit_embed_bwd<<<dim3(T, kEmbGroups), 128, 0, st>>>(B, T, D, static_cast<const __nv_bfloat16*>(gx),
+                                                      static_cast<__nv_bfloat16*>(dy), part);
+  float* tsum = part + (size_t)kEmbGroups * T * D;
+  k_vit_embed_fold<<<dim3(ceil_div(D, 256), T), 256, 0, st>>>(T, D, kEmbGroups, part, tsum, dpos, dcls);
+  note_launch(2);
+  if (dbias) {
+    k_vit_embed_bias<<<ceil_div(D, 32), 256, 0, st>>>(T, D, tsum, dbias);
+    note_launch();
+  }
   return status_from_cuda();
 }
 

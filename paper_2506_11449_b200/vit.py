@@ -110,6 +110,70 @@ class QKVAttentionFunction(torch.autograd.Function):
         return dx, gv, ga, gb, None, None, None, None, None
 
 
+class PatchEmbedFunction(torch.autograd.Function):
+    """Patch embedding + cls token + position embedding as one node (caller-side).
+
+    Forward: images -> patches by a 16-byte streaming kernel (diagmm_vit_patchify),
+    the patch projection on cuBLAS bf16 (a plain dense GEMM, as F.linear under
+    autocast), then [bf16(cls); y] + bf16(pos) in one pass (diagmm_vit_embed_fwd).
+    Backward: one pass over the gradient gives the contiguous patch gradient and the
+    pos / cls / bias sums (diagmm_vit_embed_bwd); the weight gradient is dy^T P in
+    bf16.  Same roundings as the framework's cat + broadcast-add path it replaces."""
+
+    @staticmethod
+    def forward(ctx, images, weight, bias, cls, pos, patch):
+        B, Cin, H, W = images.shape
+        D = weight.shape[0]
+        img = images.to(torch.bfloat16).contiguous()
+        gh, gw = H // patch, W // patch
+        T = gh * gw + 1
+        st = torch.cuda.current_stream(images.device).cuda_stream
+        P = torch.empty(B * gh * gw, Cin * patch * patch, dtype=torch.bfloat16, device=images.device)
+        _lib.call("diagmm_vit_patchify", B, Cin, H, W, patch, img.data_ptr(), P.data_ptr(), st)
+        w = weight.detach().reshape(D, -1).to(torch.bfloat16)
+        b = None if bias is None else bias.detach().to(torch.bfloat16)
+        with torch.autocast("cuda", enabled=False):
+            y = F.linear(P, w, b)
+        x = torch.empty(B, T, D, dtype=torch.bfloat16, device=images.device)
+        clsf = cls.detach().float().reshape(D).contiguous()
+        posf = pos.detach().float().reshape(T, D).contiguous()
+        _lib.call("diagmm_vit_embed_fwd", B, T, D, y.data_ptr(), clsf.data_ptr(), posf.data_ptr(), x.data_ptr(), st)
+        ctx.save_for_backward(P, w)
+        ctx.meta = (B, T, D, weight.shape, bias is not None, cls.shape, pos.shape)
+        return x
+
+    @staticmethod
+    def backward(ctx, gx):
+        P, w = ctx.saved_tensors
+        B, T, D, wshape, has_bias, cshape, pshape = ctx.meta
+        g = gx.to(torch.bfloat16).contiguous()
+        dev = g.device
+        dy = torch.empty(B * (T - 1), D, dtype=torch.bfloat16, device=dev)
+        dpos = torch.empty(T, D, dtype=torch.float32, device=dev)
+        dcls = torch.empty(D, dtype=torch.float32, device=dev)
+        dbias = torch.empty(D, dtype=torch.float32, device=dev) if has_bias else None
+        nws = _lib.load().diagmm_vit_embed_bwd_workspace(T, D)
+        ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+        _lib.call("diagmm_vit_embed_bwd", B, T, D, g.data_ptr(), dy.data_ptr(), dpos.data_ptr(), dcls.data_ptr(),
+                  None if dbias is None else dbias.data_ptr(), ws.data_ptr(), nws,
+                  torch.cuda.current_stream(dev).cuda_stream)
+        dw = None
+        if ctx.needs_input_grad[1]:
+            with torch.autocast("cuda", enabled=False):
+                dw = torch.mm(dy.t(), P).float().reshape(wshape)
+        return (None, dw, dbias if ctx.needs_input_grad[2] else None, dcls.reshape(cshape),
+                dpos.reshape(pshape), None)
+
+
+def _embed_fusable(images, cfg) -> bool:
+    import os
+
+    bf16 = images.dtype == torch.bfloat16 or (torch.is_autocast_enabled("cuda")
+                                               and torch.get_autocast_dtype("cuda") == torch.bfloat16)
+    return (images.is_cuda and bf16 and cfg.patch % 8 == 0 and cfg.dim % 8 == 0
+            and os.environ.get("DIAGMM_FUSE_EMBED", "1") != "0")
+
+
 def _qkv_fusable(qkv, x2: torch.Tensor, H: int) -> bool:
     import os
 
@@ -323,8 +387,12 @@ class ViT(nn.Module):
                    and torch.get_autocast_dtype("cuda") == torch.bfloat16 and tokens >= dense_route_min_tokens()
                    and _premat_enabled() else None)
             preselect(diag, diag[0].step, materialize=mat)
-        x = self._patchify(images)
-        x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
+        if _embed_fusable(images, self.cfg):
+            x = PatchEmbedFunction.apply(images, self.patch.weight, self.patch.bias, self.cls, self.pos,
+                                         self.cfg.patch)
+        else:
+            x = self._patchify(images)
+            x = torch.cat([self.cls.expand(x.shape[0], -1, -1).to(x.dtype), x], dim=1) + self.pos.to(x.dtype)
         for blk in self.blocks:
             x = blk(x)
         return self.head(self.norm(x)[:, 0])
