@@ -65,3 +65,18 @@ for e in ev:
     by[k][1] += (e.time_range.end - e.time_range.start) / 1e3 / 3
 for k, v in sorted(by.items(), key=lambda kv: -kv[1][1])[:25]:
     print(f"{v[1]:8.3f} ms  x{v[0] // 3:4d}  {k}")
+
+# idle gaps: after each kernel, the time until the next kernel starts (union timeline of one replay)
+iv = sorted((e.time_range.start, e.time_range.end, e.name[:60]) for e in ev)
+third = len(iv) // 3
+gaps = defaultdict(lambda: [0, 0.0])
+cur_end = iv[0][1]
+for k in range(1, third):
+    st, en, nm = iv[k]
+    if st > cur_end:
+        gaps[nm][0] += 1
+        gaps[nm][1] += (st - cur_end) / 1e3
+    cur_end = max(cur_end, en)
+print("idle before kernel (one replay): total %.3f ms" % sum(v[1] for v in gaps.values()))
+for k, v in sorted(gaps.items(), key=lambda kv: -kv[1][1])[:12]:
+    print(f"{v[1]:8.3f} ms  x{v[0]:4d}  {k}")
