@@ -374,6 +374,16 @@ DIAGMM_API int diagmm_pack_qkv_grad(int B, int T, int H, int hd, const void* dq,
                                     const void* dv, long long stride_b, long long stride_h,
                                     long long stride_t, void* dqkv, void* stream);
 
+/* Dense float32 GEMM on the 3xTF32 tensor-core kernel (fp32-accurate): the
+ * reference's density >= 1/4 BLAS switch (diagcore.py:226-228, layers.py:150-153)
+ * for float32 layers.  out (M x N, row stride ldo) = op(A) (M x K) . op(B) (N x K)^T
+ * (+ bias (N,)); op(A) = A given as (M x K, lda), or with trans_a the transpose of
+ * A given as (K x M, lda); op(B) likewise (trans_b: B given as (K x N, ldb)). */
+DIAGMM_API size_t diagmm_tf32x3_gemm_workspace(int M, int N, int K, int trans_a, int trans_b);
+DIAGMM_API int diagmm_tf32x3_gemm(int M, int N, int K, const float* A, int lda, int trans_a, const float* B,
+                                  int ldb, int trans_b, const float* bias, float* out, int ldo, void* workspace,
+                                  size_t ws_bytes, void* stream);
+
 /* ViT patch embedding for the caller (no reference counterpart on the path):
  * patchify: images (B, Cin, H, W) bf16 -> (B * (H/p) * (W/p), Cin*p*p) bf16 in conv2d
  * weight order (p % 8 == 0); embed_fwd: x (B, T, D) bf16 = [bf16(cls); y] + bf16(pos)

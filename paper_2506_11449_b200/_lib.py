@@ -108,6 +108,8 @@ SIGNATURES["diagmm_tc_backward_weight_split"] = (
     _i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp, _i, _vp])
 SIGNATURES["diagmm_pack_qkv_grad"] = (_i, [_i, _i, _i, _i, _vp, _vp, _vp, C.c_longlong, C.c_longlong, C.c_longlong,
                                            _vp, _vp])
+SIGNATURES["diagmm_tf32x3_gemm_workspace"] = (_sz, [_i, _i, _i, _i, _i])
+SIGNATURES["diagmm_tf32x3_gemm"] = (_i, [_i, _i, _i, _vp, _i, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _sz, _vp])
 SIGNATURES["diagmm_vit_patchify"] = (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp])
 SIGNATURES["diagmm_vit_embed_fwd"] = (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp])
 SIGNATURES["diagmm_vit_embed_bwd_workspace"] = (_sz, [_i, _i])

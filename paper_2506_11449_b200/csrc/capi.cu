@@ -56,6 +56,9 @@ int run_pack_qkv(int, int, int, int, const void*, const void*, const void*, long
                  cudaStream_t);
 int run_ln_fwd(int, int, float, const void*, const float*, const float*, void*, float*, float*, cudaStream_t);
 int run_vit_patchify(int, int, int, int, int, const void*, void*, cudaStream_t);
+size_t tf32x3_gemm_workspace(int, int, int, int, int);
+int run_tf32x3_gemm(int, int, int, const float*, int, int, const float*, int, int, const float*, float*, int, void*,
+                    size_t, cudaStream_t);
 int run_vit_embed_fwd(int, int, int, const void*, const float*, const float*, void*, cudaStream_t);
 size_t vit_embed_bwd_workspace(int, int);
 int run_vit_embed_bwd(int, int, int, const void*, void*, float*, float*, float*, void*, size_t, cudaStream_t);
@@ -269,6 +272,15 @@ int diagmm_tc_backward_weight_split(int M, int N, int B, const void* dy0, const 
 DIAGMM_API int diagmm_internal_tc_sparse_probe(int Mdim, int Ndim, int K, const void* Acomp, const void* B, void* out,
                                                void* stream) {
   return run_tc_sparse_probe(Mdim, Ndim, K, Acomp, B, out, S(stream));
+}
+
+size_t diagmm_tf32x3_gemm_workspace(int M, int N, int K, int trans_a, int trans_b) {
+  return tf32x3_gemm_workspace(M, N, K, trans_a, trans_b);
+}
+int diagmm_tf32x3_gemm(int M, int N, int K, const float* A, int lda, int trans_a, const float* B, int ldb,
+                       int trans_b, const float* bias, float* out, int ldo, void* workspace, size_t ws_bytes,
+                       void* stream) {
+  return run_tf32x3_gemm(M, N, K, A, lda, trans_a, B, ldb, trans_b, bias, out, ldo, workspace, ws_bytes, S(stream));
 }
 
 int diagmm_vit_patchify(int B, int Cin, int H, int W, int p, const void* images, void* patches, void* stream) {

@@ -513,4 +513,53 @@ int run_dw_tf32(int M, int N, int B, const float* dy, const float* x, const int3
   return status_from_cuda();
 }
 
+// ---- dense fp32 GEMM on the same kernel (the reference's density >= 1/4 switch,
+// diagcore.py:226-228 / layers.py:150-153, for float32 layers):
+//   out (M x N, ldo) = A_eff (M x K) . B_eff (N x K)^T (+ bias)
+// with A_eff = A (M x K, lda) or, trans_a, A^T for A given as (K x M, lda); B likewise.
+// Transposed or 16-byte-misaligned operands are staged into the workspace first.
+static bool tma_ok(const float* p, int ld) { return (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+size_t tf32x3_gemm_workspace(int M, int N, int K, int trans_a, int trans_b) {
+  const int kp = pad4(K > 0 ? K : 1);
+  const size_t a = trans_a ? align16((size_t)M * kp * 4) : align16((size_t)M * kp * 4);
+  const size_t b = trans_b ? align16((size_t)N * kp * 4) : align16((size_t)N * kp * 4);
+  return a + b + tf_split_bytes(M > 0 ? M : 1, N > 0 ? N : 1, K > 0 ? K : 1);
+}
+
+int run_tf32x3_gemm(int M, int N, int K, const float* A, int lda, int trans_a, const float* B, int ldb, int trans_b,
+                    const float* bias, float* out, int ldo, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (M < 1 || N < 1 || K < 1 || ldo < N) return DIAGMM_ESHAPE;
+  if (lda < (trans_a ? M : K) || ldb < (trans_b ? N : K)) return DIAGMM_ESHAPE;
+  if (ws_bytes < tf32x3_gemm_workspace(M, N, K, trans_a, trans_b)) return DIAGMM_EWORKSPACE;
+  const int kp = pad4(K);
+  char* p = static_cast<char*>(ws);
+  float* sa = reinterpret_cast<float*>(p);
+  float* sb = reinterpret_cast<float*>(p + align16((size_t)M * kp * 4));
+  float* part = reinterpret_cast<float*>(p + align16((size_t)M * kp * 4) + align16((size_t)N * kp * 4));
+  const float* a = A;
+  int la = lda;
+  if (trans_a) {
+    k_transpose_pad<<<dim3(ceil_div(M, 32), ceil_div(kp, 32)), 256, 0, st>>>(K, M, A, lda, sa, kp);
+    note_launch();
+    a = sa, la = kp;
+  } else if (!tma_ok(A, lda)) {
+    k_pad_rows<<<grid_1d((long long)M * kp), 256, 0, st>>>(M, K, A, lda, sa, kp);
+    note_launch();
+    a = sa, la = kp;
+  }
+  const float* b = B;
+  int lb = ldb;
+  if (trans_b) {
+    k_transpose_pad<<<dim3(ceil_div(N, 32), ceil_div(kp, 32)), 256, 0, st>>>(K, N, B, ldb, sb, kp);
+    note_launch();
+    b = sb, lb = kp;
+  } else if (!tma_ok(B, ldb)) {
+    k_pad_rows<<<grid_1d((long long)N * kp), 256, 0, st>>>(N, K, B, ldb, sb, kp);
+    note_launch();
+    b = sb, lb = kp;
+  }
+  return tf_gemm(M, N, K, a, la, b, lb, bias, out, ldo, part, true, nullptr, st);
+}
+
 }  // namespace diagmm

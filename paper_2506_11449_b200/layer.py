@@ -138,6 +138,13 @@ def _tc_ok(x: torch.Tensor, M: int, N: int) -> bool:
             and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas")
 
 
+def _tf32_dense(t: torch.Tensor) -> bool:
+    """float32 dense-route GEMMs on the 3xTF32 kernel (DIAGMM_DENSE_BACKEND=cublas: the library)."""
+    import os
+
+    return t.dtype == torch.float32 and t.is_cuda and os.environ.get("DIAGMM_DENSE_BACKEND", "tc") != "cublas"
+
+
 def dense_route_min_tokens() -> int:
     """Token count from which the bf16 tensor-core route beats the FMA route
     (measured on B200, profiles/r01_*; override with DIAGMM_DENSE_MIN_TOKENS)."""
@@ -286,7 +293,10 @@ class DiagMMFunction(torch.autograd.Function):
                 y = ops.tc_gemm(x.contiguous(), W, bz)
         elif dense:
             W = _w_k(spec, x.dtype, vals, sel, M, N)
-            y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
+            if _tf32_dense(x):  # float32: our 3xTF32 tensor-core GEMM, fp32-accurate
+                y = ops.tf32x3_gemm(x.contiguous(), W, bias=None if bias is None else bias.detach())
+            else:  # float64: the reference's own BLAS switch on a library DGEMM
+                y = F.linear(x, W, None if bias is None else bias.detach().to(x.dtype))
         else:
             y = ops.diag_forward(x, vals, sel, M, N, None if bias is None else bias.detach(),
                                  max_act=sel.known_count())
@@ -312,6 +322,8 @@ class DiagMMFunction(torch.autograd.Function):
             if ctx.needs_input_grad[0]:
                 if ctx.tc:  # dx = dy @ W_K on the tensor cores, W_K staged MN-major
                     dx = ops.tc_gemm_nn(dy, W)
+                elif _tf32_dense(dy):  # dx = dy @ W_K = dy . (W_K^T)^T
+                    dx = ops.tf32x3_gemm(dy, W, trans_b=True)
                 else:
                     dx = dy @ W
             out_dt = vals.dtype
@@ -323,8 +335,12 @@ class DiagMMFunction(torch.autograd.Function):
                 return dx, g_values, g_alpha, g_bias, None, d_res
             else:
                 spec.bucket = None  # this branch does not fill the exchange bucket (dp falls back to full)
-                dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt) if dy.dtype == torch.bfloat16 \
-                    else (dy.t() @ x.to(dy.dtype)).to(out_dt)
+                if dy.dtype == torch.bfloat16:
+                    dW = torch.mm(dy.t(), x.to(dy.dtype), out_dtype=out_dt)
+                elif _tf32_dense(dy):  # dW = dy^T x = (dy^T) . (x^T)^T
+                    dW = ops.tf32x3_gemm(dy, x.to(dy.dtype).contiguous(), trans_a=True, trans_b=True)
+                else:
+                    dW = (dy.t() @ x.to(dy.dtype)).to(out_dt)
                 g_values, g_soft = ops.gather_dense_grad(dW, vals, sel, M, N, need_soft=need_soft)
                 g_bias = dy.sum(0, dtype=out_dt) if ctx.has_bias else None
         else:

@@ -598,6 +598,30 @@ def layer_norm_skip_bf16(x, weight, bias, eps: float = 1e-5):
     return FusedLayerNormSkip.apply(x, weight, bias, eps)
 
 
+def tf32x3_gemm(a: torch.Tensor, b: torch.Tensor, trans_a: bool = False, trans_b: bool = False,
+                bias: torch.Tensor | None = None) -> torch.Tensor:
+    """out = op(a) @ op(b).T (+ bias) in float32 on the 3xTF32 tensor-core kernel
+    (fp32-accurate; tf32_kernels.cu): op(a) = a (M, K), or a.T for a given as (K, M)
+    with ``trans_a``; op(b) = b (N, K), or b.T for b given as (K, N) with ``trans_b``.
+    The float32 layers' dense route (the reference's density >= 1/4 switch,
+    diagcore.py:226-228 / layers.py:150-153) runs its three GEMMs here."""
+    _need_cuda(a, b)
+    if a.dtype != torch.float32 or b.dtype != torch.float32 or a.dim() != 2 or b.dim() != 2:
+        raise TypeError("tf32x3_gemm takes 2-D float32 operands")
+    a, b = a.contiguous(), b.contiguous()
+    M, K = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
+    N, Kb = (b.shape[1], b.shape[0]) if trans_b else (b.shape[0], b.shape[1])
+    if K != Kb:
+        raise ShapeMismatch(f"inner dims differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    out = torch.empty(M, N, dtype=torch.float32, device=a.device)
+    nws = _lib.load().diagmm_tf32x3_gemm_workspace(M, N, K, int(trans_a), int(trans_b))
+    ws = _workspace(a.device, nws)
+    bz = None if bias is None else bias.float().contiguous()
+    _lib.call("diagmm_tf32x3_gemm", M, N, K, _p(a), a.shape[1], int(trans_a), _p(b), b.shape[1], int(trans_b),
+              _p(bz), _p(out), N, _p(ws), nws, _stream(a))
+    return out
+
+
 def tc_gemm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None) -> torch.Tensor:
     """out = a @ b.T (+ bias) on the tcgen05 tensor cores (bf16 in/out, fp32 accumulate)."""
     _need_cuda(a, b)

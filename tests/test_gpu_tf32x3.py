@@ -158,3 +158,20 @@ def test_diaglinear_fp32_training_step_on_tf32_route(monkeypatch):
     for p, ref in zip([lyr.values, lyr.alpha, lyr.bias], tf[2:]):
         scale = max(1.0, float(ref.abs().max()))
         assert float((p.grad.double() - ref.double()).abs().max()) <= F32_TOL * scale
+
+
+@pytest.mark.parametrize("trans_a", [False, True])
+@pytest.mark.parametrize("trans_b", [False, True])
+@pytest.mark.parametrize("M,N,K", [(64, 3072, 768), (301, 257, 603), (1000, 70, 5)])
+def test_dense_tf32x3_gemm_vs_fp64(trans_a, trans_b, M, N, K):
+    """diagmm_tf32x3_gemm (the float32 layers' dense route) against an fp64 product at the
+    fp32 bar, every operand orientation, sizes that are not multiples of 4 or of a tile."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn((K, M) if trans_a else (M, K), device="cuda", generator=g)
+    b = torch.randn((K, N) if trans_b else (N, K), device="cuda", generator=g)
+    bias = torch.randn(N, device="cuda", generator=g)
+    out = ops.tf32x3_gemm(a, b, trans_a=trans_a, trans_b=trans_b, bias=bias)
+    A = (a.t() if trans_a else a).double()
+    Bm = (b.t() if trans_b else b).double()
+    ref = (A @ Bm.t() + bias.double()).cpu().numpy()
+    assert scaled_err(out.double().cpu().numpy(), ref) <= F32_TOL
