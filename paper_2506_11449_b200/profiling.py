@@ -341,6 +341,21 @@ def diag_case(M, N, B, sparsity, act_dtype, peaks, fma_tflops, seed=0, reps=20, 
         dense = [_time_call(fn, reps, flush) * 1e3 for fn in (f, b1, b2)]
         res["cublas_bf16_dense_us"] = {"fwd": dense[0], "dx": dense[1], "dw": dense[2], "total": sum(dense)}
         res["speedup_vs_cublas_bf16_fwd_bwd"] = sum(dense) / res.get("best_route_us", tot)
+        if act_dtype == torch.float32:
+            # the same-precision baseline for float32 layers: cuBLAS SGEMM with TF32 off
+            prev = torch.backends.cuda.matmul.allow_tf32
+            torch.backends.cuda.matmul.allow_tf32 = False
+            try:
+                W32 = W.float()
+                f32 = [lambda: x @ W32.t(), lambda: dy @ W32, lambda: dy.t() @ x]
+                for fn in f32:
+                    fn()
+                d32 = [_time_call(fn, reps, flush) * 1e3 for fn in f32]
+            finally:
+                torch.backends.cuda.matmul.allow_tf32 = prev
+            res["cublas_fp32_dense_us"] = {"fwd": d32[0], "dx": d32[1], "dw": d32[2], "total": sum(d32),
+                                           "note": "cuBLAS SGEMM, TF32 off: the same-precision dense baseline"}
+            res["speedup_vs_cublas_fp32_fwd_bwd"] = sum(d32) / res.get("best_route_us", tot)
     return res
 
 
