@@ -1025,19 +1025,22 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // One candidate row of the finalize (shared by the per-layer and the batched kernels):
 // reduce the dW partials over parts (fixed order), scale into g_values, zero inactive
 // rows, g_soft, the data-parallel bucket row.
-template <typename T>
+template <typename T, int U = 1, bool BLOCK = false>
 __device__ void finalize_row(int ii, int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial,
                              int max_act, const int32_t* __restrict__ slot, int n_act,
                              const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
                              typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
                              typename Traits<T>::P* __restrict__ bucket, int bucket_rows,
-                             const int32_t* __restrict__ active_rows) {
+                             const int32_t* __restrict__ active_rows, double* red = nullptr) {
   using P = typename Traits<T>::P;
   using A = typename Vec<T>::A;
   constexpr int VW = 16 / sizeof(P);
   using V = typename std::conditional<sizeof(P) == 8, double2, float4>::type;
   using VA = typename std::conditional<sizeof(A) == 8, double2, float4>::type;
-  const int lane = threadIdx.x & 31;  // one WARP per row: no barrier, rows of a CTA run concurrently
+  // one WARP per row (no barrier, rows of a CTA run concurrently), or with BLOCK the whole
+  // CTA on one row (few long rows: the FMA route's 4096-wide layers at high sparsity)
+  const int lane = BLOCK ? (int)threadIdx.x : (int)(threadIdx.x & 31);
+  const int nth = BLOCK ? (int)blockDim.x : 32;
   do {
 
   // active_rows: the CTAs walk the active list only (the zero rows are filled
@@ -1050,9 +1053,9 @@ __device__ void finalize_row(int ii, int C, int L, int nparts, const typename Ve
   if (s < 0 || s >= n_act) {
     if (vec) {
       V* g4 = reinterpret_cast<V*>(grow);
-      for (int t = lane; t < L / VW; t += 32) g4[t] = V{};
+      for (int t = lane; t < L / VW; t += nth) g4[t] = V{};
     } else {
-      for (int t = lane; t < L; t += 32) grow[t] = P(0);
+      for (int t = lane; t < L; t += nth) grow[t] = P(0);
     }
     if (g_soft && lane == 0) g_soft[i] = 0.0;
     break;
@@ -1069,38 +1072,55 @@ __device__ void finalize_row(int ii, int C, int L, int nparts, const typename Ve
     const int nv = L / VW;
     const size_t zs = (size_t)max_act * L / VW;
     const VA* pbase = reinterpret_cast<const VA*>(partial + (size_t)s * L);
-    for (int c = lane; c < nv; c += 32) {
-      const V v = reinterpret_cast<const V*>(vrow)[c];
-      VA gw = nparts > 0 ? pbase[c] : VA{};
-      A* ge = reinterpret_cast<A*>(&gw);
-      for (int p0 = 1; p0 < nparts; p0 += 8) {
-        VA x[8];
+    // U of the lane's positions per pass, their first loads all in flight (U = 4 in the
+    // per-layer kernel, whose rows can be 4096 wide; 1 in the batched one, where registers
+    // bound the occupancy); the lane still walks c = lane, lane + 32, ... in order, so
+    // g_soft's per-lane sum keeps its order and both kernels give the same bits
+    for (int c0 = lane; c0 < nv; c0 += nth * U) {
+      V v[U];
+      VA gw[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (p0 + k < nparts) x[k] = __ldcg(pbase + (size_t)(p0 + k) * zs + c);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (p0 + k >= nparts) break;
-          const A* xe = reinterpret_cast<const A*>(&x[k]);
-#pragma unroll
-          for (int e = 0; e < VW; ++e) ge[e] += xe[e];
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + nth * u;
+        if (c < nv) {
+          v[u] = reinterpret_cast<const V*>(vrow)[c];
+          gw[u] = nparts > 0 ? pbase[c] : VA{};
         }
       }
-      const P* ve = reinterpret_cast<const P*>(&v);
-      V o;
-      P* oe = reinterpret_cast<P*>(&o);
 #pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        oe[e] = (P)(sc * (double)ge[e]);
-        local += (double)ge[e] * (double)ve[e];
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + nth * u;
+        if (c >= nv) break;
+        A* ge = reinterpret_cast<A*>(&gw[u]);
+        for (int p0 = 1; p0 < nparts; p0 += 8) {
+          VA x[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (p0 + k < nparts) x[k] = __ldcg(pbase + (size_t)(p0 + k) * zs + c);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (p0 + k >= nparts) break;
+            const A* xe = reinterpret_cast<const A*>(&x[k]);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) ge[e] += xe[e];
+          }
+        }
+        const P* ve = reinterpret_cast<const P*>(&v[u]);
+        V o;
+        P* oe = reinterpret_cast<P*>(&o);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          oe[e] = (P)(sc * (double)ge[e]);
+          local += (double)ge[e] * (double)ve[e];
+        }
+        reinterpret_cast<V*>(grow)[c] = o;
+        if (bvec) reinterpret_cast<V*>(brow)[c] = o;
+        else if (brow)
+          for (int e = 0; e < VW; ++e) brow[c * VW + e] = oe[e];
       }
-      reinterpret_cast<V*>(grow)[c] = o;
-      if (bvec) reinterpret_cast<V*>(brow)[c] = o;
-      else if (brow)
-        for (int e = 0; e < VW; ++e) brow[c * VW + e] = oe[e];
     }
   } else {
-    for (int t = lane; t < L; t += 32) {
+    for (int t = lane; t < L; t += nth) {
       A gw = A(0);
       for (int p = 0; p < nparts; ++p) gw += partial[((size_t)p * max_act + s) * L + t];
       grow[t] = (P)(sc * (double)gw);
@@ -1111,7 +1131,18 @@ __device__ void finalize_row(int ii, int C, int L, int nparts, const typename Ve
   if (g_soft) {  // per-lane sums in a fixed order, then a fixed shuffle tree (deterministic)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if (lane == 0) g_soft[i] = local;
+    if constexpr (BLOCK) {  // + the warps' sums folded in warp order
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+        g_soft[i] = tot;
+      }
+      __syncthreads();
+    } else {
+      if (lane == 0) g_soft[i] = local;
+    }
   }
     } while (false);
 }
@@ -1129,12 +1160,27 @@ k_dw_finalize(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ p
   // one warp per row, grid-stride over rows: ~90 % of the rows are a zero fill
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
   for (int ii = w; ii < (active_rows ? n_act : C); ii += nw)
-    finalize_row<T>(ii, C, L, nparts, partial, max_act, slot, n_act, asoft, vals, g_values, g_soft, bucket,
-                    bucket_rows, active_rows);
+    finalize_row<T, 4>(ii, C, L, nparts, partial, max_act, slot, n_act, asoft, vals, g_values, g_soft, bucket,
+                       bucket_rows, active_rows);
 }
 
 // one CTA per candidate row: measured faster than a persistent grid-stride loop
 // (4096^2, B = 1: 22.3 vs 26.6 us for the whole dW)
+// The per-layer finalize for few, long rows (FMA route, L >= 1024): one CTA per active row.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_dw_finalize_blk(int C, int L, int nparts, const typename Vec<T>::A* __restrict__ partial, int max_act,
+                  const int32_t* __restrict__ slot, const int32_t* __restrict__ n_act_p,
+                  const double* __restrict__ asoft, const typename Traits<T>::P* __restrict__ vals,
+                  typename Traits<T>::P* __restrict__ g_values, double* __restrict__ g_soft,
+                  typename Traits<T>::P* __restrict__ bucket, int bucket_rows, const int32_t* __restrict__ active_rows) {
+  __shared__ double red[kWarps];
+  const int n_act = min(*n_act_p, max_act);
+  for (int ii = blockIdx.x; ii < n_act; ii += gridDim.x)
+    finalize_row<T, 2, true>(ii, C, L, nparts, partial, max_act, slot, n_act, asoft, vals, g_values, g_soft, bucket,
+                             bucket_rows, active_rows, red);
+}
+
 static int finalize_grid(int C) { return C; }
 
 // The reference's zero rows of g_values (inactive candidates, layers.py:159-163)
@@ -2983,7 +3029,12 @@ int run_dw(int M, int N, int B, const void* dy, const void* x, const void* vals,
   } else {
     parts = 0;
   }
-  k_dw_finalize<T><<<ceil_div(max_act > 0 ? max_act : 1, kWarps), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+  if (L >= 1024)  // few long rows: a CTA per row keeps enough loads in flight
+    k_dw_finalize_blk<T><<<max_act > 0 ? max_act : 1, 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
+                                       static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
+                                       static_cast<P*>(bucket), bucket_rows, active);
+  else
+    k_dw_finalize<T><<<ceil_div(max_act > 0 ? max_act : 1, kWarps), 256, 0, st>>>(C, L, parts, partial, max_act, slot, n_act, asoft,
                                        static_cast<const P*>(vals), static_cast<P*>(g_values), g_soft,
                                        static_cast<P*>(bucket), bucket_rows, active);
   note_launch();
