@@ -436,8 +436,9 @@ int run_tc_gemm2_bf16(int Mdim, int Ndim, int K, const void* A, const void* B, c
     else go(k_tc_gemm2<4, 2, 4, 2>, Smem2<4, 2, 4, 2>::total);
   } else if (epi == 0 && !b_kn && getenv_r2()) {
     // plain forward epilogue in 2 store rounds of 128 columns: half the proxy fences and
-    // barriers per tile — the qkv forward (K = 768) 1.89 -> 1.43 ms per ViT-B step; the
-    // input-gradient products (W_K read MN-major) measured the same either way
+    // barriers per tile — the qkv forward (K = 768) 1.89 -> 1.43 ms of kernel time per ViT-B
+    // step (the power-capped step itself did not move); the input-gradient products (W_K
+    // read MN-major) measured the same either way
     go(k_tc_gemm2<5, 1, 2, 2>, Smem2<5, 1, 2, 2>::total);
   } else {
     if (b_kn) go(k_tc_gemm2<5, 1, 4, 2, true>, Smem2<5, 1, 4, 2>::total);
